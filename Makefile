@@ -1,0 +1,56 @@
+# Build recipe for the B200-native PBD-R library (invoked by __graft_entry__.build()).
+#
+#   make            -> paper_2603_14634_b200/lib/libpbdr_gpu.so  (product: sm_100a CUDA + C-ABI)
+#                      oracle/build/liboracle.so                (test infrastructure)
+#                      build/test_dropin                        (C++ drop-in API test driver)
+#   make ref        -> oracle/_ref/libpbdr_ref.so (needs /root/reference; this container only)
+#
+# --fmad=false keeps every fp32/fp64 product and sum separately rounded, which
+# is what lets the CUDA path reproduce the CPU oracle bit for bit.
+
+NVCC     ?= /usr/local/cuda/bin/nvcc
+CXX      := /usr/bin/g++
+ARCH     := -gencode arch=compute_100a,code=sm_100a
+PKG      := paper_2603_14634_b200
+CSRC     := $(PKG)/csrc
+LIB      := $(PKG)/lib/libpbdr_gpu.so
+NVFLAGS  := $(ARCH) -std=c++17 -O3 -lineinfo --fmad=false -Xcompiler -fPIC,-ffp-contract=off \
+            -Xptxas -v -Iinclude -I$(CSRC)
+CU_SRC   := $(CSRC)/pbdr_kernels.cu $(CSRC)/pbdr_sort.cu $(CSRC)/pbdr_engine.cu
+CXX_SRC  := $(CSRC)/pbdr_scene.cpp $(CSRC)/pbdr_errors.cpp $(CSRC)/pbdr_dropin.cpp
+HDRS     := include/pbdr_gpu.h $(wildcard include/pbdr/*.hpp) $(wildcard $(CSRC)/*.h) $(wildcard $(CSRC)/*.cuh)
+OBJDIR   := build/obj
+CU_OBJ   := $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(CU_SRC))
+CXX_OBJ  := $(patsubst $(CSRC)/%.cpp,$(OBJDIR)/%.o,$(CXX_SRC))
+
+.PHONY: all lib oracle ref clean
+all: lib oracle build/test_dropin
+
+lib: $(LIB)
+
+$(OBJDIR)/%.o: $(CSRC)/%.cu $(HDRS)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(OBJDIR)/$*.ptxas.txt || (cat $(OBJDIR)/$*.ptxas.txt; false)
+
+$(OBJDIR)/%.o: $(CSRC)/%.cpp $(HDRS)
+	@mkdir -p $(OBJDIR)
+	$(CXX) -std=c++17 -O3 -fPIC -ffp-contract=off -Wall -Wextra -Iinclude -I$(CSRC) \
+	    -I/usr/local/cuda/include -c $< -o $@
+
+$(LIB): $(CU_OBJ) $(CXX_OBJ)
+	@mkdir -p $(PKG)/lib
+	$(NVCC) $(ARCH) -shared -o $@ $^ -lcudart
+
+oracle:
+	$(MAKE) -C oracle
+
+ref:
+	$(MAKE) -C oracle ref
+
+build/test_dropin: tests/cpp/test_dropin.cpp $(LIB) $(HDRS)
+	@mkdir -p build
+	$(CXX) -std=c++17 -O2 -Iinclude tests/cpp/test_dropin.cpp -o $@ \
+	    -L$(PKG)/lib -lpbdr_gpu -Wl,-rpath,'$$ORIGIN/../$(PKG)/lib'
+
+clean:
+	rm -rf build $(PKG)/lib oracle/build

@@ -1,0 +1,272 @@
+// TEST INFRASTRUCTURE ONLY — part of the CPU oracle (see pbdr_oracle.cpp).
+//
+// Double-precision 3x3 numerics restated from the reference's math module,
+// with the op order pinned so that the CUDA
+// path's per-body math is bit-identical:
+//   * adjugate inverse            — math.cpp:8-24
+//   * cyclic Jacobi eigen         — math.cpp:26-71
+//   * SPD pseudo-inverse          — math.cpp:90-108
+//   * quaternion from/to matrix   — math.cpp:117-146, math.hpp:217-227
+//   * scaled-Newton polar         — math.cpp:170-210
+// Deviations from the reference (all documented in DESIGN.md):
+//   * g = (in/xn)^(1/4) is evaluated as sqrt(sqrt(.)) (correctly rounded on
+//     both CPU and GPU) instead of std::pow; X^-T/g as X^-T * (1/g);
+//   * the polar degeneracy test is scale-relative (pbdr_pinned.h);
+//   * the inertia inverse takes the adjugate branch when provably full rank.
+// These functions are checked against the reference's own compiled math
+// (oracle/_ref) by tests/test_oracle_golden.py.
+#pragma once
+
+#include <cmath>
+
+#include "pbdr_pinned.h"
+
+namespace orc {
+
+struct M3 {
+  double a[3][3];
+};
+
+inline double det3(const M3& m) {
+  return m.a[0][0] * (m.a[1][1] * m.a[2][2] - m.a[1][2] * m.a[2][1]) -
+         m.a[0][1] * (m.a[1][0] * m.a[2][2] - m.a[1][2] * m.a[2][0]) +
+         m.a[0][2] * (m.a[1][0] * m.a[2][1] - m.a[1][1] * m.a[2][0]);
+}
+
+inline double frob(const M3& m) {
+  double s = 0.0;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) s = s + m.a[i][j] * m.a[i][j];
+  return std::sqrt(s);
+}
+
+inline bool finite3(const M3& m) {
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j)
+      if (!std::isfinite(m.a[i][j])) return false;
+  return true;
+}
+
+// Adjugate / det. Caller guarantees det != 0.
+inline M3 adj_inverse(const M3& m, double d) {
+  const double id = 1.0 / d;
+  const double(*a)[3] = m.a;
+  M3 r;
+  r.a[0][0] = (a[1][1] * a[2][2] - a[1][2] * a[2][1]) * id;
+  r.a[0][1] = (a[0][2] * a[2][1] - a[0][1] * a[2][2]) * id;
+  r.a[0][2] = (a[0][1] * a[1][2] - a[0][2] * a[1][1]) * id;
+  r.a[1][0] = (a[1][2] * a[2][0] - a[1][0] * a[2][2]) * id;
+  r.a[1][1] = (a[0][0] * a[2][2] - a[0][2] * a[2][0]) * id;
+  r.a[1][2] = (a[0][2] * a[1][0] - a[0][0] * a[1][2]) * id;
+  r.a[2][0] = (a[1][0] * a[2][1] - a[1][1] * a[2][0]) * id;
+  r.a[2][1] = (a[0][1] * a[2][0] - a[0][0] * a[2][1]) * id;
+  r.a[2][2] = (a[0][0] * a[1][1] - a[0][1] * a[1][0]) * id;
+  return r;
+}
+
+// max column abs-sum times max row abs-sum.
+inline double norm1_inf(const M3& m) {
+  double c = 0.0, r = 0.0;
+  for (int j = 0; j < 3; ++j) {
+    const double s = (std::fabs(m.a[0][j]) + std::fabs(m.a[1][j])) + std::fabs(m.a[2][j]);
+    c = s > c ? s : c;
+  }
+  for (int i = 0; i < 3; ++i) {
+    const double s = (std::fabs(m.a[i][0]) + std::fabs(m.a[i][1])) + std::fabs(m.a[i][2]);
+    r = s > r ? s : r;
+  }
+  return c * r;
+}
+
+// Unit quaternion (w, x, y, z) from a near-rotation matrix, largest-pivot
+// branch, then normalised by division.
+inline void quat_from(const M3& x, double q[4]) {
+  const double(*m)[3] = x.a;
+  const double tr = (m[0][0] + m[1][1]) + m[2][2];
+  double w, qx, qy, qz;
+  if (tr > 0.0) {
+    const double s = std::sqrt(tr + 1.0) * 2.0;
+    w = 0.25 * s;
+    qx = (m[2][1] - m[1][2]) / s;
+    qy = (m[0][2] - m[2][0]) / s;
+    qz = (m[1][0] - m[0][1]) / s;
+  } else if (m[0][0] > m[1][1] && m[0][0] > m[2][2]) {
+    const double s = std::sqrt(((1.0 + m[0][0]) - m[1][1]) - m[2][2]) * 2.0;
+    w = (m[2][1] - m[1][2]) / s;
+    qx = 0.25 * s;
+    qy = (m[0][1] + m[1][0]) / s;
+    qz = (m[0][2] + m[2][0]) / s;
+  } else if (m[1][1] > m[2][2]) {
+    const double s = std::sqrt(((1.0 + m[1][1]) - m[0][0]) - m[2][2]) * 2.0;
+    w = (m[0][2] - m[2][0]) / s;
+    qx = (m[0][1] + m[1][0]) / s;
+    qy = 0.25 * s;
+    qz = (m[1][2] + m[2][1]) / s;
+  } else {
+    const double s = std::sqrt(((1.0 + m[2][2]) - m[0][0]) - m[1][1]) * 2.0;
+    w = (m[1][0] - m[0][1]) / s;
+    qx = (m[0][2] + m[2][0]) / s;
+    qy = (m[1][2] + m[2][1]) / s;
+    qz = 0.25 * s;
+  }
+  const double n = std::sqrt(((w * w + qx * qx) + qy * qy) + qz * qz);
+  if (n > 0.0) {
+    w = w / n; qx = qx / n; qy = qy / n; qz = qz / n;
+  } else {
+    w = 1.0; qx = qy = qz = 0.0;
+  }
+  q[0] = w; q[1] = qx; q[2] = qy; q[3] = qz;
+}
+
+inline M3 quat_to(const double q[4]) {
+  const double w = q[0], x = q[1], y = q[2], z = q[3];
+  const double xx = x * x, yy = y * y, zz = z * z;
+  const double xy = x * y, xz = x * z, yz = y * z;
+  const double wx = w * x, wy = w * y, wz = w * z;
+  M3 r;
+  r.a[0][0] = 1.0 - 2.0 * (yy + zz);
+  r.a[0][1] = 2.0 * (xy - wz);
+  r.a[0][2] = 2.0 * (xz + wy);
+  r.a[1][0] = 2.0 * (xy + wz);
+  r.a[1][1] = 1.0 - 2.0 * (xx + zz);
+  r.a[1][2] = 2.0 * (yz - wx);
+  r.a[2][0] = 2.0 * (xz - wy);
+  r.a[2][1] = 2.0 * (yz + wx);
+  r.a[2][2] = 1.0 - 2.0 * (xx + yy);
+  return r;
+}
+
+// Returns false when degenerate. On success fills R (rotation matrix from the
+// normalised quaternion) and q.
+inline bool polar_rotation(const M3& A, M3& R, double q[4]) {
+  if (!finite3(A)) return false;
+  const double s = frob(A) / std::sqrt(3.0);
+  if (det3(A) <= PBDR_POLAR_REL_DET * ((s * s) * s)) return false;
+  M3 X = A;
+  for (int it = 0; it < PBDR_POLAR_MAX_IT; ++it) {
+    const double d = det3(X);
+    if (d == 0.0 || !std::isfinite(d)) return false;
+    const M3 inv = adj_inverse(X, d);
+    M3 xit;
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) xit.a[i][j] = inv.a[j][i];
+    const double xn = norm1_inf(X);
+    const double in = norm1_inf(xit);
+    const double g = (xn > 0.0 && in > 0.0) ? std::sqrt(std::sqrt(in / xn)) : 1.0;
+    const double ig = 1.0 / g;
+    M3 nx, dx;
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) {
+        nx.a[i][j] = 0.5 * (g * X.a[i][j] + xit.a[i][j] * ig);
+        dx.a[i][j] = nx.a[i][j] - X.a[i][j];
+      }
+    const double delta = frob(dx);
+    X = nx;
+    const double fx = frob(X);
+    if (delta <= PBDR_POLAR_TOL * (fx > 1e-300 ? fx : 1e-300)) break;
+  }
+  quat_from(X, q);
+  R = quat_to(q);
+  return true;
+}
+
+// Cyclic Jacobi on the symmetrised matrix; ascending eigenvalues, eigenvector
+// columns in V.
+inline void sym_eigen(const M3& m, double ev[3], M3& V) {
+  double A[3][3];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) A[i][j] = 0.5 * (m.a[i][j] + m.a[j][i]);
+  double U[3][3] = {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}};
+  for (int sweep = 0; sweep < 32; ++sweep) {
+    const double off = (std::fabs(A[0][1]) + std::fabs(A[0][2])) + std::fabs(A[1][2]);
+    const double scale = (std::fabs(A[0][0]) + std::fabs(A[1][1])) + std::fabs(A[2][2]);
+    if (off <= 1e-15 * (scale > 1e-300 ? scale : 1e-300)) break;
+    for (int p = 0; p < 2; ++p)
+      for (int qq = p + 1; qq < 3; ++qq) {
+        if (A[p][qq] == 0.0) continue;
+        const double theta = (A[qq][qq] - A[p][p]) / (2.0 * A[p][qq]);
+        const double t = (theta >= 0.0 ? 1.0 : -1.0) /
+                         (std::fabs(theta) + std::sqrt(theta * theta + 1.0));
+        const double c = 1.0 / std::sqrt(t * t + 1.0);
+        const double s = t * c;
+        const double app = A[p][p], aqq = A[qq][qq], apq = A[p][qq];
+        A[p][p] = ((c * c) * app - ((2.0 * s) * c) * apq) + (s * s) * aqq;
+        A[qq][qq] = ((s * s) * app + ((2.0 * s) * c) * apq) + (c * c) * aqq;
+        A[p][qq] = 0.0;
+        A[qq][p] = 0.0;
+        for (int k = 0; k < 3; ++k) {
+          if (k == p || k == qq) continue;
+          const double akp = A[k][p], akq = A[k][qq];
+          A[k][p] = c * akp - s * akq;
+          A[p][k] = A[k][p];
+          A[k][qq] = s * akp + c * akq;
+          A[qq][k] = A[k][qq];
+        }
+        for (int k = 0; k < 3; ++k) {
+          const double vkp = U[k][p], vkq = U[k][qq];
+          U[k][p] = c * vkp - s * vkq;
+          U[k][qq] = s * vkp + c * vkq;
+        }
+      }
+  }
+  int order[3] = {0, 1, 2};
+  const double d[3] = {A[0][0], A[1][1], A[2][2]};
+  // Stable insertion sort, ascending.
+  for (int i = 1; i < 3; ++i) {
+    const int o = order[i];
+    int j = i - 1;
+    while (j >= 0 && d[order[j]] > d[o]) {
+      order[j + 1] = order[j];
+      --j;
+    }
+    order[j + 1] = o;
+  }
+  for (int i = 0; i < 3; ++i) {
+    ev[i] = d[order[i]];
+    for (int k = 0; k < 3; ++k) V.a[k][i] = U[k][order[i]];
+  }
+}
+
+// omega = pinv(I) * dL with the reference's rank cut. Returns 0, or
+// PBDR_DEVERR_RANK_DEFICIENT (omega = 0, null axis filled).
+inline unsigned inertia_solve(const M3& I, const double dL[3], double w[3], double null_axis[3]) {
+  const double tr = (I.a[0][0] + I.a[1][1]) + I.a[2][2];
+  const double d = det3(I);
+  w[0] = w[1] = w[2] = 0.0;
+  if (tr > 0.0 && d >= PBDR_PINV_FAST_DET * ((tr * tr) * tr)) {
+    const M3 inv = adj_inverse(I, d);
+    for (int r = 0; r < 3; ++r)
+      w[r] = (inv.a[r][0] * dL[0] + inv.a[r][1] * dL[1]) + inv.a[r][2] * dL[2];
+    return 0u;
+  }
+  double ev[3];
+  M3 V;
+  sym_eigen(I, ev, V);
+  const double atr = std::fabs(tr);
+  const double cut = PBDR_PINV_REL_TOL * (atr > 1e-300 ? atr : 1e-300);
+  M3 P = {{{0, 0, 0}, {0, 0, 0}, {0, 0, 0}}};
+  int rank = 0;
+  double nax[3] = {0, 0, 0};
+  for (int k = 0; k < 3; ++k) {
+    const double u[3] = {V.a[0][k], V.a[1][k], V.a[2][k]};
+    if (ev[k] >= cut) {
+      const double il = 1.0 / ev[k];
+      for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) P.a[i][j] = P.a[i][j] + (u[i] * u[j]) * il;
+      ++rank;
+    } else {
+      nax[0] = u[0]; nax[1] = u[1]; nax[2] = u[2];
+    }
+  }
+  if (rank < 3) {
+    const double along = std::fabs((dL[0] * nax[0] + dL[1] * nax[1]) + dL[2] * nax[2]);
+    if (along > PBDR_NULL_AXIS_TOL) {
+      null_axis[0] = nax[0]; null_axis[1] = nax[1]; null_axis[2] = nax[2];
+      return PBDR_DEVERR_RANK_DEFICIENT;
+    }
+  }
+  for (int r = 0; r < 3; ++r) w[r] = (P.a[r][0] * dL[0] + P.a[r][1] * dL[1]) + P.a[r][2] * dL[2];
+  return 0u;
+}
+
+}  // namespace orc

@@ -1,0 +1,815 @@
+// Host orchestration + C-ABI implementation (include/pbdr_gpu.h).
+//
+// Replaces the missing reference solver (proj/src/solver.cpp, CMakeLists.txt:20)
+// behind the scene/step API of proj/include/pbdr/scene.hpp:17-82. One handle =
+// one scene on one device and one stream. Device state is float4 SoA in
+// body-major order (bodies own contiguous particle ranges); a frame is captured
+// once into a CUDA graph and replayed.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "pbdr_gpu.h"
+#include "pbdr_internal.h"
+#include "pbdr_kernels.cuh"
+#include "pbdr_pinned.h"
+#include "pbdr_sort.cuh"
+
+using pbdr_dev::BodyProgram;
+using pbdr_dev::DevError;
+
+struct pbdr_handle {
+  int device = 0;
+  int sm_count = 0;
+  cudaStream_t stream = nullptr;
+  int64_t n = 0;
+  int32_t nb = 0;
+  std::vector<int64_t> slot_to_particle;
+
+  float4* pos[2] = {nullptr, nullptr};
+  float4* vel = nullptr;
+  float4* rest = nullptr;
+  float4* init = nullptr;
+  int* body_of = nullptr;
+  int* body_scene = nullptr;
+  BodyProgram* programs = nullptr;
+  float2* body_mass = nullptr;
+  int4* body_desc = nullptr;
+  int2* warp_desc = nullptr;
+  float4* anchor = nullptr;
+  uint32_t* keys[2] = {nullptr, nullptr};
+  uint32_t* vals[2] = {nullptr, nullptr};
+  void* sort_temp = nullptr;
+  uint32_t* cell_start = nullptr;
+  uint32_t* cell_end = nullptr;
+  float4* sorted_pos = nullptr;
+  int* sorted_body = nullptr;
+  int* ncand = nullptr;
+  int* cand_j = nullptr;
+  float* cand_rr = nullptr;
+  DevError* err = nullptr;
+  long long* counter = nullptr;
+  double* stats = nullptr;
+  std::vector<void*> allocations;
+  size_t device_bytes = 0;
+
+  int cur = 0;         // pos buffer holding the current state
+  int sorted_buf = 0;  // keys/vals buffer holding the last sorted pairs
+  int ctas = 0;
+  int hash_bits = 10;
+  int passes = 2;
+  uint32_t mask = 0;
+  float dt = 0, inv_dt = 0, gravity = 0, relax = 1, h = 0, inv_h = 0, h2 = 0;
+  double dt_d = 0;
+  int iters = 10, substeps = 10;
+  int incremental = 1, linfix = 1, angfix = 1;
+  pbdr_dev::Planes planes{};
+
+  cudaGraphExec_t graph[2] = {nullptr, nullptr};
+  int graph_end[2] = {0, 0};
+  int64_t substeps_done = 0;
+  int64_t launches_per_frame = 0;
+};
+
+namespace {
+
+using pbdr_host::set_config_error;
+using pbdr_host::set_error;
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return set_error(PBDR_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define PBDR_CUDA(call)                                   \
+  do {                                                    \
+    cudaError_t e_ = (call);                              \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call);   \
+  } while (0)
+
+template <typename T>
+int dalloc(pbdr_handle* h, T** ptr, size_t count) {
+  void* p = nullptr;
+  const size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+  h->allocations.push_back(p);
+  h->device_bytes += bytes;
+  *ptr = static_cast<T*>(p);
+  return PBDR_OK;
+}
+
+void release(pbdr_handle* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  for (auto& g : h->graph)
+    if (g) cudaGraphExecDestroy(g);
+  for (void* p : h->allocations) cudaFree(p);
+  if (h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+}
+
+struct EventHook final : pbdr_dev::LaunchHook {
+  cudaStream_t stream;
+  float ms[PBDR_KCLASS_COUNT] = {0};
+  int64_t launches[PBDR_KCLASS_COUNT] = {0};
+  cudaEvent_t a = nullptr, b = nullptr;
+  int cls = 0;
+  explicit EventHook(cudaStream_t s) : stream(s) {
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+  }
+  ~EventHook() override {
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
+  void before(int c) override {
+    cls = c;
+    cudaEventRecord(a, stream);
+  }
+  void after(int c, int nl) override {
+    cudaEventRecord(b, stream);
+    cudaEventSynchronize(b);
+    float t = 0;
+    cudaEventElapsedTime(&t, a, b);
+    ms[c] += t;
+    launches[c] += nl;
+  }
+};
+
+// Enqueues one substep (integrate .. iterations) on h->stream.
+void enqueue_substep(pbdr_handle* h, pbdr_dev::LaunchHook* hook) {
+  using namespace pbdr_dev;
+  IntegrateArgs ia{};
+  ia.pos = h->pos[h->cur];
+  ia.vel = h->vel;
+  ia.init = h->init;
+  ia.body_of = h->body_of;
+  ia.body_scene = h->body_scene;
+  ia.programs = h->programs;
+  ia.body_mass = h->body_mass;
+  ia.keys = h->keys[0];
+  ia.vals = h->vals[0];
+  ia.substep_counter = h->counter;
+  ia.n = h->n;
+  ia.dt = h->dt;
+  ia.gravity = h->gravity;
+  ia.inv_h = h->inv_h;
+  ia.dt_d = h->dt_d;
+  ia.mask = h->mask;
+  if (hook) hook->before(kHookIntegrate);
+  launch_integrate(ia, h->stream);
+  if (hook) hook->after(kHookIntegrate);
+
+  const int sb = sort_pairs(h->keys, h->vals, h->n, h->hash_bits, h->sort_temp, h->sm_count,
+                            h->stream, hook);
+  h->sorted_buf = sb;
+
+  if (hook) hook->before(kHookMemset);
+  cudaMemsetAsync(h->cell_start, 0xFF, sizeof(uint32_t) * (size_t(1) << h->hash_bits), h->stream);
+  if (hook) hook->after(kHookMemset);
+
+  RangesArgs ra{};
+  ra.keys = h->keys[sb];
+  ra.vals = h->vals[sb];
+  ra.pos = h->pos[h->cur];
+  ra.rest = h->rest;
+  ra.body_of = h->body_of;
+  ra.cell_start = h->cell_start;
+  ra.cell_end = h->cell_end;
+  ra.sorted_pos = h->sorted_pos;
+  ra.sorted_body = h->sorted_body;
+  ra.substep_counter = h->counter;
+  ra.n = h->n;
+  if (hook) hook->before(kHookRanges);
+  launch_ranges(ra, h->stream);
+  if (hook) hook->after(kHookRanges);
+
+  NeighbourArgs na{};
+  na.pos = h->pos[h->cur];
+  na.rest = h->rest;
+  na.body_of = h->body_of;
+  na.body_scene = h->body_scene;
+  na.cell_start = h->cell_start;
+  na.cell_end = h->cell_end;
+  na.sorted_pos = h->sorted_pos;
+  na.sorted_body = h->sorted_body;
+  na.sorted_vals = h->vals[sb];
+  na.ncand = h->ncand;
+  na.cand_j = h->cand_j;
+  na.cand_rr = h->cand_rr;
+  na.err = h->err;
+  na.substep_counter = h->counter;
+  na.n = h->n;
+  na.inv_h = h->inv_h;
+  na.h2 = h->h2;
+  na.mask = h->mask;
+  if (hook) hook->before(kHookNeighbours);
+  launch_neighbours(na, h->stream);
+  if (hook) hook->after(kHookNeighbours);
+}
+
+void enqueue_iteration(pbdr_handle* h, pbdr_dev::LaunchHook* hook) {
+  using namespace pbdr_dev;
+  IterArgs it{};
+  it.pos_in = h->pos[h->cur];
+  it.pos_out = h->pos[h->cur ^ 1];
+  it.vel = h->vel;
+  it.rest = h->rest;
+  it.init = h->init;
+  it.ncand = h->ncand;
+  it.cand_j = h->cand_j;
+  it.cand_rr = h->cand_rr;
+  it.anchor = h->anchor;
+  it.warp_desc = h->warp_desc;
+  it.body_desc = h->body_desc;
+  it.body_mass = h->body_mass;
+  it.err = h->err;
+  it.substep_counter = h->counter;
+  it.n = h->n;
+  it.planes = h->planes;
+  it.dt = h->dt;
+  it.inv_dt = h->inv_dt;
+  it.relax = h->relax;
+  it.incremental = h->incremental;
+  it.linfix = h->linfix;
+  it.angfix = h->angfix;
+  if (hook) hook->before(kHookIteration);
+  launch_iteration(it, h->ctas, h->stream);
+  if (hook) hook->after(kHookIteration);
+  h->cur ^= 1;
+}
+
+void enqueue_substeps(pbdr_handle* h, int64_t count, pbdr_dev::LaunchHook* hook) {
+  for (int64_t s = 0; s < count; ++s) {
+    enqueue_substep(h, hook);
+    for (int i = 0; i < h->iters; ++i) enqueue_iteration(h, hook);
+  }
+}
+
+// Reads the device error record; maps it to a status (errors.hpp classes).
+int check_errors(pbdr_handle* h) {
+  cudaError_t e = cudaStreamSynchronize(h->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "kernel execution");
+  DevError de{};
+  e = cudaMemcpy(&de, h->err, sizeof de, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(e, "error readback");
+  if (de.bits == 0u) return PBDR_OK;
+  // Errors are recorded after the substep counter advanced (cell_ranges).
+  const int64_t substep = de.substep - 1;
+  const int64_t frame = substep / std::max(1, h->substeps);
+  if (de.bits & PBDR_DEVERR_RANK_DEFICIENT)
+    return pbdr_host::set_sim_error("angular momentum fix: dL along a singular inertia axis",
+                                    frame, de.body, de.axis, PBDR_ERR_RANK_DEFICIENT);
+  if (de.bits & PBDR_DEVERR_DEGENERATE)
+    return pbdr_host::set_sim_error("shape matching: polar decomposition of a degenerate moment",
+                                    frame, de.body, nullptr, PBDR_ERR_DEGENERATE);
+  if (de.bits & PBDR_DEVERR_NBR_OVERFLOW)
+    return pbdr_host::set_sim_error("contact candidates exceed capacity " +
+                                        std::to_string(PBDR_NBR_CAP) + " per particle",
+                                    frame, de.body, nullptr, PBDR_ERR_SIMULATION);
+  return pbdr_host::set_sim_error("non-finite body sums", frame, de.body, nullptr,
+                                  PBDR_ERR_SIMULATION);
+}
+
+int reset_errors(pbdr_handle* h) {
+  DevError de{};
+  de.bits = 0u;
+  de.body = 0x7FFFFFFF;
+  de.substep = 0x7FFFFFFFFFFFFFFFll;
+  PBDR_CUDA(cudaMemcpyAsync(h->err, &de, sizeof de, cudaMemcpyHostToDevice, h->stream));
+  PBDR_CUDA(cudaStreamSynchronize(h->stream));
+  return PBDR_OK;
+}
+
+int build_graph(pbdr_handle* h, int parity) {
+  const int saved = h->cur;
+  h->cur = parity;
+  PBDR_CUDA(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+  enqueue_substeps(h, h->substeps, nullptr);
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaStreamEndCapture(h->stream, &g);
+  h->graph_end[parity] = h->cur;
+  h->cur = saved;
+  if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture");
+  e = cudaGraphInstantiate(&h->graph[parity], g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
+  return PBDR_OK;
+}
+
+int validate(const pbdr_scene_desc* d, const pbdr_solver_cfg* c) {
+  if (!d || !c) return set_config_error("scene", "null descriptor");
+  if (c->precision != PBDR_PRECISION_SINGLE)
+    return set_config_error("precision",
+                            "the B200 path computes in single precision (kSingle); "
+                            "kDouble has no device implementation and there is no CPU fallback");
+  if (!(c->frame_rate > 0.0) || !std::isfinite(c->frame_rate))
+    return set_config_error("frame_rate", "must be > 0");
+  if (c->substeps < 1) return set_config_error("substeps", "must be >= 1");
+  if (c->solver_iterations < 1) return set_config_error("solver_iterations", "must be >= 1");
+  if (!std::isfinite(c->gravity)) return set_config_error("gravity", "must be finite");
+  if (c->momentum_frequency != PBDR_MOMENTUM_PER_ITERATION)
+    return set_config_error("momentum_frequency",
+                            "kPerSubstep is not implemented on the GPU path yet");
+  if (c->velocity_update != PBDR_VELOCITY_LEGACY && c->velocity_update != PBDR_VELOCITY_INCREMENTAL)
+    return set_config_error("velocity_update", "unknown mode");
+  if (d->num_particles <= 0) return set_config_error("particles", "scene has no particles");
+  if (d->num_particles >= (int64_t(1) << 31) - 1)
+    return set_config_error("particles", "more than 2^31-2 particles per device");
+  if (d->num_bodies <= 0) return set_config_error("bodies", "scene has no bodies");
+  if (!(d->contact_relaxation >= 0.0)) return set_config_error("contact_relaxation", "must be >= 0");
+  const int planes = (d->has_ground ? 1 : 0) + std::max(0, d->num_walls);
+  if (planes > PBDR_MAX_PLANES) return set_config_error("walls", "at most 8 planes (ground + walls)");
+  if (d->programs) {
+    for (int32_t b = 0; b < d->num_bodies; ++b) {
+      const pbdr_force_program& p = d->programs[b];
+      if (p.torque[0] != 0.0 || p.torque[1] != 0.0 || p.torque[2] != 0.0)
+        return set_config_error("programs.torque",
+                                "torque programs are not implemented on the GPU path yet");
+    }
+  }
+  return PBDR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int device,
+                    pbdr_handle** out) {
+  if (!out) return set_error(PBDR_ERR_GENERIC, "null output handle");
+  *out = nullptr;
+  pbdr_host::clear_error();
+  int st = validate(d, c);
+  if (st != PBDR_OK) return st;
+
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0)
+    return set_error(PBDR_ERR_CUDA, "no CUDA device available (the PBD-R path has no CPU fallback)");
+  if (device < 0 || device >= ndev) return set_config_error("device", "out of range");
+  PBDR_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop{};
+  PBDR_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10 || prop.minor != 0)
+    return set_error(PBDR_ERR_CUDA, "this build targets sm_100a (B200); device is sm_" +
+                                        std::to_string(prop.major) + std::to_string(prop.minor));
+
+  pbdr_handle* h = new pbdr_handle();
+  h->device = device;
+  h->sm_count = prop.multiProcessorCount;
+  h->n = d->num_particles;
+  h->nb = d->num_bodies;
+  const int64_t n = h->n;
+  const int32_t nb = h->nb;
+
+  // ---- Body-major layout (host) ---------------------------------------------
+  std::vector<float4> pos(n), vel(n), rest(n);
+  std::vector<int> body_of(n), scene(nb, 0);
+  std::vector<BodyProgram> prog(nb);
+  std::vector<float2> mass(nb);
+  std::vector<float4> anchor(nb);
+  std::vector<int4> bdesc(nb);
+  std::vector<int2> wdesc;
+  std::vector<char> seen(n, 0);
+  h->slot_to_particle.resize(n);
+  double rmax = 0.0;
+  int64_t slot = 0;
+  int used = 0;
+  for (int32_t b = 0; b < nb; ++b) {
+    const int64_t k0 = d->body_offsets[b], k1 = d->body_offsets[b + 1];
+    const int64_t cnt = k1 - k0;
+    if (cnt <= 0) {
+      release(h);
+      return set_config_error("bodies.particle_indices", "empty body " + std::to_string(b));
+    }
+    if (cnt > PBDR_MAX_BODY_PARTICLES) {
+      release(h);
+      return set_config_error("bodies.particle_indices",
+                              "body " + std::to_string(b) + " has " + std::to_string(cnt) +
+                                  " particles; the fused iteration kernel holds at most " +
+                                  std::to_string(PBDR_MAX_BODY_PARTICLES));
+    }
+    const int64_t first_slot = slot;
+    for (int64_t k = k0; k < k1; ++k, ++slot) {
+      const int64_t i = d->body_indices[k];
+      if (i < 0 || i >= n || seen[i]) {
+        release(h);
+        return set_config_error("bodies.particle_indices", "particle missing or in two bodies");
+      }
+      seen[i] = 1;
+      if (!(d->inv_mass[i] > 0.0)) {
+        release(h);
+        return set_error(PBDR_ERR_GENERIC, "pinned particles are not supported in rigid bodies");
+      }
+      h->slot_to_particle[slot] = i;
+      pos[slot] = make_float4(static_cast<float>(d->position[3 * i]), static_cast<float>(d->position[3 * i + 1]),
+                              static_cast<float>(d->position[3 * i + 2]), static_cast<float>(d->inv_mass[i]));
+      vel[slot] = make_float4(static_cast<float>(d->velocity[3 * i]), static_cast<float>(d->velocity[3 * i + 1]),
+                              static_cast<float>(d->velocity[3 * i + 2]),
+                              static_cast<float>(1.0 / d->inv_mass[i]));
+      rest[slot] = make_float4(static_cast<float>(d->rest_offsets[3 * k]),
+                               static_cast<float>(d->rest_offsets[3 * k + 1]),
+                               static_cast<float>(d->rest_offsets[3 * k + 2]),
+                               static_cast<float>(d->radius[i]));
+      body_of[slot] = b;
+      rmax = std::max(rmax, d->radius[i]);
+    }
+    const int W = pbdr_body_warps(static_cast<int>(cnt));
+    if (used + W > PBDR_CTA_WARPS) {
+      for (; used < PBDR_CTA_WARPS; ++used) wdesc.push_back(make_int2(-1, 0));
+      used = 0;
+    }
+    bdesc[b] = make_int4(static_cast<int>(first_slot), static_cast<int>(cnt), W, used);
+    for (int u = 0; u < W; ++u) wdesc.push_back(make_int2(b, u));
+    used += W;
+    mass[b] = make_float2(static_cast<float>(d->total_mass[b]), static_cast<float>(1.0 / d->total_mass[b]));
+    anchor[b] = make_float4(pos[first_slot].x, pos[first_slot].y, pos[first_slot].z, 0.0f);
+    scene[b] = d->body_scene ? d->body_scene[b] : 0;
+    BodyProgram bp{};
+    if (d->programs) {
+      const pbdr_force_program& p = d->programs[b];
+      bp.fx = static_cast<float>(p.force[0]);
+      bp.fy = static_cast<float>(p.force[1]);
+      bp.fz = static_cast<float>(p.force[2]);
+      bp.flags = 1 | (p.gravity_exempt ? 2 : 0);
+      bp.t_start = p.t_start;
+      bp.t_stop = p.t_stop;
+    }
+    prog[b] = bp;
+  }
+  if (slot != n) {
+    release(h);
+    return set_config_error("bodies.particle_indices", "every particle must belong to one body");
+  }
+  for (; used < PBDR_CTA_WARPS && used > 0; ++used) wdesc.push_back(make_int2(-1, 0));
+  h->ctas = static_cast<int>(wdesc.size() / PBDR_CTA_WARPS);
+
+  // ---- Parameters ----------------------------------------------------------
+  h->substeps = c->substeps;
+  h->iters = c->solver_iterations;
+  h->dt_d = 1.0 / (c->frame_rate * c->substeps);
+  h->dt = static_cast<float>(h->dt_d);
+  h->inv_dt = static_cast<float>(c->frame_rate * c->substeps);
+  h->gravity = static_cast<float>(c->gravity);
+  h->relax = static_cast<float>(d->contact_relaxation);
+  h->incremental = c->velocity_update == PBDR_VELOCITY_INCREMENTAL;
+  h->linfix = c->linear_momentum_fix != 0;
+  h->angfix = c->angular_momentum_fix != 0;
+  h->h = static_cast<float>(2.0 * rmax);
+  h->inv_h = 1.0f / h->h;
+  h->h2 = h->h * h->h;
+  h->hash_bits = pbdr_hash_bits(n);
+  h->passes = (h->hash_bits + 7) / 8;
+  h->mask = static_cast<uint32_t>((uint64_t(1) << h->hash_bits) - 1u);
+  auto add_plane = [&](const pbdr_plane& p) {
+    const int k = h->planes.count++;
+    for (int c2 = 0; c2 < 3; ++c2) {
+      h->planes.p[k][c2] = static_cast<float>(p.point[c2]);
+      h->planes.n[k][c2] = static_cast<float>(p.normal[c2]);
+    }
+    h->planes.mu[k] = static_cast<float>(p.friction);
+  };
+  if (d->has_ground) add_plane(d->ground);
+  for (int w = 0; w < d->num_walls; ++w) add_plane(d->walls[w]);
+
+  // ---- Device buffers ------------------------------------------------------
+  const size_t T = size_t(1) << h->hash_bits;
+  int rc = PBDR_OK;
+  rc |= dalloc(h, &h->pos[0], n);
+  rc |= dalloc(h, &h->pos[1], n);
+  rc |= dalloc(h, &h->vel, n);
+  rc |= dalloc(h, &h->rest, n);
+  rc |= dalloc(h, &h->init, n);
+  rc |= dalloc(h, &h->body_of, n);
+  rc |= dalloc(h, &h->body_scene, nb);
+  rc |= dalloc(h, &h->programs, nb);
+  rc |= dalloc(h, &h->body_mass, nb);
+  rc |= dalloc(h, &h->body_desc, nb);
+  rc |= dalloc(h, &h->warp_desc, wdesc.size());
+  rc |= dalloc(h, &h->anchor, nb);
+  rc |= dalloc(h, &h->keys[0], n);
+  rc |= dalloc(h, &h->keys[1], n);
+  rc |= dalloc(h, &h->vals[0], n);
+  rc |= dalloc(h, &h->vals[1], n);
+  {
+    char* tmp = nullptr;
+    rc |= dalloc(h, &tmp, pbdr_dev::sort_temp_bytes(n, h->passes));
+    h->sort_temp = tmp;
+  }
+  rc |= dalloc(h, &h->cell_start, T);
+  rc |= dalloc(h, &h->cell_end, T);
+  rc |= dalloc(h, &h->sorted_pos, n);
+  rc |= dalloc(h, &h->sorted_body, n);
+  rc |= dalloc(h, &h->ncand, n);
+  rc |= dalloc(h, &h->cand_j, static_cast<size_t>(n) * PBDR_NBR_CAP);
+  rc |= dalloc(h, &h->cand_rr, static_cast<size_t>(n) * PBDR_NBR_CAP);
+  rc |= dalloc(h, &h->err, 1);
+  rc |= dalloc(h, &h->counter, 1);
+  rc |= dalloc(h, &h->stats, static_cast<size_t>(nb) * 13);
+  if (rc != PBDR_OK) {
+    const int code = pbdr_last_error_payload(nullptr, nullptr, nullptr);
+    release(h);
+    return code ? code : PBDR_ERR_CUDA;
+  }
+  e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    release(h);
+    return cuda_fail(e, "cudaStreamCreate");
+  }
+#define UP(dst, src, count)                                                                   \
+  e = cudaMemcpy(dst, src, sizeof(*(src)) * (count), cudaMemcpyHostToDevice);                 \
+  if (e != cudaSuccess) {                                                                     \
+    release(h);                                                                               \
+    return cuda_fail(e, "upload " #dst);                                                      \
+  }
+  UP(h->pos[0], pos.data(), n);
+  UP(h->vel, vel.data(), n);
+  UP(h->rest, rest.data(), n);
+  UP(h->body_of, body_of.data(), n);
+  UP(h->body_scene, scene.data(), nb);
+  UP(h->programs, prog.data(), nb);
+  UP(h->body_mass, mass.data(), nb);
+  UP(h->body_desc, bdesc.data(), nb);
+  UP(h->warp_desc, wdesc.data(), wdesc.size());
+  UP(h->anchor, anchor.data(), nb);
+#undef UP
+  cudaMemset(h->init, 0, sizeof(float4) * n);
+  cudaMemset(h->counter, 0, sizeof(long long));
+  cudaMemset(h->ncand, 0, sizeof(int) * n);
+  if (reset_errors(h) != PBDR_OK) {
+    const int code = pbdr_last_error_payload(nullptr, nullptr, nullptr);
+    release(h);
+    return code;
+  }
+  h->launches_per_frame = static_cast<int64_t>(h->substeps) * (1 + 2 + h->passes + 1 + 1 + h->iters);
+  *out = h;
+  return PBDR_OK;
+}
+
+void pbdr_gpu_destroy(pbdr_handle* h) { release(h); }
+
+int pbdr_gpu_step(pbdr_handle* h, int64_t substeps) {
+  if (!h) return set_error(PBDR_ERR_GENERIC, "null handle");
+  pbdr_host::clear_error();
+  PBDR_CUDA(cudaSetDevice(h->device));
+  enqueue_substeps(h, substeps, nullptr);
+  PBDR_CUDA(cudaGetLastError());
+  h->substeps_done += substeps;
+  return check_errors(h);
+}
+
+static int step_frames_async(pbdr_handle* h, int64_t frames) {
+  for (int64_t f = 0; f < frames; ++f) {
+    const int parity = h->cur;
+    if (!h->graph[parity]) {
+      const int rc = build_graph(h, parity);
+      if (rc != PBDR_OK) return rc;
+    }
+    PBDR_CUDA(cudaGraphLaunch(h->graph[parity], h->stream));
+    h->cur = h->graph_end[parity];
+    h->substeps_done += h->substeps;
+  }
+  return PBDR_OK;
+}
+
+int pbdr_gpu_step_frames(pbdr_handle* h, int64_t frames) {
+  if (!h) return set_error(PBDR_ERR_GENERIC, "null handle");
+  pbdr_host::clear_error();
+  PBDR_CUDA(cudaSetDevice(h->device));
+  const int rc = step_frames_async(h, frames);
+  if (rc != PBDR_OK) return rc;
+  return check_errors(h);
+}
+
+int pbdr_gpu_time_frames(pbdr_handle* h, int64_t frames, float* ms) {
+  if (!h || !ms) return set_error(PBDR_ERR_GENERIC, "null argument");
+  PBDR_CUDA(cudaSetDevice(h->device));
+  // Build graphs outside the timed region.
+  for (int p = 0; p < 2; ++p)
+    if (!h->graph[p]) {
+      const int rc = build_graph(h, p);
+      if (rc != PBDR_OK) return rc;
+    }
+  cudaEvent_t a, b;
+  PBDR_CUDA(cudaEventCreate(&a));
+  PBDR_CUDA(cudaEventCreate(&b));
+  PBDR_CUDA(cudaStreamSynchronize(h->stream));
+  PBDR_CUDA(cudaEventRecord(a, h->stream));
+  int rc = step_frames_async(h, frames);
+  PBDR_CUDA(cudaEventRecord(b, h->stream));
+  PBDR_CUDA(cudaEventSynchronize(b));
+  PBDR_CUDA(cudaEventElapsedTime(ms, a, b));
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  if (rc != PBDR_OK) return rc;
+  return check_errors(h);
+}
+
+int pbdr_gpu_profile_frames(pbdr_handle* h, int64_t frames, float* ms, int64_t* launches) {
+  if (!h || !ms || !launches) return set_error(PBDR_ERR_GENERIC, "null argument");
+  PBDR_CUDA(cudaSetDevice(h->device));
+  EventHook hook(h->stream);
+  enqueue_substeps(h, frames * h->substeps, &hook);
+  h->substeps_done += frames * h->substeps;
+  for (int k = 0; k < PBDR_KCLASS_COUNT; ++k) {
+    ms[k] = hook.ms[k];
+    launches[k] = hook.launches[k];
+  }
+  return check_errors(h);
+}
+
+int pbdr_gpu_read_f32(pbdr_handle* h, float* pos4, float* vel4) {
+  if (!h) return set_error(PBDR_ERR_GENERIC, "null handle");
+  PBDR_CUDA(cudaSetDevice(h->device));
+  if (pos4)
+    PBDR_CUDA(cudaMemcpyAsync(pos4, h->pos[h->cur], sizeof(float4) * h->n, cudaMemcpyDeviceToHost, h->stream));
+  if (vel4)
+    PBDR_CUDA(cudaMemcpyAsync(vel4, h->vel, sizeof(float4) * h->n, cudaMemcpyDeviceToHost, h->stream));
+  PBDR_CUDA(cudaStreamSynchronize(h->stream));
+  return PBDR_OK;
+}
+
+int pbdr_gpu_write_f32(pbdr_handle* h, const float* pos4, const float* vel4) {
+  if (!h) return set_error(PBDR_ERR_GENERIC, "null handle");
+  PBDR_CUDA(cudaSetDevice(h->device));
+  if (pos4)
+    PBDR_CUDA(cudaMemcpyAsync(h->pos[h->cur], pos4, sizeof(float4) * h->n, cudaMemcpyHostToDevice, h->stream));
+  if (vel4)
+    PBDR_CUDA(cudaMemcpyAsync(h->vel, vel4, sizeof(float4) * h->n, cudaMemcpyHostToDevice, h->stream));
+  PBDR_CUDA(cudaStreamSynchronize(h->stream));
+  return PBDR_OK;
+}
+
+int pbdr_gpu_read_particles(pbdr_handle* h, double* position, double* velocity) {
+  if (!h) return set_error(PBDR_ERR_GENERIC, "null handle");
+  std::vector<float4> p(h->n), v(h->n);
+  const int rc = pbdr_gpu_read_f32(h, reinterpret_cast<float*>(p.data()), reinterpret_cast<float*>(v.data()));
+  if (rc != PBDR_OK) return rc;
+  for (int64_t s = 0; s < h->n; ++s) {
+    const int64_t i = h->slot_to_particle[s];
+    if (position) {
+      position[3 * i] = p[s].x; position[3 * i + 1] = p[s].y; position[3 * i + 2] = p[s].z;
+    }
+    if (velocity) {
+      velocity[3 * i] = v[s].x; velocity[3 * i + 1] = v[s].y; velocity[3 * i + 2] = v[s].z;
+    }
+  }
+  return PBDR_OK;
+}
+
+int pbdr_gpu_write_particles(pbdr_handle* h, const double* position, const double* velocity) {
+  if (!h) return set_error(PBDR_ERR_GENERIC, "null handle");
+  std::vector<float4> p(h->n), v(h->n);
+  int rc = pbdr_gpu_read_f32(h, reinterpret_cast<float*>(p.data()), reinterpret_cast<float*>(v.data()));
+  if (rc != PBDR_OK) return rc;
+  for (int64_t s = 0; s < h->n; ++s) {
+    const int64_t i = h->slot_to_particle[s];
+    if (position) {
+      p[s].x = static_cast<float>(position[3 * i]);
+      p[s].y = static_cast<float>(position[3 * i + 1]);
+      p[s].z = static_cast<float>(position[3 * i + 2]);
+    }
+    if (velocity) {
+      v[s].x = static_cast<float>(velocity[3 * i]);
+      v[s].y = static_cast<float>(velocity[3 * i + 1]);
+      v[s].z = static_cast<float>(velocity[3 * i + 2]);
+    }
+  }
+  return pbdr_gpu_write_f32(h, reinterpret_cast<const float*>(p.data()), reinterpret_cast<const float*>(v.data()));
+}
+
+int pbdr_gpu_read_bodies(pbdr_handle* h, pbdr_body_stats* out) {
+  if (!h || !out) return set_error(PBDR_ERR_GENERIC, "null argument");
+  static_assert(sizeof(pbdr_body_stats) == 13 * sizeof(double), "stats layout");
+  PBDR_CUDA(cudaSetDevice(h->device));
+  pbdr_dev::StatsArgs sa{};
+  sa.pos = h->pos[h->cur];
+  sa.vel = h->vel;
+  sa.rest = h->rest;
+  sa.anchor = h->anchor;
+  sa.warp_desc = h->warp_desc;
+  sa.body_desc = h->body_desc;
+  sa.body_mass = h->body_mass;
+  sa.out = h->stats;
+  pbdr_dev::launch_stats(sa, h->ctas, h->stream);
+  PBDR_CUDA(cudaGetLastError());
+  PBDR_CUDA(cudaMemcpyAsync(out, h->stats, sizeof(double) * 13 * h->nb, cudaMemcpyDeviceToHost, h->stream));
+  PBDR_CUDA(cudaStreamSynchronize(h->stream));
+  return PBDR_OK;
+}
+
+int pbdr_gpu_info(pbdr_handle* h, pbdr_info* o) {
+  if (!h || !o) return set_error(PBDR_ERR_GENERIC, "null argument");
+  o->num_particles = h->n;
+  o->num_bodies = h->nb;
+  o->num_ctas = h->ctas;
+  o->hash_bits = h->hash_bits;
+  o->sort_passes = h->passes;
+  o->launches_per_frame = h->launches_per_frame;
+  o->device_bytes = static_cast<int64_t>(h->device_bytes);
+  o->device = h->device;
+  o->sm_count = h->sm_count;
+  o->cell_size = h->h;
+  o->dt = h->dt;
+  return PBDR_OK;
+}
+
+// ---- Replay hooks ------------------------------------------------------------
+int pbdr_gpu_debug_prologue(pbdr_handle* h) {
+  if (!h) return set_error(PBDR_ERR_GENERIC, "null handle");
+  PBDR_CUDA(cudaSetDevice(h->device));
+  enqueue_substep(h, nullptr);
+  PBDR_CUDA(cudaGetLastError());
+  return check_errors(h);
+}
+
+int pbdr_gpu_debug_iteration(pbdr_handle* h, int) {
+  if (!h) return set_error(PBDR_ERR_GENERIC, "null handle");
+  PBDR_CUDA(cudaSetDevice(h->device));
+  enqueue_iteration(h, nullptr);
+  PBDR_CUDA(cudaGetLastError());
+  return check_errors(h);
+}
+
+int pbdr_gpu_debug_read_sorted(pbdr_handle* h, uint32_t* keys, uint32_t* vals) {
+  if (!h) return set_error(PBDR_ERR_GENERIC, "null handle");
+  PBDR_CUDA(cudaSetDevice(h->device));
+  if (keys)
+    PBDR_CUDA(cudaMemcpy(keys, h->keys[h->sorted_buf], sizeof(uint32_t) * h->n, cudaMemcpyDeviceToHost));
+  if (vals)
+    PBDR_CUDA(cudaMemcpy(vals, h->vals[h->sorted_buf], sizeof(uint32_t) * h->n, cudaMemcpyDeviceToHost));
+  return PBDR_OK;
+}
+
+// Cell hash of every slot (from the last prologue's sorted pairs) and the
+// integer cell coordinates recomputed by the host from the device positions.
+int pbdr_gpu_debug_read_keys(pbdr_handle* h, uint32_t* cell_hash, int32_t* cell_xyz) {
+  if (!h) return set_error(PBDR_ERR_GENERIC, "null handle");
+  std::vector<uint32_t> k(h->n), v(h->n);
+  int rc = pbdr_gpu_debug_read_sorted(h, k.data(), v.data());
+  if (rc != PBDR_OK) return rc;
+  if (cell_hash)
+    for (int64_t s = 0; s < h->n; ++s) cell_hash[v[s]] = k[s];
+  if (cell_xyz) {
+    std::vector<float4> sp(h->n);
+    PBDR_CUDA(cudaMemcpy(sp.data(), h->sorted_pos, sizeof(float4) * h->n, cudaMemcpyDeviceToHost));
+    for (int64_t s = 0; s < h->n; ++s) {
+      const uint32_t i = v[s];
+      cell_xyz[3 * i] = pbdr_cell_coord(sp[s].x, h->inv_h);
+      cell_xyz[3 * i + 1] = pbdr_cell_coord(sp[s].y, h->inv_h);
+      cell_xyz[3 * i + 2] = pbdr_cell_coord(sp[s].z, h->inv_h);
+    }
+  }
+  return PBDR_OK;
+}
+
+int pbdr_gpu_debug_read_candidates(pbdr_handle* h, int32_t* counts, int32_t* lists) {
+  if (!h) return set_error(PBDR_ERR_GENERIC, "null handle");
+  PBDR_CUDA(cudaSetDevice(h->device));
+  std::vector<int32_t> c(h->n);
+  PBDR_CUDA(cudaMemcpy(c.data(), h->ncand, sizeof(int32_t) * h->n, cudaMemcpyDeviceToHost));
+  if (counts) std::memcpy(counts, c.data(), sizeof(int32_t) * h->n);
+  if (lists) {
+    std::vector<int32_t> sm(static_cast<size_t>(h->n) * PBDR_NBR_CAP);
+    PBDR_CUDA(cudaMemcpy(sm.data(), h->cand_j, sizeof(int32_t) * sm.size(), cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < h->n; ++i)
+      for (int k = 0; k < PBDR_NBR_CAP; ++k)
+        lists[i * PBDR_NBR_CAP + k] = k < c[i] ? sm[static_cast<size_t>(k) * h->n + i] : -1;
+  }
+  return PBDR_OK;
+}
+
+int pbdr_gpu_debug_read_init(pbdr_handle* h, float* init4) {
+  if (!h || !init4) return set_error(PBDR_ERR_GENERIC, "null argument");
+  PBDR_CUDA(cudaSetDevice(h->device));
+  PBDR_CUDA(cudaMemcpy(init4, h->init, sizeof(float4) * h->n, cudaMemcpyDeviceToHost));
+  return PBDR_OK;
+}
+
+int pbdr_gpu_debug_read_anchor(pbdr_handle* h, float* anchor3) {
+  if (!h || !anchor3) return set_error(PBDR_ERR_GENERIC, "null argument");
+  PBDR_CUDA(cudaSetDevice(h->device));
+  std::vector<float4> a(h->nb);
+  PBDR_CUDA(cudaMemcpy(a.data(), h->anchor, sizeof(float4) * h->nb, cudaMemcpyDeviceToHost));
+  for (int32_t b = 0; b < h->nb; ++b) {
+    anchor3[3 * b] = a[b].x; anchor3[3 * b + 1] = a[b].y; anchor3[3 * b + 2] = a[b].z;
+  }
+  return PBDR_OK;
+}
+
+int pbdr_gpu_debug_write_anchor(pbdr_handle* h, const float* anchor3) {
+  if (!h || !anchor3) return set_error(PBDR_ERR_GENERIC, "null argument");
+  PBDR_CUDA(cudaSetDevice(h->device));
+  std::vector<float4> a(h->nb);
+  for (int32_t b = 0; b < h->nb; ++b) a[b] = make_float4(anchor3[3 * b], anchor3[3 * b + 1], anchor3[3 * b + 2], 0.0f);
+  PBDR_CUDA(cudaMemcpy(h->anchor, a.data(), sizeof(float4) * h->nb, cudaMemcpyHostToDevice));
+  return PBDR_OK;
+}
+
+}  // extern "C"

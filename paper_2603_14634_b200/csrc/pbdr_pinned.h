@@ -1,0 +1,115 @@
+/* Pinned constants shared by the CUDA path and the CPU oracle.
+ *
+ * The reference's solver (proj/src/solver.cpp, listed at proj/CMakeLists.txt:20)
+ * is absent, so several choices its code would have fixed are pinned here once
+ * and documented in DESIGN.md section "Pinned semantics". Only data-format
+ * facts live in this header (the cell hash, the per-body reduction topology and
+ * numeric thresholds); the physics formulas are written independently in the
+ * CUDA kernels and in oracle/pbdr_oracle.cpp, so the bit-exact parity tests
+ * compare two implementations rather than one shared one.
+ *
+ * Plain C99 so that both nvcc and g++ (oracle) include it.
+ */
+#ifndef PBDR_PINNED_H
+#define PBDR_PINNED_H
+
+#include <math.h>
+#include <stdint.h>
+
+#if defined(__CUDACC__)
+#define PBDR_HD __host__ __device__ __forceinline__
+#else
+#define PBDR_HD static inline
+#endif
+
+/* ---- Per-body reduction topology ---------------------------------------
+ * A body with n particles is reduced by W = ceil(n / (32*KP)) warps. Lane l of
+ * warp wi owns the particles q = k*32*W + wi*32 + l for k = 0..K-1 with
+ * K = ceil(n / (32*W)) (q < n). Every body sum is, in this order:
+ *   1. per lane, serially over k ascending, starting from +0.0f;
+ *   2. per warp, xor-butterfly with offsets 16, 8, 4, 2, 1 (a + b per level);
+ *   3. per body, serially over warps wi ascending, starting from warp 0's value.
+ * This plays the role of the reference's fixed-chunk deterministic reduction
+ * (proj/include/pbdr/parallel.hpp:15-18, 40-63): results are independent of
+ * scheduling, and the oracle reproduces the tree exactly.
+ */
+#define PBDR_KP 2                 /* particles per lane per body (max)      */
+#define PBDR_CTA_WARPS 16         /* warps per iteration CTA                */
+#define PBDR_MAX_BODY_PARTICLES (PBDR_KP * 32 * PBDR_CTA_WARPS) /* 1024    */
+
+PBDR_HD int pbdr_body_warps(int n) { return (n + 32 * PBDR_KP - 1) / (32 * PBDR_KP); }
+PBDR_HD int pbdr_body_slots(int n, int w) { return (n + 32 * w - 1) / (32 * w); }
+
+/* ---- Uniform hash grid ----------------------------------------------------
+ * Cell edge h = 2 * max radius. Cell coordinate per axis is
+ * floorf(x * inv_h) in fp32 (inv_h = 1.0f / h_f), clamped to +-2^24 before the
+ * int conversion so that runaway particles cannot overflow. The clamp is
+ * monotone and non-expansive, so two particles closer than h still land in
+ * adjacent cells. Buckets: a murmur3-finalised mix of the Teschner primes,
+ * masked to a power-of-two table. Scene ids keep batched scenes apart.
+ */
+#define PBDR_CELL_CLAMP 16777216.0f
+
+PBDR_HD uint32_t pbdr_cell_hash(int32_t cx, int32_t cy, int32_t cz, uint32_t scene,
+                                uint32_t mask) {
+  uint32_t h = ((uint32_t)cx * 73856093u) ^ ((uint32_t)cy * 19349663u) ^
+               ((uint32_t)cz * 83492791u) ^ (scene * 2654435761u);
+  h ^= h >> 16;
+  h *= 0x85ebca6bu;
+  h ^= h >> 13;
+  h *= 0xc2b2ae35u;
+  h ^= h >> 16;
+  return h & mask;
+}
+
+/* Hash table size T = 2^bits, the smallest power of two >= max(n, 1024). */
+PBDR_HD int pbdr_hash_bits(int64_t n) {
+  int b = 10;
+  while (b < 31 && ((int64_t)1 << b) < n) ++b;
+  return b;
+}
+
+PBDR_HD int32_t pbdr_cell_coord(float x, float inv_h) {
+  float c = floorf(x * inv_h);
+  c = fminf(fmaxf(c, -PBDR_CELL_CLAMP), PBDR_CELL_CLAMP);
+  return (int32_t)c;
+}
+
+/* Maximum contact candidates per particle per substep. More raises
+ * PBDR_ERR_SIMULATION (never silently dropped). */
+#define PBDR_NBR_CAP 32
+
+/* Maximum planes (ground + walls) per scene. */
+#define PBDR_MAX_PLANES 8
+
+/* ---- Numeric thresholds (double, per body) --------------------------------
+ * Polar decomposition (math.cpp:170-210 semantics, scaled Newton, tol 1e-9,
+ * <= 64 iterations). The reference's absolute det(A) <= 1e-12 test
+ * (math.cpp:172) rejects small-but-valid bodies, so the
+ * degeneracy test is scale-relative: det(A) <= 1e-12 * (||A||_F / sqrt 3)^3.
+ */
+#define PBDR_POLAR_TOL 1e-9
+#define PBDR_POLAR_MAX_IT 64
+#define PBDR_POLAR_REL_DET 1e-12
+
+/* Inertia inverse for the angular-momentum fix: pseudo-inverse semantics of
+ * math.cpp:90-108 (rank cut at eigenvalue < 1e-10 * trace). When
+ * det(I) >= 1e-6 * trace(I)^3 the matrix is provably full rank under that cut
+ * and the adjugate inverse is used; otherwise the cyclic-Jacobi eigen path runs.
+ * dL along a null axis below 1e-12 is projected out; above it the body raises
+ * RankDeficientError. */
+#define PBDR_PINV_REL_TOL 1e-10
+#define PBDR_PINV_FAST_DET 1e-6
+#define PBDR_NULL_AXIS_TOL 1e-12
+
+/* Coincident-centre fallback axis for particle-particle contact:
+ * distance below this uses +x for the lower particle index, -x for the higher. */
+#define PBDR_COINCIDENT_EPS 1e-9f
+
+/* Device error word bits (mapped to pbdr::errors classes by the host). */
+#define PBDR_DEVERR_DEGENERATE 1u     /* polar: det at/below tolerance      */
+#define PBDR_DEVERR_RANK_DEFICIENT 2u /* dL along a singular inertia axis   */
+#define PBDR_DEVERR_NBR_OVERFLOW 4u   /* > PBDR_NBR_CAP contact candidates  */
+#define PBDR_DEVERR_NONFINITE 8u      /* NaN/Inf in a body sum              */
+
+#endif /* PBDR_PINNED_H */

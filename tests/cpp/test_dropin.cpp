@@ -1,0 +1,123 @@
+// C++ drop-in API test driver: exercises pbdr::Scene / SolverConfig / step()
+// / Solver the way the reference's own solver tests would (SPEC.md:326-334
+// worked examples), through the B200 C-ABI. Run by tests/test_dropin_cpp.py on
+// a GPU box; exits non-zero on the first failure.
+#include <cmath>
+#include <cstdio>
+#include <vector>
+
+#include "pbdr/pbdr_b200.hpp"
+
+namespace {
+
+int failures = 0;
+
+#define EXPECT(cond, ...)                    \
+  do {                                       \
+    if (!(cond)) {                           \
+      std::printf("FAIL %s:%d: ", __FILE__, __LINE__); \
+      std::printf(__VA_ARGS__);              \
+      std::printf("\n");                     \
+      ++failures;                            \
+    }                                        \
+  } while (0)
+
+std::vector<pbdr::Vec3> lattice(int n, double r) {
+  std::vector<pbdr::Vec3> c;
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j)
+      for (int k = 0; k < n; ++k)
+        c.push_back({(i - 0.5 * (n - 1)) * 2 * r, (j - 0.5 * (n - 1)) * 2 * r, (k - 0.5 * (n - 1)) * 2 * r});
+  return c;
+}
+
+pbdr::Vec3 com_of(const pbdr::Scene& s) {
+  pbdr::Vec3 c{0, 0, 0};
+  double m = 0;
+  for (const auto& p : s.particles) {
+    c += p.position * (1.0 / p.inv_mass);
+    m += 1.0 / p.inv_mass;
+  }
+  return c / m;
+}
+
+// free body, no gravity, v0 = (1,0,0), 100 steps of dt = 1 ms ->
+// com displaced 0.1 m along x.
+void free_flight() {
+  pbdr::Scene s;
+  s.has_ground = false;
+  pbdr::add_packed_body(s, lattice(4, 0.025), 0.025, 4.0, pbdr::Rotation(), {0, 0, 1}, 0.0, 0);
+  for (auto& p : s.particles) p.velocity = {1, 0, 0};
+  pbdr::SolverConfig cfg;  // 100 Hz x 10 substeps -> dt = 1 ms
+  cfg.gravity = 0.0;
+  const pbdr::Vec3 c0 = com_of(s);
+  pbdr::Solver solver(s, cfg);
+  solver.step(100);
+  solver.download(s);
+  const pbdr::Vec3 c1 = com_of(s);
+  EXPECT(std::fabs((c1.x - c0.x) - 0.1) < 1e-5, "free flight dx = %.9g", c1.x - c0.x);
+  EXPECT(std::fabs(c1.y - c0.y) < 1e-6 && std::fabs(c1.z - c0.z) < 1e-6, "free flight drift");
+  const auto st = solver.body_stats();
+  EXPECT(std::fabs(st[0].linear[0] - 4.0) < 1e-4, "P_x = %.9g", st[0].linear[0]);
+}
+
+// all dX = 0 -> V_{i+1} equals V~ exactly in incremental mode.
+void zero_delta_velocity() {
+  pbdr::Scene s;
+  s.has_ground = false;
+  pbdr::add_packed_body(s, lattice(3, 0.05), 0.05, 1.0, pbdr::Rotation(), {0, 0, 0}, 0.0, 0);
+  for (auto& p : s.particles) p.velocity = {0.25, -0.5, 0.125};
+  pbdr::SolverConfig cfg;
+  cfg.gravity = 0.0;
+  pbdr::step(s, cfg);
+  bool exact = true;
+  for (const auto& p : s.particles)
+    exact = exact && p.velocity.x == 0.25 && p.velocity.y == -0.5 && p.velocity.z == 0.125;
+  EXPECT(exact, "incremental update must return V~ bit for bit when dX = 0");
+}
+
+// Resting box on the ground: com stays put (SPEC.md:333 statics, short run).
+void resting_box() {
+  pbdr::Scene s;
+  s.ground.friction = 0.4;
+  pbdr::add_packed_body(s, lattice(4, 0.025), 0.025, 4.0, pbdr::Rotation(), {0, 0, 0.1}, 0.0, 0);
+  pbdr::SolverConfig cfg;
+  const pbdr::Vec3 c0 = com_of(s);
+  pbdr::Solver solver(s, cfg);
+  solver.step_frames(100);
+  solver.download(s);
+  const pbdr::Vec3 c1 = com_of(s);
+  const double d = std::sqrt((c1.x - c0.x) * (c1.x - c0.x) + (c1.y - c0.y) * (c1.y - c0.y) +
+                             (c1.z - c0.z) * (c1.z - c0.z));
+  EXPECT(d < 1e-3, "resting box drift %.3g m", d);
+}
+
+void config_errors() {
+  pbdr::Scene s;
+  pbdr::add_packed_body(s, lattice(2, 0.05), 0.05, 1.0, pbdr::Rotation(), {0, 0, 1}, 0.0, 0);
+  pbdr::SolverConfig cfg;
+  cfg.precision = pbdr::Precision::kDouble;
+  bool threw = false;
+  try {
+    pbdr::Solver solver(s, cfg);
+  } catch (const pbdr::ConfigError& e) {
+    threw = e.key_path == "precision";
+  }
+  EXPECT(threw, "kDouble must raise ConfigError('precision')");
+}
+
+}  // namespace
+
+int main() {
+  try {
+    free_flight();
+    zero_delta_velocity();
+    resting_box();
+    config_errors();
+  } catch (const pbdr::Error& e) {
+    std::printf("FAIL: uncaught pbdr::Error: %s\n", e.what());
+    return 2;
+  }
+  if (failures == 0) std::printf("test_dropin: all passed\n");
+  return failures == 0 ? 0 : 1;
+}

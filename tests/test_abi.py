@@ -1,0 +1,111 @@
+"""C-ABI boundary checks that need no GPU: the in-tree CUDA library loads,
+exports every function include/pbdr_gpu.h declares, maps configuration errors
+to the reference's exception classes, and refuses to compute without a device
+(no CPU fallback). Also the scene generators' sizes and determinism."""
+import ctypes as C
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from paper_2603_14634_b200 import pbdr as P
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_functions():
+    text = open(os.path.join(ROOT, "include", "pbdr_gpu.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(pbdr_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol(pbdr):
+    names = declared_functions()
+    assert len(names) >= 30
+    out = subprocess.run(["nm", "-D", "--defined-only", P.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(line.split()[-1] for line in out.splitlines() if line.strip())
+    missing = [n for n in names if n not in exported]
+    assert not missing, missing
+    L = pbdr.lib()
+    for n in names:
+        getattr(L, n)
+    assert L.pbdr_abi_version() == 1
+
+
+def test_library_is_sm100a_only(pbdr):
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", P.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert all("sm_100a" in line for line in out.splitlines() if ".cubin" in line)
+
+
+def test_no_device_means_loud_failure(pbdr):
+    if P.cuda_device_count() > 0:
+        pytest.skip("a CUDA device is visible")
+    g = P.GeneratedScene(1)
+    with pytest.raises(P.CudaUnavailableError):
+        P.GpuSolver(g.desc, g.cfg)
+
+
+def test_config_errors_map_to_key_paths(pbdr):
+    g = P.GeneratedScene(1)
+    cfg = P.solver_cfg(precision=1)
+    with pytest.raises(P.ConfigError) as e:
+        P.GpuSolver(g.desc, cfg)
+    assert e.value.key_path == "precision"
+    cfg = P.solver_cfg(substeps=0)
+    with pytest.raises(P.ConfigError) as e:
+        P.GpuSolver(g.desc, cfg)
+    assert e.value.key_path == "substeps"
+    with pytest.raises(P.ConfigError):
+        P.GeneratedScene(9)
+
+
+@pytest.mark.parametrize("cid,n,nb", [(1, 512, 1), (2, 13824, 64)])
+def test_generated_small_configs(pbdr, cid, n, nb):
+    g = P.GeneratedScene(cid, seed=0)
+    assert g.num_particles == n and g.num_bodies == nb
+    assert g.forced_overlaps == 0
+    assert g.cfg.frame_rate == 240.0 and g.cfg.substeps == 10 and g.cfg.solver_iterations == 10
+    offs = g.body_offsets()
+    assert offs[0] == 0 and offs[-1] == n
+    x = g.positions()
+    if cid == 1:
+        np.testing.assert_allclose(x.mean(0), [0, 0, 0.5], atol=1e-12)
+        m = 1.0 / g.array("inv_mass", n)
+        np.testing.assert_allclose(m.sum(), 1.0)
+
+
+def test_generated_scaled_configs(pbdr):
+    g3 = P.GeneratedScene(3, seed=0, scale=64)
+    assert g3.num_bodies == 64
+    offs = g3.body_offsets()
+    sizes = np.diff(offs)
+    assert sizes.min() >= 27 and sizes.max() <= 1000
+    g4 = P.GeneratedScene(4, seed=0, scale=8)
+    assert g4.num_bodies == 128 and g4.num_particles == 8 * 3456
+    scenes = np.ctypeslib.as_array(g4.desc.body_scene, shape=(128,))
+    assert list(np.unique(scenes)) == list(range(8))
+    assert g4.forced_overlaps == 0
+    g5 = P.GeneratedScene(5, seed=0, scale=8)
+    assert g5.num_bodies == 8 * 8 * 4 and g5.num_particles == 256 * 512
+    assert g5.forced_overlaps == 0
+
+
+def test_generation_is_deterministic_and_seeded(pbdr):
+    a = P.GeneratedScene(2, seed=7).positions()
+    b = P.GeneratedScene(2, seed=7).positions()
+    c = P.GeneratedScene(2, seed=8).positions()
+    assert np.array_equal(a, b)
+    assert not np.array_equal(a, c)
+
+
+def test_c4_shards_concatenate_to_whole(pbdr):
+    # Weak-scaling shards (scene ranges per rank) reproduce the 1-GPU scenes.
+    whole = P.GeneratedScene(4, seed=0, scale=6)
+    s0 = P.GeneratedScene(4, seed=0, scale=3, c4_first_scene=0)
+    s1 = P.GeneratedScene(4, seed=0, scale=3, c4_first_scene=3)
+    cat = np.concatenate([s0.positions(), s1.positions()])
+    assert np.array_equal(cat, whole.positions())

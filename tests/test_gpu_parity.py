@@ -1,0 +1,209 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on
+identical seeded inputs.
+
+north_star bars: hash-cell assignments and contact-pair sets bit-exact;
+positions after one step within 1e-5 m; single-body com/orientation
+trajectories over 1000 steps within 1e-3 relative; free-flight P/L conserved
+within 1e-5 relative; piles' aggregates within 1%. Because both sides follow
+the same pinned op order, most comparisons here are bit-exact; the
+north_star tolerances are asserted as well, in the test bodies.
+"""
+import numpy as np
+import pytest
+
+from paper_2603_14634_b200 import pbdr as P
+
+pytestmark = pytest.mark.gpu
+
+# (config, scale): scaled-down configs keep the oracle within seconds.
+CASES = [(1, 0), (2, 0), (3, 24), (4, 3), (5, 6)]
+
+
+def pair(pyoracle, cid, scale=0, seed=0, cfg=None):
+    g = P.GeneratedScene(cid, seed=seed, scale=scale)
+    c = g.cfg if cfg is None else cfg
+    return g, P.GpuSolver(g.desc, c), pyoracle.Oracle(g.desc, c)
+
+
+def assert_same(a, b, what):
+    if not np.array_equal(a, b):
+        diff = np.abs(a.astype(np.float64) - b.astype(np.float64))
+        idx = np.unravel_index(np.argmax(diff), diff.shape)
+        raise AssertionError(f"{what}: {np.count_nonzero(diff)} differ, max {diff.max():.3g} at {idx}")
+
+
+@pytest.mark.parametrize("cid,scale", CASES)
+def test_prologue_bit_exact(pbdr, pyoracle, cid, scale):
+    g, gpu, orc = pair(pyoracle, cid, scale)
+    gpu.debug_prologue()
+    orc.integrate()
+    orc.candidates()
+    gp, gv = gpu.read_f32()
+    op, ov = orc.read_f32()
+    assert_same(gp, op, "integrated positions")
+    assert_same(gv, ov, "integrated velocities")
+    assert_same(gpu.debug_init(), orc.read_init(), "x_init")
+    # Hash-cell assignment (cell coordinates and bucket) bit-exact.
+    gh, gc = gpu.debug_keys()
+    oh, oc = orc.keys()
+    assert_same(gc, oc, "cell coordinates")
+    assert_same(gh, oh, "cell hash")
+    # Onesweep output: sorted, a permutation, stable.
+    k, v = gpu.debug_sorted()
+    assert np.all(k[1:] >= k[:-1])
+    assert np.array_equal(np.sort(v), np.arange(gpu.n, dtype=np.uint32))
+    same = k[1:] == k[:-1]
+    assert np.all(v[1:][same] > v[:-1][same])
+    assert np.array_equal(k, oh[v])
+    # Contact candidate sets bit-exact (ascending slot order).
+    gcnt, glst = gpu.debug_candidates()
+    ocnt, olst = orc.read_candidates()
+    assert_same(gcnt, ocnt, "candidate counts")
+    mask = np.arange(P.NBR_CAP)[None, :] < gcnt[:, None]
+    assert_same(np.where(mask, glst, -1), np.where(mask, olst, -1), "candidate lists")
+    if cid > 1:
+        assert gcnt.sum() > 0 or cid == 5
+    # Symmetry of the pair set.
+    ii = np.repeat(np.arange(gpu.n), gcnt)
+    jj = glst[mask]
+    fwd = set(zip(ii.tolist(), jj.tolist()))
+    assert all((j, i) in fwd for i, j in fwd)
+
+
+@pytest.mark.parametrize("cid,scale", CASES)
+def test_iterations_bit_exact(pbdr, pyoracle, cid, scale):
+    g, gpu, orc = pair(pyoracle, cid, scale)
+    gpu.debug_prologue()
+    orc.integrate()
+    orc.candidates()
+    for it in range(g.cfg.solver_iterations):
+        gpu.debug_iteration()
+        orc.iteration()
+        gp, gv = gpu.read_f32()
+        op, ov = orc.read_f32()
+        assert_same(gp, op, f"positions after iteration {it}")
+        assert_same(gv, ov, f"velocities after iteration {it}")
+        assert_same(gpu.debug_anchor(), orc.read_anchor(), f"anchors after iteration {it}")
+
+
+@pytest.mark.parametrize("cid,scale", CASES)
+def test_one_frame_matches_oracle(pbdr, pyoracle, cid, scale):
+    g, gpu, orc = pair(pyoracle, cid, scale)
+    gpu.step_frames(1)  # CUDA-graph replay of one frame (10 substeps)
+    assert orc.step(g.cfg.substeps) == 0
+    gp, gv = gpu.read_particles()
+    op, ov = orc.read_particles()
+    assert np.abs(gp - op).max() <= 1e-5  # north_star: one step within 1e-5 m
+    assert np.array_equal(gp, op) and np.array_equal(gv, ov)
+    assert_same(gpu.read_bodies(), orc.body_stats(), "body stats")
+
+
+def test_graph_replay_equals_direct_substeps(pbdr):
+    g = P.GeneratedScene(2)
+    a = P.GpuSolver(g.desc, g.cfg)
+    b = P.GpuSolver(g.desc, g.cfg)
+    a.step_frames(3)
+    b.step(3 * g.cfg.substeps)
+    pa, va = a.read_f32()
+    pb, vb = b.read_f32()
+    assert np.array_equal(pa, pb) and np.array_equal(va, vb)
+
+
+def test_odd_iteration_count_parity(pbdr, pyoracle):
+    g = P.GeneratedScene(2)
+    cfg = P.solver_cfg(frame_rate=240.0, substeps=3, solver_iterations=5)
+    gpu = P.GpuSolver(g.desc, cfg)
+    orc = pyoracle.Oracle(g.desc, cfg)
+    gpu.step_frames(3)
+    assert orc.step(9) == 0
+    assert np.array_equal(gpu.read_f32()[0], orc.read_f32()[0])
+
+
+@pytest.mark.parametrize("variant", ["pbd", "linear_only", "angular_only", "legacy_fixed"])
+def test_solver_variants_bit_exact(pbdr, pyoracle, variant):
+    # SolverConfig::pbd() and the Table IV ablations (scene.hpp:22-24, 33-39).
+    cfg = {"pbd": P.pbd_cfg(frame_rate=240.0),
+           "linear_only": P.solver_cfg(frame_rate=240.0, angular_momentum_fix=False),
+           "angular_only": P.solver_cfg(frame_rate=240.0, linear_momentum_fix=False),
+           "legacy_fixed": P.solver_cfg(frame_rate=240.0, velocity_update=0)}[variant]
+    g = P.GeneratedScene(2)
+    gpu = P.GpuSolver(g.desc, cfg)
+    orc = pyoracle.Oracle(g.desc, cfg)
+    gpu.step_frames(2)
+    assert orc.step(2 * cfg.substeps) == 0
+    gp, gv = gpu.read_f32()
+    op, ov = orc.read_f32()
+    assert_same(gp, op, variant + " positions")
+    assert_same(gv, ov, variant + " velocities")
+
+
+@pytest.mark.slow
+def test_c1_trajectory_1000_steps(pbdr, pyoracle):
+    # north_star: single-body com / orientation over 1000 steps within 1e-3 rel.
+    g, gpu, orc = pair(pyoracle, 1)
+    worst_com, worst_ang = 0.0, 0.0
+    for frame in range(1000):
+        gpu.step_frames(1)
+        assert orc.step(g.cfg.substeps) == 0
+        if frame % 50 == 49 or frame == 999:
+            sg, so = gpu.read_bodies()[0], orc.body_stats()[0]
+            worst_com = max(worst_com, np.abs(sg[0:3] - so[0:3]).max() / max(1e-3, np.abs(so[0:3]).max()))
+            d = abs(float(np.dot(sg[3:7], so[3:7])))
+            worst_ang = max(worst_ang, 2 * np.arccos(min(1.0, d)))
+    assert worst_com <= 1e-3 and worst_ang <= 1e-3
+    assert np.array_equal(gpu.read_f32()[0], orc.read_f32()[0])
+
+
+def test_free_flight_momentum_gpu(pbdr):
+    # north_star: free-flight P and L conserved within 1e-5 relative.
+    g = P.GeneratedScene(1)
+    cfg = P.solver_cfg(frame_rate=240.0, gravity=0.0)
+    sc = P.ArrayScene(position=g.positions(), velocity=g.velocities(), inv_mass=g.array("inv_mass", 512),
+                      radius=g.array("radius", 512), body_offsets=[0, 512],
+                      rest_offsets=g.array("rest_offsets", 3 * 512), total_mass=[1.0],
+                      rest_com=g.array("rest_com", 3), has_ground=False)
+    gpu = P.GpuSolver(sc.desc, cfg)
+    s0 = gpu.read_bodies()[0]
+    gpu.step_frames(1000)
+    s1 = gpu.read_bodies()[0]
+    np.testing.assert_allclose(s1[7:10], s0[7:10], rtol=1e-5, atol=1e-5 * np.linalg.norm(s0[7:10]))
+    np.testing.assert_allclose(s1[10:13], s0[10:13], rtol=1e-5, atol=1e-5 * np.linalg.norm(s0[10:13]))
+
+
+@pytest.mark.slow
+def test_c2_pile_aggregates(pbdr, pyoracle):
+    # north_star: chaotic piles agree on aggregates (pile com, KE) within 1%.
+    g, gpu, orc = pair(pyoracle, 2)
+    frames = 120
+    gpu.step_frames(frames)
+    assert orc.step(frames * g.cfg.substeps) == 0
+    gp, gv = gpu.read_particles()
+    op, ov = orc.read_particles()
+    m = 1.0 / g.array("inv_mass", g.num_particles)
+    com_g = (gp * m[:, None]).sum(0) / m.sum()
+    com_o = (op * m[:, None]).sum(0) / m.sum()
+    ke_g = 0.5 * (m * (gv ** 2).sum(1)).sum()
+    ke_o = 0.5 * (m * (ov ** 2).sum(1)).sum()
+    assert np.abs(com_g - com_o).max() <= 0.01 * np.abs(com_o).max()
+    assert abs(ke_g - ke_o) <= 0.01 * max(ke_o, 1e-12)
+    assert np.array_equal(gp, op)
+
+
+def test_deterministic_reruns(pbdr):
+    # identical scene + config + seed -> bit-identical trajectory.
+    g = P.GeneratedScene(3, scale=64)
+    a = P.GpuSolver(g.desc, g.cfg)
+    b = P.GpuSolver(g.desc, g.cfg)
+    a.step_frames(2)
+    b.step_frames(2)
+    assert np.array_equal(a.read_f32()[0], b.read_f32()[0])
+
+
+def test_penetration_bound_c2(pbdr):
+    # SPEC.md:341 (frame-boundary penetration <= 10% of r) on the settling pile.
+    g = P.GeneratedScene(2)
+    gpu = P.GpuSolver(g.desc, g.cfg)
+    gpu.step_frames(240)
+    p, _ = gpu.read_particles()
+    r = g.array("radius", g.num_particles)
+    assert (p[:, 2] - r).min() >= -0.1 * r.max()
