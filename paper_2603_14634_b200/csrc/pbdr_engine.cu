@@ -47,7 +47,6 @@ struct pbdr_handle {
   void* sort_temp = nullptr;
   uint32_t* cell_start = nullptr;
   uint32_t* cell_end = nullptr;
-  float4* sorted_pos = nullptr;
   int* sorted_body = nullptr;
   int* ncand = nullptr;
   int* cand_j = nullptr;
@@ -176,12 +175,9 @@ void enqueue_substep(pbdr_handle* h, pbdr_dev::LaunchHook* hook) {
   RangesArgs ra{};
   ra.keys = h->keys[sb];
   ra.vals = h->vals[sb];
-  ra.pos = h->pos[h->cur];
-  ra.rest = h->rest;
   ra.body_of = h->body_of;
   ra.cell_start = h->cell_start;
   ra.cell_end = h->cell_end;
-  ra.sorted_pos = h->sorted_pos;
   ra.sorted_body = h->sorted_body;
   ra.substep_counter = h->counter;
   ra.n = h->n;
@@ -196,7 +192,6 @@ void enqueue_substep(pbdr_handle* h, pbdr_dev::LaunchHook* hook) {
   na.body_scene = h->body_scene;
   na.cell_start = h->cell_start;
   na.cell_end = h->cell_end;
-  na.sorted_pos = h->sorted_pos;
   na.sorted_body = h->sorted_body;
   na.sorted_vals = h->vals[sb];
   na.ncand = h->ncand;
@@ -504,7 +499,6 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
   }
   rc |= dalloc(h, &h->cell_start, T);
   rc |= dalloc(h, &h->cell_end, T);
-  rc |= dalloc(h, &h->sorted_pos, n);
   rc |= dalloc(h, &h->sorted_body, n);
   rc |= dalloc(h, &h->ncand, n);
   rc |= dalloc(h, &h->cand_j, static_cast<size_t>(n) * PBDR_NBR_CAP);
@@ -757,13 +751,13 @@ int pbdr_gpu_debug_read_keys(pbdr_handle* h, uint32_t* cell_hash, int32_t* cell_
   if (cell_hash)
     for (int64_t s = 0; s < h->n; ++s) cell_hash[v[s]] = k[s];
   if (cell_xyz) {
-    std::vector<float4> sp(h->n);
-    PBDR_CUDA(cudaMemcpy(sp.data(), h->sorted_pos, sizeof(float4) * h->n, cudaMemcpyDeviceToHost));
-    for (int64_t s = 0; s < h->n; ++s) {
-      const uint32_t i = v[s];
-      cell_xyz[3 * i] = pbdr_cell_coord(sp[s].x, h->inv_h);
-      cell_xyz[3 * i + 1] = pbdr_cell_coord(sp[s].y, h->inv_h);
-      cell_xyz[3 * i + 2] = pbdr_cell_coord(sp[s].z, h->inv_h);
+    // Positions are still X~ between the prologue and the first iteration.
+    std::vector<float4> xp(h->n);
+    PBDR_CUDA(cudaMemcpy(xp.data(), h->pos[h->cur], sizeof(float4) * h->n, cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < h->n; ++i) {
+      cell_xyz[3 * i] = pbdr_cell_coord(xp[i].x, h->inv_h);
+      cell_xyz[3 * i + 1] = pbdr_cell_coord(xp[i].y, h->inv_h);
+      cell_xyz[3 * i + 2] = pbdr_cell_coord(xp[i].z, h->inv_h);
     }
   }
   return PBDR_OK;

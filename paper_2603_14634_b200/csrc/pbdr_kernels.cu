@@ -93,7 +93,8 @@ __global__ void __launch_bounds__(256) k_integrate_key(IntegrateArgs A) {
 }
 
 // ---------------------------------------------------------------------------
-// cell ranges + sorted copy of the predicted positions
+// cell ranges: per-bucket [start, end) in sorted order, and the body of every
+// sorted entry (slots are ascending within a bucket, so bodies are too).
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_cell_ranges(RangesArgs A) {
   const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -102,15 +103,14 @@ __global__ void __launch_bounds__(256) k_cell_ranges(RangesArgs A) {
   const uint32_t k = A.keys[s];
   if (s == 0 || A.keys[s - 1] != k) A.cell_start[k] = static_cast<uint32_t>(s);
   if (s == A.n - 1 || A.keys[s + 1] != k) A.cell_end[k] = static_cast<uint32_t>(s + 1);
-  const uint32_t j = A.vals[s];
-  const float4 x = A.pos[j];
-  A.sorted_pos[s] = make_float4(x.x, x.y, x.z, A.rest[j].w);
-  A.sorted_body[s] = A.body_of[j];
+  A.sorted_body[s] = A.body_of[A.vals[s]];
 }
 
 // ---------------------------------------------------------------------------
 // contact candidates (pinned P4): {j : same scene, other body,
 // |cell_j - cell_i|_inf <= 1, |x~_i - x~_j|^2 < h^2}, ascending j, <= CAP.
+// A bucket whose first and last entries belong to particle i's own body holds
+// only own-body particles and is skipped without a scan (most buckets).
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(128) k_neighbours(NeighbourArgs A) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -140,11 +140,13 @@ __global__ void __launch_bounds__(128) k_neighbours(NeighbourArgs A) {
     const uint32_t s0 = A.cell_start[hb];
     if (s0 == 0xFFFFFFFFu) continue;
     const uint32_t s1 = A.cell_end[hb];
+    if (A.sorted_body[s0] == bi && A.sorted_body[s1 - 1] == bi) continue;
     for (uint32_t s = s0; s < s1; ++s) {
       const int bj = A.sorted_body[s];
       if (bj == bi) continue;
       if (A.body_scene[bj] != si) continue;
-      const float4 xj = A.sorted_pos[s];
+      const int j = static_cast<int>(A.sorted_vals[s]);
+      const float4 xj = A.pos[j];
       const int32_t jx = pbdr_cell_coord(xj.x, A.inv_h);
       const int32_t jy = pbdr_cell_coord(xj.y, A.inv_h);
       const int32_t jz = pbdr_cell_coord(xj.z, A.inv_h);
@@ -153,7 +155,6 @@ __global__ void __launch_bounds__(128) k_neighbours(NeighbourArgs A) {
       const float ex = xi.x - xj.x, ey = xi.y - xj.y, ez = xi.z - xj.z;
       const float d2 = (ex * ex + ey * ey) + ez * ez;
       if (!(d2 < A.h2)) continue;
-      const int j = static_cast<int>(A.sorted_vals[s]);
       // Keep the CAP smallest j in ascending order.
       if (count == PBDR_NBR_CAP) {
         overflow = true;
@@ -167,7 +168,7 @@ __global__ void __launch_bounds__(128) k_neighbours(NeighbourArgs A) {
         --pos;
       }
       cand[pos] = j;
-      cr[pos] = ri + xj.w;
+      cr[pos] = ri + A.rest[j].w;
       ++count;
     }
   }

@@ -50,12 +50,9 @@ struct IntegrateArgs {
 struct RangesArgs {
   const uint32_t* keys;  // sorted
   const uint32_t* vals;  // sorted slots
-  const float4* pos;     // X~
-  const float4* rest;
   const int* body_of;
   uint32_t* cell_start;
   uint32_t* cell_end;
-  float4* sorted_pos;  // (x, y, z, radius)
   int* sorted_body;
   long long* substep_counter;
   int64_t n;
@@ -68,7 +65,6 @@ struct NeighbourArgs {
   const int* body_scene;
   const uint32_t* cell_start;
   const uint32_t* cell_end;
-  const float4* sorted_pos;
   const int* sorted_body;
   const uint32_t* sorted_vals;
   int* ncand;
