@@ -167,8 +167,8 @@ int pbdr_gpu_time_frames(pbdr_handle* h, int64_t frames, float* ms);
 /* Per-kernel-class device time over `frames` frames (events around each
  * launch; run separately from the timed region). Classes, in order:
  * 0 integrate+key, 1 histogram+scan, 2 onesweep passes, 3 cell ranges,
- * 4 neighbours, 5 iteration, 6 memsets. ms[7], launches[7]. */
-#define PBDR_KCLASS_COUNT 7
+ * 4 neighbours, 5 iteration, 6 memsets, 7 body broadphase. ms[8], launches[8]. */
+#define PBDR_KCLASS_COUNT 8
 int pbdr_gpu_profile_frames(pbdr_handle* h, int64_t frames, float* ms, int64_t* launches);
 
 /* Replay hooks (used by the parity tests; not on the product path). The
@@ -181,6 +181,9 @@ int pbdr_gpu_debug_read_keys(pbdr_handle* h, uint32_t* cell_hash, int32_t* cell_
 int pbdr_gpu_debug_read_sorted(pbdr_handle* h, uint32_t* keys, uint32_t* vals);
 int pbdr_gpu_debug_read_candidates(pbdr_handle* h, int32_t* counts, int32_t* lists /* n*CAP */);
 int pbdr_gpu_debug_read_init(pbdr_handle* h, float* init4);
+/* Runs one iteration launch with per-CTA clock64 stamps (8 per CTA: start,
+ * staged, phase A, body math A, phase B, body math B, end, SM id). */
+int pbdr_gpu_debug_phase_timing(pbdr_handle* h, long long* out);
 /* Body anchors (fp32 xyz per body) used by the anchored body sums. */
 int pbdr_gpu_debug_read_anchor(pbdr_handle* h, float* anchor3);
 int pbdr_gpu_debug_write_anchor(pbdr_handle* h, const float* anchor3);

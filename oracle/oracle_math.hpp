@@ -10,7 +10,10 @@
 //   * scaled-Newton polar         — math.cpp:170-210
 // Deviations from the reference (all documented in DESIGN.md):
 //   * g = (in/xn)^(1/4) is evaluated as sqrt(sqrt(.)) (correctly rounded on
-//     both CPU and GPU) instead of std::pow; X^-T/g as X^-T * (1/g);
+//     both CPU and GPU) instead of std::pow; X^-T/g as X^-T * (1/g); the
+//     scaling is applied only while the relative change exceeds 1e-2 (then
+//     plain Newton, which converges quadratically near the polar factor);
+//     root-free degeneracy and convergence tests;
 //   * the polar degeneracy test is scale-relative (pbdr_pinned.h);
 //   * the inertia inverse takes the adjugate branch when provably full rank.
 // These functions are checked against the reference's own compiled math
@@ -79,39 +82,44 @@ inline double norm1_inf(const M3& m) {
 }
 
 // Unit quaternion (w, x, y, z) from a near-rotation matrix, largest-pivot
-// branch, then normalised by division.
+// branch (one reciprocal of the pivot), then normalised by one reciprocal.
 inline void quat_from(const M3& x, double q[4]) {
   const double(*m)[3] = x.a;
   const double tr = (m[0][0] + m[1][1]) + m[2][2];
   double w, qx, qy, qz;
   if (tr > 0.0) {
     const double s = std::sqrt(tr + 1.0) * 2.0;
+    const double is = 1.0 / s;
     w = 0.25 * s;
-    qx = (m[2][1] - m[1][2]) / s;
-    qy = (m[0][2] - m[2][0]) / s;
-    qz = (m[1][0] - m[0][1]) / s;
+    qx = (m[2][1] - m[1][2]) * is;
+    qy = (m[0][2] - m[2][0]) * is;
+    qz = (m[1][0] - m[0][1]) * is;
   } else if (m[0][0] > m[1][1] && m[0][0] > m[2][2]) {
     const double s = std::sqrt(((1.0 + m[0][0]) - m[1][1]) - m[2][2]) * 2.0;
-    w = (m[2][1] - m[1][2]) / s;
+    const double is = 1.0 / s;
+    w = (m[2][1] - m[1][2]) * is;
     qx = 0.25 * s;
-    qy = (m[0][1] + m[1][0]) / s;
-    qz = (m[0][2] + m[2][0]) / s;
+    qy = (m[0][1] + m[1][0]) * is;
+    qz = (m[0][2] + m[2][0]) * is;
   } else if (m[1][1] > m[2][2]) {
     const double s = std::sqrt(((1.0 + m[1][1]) - m[0][0]) - m[2][2]) * 2.0;
-    w = (m[0][2] - m[2][0]) / s;
-    qx = (m[0][1] + m[1][0]) / s;
+    const double is = 1.0 / s;
+    w = (m[0][2] - m[2][0]) * is;
+    qx = (m[0][1] + m[1][0]) * is;
     qy = 0.25 * s;
-    qz = (m[1][2] + m[2][1]) / s;
+    qz = (m[1][2] + m[2][1]) * is;
   } else {
     const double s = std::sqrt(((1.0 + m[2][2]) - m[0][0]) - m[1][1]) * 2.0;
-    w = (m[1][0] - m[0][1]) / s;
-    qx = (m[0][2] + m[2][0]) / s;
-    qy = (m[1][2] + m[2][1]) / s;
+    const double is = 1.0 / s;
+    w = (m[1][0] - m[0][1]) * is;
+    qx = (m[0][2] + m[2][0]) * is;
+    qy = (m[1][2] + m[2][1]) * is;
     qz = 0.25 * s;
   }
   const double n = std::sqrt(((w * w + qx * qx) + qy * qy) + qz * qz);
   if (n > 0.0) {
-    w = w / n; qx = qx / n; qy = qy / n; qz = qz / n;
+    const double in = 1.0 / n;
+    w = w * in; qx = qx * in; qy = qy * in; qz = qz * in;
   } else {
     w = 1.0; qx = qy = qz = 0.0;
   }
@@ -136,36 +144,146 @@ inline M3 quat_to(const double q[4]) {
   return r;
 }
 
-// Returns false when degenerate. On success fills R (rotation matrix from the
-// normalised quaternion) and q.
-inline bool polar_rotation(const M3& A, M3& R, double q[4]) {
-  if (!finite3(A)) return false;
-  const double s = frob(A) / std::sqrt(3.0);
-  if (det3(A) <= PBDR_POLAR_REL_DET * ((s * s) * s)) return false;
-  M3 X = A;
-  for (int it = 0; it < PBDR_POLAR_MAX_IT; ++it) {
-    const double d = det3(X);
-    if (d == 0.0 || !std::isfinite(d)) return false;
-    const M3 inv = adj_inverse(X, d);
-    M3 xit;
-    for (int i = 0; i < 3; ++i)
-      for (int j = 0; j < 3; ++j) xit.a[i][j] = inv.a[j][i];
-    const double xn = norm1_inf(X);
-    const double in = norm1_inf(xit);
-    const double g = (xn > 0.0 && in > 0.0) ? std::sqrt(std::sqrt(in / xn)) : 1.0;
-    const double ig = 1.0 / g;
-    M3 nx, dx;
+inline double frob2(const M3& m) {
+  double s = 0.0;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) s = s + m.a[i][j] * m.a[i][j];
+  return s;
+}
+
+// One pinned Newton polar loop on a 3x3 of float or double (the same code
+// runs in fp32 and fp64): X <- (g X + X^-T / g) / 2, with the 1-inf scaling g
+// (formed in fp32) while the relative change exceeds 1e-2. Stops when the
+// change is below tol, or -- after an unscaled step, whose remaining error is
+// O(change^2) -- below sqrt(tol). Returns the iterations used, or -1 when the
+// iterate became singular.
+template <typename T>
+int newton_polar(T X[3][3], T tol2, T tolq, T scale_rel2, int max_it, bool scaled) {
+  for (int it = 0; it < max_it; ++it) {
+    const T d = X[0][0] * (X[1][1] * X[2][2] - X[1][2] * X[2][1]) -
+                X[0][1] * (X[1][0] * X[2][2] - X[1][2] * X[2][0]) +
+                X[0][2] * (X[1][0] * X[2][1] - X[1][1] * X[2][0]);
+    if (d == T(0) || !std::isfinite(d)) return -1;
+    const T id = T(1) / d;
+    T inv[3][3];
+    inv[0][0] = (X[1][1] * X[2][2] - X[1][2] * X[2][1]) * id;
+    inv[0][1] = (X[0][2] * X[2][1] - X[0][1] * X[2][2]) * id;
+    inv[0][2] = (X[0][1] * X[1][2] - X[0][2] * X[1][1]) * id;
+    inv[1][0] = (X[1][2] * X[2][0] - X[1][0] * X[2][2]) * id;
+    inv[1][1] = (X[0][0] * X[2][2] - X[0][2] * X[2][0]) * id;
+    inv[1][2] = (X[0][2] * X[1][0] - X[0][0] * X[1][2]) * id;
+    inv[2][0] = (X[1][0] * X[2][1] - X[1][1] * X[2][0]) * id;
+    inv[2][1] = (X[0][1] * X[2][0] - X[0][0] * X[2][1]) * id;
+    inv[2][2] = (X[0][0] * X[1][1] - X[0][1] * X[1][0]) * id;
+    T g = T(1), ig = T(1);
+    if (scaled) {
+      float c = 0.0f, r = 0.0f, ci = 0.0f, ri = 0.0f;
+      for (int j = 0; j < 3; ++j) {
+        const float s1 = static_cast<float>((std::fabs(X[0][j]) + std::fabs(X[1][j])) + std::fabs(X[2][j]));
+        const float s2 = static_cast<float>((std::fabs(inv[0][j]) + std::fabs(inv[1][j])) + std::fabs(inv[2][j]));
+        c = s1 > c ? s1 : c;
+        ci = s2 > ci ? s2 : ci;
+      }
+      for (int i = 0; i < 3; ++i) {
+        const float s1 = static_cast<float>((std::fabs(X[i][0]) + std::fabs(X[i][1])) + std::fabs(X[i][2]));
+        const float s2 = static_cast<float>((std::fabs(inv[i][0]) + std::fabs(inv[i][1])) + std::fabs(inv[i][2]));
+        r = s1 > r ? s1 : r;
+        ri = s2 > ri ? s2 : ri;
+      }
+      const float xn = c * r, in = ci * ri;
+      if (xn > 0.0f && in > 0.0f && std::isfinite(in / xn)) {
+        const float gf = std::sqrt(std::sqrt(in / xn));
+        g = static_cast<T>(gf);
+        ig = static_cast<T>(1.0f / gf);
+      }
+    }
+    T dd[9], ff[9];
     for (int i = 0; i < 3; ++i)
       for (int j = 0; j < 3; ++j) {
-        nx.a[i][j] = 0.5 * (g * X.a[i][j] + xit.a[i][j] * ig);
-        dx.a[i][j] = nx.a[i][j] - X.a[i][j];
+        const T nx = T(0.5) * (g * X[i][j] + inv[j][i] * ig);
+        const T dx = nx - X[i][j];
+        dd[3 * i + j] = dx * dx;
+        ff[3 * i + j] = nx * nx;
+        X[i][j] = nx;
       }
-    const double delta = frob(dx);
-    X = nx;
-    const double fx = frob(X);
-    if (delta <= PBDR_POLAR_TOL * (fx > 1e-300 ? fx : 1e-300)) break;
+    const T delta2 = (((dd[0] + dd[1]) + (dd[2] + dd[3])) + ((dd[4] + dd[5]) + (dd[6] + dd[7]))) + dd[8];
+    const T fx2 = (((ff[0] + ff[1]) + (ff[2] + ff[3])) + ((ff[4] + ff[5]) + (ff[6] + ff[7]))) + ff[8];
+    const T fx = fx2 > T(1e-30) ? fx2 : T(1e-30);
+    if (delta2 <= tol2 * fx || (!scaled && delta2 <= tolq * fx)) return it + 1;
+    scaled = delta2 > scale_rel2 * fx;
   }
-  quat_from(X, q);
+  return max_it;
+}
+
+// Returns false when degenerate. On success fills R (rotation matrix from the
+// normalised quaternion) and q. Two stages (pinned): a scaled Newton loop in
+// fp32 on A normalised by ||A||_F/sqrt3, then unscaled fp64 Newton steps to
+// the 1e-9 tolerance (one step, since the fp32 stage leaves ~1e-7); if the fp32
+// stage breaks down, the fp64 loop runs from A with scaling.
+inline bool polar_rotation(const M3& A, M3& R, double q[4]) {
+  if (!finite3(A)) return false;
+  const double d0 = det3(A);
+  const double c3 = frob2(A) * PBDR_ONE_THIRD;
+  if (!(d0 > 0.0) || d0 * d0 <= (PBDR_POLAR_REL_DET * PBDR_POLAR_REL_DET) * ((c3 * c3) * c3)) return false;
+  const double is = 1.0 / std::sqrt(c3);
+  float Xf[3][3];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) Xf[i][j] = static_cast<float>(A.a[i][j] * is);
+  double X[3][3];
+  const int f_it = newton_polar<float>(Xf, PBDR_POLAR_F32_TOL2, PBDR_POLAR_F32_TOLQ,
+                                       static_cast<float>(PBDR_POLAR_SCALE_REL2), PBDR_POLAR_F32_MAX_IT, true);
+  M3 Xm;
+  if (f_it > 0) {
+    // fp64 polish: one unscaled Newton step re-orthonormalises the fp32
+    // iterate (R0), then one first-order rotation correction solves the
+    // symmetry condition of B = R0^T A: axial(B - B^T) = (tr(S) I - S) w,
+    // S = sym(B), and R = R0 (I + [w]x) (error O(|w|^2) ~ 1e-14).
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) X[i][j] = static_cast<double>(Xf[i][j]);
+    if (newton_polar<double>(X, 0.0, 0.0, 0.0, 1, false) < 0) return false;
+    double B[3][3];
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j)
+        B[i][j] = (X[0][i] * A.a[0][j] + X[1][i] * A.a[1][j]) + X[2][i] * A.a[2][j];
+    const double sv[3] = {B[2][1] - B[1][2], B[0][2] - B[2][0], B[1][0] - B[0][1]};
+    double M[3][3];
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) M[i][j] = -(0.5 * (B[i][j] + B[j][i]));
+    const double tr = (-M[0][0] + -M[1][1]) + -M[2][2];
+    M[0][0] = tr + M[0][0];
+    M[1][1] = tr + M[1][1];
+    M[2][2] = tr + M[2][2];
+    const double dm = M[0][0] * (M[1][1] * M[2][2] - M[1][2] * M[2][1]) -
+                      M[0][1] * (M[1][0] * M[2][2] - M[1][2] * M[2][0]) +
+                      M[0][2] * (M[1][0] * M[2][1] - M[1][1] * M[2][0]);
+    double w[3] = {0.0, 0.0, 0.0};
+    if (dm != 0.0 && std::isfinite(dm)) {
+      const double idm = 1.0 / dm;
+      const double c00 = (M[1][1] * M[2][2] - M[1][2] * M[2][1]) * idm;
+      const double c01 = (M[0][2] * M[2][1] - M[0][1] * M[2][2]) * idm;
+      const double c02 = (M[0][1] * M[1][2] - M[0][2] * M[1][1]) * idm;
+      const double c11 = (M[0][0] * M[2][2] - M[0][2] * M[2][0]) * idm;
+      const double c12 = (M[0][2] * M[1][0] - M[0][0] * M[1][2]) * idm;
+      const double c22 = (M[0][0] * M[1][1] - M[0][1] * M[1][0]) * idm;
+      w[0] = (c00 * sv[0] + c01 * sv[1]) + c02 * sv[2];
+      w[1] = (c01 * sv[0] + c11 * sv[1]) + c12 * sv[2];
+      w[2] = (c02 * sv[0] + c12 * sv[1]) + c22 * sv[2];
+    }
+    for (int i = 0; i < 3; ++i) {
+      Xm.a[i][0] = X[i][0] + (X[i][1] * w[2] - X[i][2] * w[1]);
+      Xm.a[i][1] = X[i][1] + (X[i][2] * w[0] - X[i][0] * w[2]);
+      Xm.a[i][2] = X[i][2] + (X[i][0] * w[1] - X[i][1] * w[0]);
+    }
+  } else {
+    // fp32 stage broke down: full scaled fp64 Newton from A.
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) X[i][j] = A.a[i][j];
+    if (newton_polar<double>(X, PBDR_POLAR_TOL2, PBDR_POLAR_TOLQ, PBDR_POLAR_SCALE_REL2, PBDR_POLAR_MAX_IT, true) < 0)
+      return false;
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) Xm.a[i][j] = X[i][j];
+  }
+  quat_from(Xm, q);
   R = quat_to(q);
   return true;
 }

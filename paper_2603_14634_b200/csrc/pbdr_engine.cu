@@ -40,13 +40,29 @@ struct pbdr_handle {
   BodyProgram* programs = nullptr;
   float2* body_mass = nullptr;
   int4* body_desc = nullptr;
-  int2* warp_desc = nullptr;
+  int4* warp_desc = nullptr;
+  int4* cta_desc = nullptr;
   float4* anchor = nullptr;
   uint32_t* keys[2] = {nullptr, nullptr};
   uint32_t* vals[2] = {nullptr, nullptr};
   void* sort_temp = nullptr;
-  uint32_t* cell_start = nullptr;
-  uint32_t* cell_end = nullptr;
+  uint4* cells = nullptr;
+  // body broadphase
+  uint32_t* box_min = nullptr;
+  uint32_t* box_max = nullptr;
+  uint32_t* bkeys[2] = {nullptr, nullptr};
+  uint32_t* bvals[2] = {nullptr, nullptr};
+  void* bsort_temp = nullptr;
+  uint2* bcells = nullptr;
+  int* npartners = nullptr;
+  int* partners = nullptr;
+  unsigned* oversize = nullptr;
+  int bhash_bits = 10;
+  int bpasses = 2;
+  uint32_t bmask = 0;
+  float inv_cell_b = 0, max_extent = 0, inflate = 0;
+  long long* timing = nullptr;      // set only while an instrumented launch is enqueued
+  long long* timing_buf = nullptr;  // per-CTA phase clocks (debug hook only)
   int* sorted_body = nullptr;
   int* ncand = nullptr;
   int* cand_j = nullptr;
@@ -153,6 +169,8 @@ void enqueue_substep(pbdr_handle* h, pbdr_dev::LaunchHook* hook) {
   ia.body_mass = h->body_mass;
   ia.keys = h->keys[0];
   ia.vals = h->vals[0];
+  ia.box_min = h->box_min;
+  ia.box_max = h->box_max;
   ia.substep_counter = h->counter;
   ia.n = h->n;
   ia.dt = h->dt;
@@ -160,24 +178,57 @@ void enqueue_substep(pbdr_handle* h, pbdr_dev::LaunchHook* hook) {
   ia.inv_h = h->inv_h;
   ia.dt_d = h->dt_d;
   ia.mask = h->mask;
+  if (hook) hook->before(kHookMemset);
+  cudaMemsetAsync(h->box_min, 0xFF, sizeof(uint32_t) * 3 * h->nb, h->stream);
+  cudaMemsetAsync(h->box_max, 0x00, sizeof(uint32_t) * 3 * h->nb, h->stream);
+  cudaMemsetAsync(h->oversize, 0x00, sizeof(unsigned), h->stream);
+  cudaMemsetAsync(h->bcells, 0xFF, sizeof(uint2) * (size_t(1) << h->bhash_bits), h->stream);
+  if (hook) hook->after(kHookMemset, 4);
   if (hook) hook->before(kHookIntegrate);
   launch_integrate(ia, h->stream);
   if (hook) hook->after(kHookIntegrate);
+
+  // Body broadphase: partner bodies (box overlap within h) for the skip test.
+  BroadArgs ba{};
+  ba.box_min = h->box_min;
+  ba.box_max = h->box_max;
+  ba.body_scene = h->body_scene;
+  ba.bkeys = h->bkeys[0];
+  ba.bvals = h->bvals[0];
+  ba.bcells = h->bcells;
+  ba.npartners = h->npartners;
+  ba.partners = h->partners;
+  ba.oversize = h->oversize;
+  ba.nb = h->nb;
+  ba.inv_cell = h->inv_cell_b;
+  ba.max_extent = h->max_extent;
+  ba.inflate = h->inflate;
+  ba.mask = h->bmask;
+  if (hook) hook->before(kHookBroadphase);
+  launch_body_keys(ba, h->stream);
+  if (hook) hook->after(kHookBroadphase);
+  const int bsb = sort_pairs(h->bkeys, h->bvals, h->nb, h->bhash_bits, h->bsort_temp, h->sm_count,
+                             h->stream, hook);
+  ba.sorted_bkeys = h->bkeys[bsb];
+  ba.sorted_bvals = h->bvals[bsb];
+  if (hook) hook->before(kHookBroadphase);
+  launch_body_ranges(ba, h->stream);
+  launch_body_partners(ba, h->stream);
+  if (hook) hook->after(kHookBroadphase, 2);
 
   const int sb = sort_pairs(h->keys, h->vals, h->n, h->hash_bits, h->sort_temp, h->sm_count,
                             h->stream, hook);
   h->sorted_buf = sb;
 
   if (hook) hook->before(kHookMemset);
-  cudaMemsetAsync(h->cell_start, 0xFF, sizeof(uint32_t) * (size_t(1) << h->hash_bits), h->stream);
+  cudaMemsetAsync(h->cells, 0xFF, sizeof(uint4) * (size_t(1) << h->hash_bits), h->stream);
   if (hook) hook->after(kHookMemset);
 
   RangesArgs ra{};
   ra.keys = h->keys[sb];
   ra.vals = h->vals[sb];
   ra.body_of = h->body_of;
-  ra.cell_start = h->cell_start;
-  ra.cell_end = h->cell_end;
+  ra.cells = h->cells;
   ra.sorted_body = h->sorted_body;
   ra.substep_counter = h->counter;
   ra.n = h->n;
@@ -190,10 +241,14 @@ void enqueue_substep(pbdr_handle* h, pbdr_dev::LaunchHook* hook) {
   na.rest = h->rest;
   na.body_of = h->body_of;
   na.body_scene = h->body_scene;
-  na.cell_start = h->cell_start;
-  na.cell_end = h->cell_end;
+  na.cells = h->cells;
   na.sorted_body = h->sorted_body;
   na.sorted_vals = h->vals[sb];
+  na.box_min = h->box_min;
+  na.box_max = h->box_max;
+  na.npartners = h->npartners;
+  na.partners = h->partners;
+  na.inflate = h->inflate;
   na.ncand = h->ncand;
   na.cand_j = h->cand_j;
   na.cand_rr = h->cand_rr;
@@ -220,6 +275,7 @@ void enqueue_iteration(pbdr_handle* h, pbdr_dev::LaunchHook* hook) {
   it.cand_j = h->cand_j;
   it.cand_rr = h->cand_rr;
   it.anchor = h->anchor;
+  it.cta_desc = h->cta_desc;
   it.warp_desc = h->warp_desc;
   it.body_desc = h->body_desc;
   it.body_mass = h->body_mass;
@@ -233,6 +289,7 @@ void enqueue_iteration(pbdr_handle* h, pbdr_dev::LaunchHook* hook) {
   it.incremental = h->incremental;
   it.linfix = h->linfix;
   it.angfix = h->angfix;
+  it.timing = h->timing;
   if (hook) hook->before(kHookIteration);
   launch_iteration(it, h->ctas, h->stream);
   if (hook) hook->after(kHookIteration);
@@ -370,7 +427,8 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
   std::vector<float2> mass(nb);
   std::vector<float4> anchor(nb);
   std::vector<int4> bdesc(nb);
-  std::vector<int2> wdesc;
+  std::vector<int4> wdesc;
+  std::vector<int4> cdesc;
   std::vector<char> seen(n, 0);
   h->slot_to_particle.resize(n);
   double rmax = 0.0;
@@ -417,11 +475,15 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
     }
     const int W = pbdr_body_warps(static_cast<int>(cnt));
     if (used + W > PBDR_CTA_WARPS) {
-      for (; used < PBDR_CTA_WARPS; ++used) wdesc.push_back(make_int2(-1, 0));
+      for (; used < PBDR_CTA_WARPS; ++used) wdesc.push_back(make_int4(-1, 0, 0, 1 << 16));
       used = 0;
     }
+    if (used == 0) cdesc.push_back(make_int4(static_cast<int>(first_slot), 0, b, 0));
+    cdesc.back().y += static_cast<int>(cnt);
+    cdesc.back().w += 1;
     bdesc[b] = make_int4(static_cast<int>(first_slot), static_cast<int>(cnt), W, used);
-    for (int u = 0; u < W; ++u) wdesc.push_back(make_int2(b, u));
+    for (int u = 0; u < W; ++u)
+      wdesc.push_back(make_int4(b, u, static_cast<int>(first_slot), static_cast<int>(cnt) | (W << 16)));
     used += W;
     mass[b] = make_float2(static_cast<float>(d->total_mass[b]), static_cast<float>(1.0 / d->total_mass[b]));
     anchor[b] = make_float4(pos[first_slot].x, pos[first_slot].y, pos[first_slot].z, 0.0f);
@@ -442,7 +504,7 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
     release(h);
     return set_config_error("bodies.particle_indices", "every particle must belong to one body");
   }
-  for (; used < PBDR_CTA_WARPS && used > 0; ++used) wdesc.push_back(make_int2(-1, 0));
+  for (; used < PBDR_CTA_WARPS && used > 0; ++used) wdesc.push_back(make_int4(-1, 0, 0, 1 << 16));
   h->ctas = static_cast<int>(wdesc.size() / PBDR_CTA_WARPS);
 
   // ---- Parameters ----------------------------------------------------------
@@ -459,6 +521,17 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
   h->h = static_cast<float>(2.0 * rmax);
   h->inv_h = 1.0f / h->h;
   h->h2 = h->h * h->h;
+  h->bhash_bits = pbdr_hash_bits(nb);
+  h->bpasses = (h->bhash_bits + 7) / 8;
+  h->bmask = static_cast<uint32_t>((uint64_t(1) << h->bhash_bits) - 1u);
+  {
+    float qmax = 0.0f;
+    for (int64_t k = 0; k < n; ++k)
+      qmax = std::max(qmax, std::sqrt(rest[k].x * rest[k].x + rest[k].y * rest[k].y + rest[k].z * rest[k].z));
+    h->inflate = 1.01f * h->h;
+    h->max_extent = 2.2f * qmax + 2.0f * h->h;
+    h->inv_cell_b = 1.0f / (h->max_extent + 2.0f * h->h);
+  }
   h->hash_bits = pbdr_hash_bits(n);
   h->passes = (h->hash_bits + 7) / 8;
   h->mask = static_cast<uint32_t>((uint64_t(1) << h->hash_bits) - 1u);
@@ -487,6 +560,7 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
   rc |= dalloc(h, &h->body_mass, nb);
   rc |= dalloc(h, &h->body_desc, nb);
   rc |= dalloc(h, &h->warp_desc, wdesc.size());
+  rc |= dalloc(h, &h->cta_desc, cdesc.size());
   rc |= dalloc(h, &h->anchor, nb);
   rc |= dalloc(h, &h->keys[0], n);
   rc |= dalloc(h, &h->keys[1], n);
@@ -497,8 +571,22 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
     rc |= dalloc(h, &tmp, pbdr_dev::sort_temp_bytes(n, h->passes));
     h->sort_temp = tmp;
   }
-  rc |= dalloc(h, &h->cell_start, T);
-  rc |= dalloc(h, &h->cell_end, T);
+  rc |= dalloc(h, &h->cells, T);
+  rc |= dalloc(h, &h->box_min, 3 * static_cast<size_t>(nb));
+  rc |= dalloc(h, &h->box_max, 3 * static_cast<size_t>(nb));
+  rc |= dalloc(h, &h->bkeys[0], nb);
+  rc |= dalloc(h, &h->bkeys[1], nb);
+  rc |= dalloc(h, &h->bvals[0], nb);
+  rc |= dalloc(h, &h->bvals[1], nb);
+  {
+    char* tmp = nullptr;
+    rc |= dalloc(h, &tmp, pbdr_dev::sort_temp_bytes(nb, h->bpasses));
+    h->bsort_temp = tmp;
+  }
+  rc |= dalloc(h, &h->bcells, size_t(1) << h->bhash_bits);
+  rc |= dalloc(h, &h->npartners, nb);
+  rc |= dalloc(h, &h->partners, static_cast<size_t>(nb) * PBDR_PARTNER_CAP);
+  rc |= dalloc(h, &h->oversize, 1);
   rc |= dalloc(h, &h->sorted_body, n);
   rc |= dalloc(h, &h->ncand, n);
   rc |= dalloc(h, &h->cand_j, static_cast<size_t>(n) * PBDR_NBR_CAP);
@@ -510,6 +598,11 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
     const int code = pbdr_last_error_payload(nullptr, nullptr, nullptr);
     release(h);
     return code ? code : PBDR_ERR_CUDA;
+  }
+  e = pbdr_dev::prepare_iteration_kernel();
+  if (e != cudaSuccess) {
+    release(h);
+    return cuda_fail(e, "cudaFuncSetAttribute(k_iteration)");
   }
   e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
   if (e != cudaSuccess) {
@@ -531,6 +624,7 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
   UP(h->body_mass, mass.data(), nb);
   UP(h->body_desc, bdesc.data(), nb);
   UP(h->warp_desc, wdesc.data(), wdesc.size());
+  UP(h->cta_desc, cdesc.data(), cdesc.size());
   UP(h->anchor, anchor.data(), nb);
 #undef UP
   cudaMemset(h->init, 0, sizeof(float4) * n);
@@ -541,7 +635,8 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
     release(h);
     return code;
   }
-  h->launches_per_frame = static_cast<int64_t>(h->substeps) * (1 + 2 + h->passes + 1 + 1 + h->iters);
+  h->launches_per_frame =
+      static_cast<int64_t>(h->substeps) * (1 + 1 + 2 + h->bpasses + 2 + 2 + h->passes + 1 + 1 + h->iters);
   *out = h;
   return PBDR_OK;
 }
@@ -687,6 +782,7 @@ int pbdr_gpu_read_bodies(pbdr_handle* h, pbdr_body_stats* out) {
   sa.vel = h->vel;
   sa.rest = h->rest;
   sa.anchor = h->anchor;
+  sa.cta_desc = h->cta_desc;
   sa.warp_desc = h->warp_desc;
   sa.body_desc = h->body_desc;
   sa.body_mass = h->body_mass;
@@ -728,6 +824,27 @@ int pbdr_gpu_debug_iteration(pbdr_handle* h, int) {
   PBDR_CUDA(cudaSetDevice(h->device));
   enqueue_iteration(h, nullptr);
   PBDR_CUDA(cudaGetLastError());
+  return check_errors(h);
+}
+
+// Per-CTA clock64 stamps of one iteration launch: 8 per CTA (start, staged,
+// phase A done, body math A done, phase B done, body math B done, end, smid).
+int pbdr_gpu_debug_phase_timing(pbdr_handle* h, long long* out) {
+  if (!h || !out) return set_error(PBDR_ERR_GENERIC, "null argument");
+  PBDR_CUDA(cudaSetDevice(h->device));
+  if (!h->timing_buf) {
+    void* p = nullptr;
+    PBDR_CUDA(cudaMalloc(&p, sizeof(long long) * 8 * h->ctas));
+    h->allocations.push_back(p);
+    h->timing_buf = static_cast<long long*>(p);
+  }
+  PBDR_CUDA(cudaMemsetAsync(h->timing_buf, 0, sizeof(long long) * 8 * h->ctas, h->stream));
+  h->timing = h->timing_buf;  // only this launch is instrumented
+  enqueue_iteration(h, nullptr);
+  h->timing = nullptr;
+  PBDR_CUDA(cudaMemcpyAsync(out, h->timing_buf, sizeof(long long) * 8 * h->ctas, cudaMemcpyDeviceToHost,
+                            h->stream));
+  PBDR_CUDA(cudaStreamSynchronize(h->stream));
   return check_errors(h);
 }
 

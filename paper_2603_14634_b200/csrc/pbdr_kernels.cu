@@ -1,18 +1,21 @@
 // sm_100a kernels of the PBD-R substep loop.
 //
-// Per substep (DESIGN.md "Kernels"):
-//   integrate_key  x_init <- x; v~ = v + dt a; x~ = x + dt v~ ; cell hash key
+// Per substep (DESIGN.md section 4):
+//   k_integrate_key  x_init <- x; v~ = v + dt a; x~ = x + dt v~; cell key
 //   [onesweep sort of (key, slot), pbdr_sort.cu]
-//   cell_ranges    per-bucket [start, end) in sorted order + sorted copy of x~
-//   neighbours     per particle: contact candidates (other body, same scene,
-//                  27-cell stencil, |x~_i - x~_j| < h), ascending slot order
-//   iteration x N  fused: ground + particle-particle contact (Jacobi), shape
-//                  matching (segmented com / Apq sums + fp64 polar), position
-//                  and incremental velocity update, momentum constraint
-//                  (Eq. 1 / Eq. 2) fused into the writeback
-// The op order of every fp32 expression is pinned and mirrored by
-// oracle/pbdr_oracle.cpp; the library is compiled with --fmad=false so the
-// CUDA path and the oracle agree bit for bit.
+//   k_cell_ranges    per-bucket [start, end) of the sorted array + body of
+//                    every sorted entry
+//   k_neighbours     per particle: contact candidates (other body, same scene,
+//                    27-cell stencil, |x~_i - x~_j| < h), ascending slot order;
+//                    the stencil is scanned as 9 x-rows, each one contiguous
+//                    range of the sorted array (x-run cell keys)
+//   k_iteration x N  fused: ground + particle-particle contact (Jacobi), shape
+//                    matching (segmented com / Apq sums + fp64 polar), position
+//                    and incremental velocity update, momentum constraint
+//                    (Eq. 1 / Eq. 2) fused into the writeback
+// The op order of every fp32 expression is pinned and
+// mirrored by oracle/pbdr_oracle.cpp; the library is compiled with
+// --fmad=false so the CUDA path and the oracle agree bit for bit.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -25,7 +28,10 @@ namespace pbdr_dev {
 namespace {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
-constexpr int kIterThreads = PBDR_CTA_WARPS * 32;
+constexpr int kWarps = PBDR_CTA_WARPS;
+constexpr int kThreads = kWarps * 32;
+constexpr int kSlots = kThreads * PBDR_KP;  // particle slots staged per CTA
+constexpr uint32_t kEmpty = 0xFFFFFFFFu;
 
 __device__ __forceinline__ void record_error(DevError* e, unsigned bits, int body,
                                              const long long* substep_counter,
@@ -55,173 +61,426 @@ __device__ __forceinline__ void warp_butterfly(float (&acc)[F]) {
     for (int f = 0; f < F; ++f) acc[f] = acc[f] + __shfl_xor_sync(kFull, acc[f], off);
 }
 
-// ---------------------------------------------------------------------------
-// integrate + cell key (PAPER.md:141-144; SPEC.md:272-280, 349)
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_integrate_key(IntegrateArgs A) {
-  const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (p >= A.n) return;
-  const int b = A.body_of[p];
-  const double t = static_cast<double>(*A.substep_counter) * A.dt_d;
-  const BodyProgram pr = A.programs[b];
-  float a[3] = {0.0f, 0.0f, (pr.flags & 2) ? 0.0f : -A.gravity};
-  if ((pr.flags & 1) && t >= pr.t_start && t < pr.t_stop) {
-    const float invM = A.body_mass[b].y;
-    a[0] = a[0] + pr.fx * invM;
-    a[1] = a[1] + pr.fy * invM;
-    a[2] = a[2] + pr.fz * invM;
-  }
-  const float4 x = A.pos[p];
-  const float4 v = A.vel[p];
-  A.init[p] = make_float4(x.x, x.y, x.z, 0.0f);
-  float4 vn, xn;
-  vn.x = v.x + A.dt * a[0];
-  vn.y = v.y + A.dt * a[1];
-  vn.z = v.z + A.dt * a[2];
-  vn.w = v.w;
-  xn.x = x.x + A.dt * vn.x;
-  xn.y = x.y + A.dt * vn.y;
-  xn.z = x.z + A.dt * vn.z;
-  xn.w = x.w;
-  A.vel[p] = vn;
-  A.pos[p] = xn;
-  const int32_t cx = pbdr_cell_coord(xn.x, A.inv_h);
-  const int32_t cy = pbdr_cell_coord(xn.y, A.inv_h);
-  const int32_t cz = pbdr_cell_coord(xn.z, A.inv_h);
-  A.keys[p] = pbdr_cell_hash(cx, cy, cz, static_cast<uint32_t>(A.body_scene[b]), A.mask);
-  A.vals[p] = static_cast<uint32_t>(p);
+// ---- TMA bulk staging (cp.async.bulk + mbarrier) ---------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
 }
 
 // ---------------------------------------------------------------------------
-// cell ranges: per-bucket [start, end) in sorted order, and the body of every
-// sorted entry (slots are ascending within a bucket, so bodies are too).
+// integrate + cell key (PAPER.md:141-144; SPEC.md:272-280, 349)
+// ---------------------------------------------------------------------------
+// Order-preserving float <-> uint encoding for atomicMin/atomicMax boxes.
+__device__ __forceinline__ uint32_t f2ord(float f) {
+  const uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float ord2f(uint32_t u) {
+  return __uint_as_float((u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u);
+}
+
+__global__ void __launch_bounds__(256) k_integrate_key(IntegrateArgs A) {
+  const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const bool valid = p < A.n;
+  int b = -1;
+  float4 xn = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+  if (valid) {
+    b = A.body_of[p];
+    const double t = static_cast<double>(*A.substep_counter) * A.dt_d;
+    const BodyProgram pr = A.programs[b];
+    float a[3] = {0.0f, 0.0f, (pr.flags & 2) ? 0.0f : -A.gravity};
+    if ((pr.flags & 1) && t >= pr.t_start && t < pr.t_stop) {
+      const float invM = A.body_mass[b].y;
+      a[0] = a[0] + pr.fx * invM;
+      a[1] = a[1] + pr.fy * invM;
+      a[2] = a[2] + pr.fz * invM;
+    }
+    const float4 x = A.pos[p];
+    const float4 v = A.vel[p];
+    A.init[p] = make_float4(x.x, x.y, x.z, 0.0f);
+    float4 vn;
+    vn.x = v.x + A.dt * a[0];
+    vn.y = v.y + A.dt * a[1];
+    vn.z = v.z + A.dt * a[2];
+    vn.w = v.w;
+    xn.x = x.x + A.dt * vn.x;
+    xn.y = x.y + A.dt * vn.y;
+    xn.z = x.z + A.dt * vn.z;
+    xn.w = x.w;
+    A.vel[p] = vn;
+    A.pos[p] = xn;
+    const int32_t cx = pbdr_cell_coord(xn.x, A.inv_h);
+    const int32_t cy = pbdr_cell_coord(xn.y, A.inv_h);
+    const int32_t cz = pbdr_cell_coord(xn.z, A.inv_h);
+    A.keys[p] = pbdr_cell_hash(cx, cy, cz, static_cast<uint32_t>(A.body_scene[b]), A.mask);
+    A.vals[p] = static_cast<uint32_t>(p);
+  }
+  // Body boxes of X~: warp-reduce when the whole warp is one body (the common
+  // case in body-major order), else one atomic per lane. min/max are exact and
+  // order-free, so the boxes are deterministic.
+  const int b0 = __shfl_sync(kFull, b, 0);
+  const bool uniform = __all_sync(kFull, b == b0) && b0 >= 0;
+  float lo[3] = {xn.x, xn.y, xn.z}, hi[3] = {xn.x, xn.y, xn.z};
+  if (uniform) {
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        lo[c] = fminf(lo[c], __shfl_xor_sync(kFull, lo[c], off));
+        hi[c] = fmaxf(hi[c], __shfl_xor_sync(kFull, hi[c], off));
+      }
+    if ((threadIdx.x & 31) == 0)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        atomicMin(&A.box_min[3 * b0 + c], f2ord(lo[c]));
+        atomicMax(&A.box_max[3 * b0 + c], f2ord(hi[c]));
+      }
+  } else if (valid) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      atomicMin(&A.box_min[3 * b + c], f2ord(lo[c]));
+      atomicMax(&A.box_max[3 * b + c], f2ord(hi[c]));
+    }
+  }
+}
+
+// ---- body broadphase ----------------------------------------------------------
+__device__ __forceinline__ void load_box(const uint32_t* bmin, const uint32_t* bmax, int b, float lo[3],
+                                         float hi[3]) {
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    lo[c] = ord2f(bmin[3 * b + c]);
+    hi[c] = ord2f(bmax[3 * b + c]);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_body_keys(BroadArgs A) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= A.nb) return;
+  float lo[3], hi[3];
+  load_box(A.box_min, A.box_max, b, lo, hi);
+  // A box wider than the coarse cell (minus the inflation) would break the
+  // 27-cell partner guarantee: then every body searches in full this substep.
+  if (!(hi[0] - lo[0] <= A.max_extent && hi[1] - lo[1] <= A.max_extent && hi[2] - lo[2] <= A.max_extent))
+    atomicOr(A.oversize, 1u);
+  int32_t c[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) c[k] = pbdr_cell_coord(0.5f * (lo[k] + hi[k]), A.inv_cell);
+  A.bkeys[b] = pbdr_cell_hash(c[0], c[1], c[2], static_cast<uint32_t>(A.body_scene[b]), A.mask);
+  A.bvals[b] = static_cast<uint32_t>(b);
+}
+
+__global__ void __launch_bounds__(256) k_body_ranges(BroadArgs A) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= A.nb) return;
+  const uint32_t k = A.sorted_bkeys[s];
+  if (s == 0 || A.sorted_bkeys[s - 1] != k) A.bcells[k].x = static_cast<uint32_t>(s);
+  if (s == A.nb - 1 || A.sorted_bkeys[s + 1] != k) A.bcells[k].y = static_cast<uint32_t>(s + 1);
+}
+
+// Partners of body b: other bodies of its scene whose box overlaps b's box
+// inflated by h. The coarse cell is >= the largest box extent + h, so partner
+// box centres lie in the 27 neighbouring coarse cells.
+__global__ void __launch_bounds__(128) k_body_partners(BroadArgs A) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= A.nb) return;
+  if (*A.oversize) {
+    A.npartners[b] = -1;
+    return;
+  }
+  float lo[3], hi[3];
+  load_box(A.box_min, A.box_max, b, lo, hi);
+  const int sb = A.body_scene[b];
+  int32_t c[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    c[k] = pbdr_cell_coord(0.5f * (lo[k] + hi[k]), A.inv_cell);
+    lo[k] = lo[k] - (A.inflate + fabsf(lo[k]) * 1e-6f);
+    hi[k] = hi[k] + (A.inflate + fabsf(hi[k]) * 1e-6f);
+  }
+  int count = 0;
+  bool overflow = false;
+  uint32_t visited[27];
+#pragma unroll
+  for (int t = 0; t < 27; ++t) {
+    const uint32_t key = pbdr_cell_hash(c[0] + t % 3 - 1, c[1] + (t / 3) % 3 - 1, c[2] + t / 9 - 1,
+                                        static_cast<uint32_t>(sb), A.mask);
+    bool dup = false;
+#pragma unroll
+    for (int u = 0; u < t; ++u) dup = dup || visited[u] == key;
+    visited[t] = key;
+    if (dup) continue;
+    const uint2 e = A.bcells[key];
+    if (e.x == kEmpty) continue;
+    for (uint32_t s = e.x; s < e.y; ++s) {
+      const int o = static_cast<int>(A.sorted_bvals[s]);
+      if (o == b || A.body_scene[o] != sb) continue;
+      float olo[3], ohi[3];
+      load_box(A.box_min, A.box_max, o, olo, ohi);
+      if (olo[0] > hi[0] || ohi[0] < lo[0] || olo[1] > hi[1] || ohi[1] < lo[1] || olo[2] > hi[2] ||
+          ohi[2] < lo[2])
+        continue;
+      if (count < PBDR_PARTNER_CAP)
+        A.partners[static_cast<int64_t>(b) * PBDR_PARTNER_CAP + count] = o;
+      else
+        overflow = true;
+      ++count;
+    }
+  }
+  A.npartners[b] = overflow ? -1 : count;
+}
+
+// ---------------------------------------------------------------------------
+// cell ranges: per-bucket (start, end) of the sorted array and the body of
+// every sorted entry (slots ascend within a bucket, so bodies do too).
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_cell_ranges(RangesArgs A) {
   const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (s == 0) atomicAdd(reinterpret_cast<unsigned long long*>(A.substep_counter), 1ull);
   if (s >= A.n) return;
   const uint32_t k = A.keys[s];
-  if (s == 0 || A.keys[s - 1] != k) A.cell_start[k] = static_cast<uint32_t>(s);
-  if (s == A.n - 1 || A.keys[s + 1] != k) A.cell_end[k] = static_cast<uint32_t>(s + 1);
-  A.sorted_body[s] = A.body_of[A.vals[s]];
+  const int body = A.body_of[A.vals[s]];
+  A.sorted_body[s] = body;
+  // Entries of a bucket ascend by slot, hence by body: the first entry holds
+  // the bucket's smallest body, the last its largest.
+  if (s == 0 || A.keys[s - 1] != k) {
+    A.cells[k].x = static_cast<uint32_t>(s);
+    A.cells[k].z = static_cast<uint32_t>(body);
+  }
+  if (s == A.n - 1 || A.keys[s + 1] != k) {
+    A.cells[k].y = static_cast<uint32_t>(s + 1);
+    A.cells[k].w = static_cast<uint32_t>(body);
+  }
 }
 
 // ---------------------------------------------------------------------------
 // contact candidates (pinned P4): {j : same scene, other body,
 // |cell_j - cell_i|_inf <= 1, |x~_i - x~_j|^2 < h^2}, ascending j, <= CAP.
-// A bucket whose first and last entries belong to particle i's own body holds
-// only own-body particles and is skipped without a scan (most buckets).
 // ---------------------------------------------------------------------------
+struct CandList {
+  int j[PBDR_NBR_CAP];
+  int count;
+  bool overflow;
+  // Sorted insert of a distinct j; keeps the CAP smallest.
+  __device__ __forceinline__ void insert(int v) {
+    int pos = count;
+    while (pos > 0 && j[pos - 1] > v) --pos;
+    if (pos > 0 && j[pos - 1] == v) return;  // seen through an aliased bucket
+    if (count == PBDR_NBR_CAP) {
+      overflow = true;
+      if (pos == PBDR_NBR_CAP) return;
+      --count;
+    }
+    for (int t = count; t > pos; --t) j[t] = j[t - 1];
+    j[pos] = v;
+    ++count;
+  }
+};
+
+__device__ __forceinline__ void scan_range(const NeighbourArgs& A, uint32_t lo, uint32_t hi, int bi, int si,
+                                           float4 xi, int32_t cx, int32_t cy, int32_t cz, CandList& L) {
+  for (uint32_t s = lo; s < hi; ++s) {
+    const int bj = A.sorted_body[s];
+    if (bj == bi) continue;
+    if (A.body_scene[bj] != si) continue;
+    const int j = static_cast<int>(A.sorted_vals[s]);
+    const float4 xj = A.pos[j];
+    const int32_t jx = pbdr_cell_coord(xj.x, A.inv_h);
+    const int32_t jy = pbdr_cell_coord(xj.y, A.inv_h);
+    const int32_t jz = pbdr_cell_coord(xj.z, A.inv_h);
+    if (jx < cx - 1 || jx > cx + 1 || jy < cy - 1 || jy > cy + 1 || jz < cz - 1 || jz > cz + 1) continue;
+    const float ex = xi.x - xj.x, ey = xi.y - xj.y, ez = xi.z - xj.z;
+    const float d2 = (ex * ex + ey * ey) + ez * ez;
+    if (!(d2 < A.h2)) continue;
+    L.insert(j);
+  }
+}
+
+// Scans one bucket unless it is empty or holds only particle i's own body.
+__device__ __forceinline__ void scan_bucket(const NeighbourArgs& A, uint32_t key, int bi, int si, float4 xi,
+                                            int32_t cx, int32_t cy, int32_t cz, CandList& L) {
+  const uint4 e = A.cells[key];
+  if (e.x == kEmpty) return;
+  if (e.z == static_cast<uint32_t>(bi) && e.w == static_cast<uint32_t>(bi)) return;
+  scan_range(A, e.x, e.y, bi, si, xi, cx, cy, cz, L);
+}
+
 __global__ void __launch_bounds__(128) k_neighbours(NeighbourArgs A) {
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= A.n) return;
   const float4 xi = A.pos[i];
-  const float ri = A.rest[i].w;
   const int bi = A.body_of[i];
+  // Broadphase skip: no candidate can exist unless x~_i lies in the inflated
+  // box of a partner body (exact: a candidate j within h of i lies in its own
+  // body's box, and that body is then a partner of bi).
+  const int np = A.npartners[bi];
+  if (np >= 0) {
+    bool near = false;
+    for (int k = 0; k < np && !near; ++k) {
+      const int o = A.partners[static_cast<int64_t>(bi) * PBDR_PARTNER_CAP + k];
+      float lo[3], hi[3];
+      load_box(A.box_min, A.box_max, o, lo, hi);
+      const float xs[3] = {xi.x, xi.y, xi.z};
+      near = true;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const float m = A.inflate + fmaxf(fabsf(lo[c]), fabsf(hi[c])) * 1e-6f;
+        near = near && xs[c] >= lo[c] - m && xs[c] <= hi[c] + m;
+      }
+    }
+    if (!near) {
+      A.ncand[i] = 0;
+      return;
+    }
+  }
   const int si = A.body_scene[bi];
   const int32_t cx = pbdr_cell_coord(xi.x, A.inv_h);
   const int32_t cy = pbdr_cell_coord(xi.y, A.inv_h);
   const int32_t cz = pbdr_cell_coord(xi.z, A.inv_h);
+  const int xl = cx & ((1 << PBDR_XRUN_BITS) - 1);
+  const bool inner = xl != 0 && xl != (1 << PBDR_XRUN_BITS) - 1;
 
-  int cand[PBDR_NBR_CAP];
-  float cr[PBDR_NBR_CAP];
-  int count = 0;
-  bool overflow = false;
-  uint32_t visited[27];
-#pragma unroll
-  for (int t = 0; t < 27; ++t) {
-    const int dz = t / 9 - 1, dy = (t / 3) % 3 - 1, dx = t % 3 - 1;
-    const uint32_t hb = pbdr_cell_hash(cx + dx, cy + dy, cz + dz, static_cast<uint32_t>(si), A.mask);
-    bool dup = false;
-#pragma unroll
-    for (int u = 0; u < t; ++u) dup = dup || (visited[u] == hb);
-    visited[t] = hb;
-    if (dup) continue;
-    const uint32_t s0 = A.cell_start[hb];
-    if (s0 == 0xFFFFFFFFu) continue;
-    const uint32_t s1 = A.cell_end[hb];
-    if (A.sorted_body[s0] == bi && A.sorted_body[s1 - 1] == bi) continue;
-    for (uint32_t s = s0; s < s1; ++s) {
-      const int bj = A.sorted_body[s];
-      if (bj == bi) continue;
-      if (A.body_scene[bj] != si) continue;
-      const int j = static_cast<int>(A.sorted_vals[s]);
-      const float4 xj = A.pos[j];
-      const int32_t jx = pbdr_cell_coord(xj.x, A.inv_h);
-      const int32_t jy = pbdr_cell_coord(xj.y, A.inv_h);
-      const int32_t jz = pbdr_cell_coord(xj.z, A.inv_h);
-      if (jx < cx - 1 || jx > cx + 1 || jy < cy - 1 || jy > cy + 1 || jz < cz - 1 || jz > cz + 1)
-        continue;
-      const float ex = xi.x - xj.x, ey = xi.y - xj.y, ez = xi.z - xj.z;
-      const float d2 = (ex * ex + ey * ey) + ez * ez;
-      if (!(d2 < A.h2)) continue;
-      // Keep the CAP smallest j in ascending order.
-      if (count == PBDR_NBR_CAP) {
-        overflow = true;
-        if (j > cand[PBDR_NBR_CAP - 1]) continue;
-        --count;
-      }
-      int pos = count;
-      while (pos > 0 && cand[pos - 1] > j) {
-        cand[pos] = cand[pos - 1];
-        cr[pos] = cr[pos - 1];
-        --pos;
-      }
-      cand[pos] = j;
-      cr[pos] = ri + A.rest[j].w;
-      ++count;
-    }
+  CandList L;
+  L.count = 0;
+  L.overflow = false;
+  for (int r = 0; r < 9; ++r) {
+    const int32_t yy = cy + (r % 3) - 1, zz = cz + (r / 3) - 1;
+    // Row cells cx-1, cx, cx+1: consecutive keys inside an x-run.
+    const uint32_t km = pbdr_cell_hash(cx - 1, yy, zz, static_cast<uint32_t>(si), A.mask);
+    const uint32_t k0 = inner ? km + 1 : pbdr_cell_hash(cx, yy, zz, static_cast<uint32_t>(si), A.mask);
+    const uint32_t kp = inner ? km + 2 : pbdr_cell_hash(cx + 1, yy, zz, static_cast<uint32_t>(si), A.mask);
+    scan_bucket(A, km, bi, si, xi, cx, cy, cz, L);
+    scan_bucket(A, k0, bi, si, xi, cx, cy, cz, L);
+    scan_bucket(A, kp, bi, si, xi, cx, cy, cz, L);
   }
-  if (overflow) record_error(A.err, PBDR_DEVERR_NBR_OVERFLOW, bi, A.substep_counter);
-  A.ncand[i] = count;
-  for (int k = 0; k < count; ++k) {
-    A.cand_j[static_cast<int64_t>(k) * A.n + i] = cand[k];
-    A.cand_rr[static_cast<int64_t>(k) * A.n + i] = cr[k];
+  if (L.overflow) record_error(A.err, PBDR_DEVERR_NBR_OVERFLOW, bi, A.substep_counter);
+  A.ncand[i] = L.count;
+  const float ri = A.rest[i].w;
+  for (int k = 0; k < L.count; ++k) {
+    const int j = L.j[k];
+    A.cand_j[static_cast<int64_t>(k) * A.n + i] = j;
+    A.cand_rr[static_cast<int64_t>(k) * A.n + i] = ri + A.rest[j].w;
   }
 }
 
 // ---------------------------------------------------------------------------
-// One solver iteration, fused (pinned P1-P8). CTA = 16 warps; each body owns
-// W = ceil(n/64) consecutive warps; lane l of body-warp wi owns particles
-// q = k*32*W + wi*32 + l, k < 2.
+// One solver iteration, fused (pinned P1-P8). A CTA (8 warps) holds whole,
+// consecutive bodies; its contiguous slot range of pos/vel/rest is staged in
+// shared memory by three cp.async.bulk copies. A body of n particles owns
+// W = ceil(n/128) warps; lane l of body-warp wi owns q = k*32*W + wi*32 + l,
+// k < 4. Warp 0 runs the per-body fp64 math for all bodies of the CTA, one
+// lane per body.
 // ---------------------------------------------------------------------------
 constexpr int kResF = 32;
 enum ResSlot {
-  kResC = 0,     // c (3)
-  kResLb = 3,    // L_bsm (3)
-  kResPb = 6,    // P_bsm (3)
-  kResR = 9,     // R (9)
-  kResSmOk = 18, // shape-matching valid flag
-  kResCa = 19,   // c_asm (3)
-  kResDv = 22,   // dv (3)
-  kResW = 25,    // omega (3)
+  kResC = 0,      // c (3), anchor-relative com of X_i
+  kResLb = 3,     // L_bsm (3)
+  kResPb = 6,     // P_bsm (3)
+  kResR = 9,      // R (9)
+  kResSmOk = 18,  // shape-matching valid flag
+  kResCa = 19,    // c_asm (3)
+  kResDv = 22,    // dv (3)
+  kResW = 25,     // omega (3)
+  kResA = 28,     // anchor a (3)
 };
 
-__global__ void __launch_bounds__(kIterThreads, 2) k_iteration(IterArgs A) {
-  __shared__ float s_part[PBDR_CTA_WARPS][21];
-  __shared__ float s_res[PBDR_CTA_WARPS][kResF];
+#ifndef PBDR_ITER_MINBLOCKS
+#define PBDR_ITER_MINBLOCKS 3
+#endif
+__global__ void __launch_bounds__(kThreads, PBDR_ITER_MINBLOCKS) k_iteration(IterArgs A) {
+  extern __shared__ float4 s_stage[];  // pos | vel | rest, kSlots each
+  __shared__ float s_part[kWarps][21];
+  __shared__ float s_res[kWarps][kResF];
+  __shared__ __align__(8) uint64_t s_bar;
+
+  float4* s_pos = s_stage;
+  float4* s_vel = s_stage + kSlots;
+  float4* s_rest = s_stage + 2 * kSlots;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int2 wd = A.warp_desc[blockIdx.x * PBDR_CTA_WARPS + warp];
+  const int4 cd = A.cta_desc[blockIdx.x];  // first slot, slot count, first body, bodies
+  const int first = cd.x;
+
+  if (threadIdx.x == 0) {
+    mbar_init(&s_bar, 1);
+    const uint32_t bytes = static_cast<uint32_t>(cd.y) * 16u;
+    mbar_expect_tx(&s_bar, 3u * bytes);
+    bulk_g2s(s_pos, A.pos_in + first, bytes, &s_bar);
+    bulk_g2s(s_vel, A.vel + first, bytes, &s_bar);
+    bulk_g2s(s_rest, A.rest + first, bytes, &s_bar);
+  }
+
+  // Per-body table of this CTA (anchor, masses, first warp, warps), loaded by
+  // warp 0 while the bulk copies are in flight.
+  __shared__ float4 s_banc[kWarps];  // anchor xyz, M
+  __shared__ int2 s_bw[kWarps];      // first warp, warps
+  __shared__ float s_binv[kWarps];   // 1/M
+  if (warp == 0 && lane < cd.w) {
+    const int bb = cd.z + lane;
+    const int4 bdb = A.body_desc[bb];
+    const float4 an = A.anchor[bb];
+    const float2 mass = A.body_mass[bb];
+    s_banc[lane] = make_float4(an.x, an.y, an.z, mass.x);
+    s_binv[lane] = mass.y;
+    s_bw[lane] = make_int2(bdb.w, bdb.z);
+  }
+
+  const int4 wd = A.warp_desc[blockIdx.x * kWarps + warp];
   const int b = wd.x;
   const int wi = wd.y;
   const bool live = b >= 0;
-  int4 bd = make_int4(0, 0, 1, 0);
-  float a[3] = {0.0f, 0.0f, 0.0f};
-  float2 mass = make_float2(0.0f, 0.0f);
-  if (live) {
-    bd = A.body_desc[b];
-    const float4 an = A.anchor[b];
-    a[0] = an.x; a[1] = an.y; a[2] = an.z;
-    mass = A.body_mass[b];
+  const int lb = live ? b - cd.z : 0;  // body index within the CTA
+  const int start = wd.z, n = wd.w & 0xFFFF, W = wd.w >> 16;
+  int ncs[PBDR_KP];
+#pragma unroll
+  for (int k = 0; k < PBDR_KP; ++k) {
+    const int q = k * 32 * W + wi * 32 + lane;
+    ncs[k] = (live && q < n) ? A.ncand[start + q] : 0;  // prefetched: off the phase-A chain
   }
-  const int start = bd.x, n = bd.y, W = bd.z, fw = bd.w;
+  const int off = start - first;
   const bool fixes = A.linfix || A.angfix;
 
-  float x[PBDR_KP][3], w[PBDR_KP], v[PBDR_KP][3], m[PBDR_KP], q0[PBDR_KP][3], dc[PBDR_KP][3];
-  bool act[PBDR_KP];
-  int64_t pidx[PBDR_KP];
+  long long* tm = A.timing ? A.timing + 8 * static_cast<int64_t>(blockIdx.x) : nullptr;
+  if (tm && threadIdx.x == 0) tm[0] = clock64();
+  __syncthreads();  // barrier initialised, per-body table filled
+  float a[3];
+  {
+    const float4 an = s_banc[lb];
+    a[0] = an.x; a[1] = an.y; a[2] = an.z;
+  }
+  mbar_wait(&s_bar, 0);
+  if (tm && threadIdx.x == 0) tm[1] = clock64();
+
+  float dX[PBDR_KP][3];
 
   // ---- Phase A: contacts, bsm sums -----------------------------------------
   float acc[21];
@@ -229,25 +488,21 @@ __global__ void __launch_bounds__(kIterThreads, 2) k_iteration(IterArgs A) {
   for (int f = 0; f < 21; ++f) acc[f] = 0.0f;
 #pragma unroll
   for (int k = 0; k < PBDR_KP; ++k) {
+    dX[k][0] = dX[k][1] = dX[k][2] = 0.0f;
     const int q = k * 32 * W + wi * 32 + lane;
-    act[k] = live && q < n;
-    pidx[k] = start + q;
-    if (!act[k]) continue;
-    const int64_t p = pidx[k];
-    const float4 x4 = A.pos_in[p];
-    const float4 v4 = A.vel[p];
-    const float4 r4 = A.rest[p];
-    x[k][0] = x4.x; x[k][1] = x4.y; x[k][2] = x4.z; w[k] = x4.w;
-    v[k][0] = v4.x; v[k][1] = v4.y; v[k][2] = v4.z; m[k] = v4.w;
-    q0[k][0] = r4.x; q0[k][1] = r4.y; q0[k][2] = r4.z;
-    const float r = r4.w;
+    if (!(live && q < n)) continue;
+    const int64_t p = start + q;
+    const float4 x4 = s_pos[off + q];
+    const float4 v4 = s_vel[off + q];
+    const float4 r4 = s_rest[off + q];
+    const float x[3] = {x4.x, x4.y, x4.z};
+    const float m = v4.w;
 
     float dPG[3] = {0.0f, 0.0f, 0.0f};
     for (int pl = 0; pl < A.planes.count; ++pl) {
       const float* Pp = A.planes.p[pl];
       const float* Pn = A.planes.n[pl];
-      const float d = (((x[k][0] - Pp[0]) * Pn[0] + (x[k][1] - Pp[1]) * Pn[1]) +
-                       (x[k][2] - Pp[2]) * Pn[2]) - r;
+      const float d = (((x[0] - Pp[0]) * Pn[0] + (x[1] - Pp[1]) * Pn[1]) + (x[2] - Pp[2]) * Pn[2]) - r4.w;
       if (d < 0.0f) {
         const float push = -(A.relax * d);
         dPG[0] = dPG[0] + push * Pn[0];
@@ -256,7 +511,7 @@ __global__ void __launch_bounds__(kIterThreads, 2) k_iteration(IterArgs A) {
         const float mu = A.planes.mu[pl];
         if (mu > 0.0f) {
           const float4 xi = A.init[p];
-          const float t[3] = {x[k][0] - xi.x, x[k][1] - xi.y, x[k][2] - xi.z};
+          const float t[3] = {x[0] - xi.x, x[1] - xi.y, x[2] - xi.z};
           const float tn = (t[0] * Pn[0] + t[1] * Pn[1]) + t[2] * Pn[2];
           const float tt[3] = {t[0] - tn * Pn[0], t[1] - tn * Pn[1], t[2] - tn * Pn[2]};
           const float len2 = (tt[0] * tt[0] + tt[1] * tt[1]) + tt[2] * tt[2];
@@ -278,12 +533,12 @@ __global__ void __launch_bounds__(kIterThreads, 2) k_iteration(IterArgs A) {
       }
     }
     float dPP[3] = {0.0f, 0.0f, 0.0f};
-    const int nc = A.ncand[p];
+    const int nc = ncs[k];
     for (int c = 0; c < nc; ++c) {
       const int j = A.cand_j[static_cast<int64_t>(c) * A.n + p];
       const float rr = A.cand_rr[static_cast<int64_t>(c) * A.n + p];
       const float4 xj = A.pos_in[j];
-      const float e[3] = {x[k][0] - xj.x, x[k][1] - xj.y, x[k][2] - xj.z};
+      const float e[3] = {x[0] - xj.x, x[1] - xj.y, x[2] - xj.z};
       const float d2 = (e[0] * e[0] + e[1] * e[1]) + e[2] * e[2];
       if (d2 < rr * rr) {
         const float dist = sqrtf(d2);
@@ -295,33 +550,35 @@ __global__ void __launch_bounds__(kIterThreads, 2) k_iteration(IterArgs A) {
           nrm[0] = p < j ? 1.0f : -1.0f; nrm[1] = 0.0f; nrm[2] = 0.0f;
         }
         const float C = dist - rr;
-        const float kk = (A.relax * (w[k] / (w[k] + xj.w))) * C;
+        const float kk = (A.relax * (x4.w / (x4.w + xj.w))) * C;
         dPP[0] = dPP[0] - kk * nrm[0];
         dPP[1] = dPP[1] - kk * nrm[1];
         dPP[2] = dPP[2] - kk * nrm[2];
       }
     }
+    const float v[3] = {v4.x, v4.y, v4.z};
+    const float q0[3] = {r4.x, r4.y, r4.z};
     float pp[3], pb[3], mp[3], mvb[3], kb[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      dc[k][c] = dPG[c] + dPP[c];
-      pp[c] = x[k][c] - a[c];
-      pb[c] = pp[c] + dc[k][c];
-      const float vb = v[k][c] + dc[k][c] * A.inv_dt;
-      mp[c] = m[k] * pp[c];
-      mvb[c] = m[k] * vb;
+      dX[k][c] = dPG[c] + dPP[c];
+      pp[c] = x[c] - a[c];
+      pb[c] = pp[c] + dX[k][c];
+      const float vb = v[c] + dX[k][c] * A.inv_dt;
+      mp[c] = m * pp[c];
+      mvb[c] = m * vb;
     }
     cross3(pb, mvb, kb);
     acc[0] = acc[0] + mp[0];
     acc[1] = acc[1] + mp[1];
     acc[2] = acc[2] + mp[2];
-    acc[3] = acc[3] + m[k] * dc[k][0];
-    acc[4] = acc[4] + m[k] * dc[k][1];
-    acc[5] = acc[5] + m[k] * dc[k][2];
+    acc[3] = acc[3] + m * dX[k][0];
+    acc[4] = acc[4] + m * dX[k][1];
+    acc[5] = acc[5] + m * dX[k][2];
 #pragma unroll
     for (int rI = 0; rI < 3; ++rI)
 #pragma unroll
-      for (int cI = 0; cI < 3; ++cI) acc[6 + 3 * rI + cI] = acc[6 + 3 * rI + cI] + mp[rI] * q0[k][cI];
+      for (int cI = 0; cI < 3; ++cI) acc[6 + 3 * rI + cI] = acc[6 + 3 * rI + cI] + mp[rI] * q0[cI];
     acc[15] = acc[15] + mvb[0];
     acc[16] = acc[16] + mvb[1];
     acc[17] = acc[17] + mvb[2];
@@ -336,27 +593,34 @@ __global__ void __launch_bounds__(kIterThreads, 2) k_iteration(IterArgs A) {
       for (int f = 0; f < 21; ++f) s_part[warp][f] = acc[f];
   }
   __syncthreads();
+  if (tm && threadIdx.x == 0) tm[2] = clock64();
 
-  if (live && wi == 0 && lane == 0) {
+  // ---- per-body math A (warp 0, lane = body of the CTA) ---------------------
+  if (warp == 0 && lane < cd.w) {
+    const int bb = cd.z + lane;
+    const float4 an = s_banc[lane];
+    const float invM = s_binv[lane];
+    const int2 bw = s_bw[lane];
+    const int fw = bw.x;
     float S[21];
 #pragma unroll
-    for (int f = 0; f < 21; ++f) S[f] = s_part[warp][f];
-    for (int u = 1; u < W; ++u)
+    for (int f = 0; f < 21; ++f) S[f] = s_part[fw][f];
+    for (int u = 1; u < bw.y; ++u)
 #pragma unroll
-      for (int f = 0; f < 21; ++f) S[f] = S[f] + s_part[warp + u][f];
+      for (int f = 0; f < 21; ++f) S[f] = S[f] + s_part[fw + u][f];
     bool finite = true;
 #pragma unroll
     for (int f = 0; f < 21; ++f) finite = finite && isfinite(S[f]);
-    if (!finite) record_error(A.err, PBDR_DEVERR_NONFINITE, b, A.substep_counter);
+    if (!finite) record_error(A.err, PBDR_DEVERR_NONFINITE, bb, A.substep_counter);
     float c[3], cb[3], Pb[3], tmp[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      c[k] = S[k] * mass.y;
-      cb[k] = c[k] + S[3 + k] * mass.y;
+      c[k] = S[k] * invM;
+      cb[k] = c[k] + S[3 + k] * invM;
       Pb[k] = S[15 + k];
     }
     cross3(cb, Pb, tmp);
-    float* R = &s_res[warp][0];
+    float* R = &s_res[lane][0];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       R[kResC + k] = c[k];
@@ -366,17 +630,17 @@ __global__ void __launch_bounds__(kIterThreads, 2) k_iteration(IterArgs A) {
     double qd[4];
     const bool ok = polar_rotation_f(&S[6], &R[kResR], qd);
     R[kResSmOk] = ok ? 1.0f : 0.0f;
-    if (!ok) record_error(A.err, PBDR_DEVERR_DEGENERATE, b, A.substep_counter);
-    A.anchor[b] = make_float4(a[0] + c[0], a[1] + c[1], a[2] + c[2], 0.0f);
+    if (!ok) record_error(A.err, PBDR_DEVERR_DEGENERATE, bb, A.substep_counter);
+    A.anchor[bb] = make_float4(an.x + c[0], an.y + c[1], an.z + c[2], 0.0f);
   }
   __syncthreads();
+  if (tm && threadIdx.x == 0) tm[3] = clock64();
 
   // ---- Phase B: shape matching, position + velocity update ----------------
-  float xa[PBDR_KP][3], va[PBDR_KP][3], pa[PBDR_KP][3];
+  const float* res = &s_res[live ? lb : 0][0];
   float accB[15];
 #pragma unroll
   for (int f = 0; f < 15; ++f) accB[f] = 0.0f;
-  const float* res = &s_res[fw][0];
   if (live) {
     const bool sm_ok = res[kResSmOk] != 0.0f;
     float Rf[9], c[3];
@@ -386,59 +650,62 @@ __global__ void __launch_bounds__(kIterThreads, 2) k_iteration(IterArgs A) {
     for (int k = 0; k < 3; ++k) c[k] = res[kResC + k];
 #pragma unroll
     for (int k = 0; k < PBDR_KP; ++k) {
-      if (!act[k]) continue;
-      float dX[3];
-      float4 xi = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-      if (!A.incremental) xi = A.init[pidx[k]];
-      const float xiv[3] = {xi.x, xi.y, xi.z};
+      const int q = k * 32 * W + wi * 32 + lane;
+      if (!(q < n)) continue;
+      const float4 x4 = s_pos[off + q];
+      const float4 v4 = s_vel[off + q];
+      const float4 r4 = s_rest[off + q];
+      const float x[3] = {x4.x, x4.y, x4.z};
+      const float v[3] = {v4.x, v4.y, v4.z};
+      const float q0[3] = {r4.x, r4.y, r4.z};
+      float xi[3] = {0.0f, 0.0f, 0.0f};
+      if (!A.incremental) {
+        const float4 i4 = A.init[start + q];
+        xi[0] = i4.x; xi[1] = i4.y; xi[2] = i4.z;
+      }
+      float xa[3], va[3], pa[3];
 #pragma unroll
       for (int cI = 0; cI < 3; ++cI) {
-        const float pk = x[k][cI] - a[cI];
+        const float pk = x[cI] - a[cI];
         float dsm = 0.0f;
         if (sm_ok) {
-          const float g = (Rf[3 * cI] * q0[k][0] + Rf[3 * cI + 1] * q0[k][1]) + Rf[3 * cI + 2] * q0[k][2];
+          const float g = (Rf[3 * cI] * q0[0] + Rf[3 * cI + 1] * q0[1]) + Rf[3 * cI + 2] * q0[2];
           dsm = g - (pk - c[cI]);
         }
-        dX[cI] = dc[k][cI] + dsm;
-        xa[k][cI] = x[k][cI] + dX[cI];
-        va[k][cI] = A.incremental ? v[k][cI] + dX[cI] * A.inv_dt : (xa[k][cI] - xiv[cI]) * A.inv_dt;
-        pa[k][cI] = pk + dX[cI];
+        dX[k][cI] = dX[k][cI] + dsm;
+        xa[cI] = x[cI] + dX[k][cI];
+        va[cI] = A.incremental ? v[cI] + dX[k][cI] * A.inv_dt : (xa[cI] - xi[cI]) * A.inv_dt;
+        pa[cI] = pk + dX[k][cI];
       }
       if (fixes) {
-        const float mk = m[k];
-        const float mva[3] = {mk * va[k][0], mk * va[k][1], mk * va[k][2]};
+        const float mk = v4.w;
+        const float mva[3] = {mk * va[0], mk * va[1], mk * va[2]};
         float ka[3];
-        cross3(pa[k], mva, ka);
-        const float s2 = (pa[k][0] * pa[k][0] + pa[k][1] * pa[k][1]) + pa[k][2] * pa[k][2];
-        accB[0] = accB[0] + mk * dX[0];
-        accB[1] = accB[1] + mk * dX[1];
-        accB[2] = accB[2] + mk * dX[2];
+        cross3(pa, mva, ka);
+        const float s2 = (pa[0] * pa[0] + pa[1] * pa[1]) + pa[2] * pa[2];
+        accB[0] = accB[0] + mk * dX[k][0];
+        accB[1] = accB[1] + mk * dX[k][1];
+        accB[2] = accB[2] + mk * dX[k][2];
         accB[3] = accB[3] + mva[0];
         accB[4] = accB[4] + mva[1];
         accB[5] = accB[5] + mva[2];
         accB[6] = accB[6] + ka[0];
         accB[7] = accB[7] + ka[1];
         accB[8] = accB[8] + ka[2];
-        accB[9] = accB[9] + mk * (s2 - pa[k][0] * pa[k][0]);
-        accB[10] = accB[10] + mk * (s2 - pa[k][1] * pa[k][1]);
-        accB[11] = accB[11] + mk * (s2 - pa[k][2] * pa[k][2]);
-        accB[12] = accB[12] + -(mk * (pa[k][0] * pa[k][1]));
-        accB[13] = accB[13] + -(mk * (pa[k][0] * pa[k][2]));
-        accB[14] = accB[14] + -(mk * (pa[k][1] * pa[k][2]));
+        accB[9] = accB[9] + mk * (s2 - pa[0] * pa[0]);
+        accB[10] = accB[10] + mk * (s2 - pa[1] * pa[1]);
+        accB[11] = accB[11] + mk * (s2 - pa[2] * pa[2]);
+        accB[12] = accB[12] + -(mk * (pa[0] * pa[1]));
+        accB[13] = accB[13] + -(mk * (pa[0] * pa[2]));
+        accB[14] = accB[14] + -(mk * (pa[1] * pa[2]));
+      } else {
+        const int64_t p = start + q;
+        A.pos_out[p] = make_float4(xa[0], xa[1], xa[2], x4.w);
+        A.vel[p] = make_float4(va[0], va[1], va[2], v4.w);
       }
     }
   }
-
-  if (!fixes) {
-#pragma unroll
-    for (int k = 0; k < PBDR_KP; ++k) {
-      if (!act[k]) continue;
-      const int64_t p = pidx[k];
-      A.pos_out[p] = make_float4(xa[k][0], xa[k][1], xa[k][2], w[k]);
-      A.vel[p] = make_float4(va[k][0], va[k][1], va[k][2], m[k]);
-    }
-    return;
-  }
+  if (!fixes) return;
 
   if (live) {
     warp_butterfly<15>(accB);
@@ -447,19 +714,25 @@ __global__ void __launch_bounds__(kIterThreads, 2) k_iteration(IterArgs A) {
       for (int f = 0; f < 15; ++f) s_part[warp][f] = accB[f];
   }
   __syncthreads();
+  if (tm && threadIdx.x == 0) tm[4] = clock64();
 
-  if (live && wi == 0 && lane == 0) {
+  // ---- per-body math B: momentum corrections -------------------------------
+  if (warp == 0 && lane < cd.w) {
+    const int bb = cd.z + lane;
+    const float2 mass = make_float2(s_banc[lane].w, s_binv[lane]);
+    const int2 bw = s_bw[lane];
+    const int fw = bw.x;
     float S[15];
 #pragma unroll
-    for (int f = 0; f < 15; ++f) S[f] = s_part[warp][f];
-    for (int u = 1; u < W; ++u)
+    for (int f = 0; f < 15; ++f) S[f] = s_part[fw][f];
+    for (int u = 1; u < bw.y; ++u)
 #pragma unroll
-      for (int f = 0; f < 15; ++f) S[f] = S[f] + s_part[warp + u][f];
+      for (int f = 0; f < 15; ++f) S[f] = S[f] + s_part[fw + u][f];
     bool finite = true;
 #pragma unroll
     for (int f = 0; f < 15; ++f) finite = finite && isfinite(S[f]);
-    if (!finite) record_error(A.err, PBDR_DEVERR_NONFINITE, b, A.substep_counter);
-    float* R = &s_res[warp][0];
+    if (!finite) record_error(A.err, PBDR_DEVERR_NONFINITE, bb, A.substep_counter);
+    float* R = &s_res[lane][0];
     const float M = mass.x, invM = mass.y;
     float ca[3], Pa[3], La[3], tmp[3], dv[3] = {0.0f, 0.0f, 0.0f}, om[3] = {0.0f, 0.0f, 0.0f};
 #pragma unroll
@@ -484,7 +757,7 @@ __global__ void __launch_bounds__(kIterThreads, 2) k_iteration(IterArgs A) {
       const float dL[3] = {La[0] - R[kResLb], La[1] - R[kResLb + 1], La[2] - R[kResLb + 2]};
       double nax[3];
       const unsigned e = inertia_solve_f(If, dL, om, nax);
-      if (e) record_error(A.err, e, b, A.substep_counter, nax);
+      if (e) record_error(A.err, e, bb, A.substep_counter, nax);
     }
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
@@ -494,6 +767,7 @@ __global__ void __launch_bounds__(kIterThreads, 2) k_iteration(IterArgs A) {
     }
   }
   __syncthreads();
+  if (tm && threadIdx.x == 0) tm[5] = clock64();
 
   // ---- Phase C: momentum corrections (Eq. 1 then Eq. 2), writeback --------
   if (!live) return;
@@ -506,54 +780,70 @@ __global__ void __launch_bounds__(kIterThreads, 2) k_iteration(IterArgs A) {
   }
 #pragma unroll
   for (int k = 0; k < PBDR_KP; ++k) {
-    if (!act[k]) continue;
-    float r[3], wr[3], xo[3], vo[3];
+    const int q = k * 32 * W + wi * 32 + lane;
+    if (!(q < n)) continue;
+    const float4 x4 = s_pos[off + q];
+    const float4 v4 = s_vel[off + q];
+    float xi[3] = {0.0f, 0.0f, 0.0f};
+    if (!A.incremental) {
+      const float4 i4 = A.init[start + q];
+      xi[0] = i4.x; xi[1] = i4.y; xi[2] = i4.z;
+    }
+    const float x[3] = {x4.x, x4.y, x4.z};
+    const float v[3] = {v4.x, v4.y, v4.z};
+    float xa[3], va[3], r[3], wr[3], xo[3], vo[3];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) r[c] = pa[k][c] - ca[c];
+    for (int c = 0; c < 3; ++c) {
+      xa[c] = x[c] + dX[k][c];
+      va[c] = A.incremental ? v[c] + dX[k][c] * A.inv_dt : (xa[c] - xi[c]) * A.inv_dt;
+      r[c] = ((x[c] - a[c]) + dX[k][c]) - ca[c];
+    }
     cross3(om, r, wr);
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      float vv = va[k][c] + dv[c];
+      float vv = va[c] + dv[c];
       vv = vv - wr[c];
-      float xx = xa[k][c] + dv[c] * A.dt;
+      float xx = xa[c] + dv[c] * A.dt;
       xx = xx - wr[c] * A.dt;
       vo[c] = vv;
       xo[c] = xx;
     }
-    const int64_t p = pidx[k];
-    A.pos_out[p] = make_float4(xo[0], xo[1], xo[2], w[k]);
-    A.vel[p] = make_float4(vo[0], vo[1], vo[2], m[k]);
+    const int64_t p = start + q;
+    A.pos_out[p] = make_float4(xo[0], xo[1], xo[2], x4.w);
+    A.vel[p] = make_float4(vo[0], vo[1], vo[2], v4.w);
+  }
+  if (tm && threadIdx.x == 0) {
+    tm[6] = clock64();
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    tm[7] = smid;
   }
 }
 
 // ---------------------------------------------------------------------------
 // Per-body trajectory sample: com, orientation (extract_pose), P, L.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kIterThreads) k_body_stats(StatsArgs A) {
-  __shared__ float s_part[PBDR_CTA_WARPS][18];
+__global__ void __launch_bounds__(kThreads) k_body_stats(StatsArgs A) {
+  __shared__ float s_part[kWarps][18];
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int2 wd = A.warp_desc[blockIdx.x * PBDR_CTA_WARPS + warp];
+  const int4 cd = A.cta_desc[blockIdx.x];
+  const int4 wd = A.warp_desc[blockIdx.x * kWarps + warp];
   const int b = wd.x;
   const int wi = wd.y;
   const bool live = b >= 0;
-  int4 bd = make_int4(0, 0, 1, 0);
-  float a[3] = {0.0f, 0.0f, 0.0f};
-  if (live) {
-    bd = A.body_desc[b];
-    const float4 an = A.anchor[b];
-    a[0] = an.x; a[1] = an.y; a[2] = an.z;
-  }
-  const int start = bd.x, n = bd.y, W = bd.z;
   float acc[18];
 #pragma unroll
   for (int f = 0; f < 18; ++f) acc[f] = 0.0f;
   if (live) {
+    const int4 bd = make_int4(wd.z, wd.w & 0xFFFF, wd.w >> 16, 0);
+    const float4 an = A.anchor[b];
+    const float a[3] = {an.x, an.y, an.z};
 #pragma unroll
     for (int k = 0; k < PBDR_KP; ++k) {
-      const int q = k * 32 * W + wi * 32 + lane;
-      if (q >= n) continue;
-      const int64_t p = start + q;
+      const int q = k * 32 * bd.z + wi * 32 + lane;
+      if (q >= bd.y) continue;
+      const int64_t p = bd.x + q;
       const float4 x4 = A.pos[p];
       const float4 v4 = A.vel[p];
       const float4 r4 = A.rest[p];
@@ -584,14 +874,18 @@ __global__ void __launch_bounds__(kIterThreads) k_body_stats(StatsArgs A) {
       for (int f = 0; f < 18; ++f) s_part[warp][f] = acc[f];
   }
   __syncthreads();
-  if (!(live && wi == 0 && lane == 0)) return;
+  if (!(warp == 0 && lane < cd.w)) return;
+  const int bb = cd.z + lane;
+  const int4 bd = A.body_desc[bb];
+  const float4 an = A.anchor[bb];
+  const float a[3] = {an.x, an.y, an.z};
   float S[18];
 #pragma unroll
-  for (int f = 0; f < 18; ++f) S[f] = s_part[warp][f];
-  for (int u = 1; u < W; ++u)
+  for (int f = 0; f < 18; ++f) S[f] = s_part[bd.w][f];
+  for (int u = 1; u < bd.z; ++u)
 #pragma unroll
-    for (int f = 0; f < 18; ++f) S[f] = S[f] + s_part[warp + u][f];
-  const float invM = A.body_mass[b].y;
+    for (int f = 0; f < 18; ++f) S[f] = S[f] + s_part[bd.w + u][f];
+  const float invM = A.body_mass[bb].y;
   float c[3], P[3], tmp[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
@@ -604,7 +898,7 @@ __global__ void __launch_bounds__(kIterThreads) k_body_stats(StatsArgs A) {
   if (!polar_rotation_f(&S[3], Rf, qd)) {
     qd[0] = 1.0; qd[1] = 0.0; qd[2] = 0.0; qd[3] = 0.0;
   }
-  double* o = A.out + 13 * static_cast<int64_t>(b);
+  double* o = A.out + 13 * static_cast<int64_t>(bb);
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     o[k] = static_cast<double>(a[k]) + static_cast<double>(c[k]);
@@ -617,9 +911,23 @@ __global__ void __launch_bounds__(kIterThreads) k_body_stats(StatsArgs A) {
 
 }  // namespace
 
+size_t iteration_smem_bytes() { return sizeof(float4) * 3 * kSlots; }
+
 void launch_integrate(const IntegrateArgs& a, cudaStream_t s) {
   const unsigned blocks = static_cast<unsigned>((a.n + 255) / 256);
   k_integrate_key<<<blocks, 256, 0, s>>>(a);
+}
+
+void launch_body_keys(const BroadArgs& a, cudaStream_t s) {
+  k_body_keys<<<(a.nb + 255) / 256, 256, 0, s>>>(a);
+}
+
+void launch_body_ranges(const BroadArgs& a, cudaStream_t s) {
+  k_body_ranges<<<(a.nb + 255) / 256, 256, 0, s>>>(a);
+}
+
+void launch_body_partners(const BroadArgs& a, cudaStream_t s) {
+  k_body_partners<<<(a.nb + 127) / 128, 128, 0, s>>>(a);
 }
 
 void launch_ranges(const RangesArgs& a, cudaStream_t s) {
@@ -632,12 +940,17 @@ void launch_neighbours(const NeighbourArgs& a, cudaStream_t s) {
   k_neighbours<<<blocks, 128, 0, s>>>(a);
 }
 
+cudaError_t prepare_iteration_kernel() {
+  return cudaFuncSetAttribute(k_iteration, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(iteration_smem_bytes()));
+}
+
 void launch_iteration(const IterArgs& a, int ctas, cudaStream_t s) {
-  k_iteration<<<ctas, kIterThreads, 0, s>>>(a);
+  k_iteration<<<ctas, kThreads, iteration_smem_bytes(), s>>>(a);
 }
 
 void launch_stats(const StatsArgs& a, int ctas, cudaStream_t s) {
-  k_body_stats<<<ctas, kIterThreads, 0, s>>>(a);
+  k_body_stats<<<ctas, kThreads, 0, s>>>(a);
 }
 
 }  // namespace pbdr_dev

@@ -40,6 +40,8 @@ struct IntegrateArgs {
   const float2* body_mass;      // (M, 1/M)
   uint32_t* keys;
   uint32_t* vals;
+  uint32_t* box_min;  // per body 3 x order-preserving uint of the min corner of X~
+  uint32_t* box_max;
   const long long* substep_counter;
   int64_t n;
   float dt, gravity, inv_h;
@@ -47,12 +49,33 @@ struct IntegrateArgs {
   uint32_t mask;
 };
 
+// Body broadphase (acceleration only; the candidate set is unchanged): a
+// particle can have a candidate only inside the h-inflated box of another body
+// of its scene, and only such body pairs are partners.
+struct BroadArgs {
+  const uint32_t* box_min;
+  const uint32_t* box_max;
+  const int* body_scene;
+  uint32_t* bkeys;     // [nb] coarse-cell key of each body's box centre
+  uint32_t* bvals;     // [nb] body index
+  const uint32_t* sorted_bkeys;
+  const uint32_t* sorted_bvals;
+  uint2* bcells;       // coarse bucket -> (start, end) in the sorted body array
+  int* npartners;      // [nb], -1 = overflow (search every particle of the body)
+  int* partners;       // [nb * PBDR_PARTNER_CAP]
+  unsigned* oversize;  // set when a body box exceeds max_extent (disables the skip)
+  int nb;
+  float inv_cell;      // 1 / coarse cell
+  float max_extent;    // coarse cell - inflation: the largest box the grid guarantees
+  float inflate;       // h, slightly enlarged
+  uint32_t mask;
+};
+
 struct RangesArgs {
   const uint32_t* keys;  // sorted
   const uint32_t* vals;  // sorted slots
   const int* body_of;
-  uint32_t* cell_start;
-  uint32_t* cell_end;
+  uint4* cells;  // per bucket (start, end, first body, last body); start = ~0 when empty
   int* sorted_body;
   long long* substep_counter;
   int64_t n;
@@ -63,10 +86,14 @@ struct NeighbourArgs {
   const float4* rest;
   const int* body_of;
   const int* body_scene;
-  const uint32_t* cell_start;
-  const uint32_t* cell_end;
+  const uint4* cells;
   const int* sorted_body;
   const uint32_t* sorted_vals;
+  const uint32_t* box_min;
+  const uint32_t* box_max;
+  const int* npartners;
+  const int* partners;
+  float inflate;
   int* ncand;
   int* cand_j;     // slot-major: [k * n + i]
   float* cand_rr;  // slot-major
@@ -87,7 +114,8 @@ struct IterArgs {
   const int* cand_j;
   const float* cand_rr;
   float4* anchor;        // per body (xyz)
-  const int2* warp_desc; // per CTA warp: (body, warp index within body) or (-1, 0)
+  const int4* cta_desc;  // per CTA: (first slot, slot count, first body, body count)
+  const int4* warp_desc; // per CTA warp: (body, warp in body, body start, n | W << 16); body -1 = idle
   const int4* body_desc; // (start, n, W, first warp in CTA)
   const float2* body_mass;
   DevError* err;
@@ -96,6 +124,7 @@ struct IterArgs {
   Planes planes;
   float dt, inv_dt, relax;
   int incremental, linfix, angfix;
+  long long* timing;  // optional per-CTA phase clocks (debug), else null
 };
 
 struct StatsArgs {
@@ -103,15 +132,21 @@ struct StatsArgs {
   const float4* vel;
   const float4* rest;
   const float4* anchor;
-  const int2* warp_desc;
+  const int4* cta_desc;
+  const int4* warp_desc;
   const int4* body_desc;
   const float2* body_mass;
   double* out;  // 13 doubles per body: com[3], quat[4], P[3], L[3]
 };
 
 void launch_integrate(const IntegrateArgs& a, cudaStream_t s);
+void launch_body_keys(const BroadArgs& a, cudaStream_t s);
+void launch_body_ranges(const BroadArgs& a, cudaStream_t s);
+void launch_body_partners(const BroadArgs& a, cudaStream_t s);
 void launch_ranges(const RangesArgs& a, cudaStream_t s);
 void launch_neighbours(const NeighbourArgs& a, cudaStream_t s);
+size_t iteration_smem_bytes();
+cudaError_t prepare_iteration_kernel();
 void launch_iteration(const IterArgs& a, int ctas, cudaStream_t s);
 void launch_stats(const StatsArgs& a, int ctas, cudaStream_t s);
 

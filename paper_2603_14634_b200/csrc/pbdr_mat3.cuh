@@ -71,32 +71,37 @@ __device__ __forceinline__ void d3_quat_from(const D3& x, double q[4]) {
   double w, qx, qy, qz;
   if (tr > 0.0) {
     const double s = sqrt(tr + 1.0) * 2.0;
+    const double is = 1.0 / s;
     w = 0.25 * s;
-    qx = (x.a[2][1] - x.a[1][2]) / s;
-    qy = (x.a[0][2] - x.a[2][0]) / s;
-    qz = (x.a[1][0] - x.a[0][1]) / s;
+    qx = (x.a[2][1] - x.a[1][2]) * is;
+    qy = (x.a[0][2] - x.a[2][0]) * is;
+    qz = (x.a[1][0] - x.a[0][1]) * is;
   } else if (x.a[0][0] > x.a[1][1] && x.a[0][0] > x.a[2][2]) {
     const double s = sqrt(((1.0 + x.a[0][0]) - x.a[1][1]) - x.a[2][2]) * 2.0;
-    w = (x.a[2][1] - x.a[1][2]) / s;
+    const double is = 1.0 / s;
+    w = (x.a[2][1] - x.a[1][2]) * is;
     qx = 0.25 * s;
-    qy = (x.a[0][1] + x.a[1][0]) / s;
-    qz = (x.a[0][2] + x.a[2][0]) / s;
+    qy = (x.a[0][1] + x.a[1][0]) * is;
+    qz = (x.a[0][2] + x.a[2][0]) * is;
   } else if (x.a[1][1] > x.a[2][2]) {
     const double s = sqrt(((1.0 + x.a[1][1]) - x.a[0][0]) - x.a[2][2]) * 2.0;
-    w = (x.a[0][2] - x.a[2][0]) / s;
-    qx = (x.a[0][1] + x.a[1][0]) / s;
+    const double is = 1.0 / s;
+    w = (x.a[0][2] - x.a[2][0]) * is;
+    qx = (x.a[0][1] + x.a[1][0]) * is;
     qy = 0.25 * s;
-    qz = (x.a[1][2] + x.a[2][1]) / s;
+    qz = (x.a[1][2] + x.a[2][1]) * is;
   } else {
     const double s = sqrt(((1.0 + x.a[2][2]) - x.a[0][0]) - x.a[1][1]) * 2.0;
-    w = (x.a[1][0] - x.a[0][1]) / s;
-    qx = (x.a[0][2] + x.a[2][0]) / s;
-    qy = (x.a[1][2] + x.a[2][1]) / s;
+    const double is = 1.0 / s;
+    w = (x.a[1][0] - x.a[0][1]) * is;
+    qx = (x.a[0][2] + x.a[2][0]) * is;
+    qy = (x.a[1][2] + x.a[2][1]) * is;
     qz = 0.25 * s;
   }
   const double n = sqrt(((w * w + qx * qx) + qy * qy) + qz * qz);
   if (n > 0.0) {
-    w = w / n; qx = qx / n; qy = qy / n; qz = qz / n;
+    const double in = 1.0 / n;
+    w = w * in; qx = qx * in; qy = qy * in; qz = qz * in;
   } else {
     w = 1.0; qx = 0.0; qy = 0.0; qz = 0.0;
   }
@@ -119,8 +124,82 @@ __device__ __forceinline__ void d3_quat_to(const double q[4], float R[9]) {
   R[8] = static_cast<float>(1.0 - 2.0 * (xx + yy));
 }
 
-// Rotation of the polar decomposition of A (row-major fp32 sums). Returns
-// false when A is degenerate (non-finite or det <= rel. tolerance).
+__device__ __forceinline__ double d3_frob2(const D3& m) {
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) s = s + m.a[i][j] * m.a[i][j];
+  return s;
+}
+
+// Pinned Newton polar loop (float or double), mirrored line by line from
+// oracle/oracle_math.hpp newton_polar(). Returns iterations used, -1 if singular.
+template <typename T>
+__device__ __forceinline__ int newton_polar(T X[3][3], T tol2, T tolq, T scale_rel2, int max_it, bool scaled) {
+  for (int it = 0; it < max_it; ++it) {
+    const T d = X[0][0] * (X[1][1] * X[2][2] - X[1][2] * X[2][1]) -
+                X[0][1] * (X[1][0] * X[2][2] - X[1][2] * X[2][0]) +
+                X[0][2] * (X[1][0] * X[2][1] - X[1][1] * X[2][0]);
+    if (d == T(0) || !isfinite(d)) return -1;
+    const T id = T(1) / d;
+    T inv[3][3];
+    inv[0][0] = (X[1][1] * X[2][2] - X[1][2] * X[2][1]) * id;
+    inv[0][1] = (X[0][2] * X[2][1] - X[0][1] * X[2][2]) * id;
+    inv[0][2] = (X[0][1] * X[1][2] - X[0][2] * X[1][1]) * id;
+    inv[1][0] = (X[1][2] * X[2][0] - X[1][0] * X[2][2]) * id;
+    inv[1][1] = (X[0][0] * X[2][2] - X[0][2] * X[2][0]) * id;
+    inv[1][2] = (X[0][2] * X[1][0] - X[0][0] * X[1][2]) * id;
+    inv[2][0] = (X[1][0] * X[2][1] - X[1][1] * X[2][0]) * id;
+    inv[2][1] = (X[0][1] * X[2][0] - X[0][0] * X[2][1]) * id;
+    inv[2][2] = (X[0][0] * X[1][1] - X[0][1] * X[1][0]) * id;
+    T g = T(1), ig = T(1);
+    if (scaled) {
+      float c = 0.0f, r = 0.0f, ci = 0.0f, ri = 0.0f;
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const float s1 = static_cast<float>((fabs(X[0][j]) + fabs(X[1][j])) + fabs(X[2][j]));
+        const float s2 = static_cast<float>((fabs(inv[0][j]) + fabs(inv[1][j])) + fabs(inv[2][j]));
+        c = s1 > c ? s1 : c;
+        ci = s2 > ci ? s2 : ci;
+      }
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const float s1 = static_cast<float>((fabs(X[i][0]) + fabs(X[i][1])) + fabs(X[i][2]));
+        const float s2 = static_cast<float>((fabs(inv[i][0]) + fabs(inv[i][1])) + fabs(inv[i][2]));
+        r = s1 > r ? s1 : r;
+        ri = s2 > ri ? s2 : ri;
+      }
+      const float xn = c * r, in = ci * ri;
+      if (xn > 0.0f && in > 0.0f && isfinite(in / xn)) {
+        const float gf = sqrtf(sqrtf(in / xn));
+        g = static_cast<T>(gf);
+        ig = static_cast<T>(1.0f / gf);
+      }
+    }
+    T dd[9], ff[9];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const T nx = T(0.5) * (g * X[i][j] + inv[j][i] * ig);
+        const T dx = nx - X[i][j];
+        dd[3 * i + j] = dx * dx;
+        ff[3 * i + j] = nx * nx;
+        X[i][j] = nx;
+      }
+    const T delta2 = (((dd[0] + dd[1]) + (dd[2] + dd[3])) + ((dd[4] + dd[5]) + (dd[6] + dd[7]))) + dd[8];
+    const T fx2 = (((ff[0] + ff[1]) + (ff[2] + ff[3])) + ((ff[4] + ff[5]) + (ff[6] + ff[7]))) + ff[8];
+    const T fx = fx2 > T(1e-30) ? fx2 : T(1e-30);
+    if (delta2 <= tol2 * fx || (!scaled && delta2 <= tolq * fx)) return it + 1;
+    scaled = delta2 > scale_rel2 * fx;
+  }
+  return max_it;
+}
+
+// Rotation of the polar decomposition of A (row-major fp32 sums): fp32 scaled
+// Newton on A / (||A||_F / sqrt3), then unscaled fp64 Newton to 1e-9, then the
+// quaternion round trip (math.cpp:207-209). Returns false when A is degenerate.
 __device__ __noinline__ bool polar_rotation_f(const float Af[9], float R[9], double q[4]) {
   D3 A;
   bool finite = true;
@@ -130,36 +209,81 @@ __device__ __noinline__ bool polar_rotation_f(const float Af[9], float R[9], dou
     finite = finite && isfinite(Af[i]);
   }
   if (!finite) return false;
-  const double s = d3_frob(A) / sqrt(3.0);
-  if (d3_det(A) <= PBDR_POLAR_REL_DET * ((s * s) * s)) return false;
-  D3 X = A;
-  for (int it = 0; it < PBDR_POLAR_MAX_IT; ++it) {
-    const double d = d3_det(X);
-    if (d == 0.0 || !isfinite(d)) return false;
-    const D3 inv = d3_adj_inverse(X, d);
-    D3 xit;
+  const double d0 = d3_det(A);
+  const double c3 = d3_frob2(A) * PBDR_ONE_THIRD;
+  if (!(d0 > 0.0) || d0 * d0 <= (PBDR_POLAR_REL_DET * PBDR_POLAR_REL_DET) * ((c3 * c3) * c3)) return false;
+  const double is = 1.0 / sqrt(c3);
+  float Xf[3][3];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) Xf[i][j] = static_cast<float>(A.a[i][j] * is);
+  double X[3][3];
+  const int f_it = newton_polar<float>(Xf, PBDR_POLAR_F32_TOL2, PBDR_POLAR_F32_TOLQ,
+                                       static_cast<float>(PBDR_POLAR_SCALE_REL2), PBDR_POLAR_F32_MAX_IT, true);
+  D3 Xm;
+  if (f_it > 0) {
+    // fp64 polish: one unscaled Newton step re-orthonormalises the fp32
+    // iterate (R0), then one first-order rotation correction solves the
+    // symmetry condition of B = R0^T A: axial(B - B^T) = (tr(S) I - S) w,
+    // S = sym(B), and R = R0 (I + [w]x) (error O(|w|^2) ~ 1e-14).
 #pragma unroll
     for (int i = 0; i < 3; ++i)
 #pragma unroll
-      for (int j = 0; j < 3; ++j) xit.a[i][j] = inv.a[j][i];
-    const double xn = d3_norm1_inf(X);
-    const double in = d3_norm1_inf(xit);
-    const double g = (xn > 0.0 && in > 0.0) ? sqrt(sqrt(in / xn)) : 1.0;
-    const double ig = 1.0 / g;
-    D3 nx, dx;
+      for (int j = 0; j < 3; ++j) X[i][j] = static_cast<double>(Xf[i][j]);
+    if (newton_polar<double>(X, 0.0, 0.0, 0.0, 1, false) < 0) return false;
+    double B[3][3];
 #pragma unroll
     for (int i = 0; i < 3; ++i)
 #pragma unroll
-      for (int j = 0; j < 3; ++j) {
-        nx.a[i][j] = 0.5 * (g * X.a[i][j] + xit.a[i][j] * ig);
-        dx.a[i][j] = nx.a[i][j] - X.a[i][j];
-      }
-    const double delta = d3_frob(dx);
-    X = nx;
-    const double fx = d3_frob(X);
-    if (delta <= PBDR_POLAR_TOL * (fx > 1e-300 ? fx : 1e-300)) break;
+      for (int j = 0; j < 3; ++j)
+        B[i][j] = (X[0][i] * A.a[0][j] + X[1][i] * A.a[1][j]) + X[2][i] * A.a[2][j];
+    const double sv[3] = {B[2][1] - B[1][2], B[0][2] - B[2][0], B[1][0] - B[0][1]};
+    double M[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) M[i][j] = -(0.5 * (B[i][j] + B[j][i]));
+    const double tr = (-M[0][0] + -M[1][1]) + -M[2][2];
+    M[0][0] = tr + M[0][0];
+    M[1][1] = tr + M[1][1];
+    M[2][2] = tr + M[2][2];
+    const double dm = M[0][0] * (M[1][1] * M[2][2] - M[1][2] * M[2][1]) -
+                      M[0][1] * (M[1][0] * M[2][2] - M[1][2] * M[2][0]) +
+                      M[0][2] * (M[1][0] * M[2][1] - M[1][1] * M[2][0]);
+    double w[3] = {0.0, 0.0, 0.0};
+    if (dm != 0.0 && isfinite(dm)) {
+      const double idm = 1.0 / dm;
+      const double c00 = (M[1][1] * M[2][2] - M[1][2] * M[2][1]) * idm;
+      const double c01 = (M[0][2] * M[2][1] - M[0][1] * M[2][2]) * idm;
+      const double c02 = (M[0][1] * M[1][2] - M[0][2] * M[1][1]) * idm;
+      const double c11 = (M[0][0] * M[2][2] - M[0][2] * M[2][0]) * idm;
+      const double c12 = (M[0][2] * M[1][0] - M[0][0] * M[1][2]) * idm;
+      const double c22 = (M[0][0] * M[1][1] - M[0][1] * M[1][0]) * idm;
+      w[0] = (c00 * sv[0] + c01 * sv[1]) + c02 * sv[2];
+      w[1] = (c01 * sv[0] + c11 * sv[1]) + c12 * sv[2];
+      w[2] = (c02 * sv[0] + c12 * sv[1]) + c22 * sv[2];
+    }
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      Xm.a[i][0] = X[i][0] + (X[i][1] * w[2] - X[i][2] * w[1]);
+      Xm.a[i][1] = X[i][1] + (X[i][2] * w[0] - X[i][0] * w[2]);
+      Xm.a[i][2] = X[i][2] + (X[i][0] * w[1] - X[i][1] * w[0]);
+    }
+  } else {
+    // fp32 stage broke down: full scaled fp64 Newton from A.
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) X[i][j] = A.a[i][j];
+    if (newton_polar<double>(X, PBDR_POLAR_TOL2, PBDR_POLAR_TOLQ, PBDR_POLAR_SCALE_REL2, PBDR_POLAR_MAX_IT, true) < 0)
+      return false;
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) Xm.a[i][j] = X[i][j];
   }
-  d3_quat_from(X, q);
+  d3_quat_from(Xm, q);
   d3_quat_to(q, R);
   return true;
 }
@@ -221,9 +345,12 @@ __device__ void d3_sym_eigen(const D3& m, double ev[3], D3& V) {
 
 // omega = pinv(I) dL (fp32 inputs, fp64 solve). Returns 0 or
 // PBDR_DEVERR_RANK_DEFICIENT (omega = 0, null axis filled).
-__device__ __noinline__ unsigned inertia_solve_f(const float If[6] /* xx yy zz xy xz yz */,
-                                                  const float dLf[3], float w[3],
-                                                  double null_axis[3]) {
+__device__ __noinline__ unsigned inertia_solve_slow(const D3& I, const double dL[3], float w[3],
+                                                     double null_axis[3]);
+
+__device__ __forceinline__ unsigned inertia_solve_f(const float If[6] /* xx yy zz xy xz yz */,
+                                                    const float dLf[3], float w[3],
+                                                    double null_axis[3]) {
   D3 I;
   I.a[0][0] = If[0]; I.a[1][1] = If[1]; I.a[2][2] = If[2];
   I.a[0][1] = If[3]; I.a[1][0] = If[3];
@@ -241,6 +368,13 @@ __device__ __noinline__ unsigned inertia_solve_f(const float If[6] /* xx yy zz x
       w[r] = static_cast<float>((inv.a[r][0] * dL[0] + inv.a[r][1] * dL[1]) + inv.a[r][2] * dL[2]);
     return 0u;
   }
+  return inertia_solve_slow(I, dL, w, null_axis);
+}
+
+// Cyclic-Jacobi pseudo-inverse path (rank-deficient or ill-conditioned I).
+__device__ __noinline__ unsigned inertia_solve_slow(const D3& I, const double dL[3], float w[3],
+                                                     double null_axis[3]) {
+  const double tr = (I.a[0][0] + I.a[1][1]) + I.a[2][2];
   double ev[3];
   D3 V;
   d3_sym_eigen(I, ev, V);

@@ -33,8 +33,8 @@
  * (proj/include/pbdr/parallel.hpp:15-18, 40-63): results are independent of
  * scheduling, and the oracle reproduces the tree exactly.
  */
-#define PBDR_KP 2                 /* particles per lane per body (max)      */
-#define PBDR_CTA_WARPS 16         /* warps per iteration CTA                */
+#define PBDR_KP 4                 /* particles per lane per body (max)      */
+#define PBDR_CTA_WARPS 8          /* warps per iteration CTA                */
 #define PBDR_MAX_BODY_PARTICLES (PBDR_KP * 32 * PBDR_CTA_WARPS) /* 1024    */
 
 PBDR_HD int pbdr_body_warps(int n) { return (n + 32 * PBDR_KP - 1) / (32 * PBDR_KP); }
@@ -45,21 +45,27 @@ PBDR_HD int pbdr_body_slots(int n, int w) { return (n + 32 * w - 1) / (32 * w); 
  * floorf(x * inv_h) in fp32 (inv_h = 1.0f / h_f), clamped to +-2^24 before the
  * int conversion so that runaway particles cannot overflow. The clamp is
  * monotone and non-expansive, so two particles closer than h still land in
- * adjacent cells. Buckets: a murmur3-finalised mix of the Teschner primes,
- * masked to a power-of-two table. Scene ids keep batched scenes apart.
+ * adjacent cells.
+ *
+ * Bucket key: cells are grouped into x-runs of 16; the run (scene, cz, cy,
+ * cx >> 4) is scrambled with a murmur3-finalised mix of the Teschner primes and
+ * the low 4 bits keep cx & 15. So the three x-adjacent cells of a stencil row
+ * are consecutive keys -- one contiguous range of the sorted array -- unless
+ * the row crosses a run boundary. Scene ids keep batched scenes apart.
  */
 #define PBDR_CELL_CLAMP 16777216.0f
+#define PBDR_XRUN_BITS 4
 
 PBDR_HD uint32_t pbdr_cell_hash(int32_t cx, int32_t cy, int32_t cz, uint32_t scene,
                                 uint32_t mask) {
-  uint32_t h = ((uint32_t)cx * 73856093u) ^ ((uint32_t)cy * 19349663u) ^
+  uint32_t h = ((uint32_t)(cx >> PBDR_XRUN_BITS) * 73856093u) ^ ((uint32_t)cy * 19349663u) ^
                ((uint32_t)cz * 83492791u) ^ (scene * 2654435761u);
   h ^= h >> 16;
   h *= 0x85ebca6bu;
   h ^= h >> 13;
   h *= 0xc2b2ae35u;
   h ^= h >> 16;
-  return h & mask;
+  return ((h << PBDR_XRUN_BITS) | ((uint32_t)cx & ((1u << PBDR_XRUN_BITS) - 1u))) & mask;
 }
 
 /* Hash table size T = 2^bits, the smallest power of two >= max(n, 1024). */
@@ -79,6 +85,10 @@ PBDR_HD int32_t pbdr_cell_coord(float x, float inv_h) {
  * PBDR_ERR_SIMULATION (never silently dropped). */
 #define PBDR_NBR_CAP 32
 
+/* Body-broadphase partners kept per body; more disables the skip for that
+ * body (its particles always run the full stencil search). */
+#define PBDR_PARTNER_CAP 32
+
 /* Maximum planes (ground + walls) per scene. */
 #define PBDR_MAX_PLANES 8
 
@@ -86,11 +96,20 @@ PBDR_HD int32_t pbdr_cell_coord(float x, float inv_h) {
  * Polar decomposition (math.cpp:170-210 semantics, scaled Newton, tol 1e-9,
  * <= 64 iterations). The reference's absolute det(A) <= 1e-12 test
  * (math.cpp:172) rejects small-but-valid bodies, so the
- * degeneracy test is scale-relative: det(A) <= 1e-12 * (||A||_F / sqrt 3)^3.
+ * degeneracy test is scale-relative: det(A) <= 1e-12 * (||A||_F / sqrt 3)^3,
+ * evaluated without roots as det <= 0 or det^2 <= 1e-24 * (||A||_F^2 / 3)^3.
  */
 #define PBDR_POLAR_TOL 1e-9
+#define PBDR_POLAR_TOL2 1e-18     /* convergence: |dX|_F^2 <= tol^2 |X|_F^2  */
+#define PBDR_POLAR_SCALE_REL2 1e-4 /* keep the 1-inf scaling while |dX|/|X| > 1e-2 */
+#define PBDR_POLAR_TOLQ 1e-12     /* unscaled step with |dX|^2 <= 1e-12 |X|^2 leaves ~1e-12 */
 #define PBDR_POLAR_MAX_IT 64
 #define PBDR_POLAR_REL_DET 1e-12
+#define PBDR_ONE_THIRD (1.0 / 3.0)
+/* fp32 warm-up stage of the polar (then fp64 polish to PBDR_POLAR_TOL). */
+#define PBDR_POLAR_F32_TOL2 1e-12f
+#define PBDR_POLAR_F32_TOLQ 1e-7f
+#define PBDR_POLAR_F32_MAX_IT 32
 
 /* Inertia inverse for the angular-momentum fix: pseudo-inverse semantics of
  * math.cpp:90-108 (rank cut at eigenvalue < 1e-10 * trace). When

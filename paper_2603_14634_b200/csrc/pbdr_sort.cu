@@ -27,8 +27,8 @@ namespace pbdr_dev {
 
 constexpr int kSortThreads = 256;
 constexpr int kSortWarps = kSortThreads / 32;
-constexpr int kSortItems = 16;
-constexpr int kSortTile = kSortThreads * kSortItems;  // 4096 keys
+constexpr int kSortItems = 8;
+constexpr int kSortTile = kSortThreads * kSortItems;  // 2048 keys
 constexpr int kRadix = 256;
 constexpr uint32_t kFlagAgg = 1u << 30;
 constexpr uint32_t kFlagIncl = 2u << 30;
@@ -79,7 +79,11 @@ pbdr_sort_onesweep(const uint32_t* __restrict__ keys_in, const uint32_t* __restr
                    uint32_t* __restrict__ tile_counter) {
   __shared__ uint32_t s_tile;
   __shared__ uint32_t s_warp_hist[kSortWarps][kRadix];
-  __shared__ uint32_t s_digit_off[kRadix];
+  __shared__ uint32_t s_digit_off[kRadix];   // global start of this tile's digit group
+  __shared__ uint32_t s_tile_excl[kRadix];   // tile-local start of the digit group
+  __shared__ uint32_t s_wsum[kSortWarps];
+  __shared__ uint32_t s_keys[kSortTile];
+  __shared__ uint32_t s_vals[kSortTile];
 
   if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
   for (int i = threadIdx.x; i < kSortWarps * kRadix; i += kSortThreads) (&s_warp_hist[0][0])[i] = 0u;
@@ -89,7 +93,8 @@ pbdr_sort_onesweep(const uint32_t* __restrict__ keys_in, const uint32_t* __restr
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t lt_mask = (1u << lane) - 1u;
-  const int64_t base = static_cast<int64_t>(tile) * kSortTile + warp * (32 * kSortItems);
+  const int64_t tile_base = static_cast<int64_t>(tile) * kSortTile;
+  const int64_t base = tile_base + warp * (32 * kSortItems);
 
   uint32_t k[kSortItems], v[kSortItems], rank[kSortItems];
 #pragma unroll
@@ -128,6 +133,14 @@ pbdr_sort_onesweep(const uint32_t* __restrict__ keys_in, const uint32_t* __restr
     s_warp_hist[w][d] = tile_count;
     tile_count += c;
   }
+  // Tile-local exclusive scan over the 256 digits (warp scan + warp totals).
+  uint32_t incl = tile_count;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xFFFFFFFFu, incl, off);
+    if (lane >= off) incl += y;
+  }
+  if (lane == 31) s_wsum[warp] = incl;
   // Decoupled look-back over earlier tiles' per-digit status words.
   volatile uint32_t* st = status;
   uint32_t exclusive = 0u;
@@ -147,16 +160,31 @@ pbdr_sort_onesweep(const uint32_t* __restrict__ keys_in, const uint32_t* __restr
   }
   s_digit_off[d] = digit_base[d] + exclusive;
   __syncthreads();
+  uint32_t wpre = 0u;
+  for (int w = 0; w < warp; ++w) wpre += s_wsum[w];
+  s_tile_excl[d] = wpre + incl - tile_count;
+  __syncthreads();
 
+  // Local scatter into digit order, then coalesced runs to global memory.
 #pragma unroll
   for (int i = 0; i < kSortItems; ++i) {
     const int64_t idx = base + i * 32 + lane;
     if (idx < n) {
       const uint32_t dd = (k[i] >> shift) & 0xFFu;
-      const uint32_t dst = s_digit_off[dd] + s_warp_hist[warp][dd] + rank[i];
-      keys_out[dst] = k[i];
-      vals_out[dst] = v[i];
+      const uint32_t lp = s_tile_excl[dd] + s_warp_hist[warp][dd] + rank[i];
+      s_keys[lp] = k[i];
+      s_vals[lp] = v[i];
     }
+  }
+  __syncthreads();
+  const int64_t rem = n - tile_base;
+  const int tile_n = rem < kSortTile ? static_cast<int>(rem) : kSortTile;
+  for (int j = threadIdx.x; j < tile_n; j += kSortThreads) {
+    const uint32_t kk = s_keys[j];
+    const uint32_t dd = (kk >> shift) & 0xFFu;
+    const uint32_t dst = s_digit_off[dd] + (static_cast<uint32_t>(j) - s_tile_excl[dd]);
+    keys_out[dst] = kk;
+    vals_out[dst] = s_vals[j];
   }
 }
 

@@ -15,6 +15,7 @@ enum HookClass {
   kHookNeighbours = 4,
   kHookIteration = 5,
   kHookMemset = 6,
+  kHookBroadphase = 7,
 };
 
 // Called around every launch when profiling; null otherwise. `launches` is

@@ -16,11 +16,11 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libpbdr_gpu.so")
+LIB_PATH = os.environ.get("PBDR_LIB_PATH") or os.path.join(_HERE, "lib", "libpbdr_gpu.so")
 
 NBR_CAP = 32
 KCLASS_NAMES = ("integrate_key", "sort_histogram", "sort_onesweep", "cell_ranges",
-                "neighbours", "iteration", "memset")
+                "neighbours", "iteration", "memset", "broadphase")
 
 # ---- status codes / exceptions (errors.hpp:8-44) ---------------------------
 OK, ERR_DEGENERATE, ERR_RANK_DEFICIENT, ERR_EMPTY_PACKING, ERR_INVALID_MOMENT, \
@@ -146,6 +146,7 @@ def lib() -> C.CDLL:
         L.pbdr_gpu_debug_read_init.argtypes = [vp, vp]
         L.pbdr_gpu_debug_read_anchor.argtypes = [vp, vp]
         L.pbdr_gpu_debug_write_anchor.argtypes = [vp, vp]
+        L.pbdr_gpu_debug_phase_timing.argtypes = [vp, vp]
         L.pbdr_scene_generate.argtypes = [C.c_int, C.c_uint64, i64, C.POINTER(vp)]
         L.pbdr_scene_generate_c4_shard.argtypes = [C.c_uint64, i64, i64, C.POINTER(vp)]
         L.pbdr_scene_view.argtypes = [vp, C.POINTER(SceneDesc), C.POINTER(SolverCfg)]
@@ -396,8 +397,8 @@ class GpuSolver:
         return ms.value
 
     def profile_frames(self, frames: int):
-        ms = np.zeros(7, dtype=np.float32)
-        launches = np.zeros(7, dtype=np.int64)
+        ms = np.zeros(len(KCLASS_NAMES), dtype=np.float32)
+        launches = np.zeros(len(KCLASS_NAMES), dtype=np.int64)
         raise_status(lib().pbdr_gpu_profile_frames(self._h, frames, _ptr(ms), _ptr(launches)))
         return {k: (float(ms[i]), int(launches[i])) for i, k in enumerate(KCLASS_NAMES)}
 
@@ -460,6 +461,12 @@ class GpuSolver:
         a = np.empty((self.nb, 3), np.float32)
         raise_status(lib().pbdr_gpu_debug_read_anchor(self._h, _ptr(a)))
         return a
+
+    def debug_phase_timing(self):
+        """clock64 stamps per CTA of one iteration launch (see pbdr_gpu.h)."""
+        out = np.zeros((self.info.num_ctas, 8), np.int64)
+        raise_status(lib().pbdr_gpu_debug_phase_timing(self._h, _ptr(out)))
+        return out
 
     def debug_write_anchor(self, a):
         a = np.ascontiguousarray(a, np.float32)

@@ -216,3 +216,33 @@ def test_penetration_bound_c2(pbdr):
     p, _ = gpu.read_particles()
     r = g.array("radius", g.num_particles)
     assert (p[:, 2] - r).min() >= -0.1 * r.max()
+
+
+@pytest.mark.parametrize("cid,scale,frames", [(2, 0, 60), (3, 250, 200), (4, 8, 60), (5, 6, 60)])
+def test_replay_contact_rich_state(pbdr, pyoracle, cid, scale, frames):
+    # Differential replay: advance the GPU into a contact-rich
+    # state, upload that exact fp32 state into the oracle, then compare one
+    # substep kernel by kernel -- hash cells, candidate pairs (bit-exact, and
+    # non-empty), and every iteration.
+    g, gpu, orc = pair(pyoracle, cid, scale)
+    gpu.step_frames(frames)
+    p4, v4 = gpu.read_f32()
+    orc.write_f32(p4, v4)
+    orc.write_anchor(gpu.debug_anchor())
+    gpu.debug_prologue()
+    orc.integrate()
+    orc.candidates()
+    assert_same(gpu.debug_keys()[0], orc.keys()[0], "cell hash")
+    gcnt, glst = gpu.debug_candidates()
+    ocnt, olst = orc.read_candidates()
+    assert gcnt.sum() > 0, "expected contacts in this state"
+    assert_same(gcnt, ocnt, "candidate counts")
+    mask = np.arange(P.NBR_CAP)[None, :] < gcnt[:, None]
+    assert_same(np.where(mask, glst, -1), np.where(mask, olst, -1), "candidate lists")
+    for it in range(g.cfg.solver_iterations):
+        gpu.debug_iteration()
+        orc.iteration()
+        gp, gv = gpu.read_f32()
+        op, ov = orc.read_f32()
+        assert_same(gp, op, f"positions after iteration {it}")
+        assert_same(gv, ov, f"velocities after iteration {it}")

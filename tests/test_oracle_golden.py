@@ -29,8 +29,9 @@ def test_pack_box_bit_exact(pbdr, golden):
 
 
 def test_polar_matches_reference(pyoracle, golden):
-    # math.cpp:170-210 scaled-Newton polar. Ours: sqrt(sqrt()) for the 1/4 power
-    # and a scale-relative degeneracy test, so agreement is to rounding.
+    # math.cpp:170-210 scaled-Newton polar (tol 1e-9). Ours differs in the
+    # scaling schedule, the stopping rule and a scale-relative degeneracy test
+    # (DESIGN.md), so both are within the 1e-9 tolerance of the polar factor.
     checked = 0
     for case in golden["polar"]:
         A = np.array(case["A"])
@@ -39,9 +40,9 @@ def test_polar_matches_reference(pyoracle, golden):
             continue
         assert ok, A
         Rref = np.array(case["R"]).reshape(3, 3)
-        np.testing.assert_allclose(R, Rref, atol=1e-10)
+        np.testing.assert_allclose(R, Rref, atol=2e-9)
         qref = np.array(case["q"])
-        assert min(np.abs(q - qref).max(), np.abs(q + qref).max()) < 1e-10
+        assert min(np.abs(q - qref).max(), np.abs(q + qref).max()) < 2e-9
         checked += 1
     assert checked >= 30
 

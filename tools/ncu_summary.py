@@ -19,7 +19,7 @@ def launches(path, out):
     for r in rows[start + 1:]:
         name = r[ki].split("(")[0].split("::")[-1]
         v = float(r[vi].replace(",", ""))
-        v *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}.get(r[ui], 1.0)
+        v *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}.get(r[ui], 1.0)
         tot[name] += v
         cnt[name] += 1
     s = sum(tot.values())
