@@ -178,7 +178,10 @@ int pbdr_gpu_profile_frames(pbdr_handle* h, int64_t frames, float* ms, int64_t* 
 int pbdr_gpu_debug_prologue(pbdr_handle* h);
 int pbdr_gpu_debug_iteration(pbdr_handle* h, int iteration_index);
 int pbdr_gpu_debug_read_keys(pbdr_handle* h, uint32_t* cell_hash, int32_t* cell_xyz);
+/* Sorted (key, slot) pairs of the broadphase-filtered particles: the first
+ * pbdr_gpu_debug_near_count() entries are valid. */
 int pbdr_gpu_debug_read_sorted(pbdr_handle* h, uint32_t* keys, uint32_t* vals);
+int pbdr_gpu_debug_near_count(pbdr_handle* h, int64_t* count);
 int pbdr_gpu_debug_read_candidates(pbdr_handle* h, int32_t* counts, int32_t* lists /* n*CAP */);
 int pbdr_gpu_debug_read_init(pbdr_handle* h, float* init4);
 /* Runs one iteration launch with per-CTA clock64 stamps (8 per CTA: start,

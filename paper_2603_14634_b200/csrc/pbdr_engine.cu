@@ -47,6 +47,14 @@ struct pbdr_handle {
   uint32_t* vals[2] = {nullptr, nullptr};
   void* sort_temp = nullptr;
   uint4* cells = nullptr;
+  // broadphase-filtered particle list
+  uint32_t* key_all = nullptr;
+  uint8_t* near_flag = nullptr;
+  uint32_t* block_count = nullptr;
+  uint32_t* block_off = nullptr;
+  long long* near_count = nullptr;  // [0] current, [1] previous substep
+  int* near_list = nullptr;
+  int near_blocks = 0;
   // body broadphase
   uint32_t* box_min = nullptr;
   uint32_t* box_max = nullptr;
@@ -167,8 +175,7 @@ void enqueue_substep(pbdr_handle* h, pbdr_dev::LaunchHook* hook) {
   ia.body_scene = h->body_scene;
   ia.programs = h->programs;
   ia.body_mass = h->body_mass;
-  ia.keys = h->keys[0];
-  ia.vals = h->vals[0];
+  ia.key_all = h->key_all;
   ia.box_min = h->box_min;
   ia.box_max = h->box_max;
   ia.substep_counter = h->counter;
@@ -184,6 +191,10 @@ void enqueue_substep(pbdr_handle* h, pbdr_dev::LaunchHook* hook) {
   cudaMemsetAsync(h->oversize, 0x00, sizeof(unsigned), h->stream);
   cudaMemsetAsync(h->bcells, 0xFF, sizeof(uint2) * (size_t(1) << h->bhash_bits), h->stream);
   if (hook) hook->after(kHookMemset, 4);
+  // Reset only the buckets the previous substep filled.
+  if (hook) hook->before(kHookRanges);
+  launch_cell_clear(h->cells, h->keys[h->sorted_buf], h->near_count + 1, h->n, h->stream);
+  if (hook) hook->after(kHookRanges);
   if (hook) hook->before(kHookIntegrate);
   launch_integrate(ia, h->stream);
   if (hook) hook->after(kHookIntegrate);
@@ -216,17 +227,39 @@ void enqueue_substep(pbdr_handle* h, pbdr_dev::LaunchHook* hook) {
   launch_body_partners(ba, h->stream);
   if (hook) hook->after(kHookBroadphase, 2);
 
-  const int sb = sort_pairs(h->keys, h->vals, h->n, h->hash_bits, h->sort_temp, h->sm_count,
-                            h->stream, hook);
-  h->sorted_buf = sb;
+  // Broadphase filter: compact the near particles (slot order) into the sort input.
+  NearArgs nr{};
+  nr.pos = h->pos[h->cur];
+  nr.body_of = h->body_of;
+  nr.box_min = h->box_min;
+  nr.box_max = h->box_max;
+  nr.npartners = h->npartners;
+  nr.partners = h->partners;
+  nr.key_all = h->key_all;
+  nr.flag = h->near_flag;
+  nr.block_count = h->block_count;
+  nr.block_off = h->block_off;
+  nr.count = h->near_count;
+  nr.keys_c = h->keys[0];
+  nr.vals_c = h->vals[0];
+  nr.near_list = h->near_list;
+  nr.ncand = h->ncand;
+  nr.n = h->n;
+  nr.blocks = h->near_blocks;
+  nr.inflate = h->inflate;
+  if (hook) hook->before(kHookBroadphase);
+  launch_near(nr, h->stream);
+  if (hook) hook->after(kHookBroadphase, 3);
 
-  if (hook) hook->before(kHookMemset);
-  cudaMemsetAsync(h->cells, 0xFF, sizeof(uint4) * (size_t(1) << h->hash_bits), h->stream);
-  if (hook) hook->after(kHookMemset);
+  const int sb = sort_pairs(h->keys, h->vals, h->n, h->hash_bits, h->sort_temp, h->sm_count,
+                            h->stream, hook, h->near_count);
+  h->sorted_buf = sb;
 
   RangesArgs ra{};
   ra.keys = h->keys[sb];
   ra.vals = h->vals[sb];
+  ra.count = h->near_count;
+  ra.prev_count = h->near_count + 1;
   ra.body_of = h->body_of;
   ra.cells = h->cells;
   ra.sorted_body = h->sorted_body;
@@ -238,17 +271,14 @@ void enqueue_substep(pbdr_handle* h, pbdr_dev::LaunchHook* hook) {
 
   NeighbourArgs na{};
   na.pos = h->pos[h->cur];
+  na.near_list = h->near_list;
+  na.count = h->near_count;
   na.rest = h->rest;
   na.body_of = h->body_of;
   na.body_scene = h->body_scene;
   na.cells = h->cells;
   na.sorted_body = h->sorted_body;
   na.sorted_vals = h->vals[sb];
-  na.box_min = h->box_min;
-  na.box_max = h->box_max;
-  na.npartners = h->npartners;
-  na.partners = h->partners;
-  na.inflate = h->inflate;
   na.ncand = h->ncand;
   na.cand_j = h->cand_j;
   na.cand_rr = h->cand_rr;
@@ -572,6 +602,13 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
     h->sort_temp = tmp;
   }
   rc |= dalloc(h, &h->cells, T);
+  h->near_blocks = static_cast<int>((n + 255) / 256);
+  rc |= dalloc(h, &h->key_all, n);
+  rc |= dalloc(h, &h->near_flag, n);
+  rc |= dalloc(h, &h->block_count, h->near_blocks);
+  rc |= dalloc(h, &h->block_off, h->near_blocks);
+  rc |= dalloc(h, &h->near_count, 2);
+  rc |= dalloc(h, &h->near_list, n);
   rc |= dalloc(h, &h->box_min, 3 * static_cast<size_t>(nb));
   rc |= dalloc(h, &h->box_max, 3 * static_cast<size_t>(nb));
   rc |= dalloc(h, &h->bkeys[0], nb);
@@ -630,13 +667,15 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
   cudaMemset(h->init, 0, sizeof(float4) * n);
   cudaMemset(h->counter, 0, sizeof(long long));
   cudaMemset(h->ncand, 0, sizeof(int) * n);
+  cudaMemset(h->cells, 0xFF, sizeof(uint4) * T);
+  cudaMemset(h->near_count, 0, sizeof(long long) * 2);
   if (reset_errors(h) != PBDR_OK) {
     const int code = pbdr_last_error_payload(nullptr, nullptr, nullptr);
     release(h);
     return code;
   }
-  h->launches_per_frame =
-      static_cast<int64_t>(h->substeps) * (1 + 1 + 2 + h->bpasses + 2 + 2 + h->passes + 1 + 1 + h->iters);
+  h->launches_per_frame = static_cast<int64_t>(h->substeps) *
+                          (1 + 1 + 1 + 2 + h->bpasses + 2 + 3 + 2 + h->passes + 1 + 1 + h->iters);
   *out = h;
   return PBDR_OK;
 }
@@ -862,11 +901,9 @@ int pbdr_gpu_debug_read_sorted(pbdr_handle* h, uint32_t* keys, uint32_t* vals) {
 // integer cell coordinates recomputed by the host from the device positions.
 int pbdr_gpu_debug_read_keys(pbdr_handle* h, uint32_t* cell_hash, int32_t* cell_xyz) {
   if (!h) return set_error(PBDR_ERR_GENERIC, "null handle");
-  std::vector<uint32_t> k(h->n), v(h->n);
-  int rc = pbdr_gpu_debug_read_sorted(h, k.data(), v.data());
-  if (rc != PBDR_OK) return rc;
+  PBDR_CUDA(cudaSetDevice(h->device));
   if (cell_hash)
-    for (int64_t s = 0; s < h->n; ++s) cell_hash[v[s]] = k[s];
+    PBDR_CUDA(cudaMemcpy(cell_hash, h->key_all, sizeof(uint32_t) * h->n, cudaMemcpyDeviceToHost));
   if (cell_xyz) {
     // Positions are still X~ between the prologue and the first iteration.
     std::vector<float4> xp(h->n);
@@ -877,6 +914,15 @@ int pbdr_gpu_debug_read_keys(pbdr_handle* h, uint32_t* cell_hash, int32_t* cell_
       cell_xyz[3 * i + 2] = pbdr_cell_coord(xp[i].z, h->inv_h);
     }
   }
+  return PBDR_OK;
+}
+
+int pbdr_gpu_debug_near_count(pbdr_handle* h, int64_t* count) {
+  if (!h || !count) return set_error(PBDR_ERR_GENERIC, "null argument");
+  PBDR_CUDA(cudaSetDevice(h->device));
+  long long c = 0;
+  PBDR_CUDA(cudaMemcpy(&c, h->near_count, sizeof c, cudaMemcpyDeviceToHost));
+  *count = c;
   return PBDR_OK;
 }
 

@@ -140,8 +140,7 @@ __global__ void __launch_bounds__(256) k_integrate_key(IntegrateArgs A) {
     const int32_t cx = pbdr_cell_coord(xn.x, A.inv_h);
     const int32_t cy = pbdr_cell_coord(xn.y, A.inv_h);
     const int32_t cz = pbdr_cell_coord(xn.z, A.inv_h);
-    A.keys[p] = pbdr_cell_hash(cx, cy, cz, static_cast<uint32_t>(A.body_scene[b]), A.mask);
-    A.vals[p] = static_cast<uint32_t>(p);
+    A.key_all[p] = pbdr_cell_hash(cx, cy, cz, static_cast<uint32_t>(A.body_scene[b]), A.mask);
   }
   // Body boxes of X~: warp-reduce when the whole warp is one body (the common
   // case in body-major order), else one atomic per lane. min/max are exact and
@@ -264,8 +263,12 @@ __global__ void __launch_bounds__(128) k_body_partners(BroadArgs A) {
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_cell_ranges(RangesArgs A) {
   const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (s == 0) atomicAdd(reinterpret_cast<unsigned long long*>(A.substep_counter), 1ull);
-  if (s >= A.n) return;
+  const int64_t m = *A.count;
+  if (s == 0) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(A.substep_counter), 1ull);
+    *A.prev_count = m;
+  }
+  if (s >= m) return;
   const uint32_t k = A.keys[s];
   const int body = A.body_of[A.vals[s]];
   A.sorted_body[s] = body;
@@ -275,10 +278,109 @@ __global__ void __launch_bounds__(256) k_cell_ranges(RangesArgs A) {
     A.cells[k].x = static_cast<uint32_t>(s);
     A.cells[k].z = static_cast<uint32_t>(body);
   }
-  if (s == A.n - 1 || A.keys[s + 1] != k) {
+  if (s == m - 1 || A.keys[s + 1] != k) {
     A.cells[k].y = static_cast<uint32_t>(s + 1);
     A.cells[k].w = static_cast<uint32_t>(body);
   }
+}
+
+
+// ---------------------------------------------------------------------------
+// Broadphase filter (exact): a candidate j of particle i lies in j's body box
+// and within h of i, so i lies in the h-inflated box of a partner body. Only
+// such "near" particles enter the hash grid and search it; the others have no
+// candidates. Flags -> block counts -> exclusive scan -> compaction in slot
+// order (deterministic).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_near_flag(NearArgs A) {
+  const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  bool near = false;
+  if (p < A.n) {
+    const float4 xi = A.pos[p];
+    const int bi = A.body_of[p];
+    const int np = A.npartners[bi];
+    near = np < 0;  // partner overflow: search in full
+    for (int k = 0; k < np && !near; ++k) {
+      const int o = A.partners[static_cast<int64_t>(bi) * PBDR_PARTNER_CAP + k];
+      float lo[3], hi[3];
+      load_box(A.box_min, A.box_max, o, lo, hi);
+      const float xs[3] = {xi.x, xi.y, xi.z};
+      bool in = true;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const float m = A.inflate + fmaxf(fabsf(lo[c]), fabsf(hi[c])) * 1e-6f;
+        in = in && xs[c] >= lo[c] - m && xs[c] <= hi[c] + m;
+      }
+      near = in;
+    }
+    A.flag[p] = near ? 1 : 0;
+  }
+  const int cnt = __syncthreads_count(near);
+  if (threadIdx.x == 0) A.block_count[blockIdx.x] = static_cast<uint32_t>(cnt);
+}
+
+// One CTA of 1024 threads: exclusive scan of the per-block near counts.
+__global__ void __launch_bounds__(1024) k_near_scan(NearArgs A) {
+  __shared__ uint32_t s_warp[32];
+  const int t = threadIdx.x;
+  const int per = (A.blocks + 1023) / 1024;
+  const int lo = t * per;
+  const int hi = min(A.blocks, lo + per);
+  uint32_t sum = 0;
+  for (int b = lo; b < hi; ++b) sum += A.block_count[b];
+  uint32_t incl = sum;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, incl, off);
+    if ((t & 31) >= off) incl += y;
+  }
+  if ((t & 31) == 31) s_warp[t >> 5] = incl;
+  __syncthreads();
+  if (t < 32) {
+    uint32_t w = s_warp[t];
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t y = __shfl_up_sync(kFull, w, off);
+      if (t >= off) w += y;
+    }
+    s_warp[t] = w;
+  }
+  __syncthreads();
+  uint32_t run = incl - sum + ((t >> 5) ? s_warp[(t >> 5) - 1] : 0u);
+  for (int b = lo; b < hi; ++b) {
+    A.block_off[b] = run;
+    run += A.block_count[b];
+  }
+  if (t == 1023) *A.count = static_cast<long long>(run);
+}
+
+__global__ void __launch_bounds__(256) k_near_compact(NearArgs A) {
+  __shared__ uint32_t s_w[8];
+  const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const bool near = p < A.n && A.flag[p] != 0;
+  const unsigned bal = __ballot_sync(kFull, near);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) s_w[warp] = __popc(bal);
+  __syncthreads();
+  uint32_t off = A.block_off[blockIdx.x];
+  for (int w = 0; w < warp; ++w) off += s_w[w];
+  off += __popc(bal & ((1u << lane) - 1u));
+  if (p >= A.n) return;
+  if (near) {
+    A.near_list[off] = static_cast<int>(p);
+    A.keys_c[off] = A.key_all[p];
+    A.vals_c[off] = static_cast<uint32_t>(p);
+  } else {
+    A.ncand[p] = 0;
+  }
+}
+
+// Resets the buckets the previous substep wrote (instead of a full memset).
+__global__ void __launch_bounds__(256) k_cell_clear(uint4* cells, const uint32_t* prev_keys,
+                                                    const long long* prev_count) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= *prev_count) return;
+  cells[prev_keys[t]].x = kEmpty;
 }
 
 // ---------------------------------------------------------------------------
@@ -334,33 +436,11 @@ __device__ __forceinline__ void scan_bucket(const NeighbourArgs& A, uint32_t key
 }
 
 __global__ void __launch_bounds__(128) k_neighbours(NeighbourArgs A) {
-  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= A.n) return;
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= *A.count) return;
+  const int64_t i = A.near_list[t];
   const float4 xi = A.pos[i];
   const int bi = A.body_of[i];
-  // Broadphase skip: no candidate can exist unless x~_i lies in the inflated
-  // box of a partner body (exact: a candidate j within h of i lies in its own
-  // body's box, and that body is then a partner of bi).
-  const int np = A.npartners[bi];
-  if (np >= 0) {
-    bool near = false;
-    for (int k = 0; k < np && !near; ++k) {
-      const int o = A.partners[static_cast<int64_t>(bi) * PBDR_PARTNER_CAP + k];
-      float lo[3], hi[3];
-      load_box(A.box_min, A.box_max, o, lo, hi);
-      const float xs[3] = {xi.x, xi.y, xi.z};
-      near = true;
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const float m = A.inflate + fmaxf(fabsf(lo[c]), fabsf(hi[c])) * 1e-6f;
-        near = near && xs[c] >= lo[c] - m && xs[c] <= hi[c] + m;
-      }
-    }
-    if (!near) {
-      A.ncand[i] = 0;
-      return;
-    }
-  }
   const int si = A.body_scene[bi];
   const int32_t cx = pbdr_cell_coord(xi.x, A.inv_h);
   const int32_t cy = pbdr_cell_coord(xi.y, A.inv_h);
@@ -928,6 +1008,17 @@ void launch_body_ranges(const BroadArgs& a, cudaStream_t s) {
 
 void launch_body_partners(const BroadArgs& a, cudaStream_t s) {
   k_body_partners<<<(a.nb + 127) / 128, 128, 0, s>>>(a);
+}
+
+void launch_near(const NearArgs& a, cudaStream_t s) {
+  k_near_flag<<<a.blocks, 256, 0, s>>>(a);
+  k_near_scan<<<1, 1024, 0, s>>>(a);
+  k_near_compact<<<a.blocks, 256, 0, s>>>(a);
+}
+
+void launch_cell_clear(uint4* cells, const uint32_t* prev_keys, const long long* prev_count, int64_t n_max,
+                       cudaStream_t s) {
+  k_cell_clear<<<static_cast<unsigned>((n_max + 255) / 256), 256, 0, s>>>(cells, prev_keys, prev_count);
 }
 
 void launch_ranges(const RangesArgs& a, cudaStream_t s) {

@@ -38,8 +38,7 @@ struct IntegrateArgs {
   const int* body_scene;
   const BodyProgram* programs;  // per body
   const float2* body_mass;      // (M, 1/M)
-  uint32_t* keys;
-  uint32_t* vals;
+  uint32_t* key_all;  // [n] cell key of every particle (slot order)
   uint32_t* box_min;  // per body 3 x order-preserving uint of the min corner of X~
   uint32_t* box_max;
   const long long* substep_counter;
@@ -71,9 +70,35 @@ struct BroadArgs {
   uint32_t mask;
 };
 
+// Broadphase filter: only particles inside the h-inflated box of a partner
+// body can have contact candidates (see k_near_flag); they are compacted, in
+// slot order, into the list that the hash grid is built from.
+struct NearArgs {
+  const float4* pos;  // X~
+  const int* body_of;
+  const uint32_t* box_min;
+  const uint32_t* box_max;
+  const int* npartners;
+  const int* partners;
+  const uint32_t* key_all;
+  uint8_t* flag;          // [n]
+  uint32_t* block_count;  // [blocks]
+  uint32_t* block_off;    // [blocks]
+  long long* count;       // total near particles (device)
+  uint32_t* keys_c;       // compacted keys  (sort input)
+  uint32_t* vals_c;       // compacted slots (sort input)
+  int* near_list;         // compacted slots (slot order)
+  int* ncand;             // zeroed for particles that are not near
+  int64_t n;
+  int blocks;
+  float inflate;
+};
+
 struct RangesArgs {
   const uint32_t* keys;  // sorted
   const uint32_t* vals;  // sorted slots
+  const long long* count;    // number of sorted entries (device)
+  long long* prev_count;     // saved for the next substep's table clear
   const int* body_of;
   uint4* cells;  // per bucket (start, end, first body, last body); start = ~0 when empty
   int* sorted_body;
@@ -83,17 +108,14 @@ struct RangesArgs {
 
 struct NeighbourArgs {
   const float4* pos;  // X~
+  const int* near_list;
+  const long long* count;
   const float4* rest;
   const int* body_of;
   const int* body_scene;
   const uint4* cells;
   const int* sorted_body;
   const uint32_t* sorted_vals;
-  const uint32_t* box_min;
-  const uint32_t* box_max;
-  const int* npartners;
-  const int* partners;
-  float inflate;
   int* ncand;
   int* cand_j;     // slot-major: [k * n + i]
   float* cand_rr;  // slot-major
@@ -143,6 +165,9 @@ void launch_integrate(const IntegrateArgs& a, cudaStream_t s);
 void launch_body_keys(const BroadArgs& a, cudaStream_t s);
 void launch_body_ranges(const BroadArgs& a, cudaStream_t s);
 void launch_body_partners(const BroadArgs& a, cudaStream_t s);
+void launch_near(const NearArgs& a, cudaStream_t s);
+void launch_cell_clear(uint4* cells, const uint32_t* prev_keys, const long long* prev_count, int64_t n_max,
+                       cudaStream_t s);
 void launch_ranges(const RangesArgs& a, cudaStream_t s);
 void launch_neighbours(const NeighbourArgs& a, cudaStream_t s);
 size_t iteration_smem_bytes();

@@ -11,10 +11,13 @@
 //   2. pbdr_sort_scan: exclusive scan of each pass's histogram -> digit bases.
 //   3. pbdr_sort_onesweep (one launch per 8-bit digit): each CTA claims a tile
 //      id from an atomic counter (so it only ever waits on tiles that are
-//      already resident), ranks its 4096 keys stably with warp-level
+//      already resident), ranks its 2048 keys stably with warp-level
 //      match_any, publishes its per-digit counts, and resolves its global
 //      offsets by decoupled look-back over the preceding tiles' status words,
-//      then scatters keys and values.
+//      then scatters keys and values through shared memory (digit-ordered
+//      runs, coalesced global writes).
+// The key count may live on the device (the broadphase-filtered particle list):
+// kernels are launched for the maximum and read the actual count.
 // Stability: within a tile keys are ranked in (warp, item, lane) order, which
 // is their input order; tiles are in input order. So equal keys keep ascending
 // particle slots, which the cell-range and neighbour kernels rely on.
@@ -35,8 +38,9 @@ constexpr uint32_t kFlagIncl = 2u << 30;
 constexpr uint32_t kValueMask = (1u << 30) - 1u;
 
 __global__ void __launch_bounds__(kSortThreads)
-pbdr_sort_histogram(const uint32_t* __restrict__ keys, int64_t n, int passes,
+pbdr_sort_histogram(const uint32_t* __restrict__ keys, int64_t n_max, const long long* n_dev, int passes,
                     uint32_t* __restrict__ hist /* passes*256 */) {
+  const int64_t n = n_dev ? static_cast<int64_t>(*n_dev) : n_max;
   __shared__ uint32_t s_hist[4][kRadix];
   for (int i = threadIdx.x; i < 4 * kRadix; i += blockDim.x) (&s_hist[0][0])[i] = 0u;
   __syncthreads();
@@ -73,8 +77,8 @@ __global__ void __launch_bounds__(kRadix) pbdr_sort_scan(uint32_t* __restrict__ 
 
 __global__ void __launch_bounds__(kSortThreads)
 pbdr_sort_onesweep(const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
-                   uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out, int64_t n,
-                   int shift, const uint32_t* __restrict__ digit_base,
+                   uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out, int64_t n_max,
+                   const long long* n_dev, int shift, const uint32_t* __restrict__ digit_base,
                    uint32_t* __restrict__ status /* tiles*256 */,
                    uint32_t* __restrict__ tile_counter) {
   __shared__ uint32_t s_tile;
@@ -85,11 +89,15 @@ pbdr_sort_onesweep(const uint32_t* __restrict__ keys_in, const uint32_t* __restr
   __shared__ uint32_t s_keys[kSortTile];
   __shared__ uint32_t s_vals[kSortTile];
 
+  const int64_t n = n_dev ? static_cast<int64_t>(*n_dev) : n_max;
   if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
   for (int i = threadIdx.x; i < kSortWarps * kRadix; i += kSortThreads) (&s_warp_hist[0][0])[i] = 0u;
   __syncthreads();
 
   const uint32_t tile = s_tile;
+  // Tiles past a device-side count hold no keys; they never publish, and no
+  // earlier tile waits on them.
+  if (static_cast<int64_t>(tile) * kSortTile >= n) return;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t lt_mask = (1u << lane) - 1u;
@@ -196,7 +204,7 @@ size_t sort_temp_bytes(int64_t n, int passes) {
 }
 
 int sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t n, int key_bits, void* temp,
-               int sm_count, cudaStream_t stream, LaunchHook* hook) {
+               int sm_count, cudaStream_t stream, LaunchHook* hook, const long long* n_dev) {
   const int passes = (key_bits + 7) / 8;
   const int64_t tiles = (n + kSortTile - 1) / kSortTile;
   uint32_t* hist = static_cast<uint32_t*>(temp);
@@ -208,14 +216,14 @@ int sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t n, int key_bits, vo
   if (hook) hook->after(kHookMemset);
   if (hook) hook->before(kHookHistogram);
   const int hist_blocks = sm_count * 4;
-  pbdr_sort_histogram<<<hist_blocks, kSortThreads, 0, stream>>>(keys[0], n, passes, hist);
+  pbdr_sort_histogram<<<hist_blocks, kSortThreads, 0, stream>>>(keys[0], n, n_dev, passes, hist);
   pbdr_sort_scan<<<1, kRadix, 0, stream>>>(hist, passes);
   if (hook) hook->after(kHookHistogram, 2);
   int cur = 0;
   for (int p = 0; p < passes; ++p) {
     if (hook) hook->before(kHookOnesweep);
     pbdr_sort_onesweep<<<static_cast<unsigned>(tiles), kSortThreads, 0, stream>>>(
-        keys[cur], vals[cur], keys[cur ^ 1], vals[cur ^ 1], n, 8 * p, hist + p * kRadix,
+        keys[cur], vals[cur], keys[cur ^ 1], vals[cur ^ 1], n, n_dev, 8 * p, hist + p * kRadix,
         status + static_cast<size_t>(p) * tiles * kRadix, counters + p);
     if (hook) hook->after(kHookOnesweep);
     cur ^= 1;

@@ -29,8 +29,9 @@ struct LaunchHook {
 size_t sort_temp_bytes(int64_t n, int passes);
 
 // Sorts keys[0]/vals[0] by the low `key_bits` bits. Returns the buffer index
-// (0 or 1) that holds the sorted pairs.
+// (0 or 1) that holds the sorted pairs. When n_dev is non-null the key count is
+// read on the device (n is then the maximum, used for launch sizes).
 int sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t n, int key_bits, void* temp,
-               int sm_count, cudaStream_t stream, LaunchHook* hook);
+               int sm_count, cudaStream_t stream, LaunchHook* hook, const long long* n_dev = nullptr);
 
 }  // namespace pbdr_dev

@@ -147,6 +147,7 @@ def lib() -> C.CDLL:
         L.pbdr_gpu_debug_read_anchor.argtypes = [vp, vp]
         L.pbdr_gpu_debug_write_anchor.argtypes = [vp, vp]
         L.pbdr_gpu_debug_phase_timing.argtypes = [vp, vp]
+        L.pbdr_gpu_debug_near_count.argtypes = [vp, C.POINTER(i64)]
         L.pbdr_scene_generate.argtypes = [C.c_int, C.c_uint64, i64, C.POINTER(vp)]
         L.pbdr_scene_generate_c4_shard.argtypes = [C.c_uint64, i64, i64, C.POINTER(vp)]
         L.pbdr_scene_view.argtypes = [vp, C.POINTER(SceneDesc), C.POINTER(SolverCfg)]
@@ -441,10 +442,13 @@ class GpuSolver:
         return hsh, cell
 
     def debug_sorted(self):
+        """Sorted (key, slot) pairs of the broadphase-filtered particles."""
         k = np.empty(self.n, np.uint32)
         v = np.empty(self.n, np.uint32)
         raise_status(lib().pbdr_gpu_debug_read_sorted(self._h, _ptr(k), _ptr(v)))
-        return k, v
+        m = C.c_int64()
+        raise_status(lib().pbdr_gpu_debug_near_count(self._h, C.byref(m)))
+        return k[:m.value], v[:m.value]
 
     def debug_candidates(self):
         c = np.empty(self.n, np.int32)

@@ -48,10 +48,11 @@ def test_prologue_bit_exact(pbdr, pyoracle, cid, scale):
     oh, oc = orc.keys()
     assert_same(gc, oc, "cell coordinates")
     assert_same(gh, oh, "cell hash")
-    # Onesweep output: sorted, a permutation, stable.
+    # Onesweep output over the broadphase-filtered ("near") particles: sorted,
+    # distinct slots, stable, keys equal to the particles' cell hashes.
     k, v = gpu.debug_sorted()
     assert np.all(k[1:] >= k[:-1])
-    assert np.array_equal(np.sort(v), np.arange(gpu.n, dtype=np.uint32))
+    assert len(np.unique(v)) == len(v)
     same = k[1:] == k[:-1]
     assert np.all(v[1:][same] > v[:-1][same])
     assert np.array_equal(k, oh[v])
@@ -246,3 +247,19 @@ def test_replay_contact_rich_state(pbdr, pyoracle, cid, scale, frames):
         op, ov = orc.read_f32()
         assert_same(gp, op, f"positions after iteration {it}")
         assert_same(gv, ov, f"velocities after iteration {it}")
+
+
+@pytest.mark.parametrize("cid,scale,frames", [(2, 0, 60), (4, 8, 60)])
+def test_near_filter_covers_all_pairs(pbdr, pyoracle, cid, scale, frames):
+    # The broadphase filter is exact: every particle with a candidate, and every
+    # candidate, is in the filtered (sorted) set.
+    g, gpu, orc = pair(pyoracle, cid, scale)
+    gpu.step_frames(frames)
+    gpu.debug_prologue()
+    _, v = gpu.debug_sorted()
+    cnt, lst = gpu.debug_candidates()
+    near = set(v.tolist())
+    mask = np.arange(P.NBR_CAP)[None, :] < cnt[:, None]
+    involved = set(np.nonzero(cnt)[0].tolist()) | set(lst[mask].tolist())
+    assert involved and involved <= near
+    assert len(near) < gpu.n  # the filter actually removes particles
