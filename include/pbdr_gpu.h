@@ -190,6 +190,10 @@ int pbdr_gpu_debug_phase_timing(pbdr_handle* h, long long* out);
 /* Body anchors (fp32 xyz per body) used by the anchored body sums. */
 int pbdr_gpu_debug_read_anchor(pbdr_handle* h, float* anchor3);
 int pbdr_gpu_debug_write_anchor(pbdr_handle* h, const float* anchor3);
+/* Per-body warm-start rotation of the shape-matching polar (w, x, y, z as
+ * float4; all-zero = none). pbdr_gpu_write_particles() clears it. */
+int pbdr_gpu_debug_read_rquat(pbdr_handle* h, float* q4);
+int pbdr_gpu_debug_write_rquat(pbdr_handle* h, const float* q4);
 
 /* ---- Host-side scene construction (no device work) ------------------------
  * The five BASELINE.json configs, generated deterministically from splitmix64

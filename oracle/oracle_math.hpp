@@ -288,6 +288,75 @@ inline bool polar_rotation(const M3& A, M3& R, double q[4]) {
   return true;
 }
 
+// Warm-started rotation extraction (pinned): starting from the body's rotation
+// of the previous solver iteration (quaternion rq, all-zero = none), apply
+// Gauss-Newton corrections of the polar factor's symmetry condition -- with
+// B = R^T A and S = sym(B): axial(B - B^T) = (tr(S) I - S) w, then
+// q <- normalise(q (x) (1, w/2)) -- until |w|^2 <= 1e-12 (the step then leaves
+// an O(|w|^2) error). Converges quadratically from any nearby R whatever the
+// conditioning of S. A missing warm start, |w|^2 > 0.25 (not local), a
+// singular solve, or 4 steps without convergence fall back to the cold
+// two-stage Newton polar. The result is the same polar factor to 1e-12.
+inline bool polar_warm(const M3& A, const float rq[4], M3& R, double q[4]) {
+  if (!finite3(A)) return false;
+  const double d0 = det3(A);
+  const double c3 = frob2(A) * PBDR_ONE_THIRD;
+  if (!(d0 > 0.0) || d0 * d0 <= (PBDR_POLAR_REL_DET * PBDR_POLAR_REL_DET) * ((c3 * c3) * c3)) return false;
+  if (rq[0] != 0.0f || rq[1] != 0.0f || rq[2] != 0.0f || rq[3] != 0.0f) {
+    double qc[4] = {rq[0], rq[1], rq[2], rq[3]};
+    {
+      const double n = std::sqrt(((qc[0] * qc[0] + qc[1] * qc[1]) + qc[2] * qc[2]) + qc[3] * qc[3]);
+      const double in = 1.0 / n;
+      for (int k = 0; k < 4; ++k) qc[k] = qc[k] * in;
+    }
+    for (int step = 0; step < PBDR_POLAR_WARM_STEPS; ++step) {
+      const M3 R0 = quat_to(qc);
+      double B[3][3];
+      for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j)
+          B[i][j] = (R0.a[0][i] * A.a[0][j] + R0.a[1][i] * A.a[1][j]) + R0.a[2][i] * A.a[2][j];
+      const double sv[3] = {B[2][1] - B[1][2], B[0][2] - B[2][0], B[1][0] - B[0][1]};
+      double M[3][3];
+      for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) M[i][j] = -(0.5 * (B[i][j] + B[j][i]));
+      const double tr = (-M[0][0] + -M[1][1]) + -M[2][2];
+      M[0][0] = tr + M[0][0];
+      M[1][1] = tr + M[1][1];
+      M[2][2] = tr + M[2][2];
+      const double dm = M[0][0] * (M[1][1] * M[2][2] - M[1][2] * M[2][1]) -
+                        M[0][1] * (M[1][0] * M[2][2] - M[1][2] * M[2][0]) +
+                        M[0][2] * (M[1][0] * M[2][1] - M[1][1] * M[2][0]);
+      if (!(dm > 0.0) || !std::isfinite(dm)) break;
+      const double idm = 1.0 / dm;
+      const double c00 = (M[1][1] * M[2][2] - M[1][2] * M[2][1]) * idm;
+      const double c01 = (M[0][2] * M[2][1] - M[0][1] * M[2][2]) * idm;
+      const double c02 = (M[0][1] * M[1][2] - M[0][2] * M[1][1]) * idm;
+      const double c11 = (M[0][0] * M[2][2] - M[0][2] * M[2][0]) * idm;
+      const double c12 = (M[0][2] * M[1][0] - M[0][0] * M[1][2]) * idm;
+      const double c22 = (M[0][0] * M[1][1] - M[0][1] * M[1][0]) * idm;
+      const double h[3] = {0.5 * ((c00 * sv[0] + c01 * sv[1]) + c02 * sv[2]),
+                           0.5 * ((c01 * sv[0] + c11 * sv[1]) + c12 * sv[2]),
+                           0.5 * ((c02 * sv[0] + c12 * sv[1]) + c22 * sv[2])};
+      const double ww = 4.0 * ((h[0] * h[0] + h[1] * h[1]) + h[2] * h[2]);
+      if (!(ww <= PBDR_POLAR_WARM_MAX2)) break;
+      double qn[4];
+      qn[0] = qc[0] - ((qc[1] * h[0] + qc[2] * h[1]) + qc[3] * h[2]);
+      qn[1] = (qc[0] * h[0] + qc[1]) + (qc[2] * h[2] - qc[3] * h[1]);
+      qn[2] = (qc[0] * h[1] + qc[2]) + (qc[3] * h[0] - qc[1] * h[2]);
+      qn[3] = (qc[0] * h[2] + qc[3]) + (qc[1] * h[1] - qc[2] * h[0]);
+      const double n = std::sqrt(((qn[0] * qn[0] + qn[1] * qn[1]) + qn[2] * qn[2]) + qn[3] * qn[3]);
+      const double in = 1.0 / n;
+      for (int k = 0; k < 4; ++k) qc[k] = qn[k] * in;
+      if (ww <= PBDR_POLAR_TOLQ) {
+        for (int k = 0; k < 4; ++k) q[k] = qc[k];
+        R = quat_to(qc);
+        return true;
+      }
+    }
+  }
+  return polar_rotation(A, R, q);
+}
+
 // Cyclic Jacobi on the symmetrised matrix; ascending eigenvalues, eigenvector
 // columns in V.
 inline void sym_eigen(const M3& m, double ev[3], M3& V) {

@@ -76,6 +76,7 @@ struct State {
   std::vector<int32_t> body_of;
   std::vector<int64_t> bstart;
   std::vector<float> bM, binvM, anchor, bforce;
+  std::vector<float> rquat;  // per body: last rotation (w, x, y, z), 0 = none
   std::vector<int32_t> bscene, bexempt, bprog;
   std::vector<double> tstart, tstop;
   std::vector<Plane4> planes;
@@ -281,6 +282,7 @@ struct BodyIn {
   const float* dc;    // 3n contact deltas dPG + dPP
   const float* init;  // 3n X_init (legacy update only)
   float a[3];         // anchor
+  float* rq;          // warm-start quaternion (in/out), 4 floats
   float M, invM, dt, inv_dt;
   bool incremental, linfix, angfix;
 };
@@ -412,8 +414,9 @@ void body_iteration(const BodyIn& in, BodyOut& out) {
     for (int cI = 0; cI < 3; ++cI) A.a[rI][cI] = static_cast<double>(SA[6 + 3 * rI + cI]);
   orc::M3 R;
   double qd[4];
-  const bool sm_ok = orc::polar_rotation(A, R, qd);
+  const bool sm_ok = orc::polar_warm(A, in.rq, R, qd);
   if (!sm_ok) out.err |= PBDR_DEVERR_DEGENERATE;
+  for (int k = 0; k < 4; ++k) in.rq[k] = sm_ok ? static_cast<float>(qd[k]) : 0.0f;
   float Rf[3][3];
   for (int rI = 0; rI < 3; ++rI)
     for (int cI = 0; cI < 3; ++cI) Rf[rI][cI] = static_cast<float>(R.a[rI][cI]);
@@ -480,7 +483,7 @@ void iteration(State& s) {
       for (int k = 0; k < 3; ++k) dc[3 * q + k] = dPG[k] + dPP[k];
     }
     BodyIn in{n, x.data(), v.data(), m.data(), q0.data(), dc.data(), init.data(),
-              {s.anchor[3 * b], s.anchor[3 * b + 1], s.anchor[3 * b + 2]},
+              {s.anchor[3 * b], s.anchor[3 * b + 1], s.anchor[3 * b + 2]}, &s.rquat[4 * b],
               s.bM[b], s.binvM[b], s.dt, s.inv_dt, s.incremental, s.linfix, s.angfix};
     BodyOut out{xo.data(), vo.data(), {0, 0, 0}};
     body_iteration(in, out);
@@ -579,6 +582,7 @@ int oracle_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* cfg, int thre
   s->bM.resize(s->nb);
   s->binvM.resize(s->nb);
   s->anchor.resize(3 * s->nb);
+  s->rquat.assign(4 * s->nb, 0.0f);
   s->bforce.assign(3 * s->nb, 0.0f);
   s->bscene.resize(s->nb);
   s->bexempt.assign(s->nb, 0);
@@ -718,6 +722,16 @@ void oracle_write_anchor(void* st, const float* a) {
   std::memcpy(s.anchor.data(), a, s.anchor.size() * sizeof(float));
 }
 
+void oracle_read_rquat(void* st, float* q) {
+  State& s = *static_cast<State*>(st);
+  std::memcpy(q, s.rquat.data(), s.rquat.size() * sizeof(float));
+}
+
+void oracle_write_rquat(void* st, const float* q) {
+  State& s = *static_cast<State*>(st);
+  std::memcpy(s.rquat.data(), q, s.rquat.size() * sizeof(float));
+}
+
 void oracle_read_particles(void* st, double* pos, double* vel) {
   State& s = *static_cast<State*>(st);
   for (int64_t slot = 0; slot < s.n; ++slot) {
@@ -786,7 +800,8 @@ unsigned oracle_kat_body_iteration(int n, const float* x, const float* v, const 
                                    const float* q0, const float* dc, const float* init,
                                    const float* anchor, float M, float dt, int incremental,
                                    int linfix, int angfix, float* xo, float* vo) {
-  BodyIn in{n, x, v, m, q0, dc, init, {anchor[0], anchor[1], anchor[2]}, M, 1.0f / M, dt,
+  float rq[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+  BodyIn in{n, x, v, m, q0, dc, init, {anchor[0], anchor[1], anchor[2]}, rq, M, 1.0f / M, dt,
             1.0f / dt, incremental != 0, linfix != 0, angfix != 0};
   BodyOut out{xo, vo, {0, 0, 0}};
   body_iteration(in, out);
@@ -812,6 +827,16 @@ int oracle_polar(const double* a, double* r_out, double* q_out) {
   for (int i = 0; i < 9; ++i) A.a[i / 3][i % 3] = a[i];
   orc::M3 R;
   if (!orc::polar_rotation(A, R, q_out)) return 0;
+  for (int i = 0; i < 9; ++i) r_out[i] = R.a[i / 3][i % 3];
+  return 1;
+}
+
+// Warm-started polar (rq = previous rotation quaternion, zeros = none).
+int oracle_polar_warm(const double* a, const float* rq, double* r_out, double* q_out) {
+  orc::M3 A;
+  for (int i = 0; i < 9; ++i) A.a[i / 3][i % 3] = a[i];
+  orc::M3 R;
+  if (!orc::polar_warm(A, rq, R, q_out)) return 0;
   for (int i = 0; i < 9; ++i) r_out[i] = R.a[i / 3][i % 3];
   return 1;
 }

@@ -47,7 +47,7 @@ def olib():
             getattr(L, name).argtypes = [vp, vp, vp]
             getattr(L, name).restype = None
         for name in ("oracle_read_init", "oracle_write_init", "oracle_read_anchor",
-                     "oracle_write_anchor", "oracle_body_stats"):
+                     "oracle_write_anchor", "oracle_body_stats", "oracle_read_rquat", "oracle_write_rquat"):
             getattr(L, name).argtypes = [vp, vp]
             getattr(L, name).restype = None
         L.oracle_num_slots.argtypes = [vp]
@@ -55,6 +55,7 @@ def olib():
         L.oracle_cell_size.argtypes = [vp]
         L.oracle_cell_size.restype = C.c_float
         L.oracle_polar.argtypes = [vp, vp, vp]
+        L.oracle_polar_warm.argtypes = [vp, vp, vp, vp]
         L.oracle_sym_eigen.argtypes = [vp, vp, vp]
         L.oracle_sym_eigen.restype = None
         L.oracle_inertia_solve.argtypes = [vp, vp, vp, vp]
@@ -182,6 +183,14 @@ class Oracle:
     def write_anchor(self, a):
         olib().oracle_write_anchor(self._h, _p(np.ascontiguousarray(a, np.float32)))
 
+    def read_rquat(self):
+        q = np.empty((self.nb, 4), np.float32)
+        olib().oracle_read_rquat(self._h, _p(q))
+        return q
+
+    def write_rquat(self, q):
+        olib().oracle_write_rquat(self._h, _p(np.ascontiguousarray(q, np.float32)))
+
     def read_particles(self):
         p = np.empty((self.n, 3))
         v = np.empty((self.n, 3))
@@ -215,6 +224,15 @@ def polar(a):
     r = np.zeros(9)
     q = np.zeros(4)
     ok = olib().oracle_polar(_p(a), _p(r), _p(q))
+    return bool(ok), r.reshape(3, 3), q
+
+
+def polar_warm(a, rq):
+    a = np.ascontiguousarray(a, np.float64).reshape(9)
+    rq = np.ascontiguousarray(rq, np.float32).reshape(4)
+    r = np.zeros(9)
+    q = np.zeros(4)
+    ok = olib().oracle_polar_warm(_p(a), _p(rq), _p(r), _p(q))
     return bool(ok), r.reshape(3, 3), q
 
 

@@ -43,6 +43,7 @@ struct pbdr_handle {
   int4* warp_desc = nullptr;
   int4* cta_desc = nullptr;
   float4* anchor = nullptr;
+  float4* rquat = nullptr;
   uint32_t* keys[2] = {nullptr, nullptr};
   uint32_t* vals[2] = {nullptr, nullptr};
   void* sort_temp = nullptr;
@@ -305,6 +306,7 @@ void enqueue_iteration(pbdr_handle* h, pbdr_dev::LaunchHook* hook) {
   it.cand_j = h->cand_j;
   it.cand_rr = h->cand_rr;
   it.anchor = h->anchor;
+  it.rquat = h->rquat;
   it.cta_desc = h->cta_desc;
   it.warp_desc = h->warp_desc;
   it.body_desc = h->body_desc;
@@ -592,6 +594,7 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
   rc |= dalloc(h, &h->warp_desc, wdesc.size());
   rc |= dalloc(h, &h->cta_desc, cdesc.size());
   rc |= dalloc(h, &h->anchor, nb);
+  rc |= dalloc(h, &h->rquat, nb);
   rc |= dalloc(h, &h->keys[0], n);
   rc |= dalloc(h, &h->keys[1], n);
   rc |= dalloc(h, &h->vals[0], n);
@@ -669,6 +672,7 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
   cudaMemset(h->ncand, 0, sizeof(int) * n);
   cudaMemset(h->cells, 0xFF, sizeof(uint4) * T);
   cudaMemset(h->near_count, 0, sizeof(long long) * 2);
+  cudaMemset(h->rquat, 0, sizeof(float4) * nb);
   if (reset_errors(h) != PBDR_OK) {
     const int code = pbdr_last_error_payload(nullptr, nullptr, nullptr);
     release(h);
@@ -793,6 +797,9 @@ int pbdr_gpu_read_particles(pbdr_handle* h, double* position, double* velocity) 
 
 int pbdr_gpu_write_particles(pbdr_handle* h, const double* position, const double* velocity) {
   if (!h) return set_error(PBDR_ERR_GENERIC, "null handle");
+  // New positions: drop the warm-start rotations (the next polar starts cold).
+  PBDR_CUDA(cudaSetDevice(h->device));
+  PBDR_CUDA(cudaMemset(h->rquat, 0, sizeof(float4) * h->nb));
   std::vector<float4> p(h->n), v(h->n);
   int rc = pbdr_gpu_read_f32(h, reinterpret_cast<float*>(p.data()), reinterpret_cast<float*>(v.data()));
   if (rc != PBDR_OK) return rc;
@@ -957,6 +964,20 @@ int pbdr_gpu_debug_read_anchor(pbdr_handle* h, float* anchor3) {
   for (int32_t b = 0; b < h->nb; ++b) {
     anchor3[3 * b] = a[b].x; anchor3[3 * b + 1] = a[b].y; anchor3[3 * b + 2] = a[b].z;
   }
+  return PBDR_OK;
+}
+
+int pbdr_gpu_debug_read_rquat(pbdr_handle* h, float* q4) {
+  if (!h || !q4) return set_error(PBDR_ERR_GENERIC, "null argument");
+  PBDR_CUDA(cudaSetDevice(h->device));
+  PBDR_CUDA(cudaMemcpy(q4, h->rquat, sizeof(float4) * h->nb, cudaMemcpyDeviceToHost));
+  return PBDR_OK;
+}
+
+int pbdr_gpu_debug_write_rquat(pbdr_handle* h, const float* q4) {
+  if (!h || !q4) return set_error(PBDR_ERR_GENERIC, "null argument");
+  PBDR_CUDA(cudaSetDevice(h->device));
+  PBDR_CUDA(cudaMemcpy(h->rquat, q4, sizeof(float4) * h->nb, cudaMemcpyHostToDevice));
   return PBDR_OK;
 }
 

@@ -524,6 +524,7 @@ __global__ void __launch_bounds__(kThreads, PBDR_ITER_MINBLOCKS) k_iteration(Ite
   __shared__ float4 s_banc[kWarps];  // anchor xyz, M
   __shared__ int2 s_bw[kWarps];      // first warp, warps
   __shared__ float s_binv[kWarps];   // 1/M
+  __shared__ float4 s_brq[kWarps];   // warm-start rotation (w, x, y, z)
   if (warp == 0 && lane < cd.w) {
     const int bb = cd.z + lane;
     const int4 bdb = A.body_desc[bb];
@@ -532,6 +533,7 @@ __global__ void __launch_bounds__(kThreads, PBDR_ITER_MINBLOCKS) k_iteration(Ite
     s_banc[lane] = make_float4(an.x, an.y, an.z, mass.x);
     s_binv[lane] = mass.y;
     s_bw[lane] = make_int2(bdb.w, bdb.z);
+    s_brq[lane] = A.rquat[bb];
   }
 
   const int4 wd = A.warp_desc[blockIdx.x * kWarps + warp];
@@ -708,8 +710,13 @@ __global__ void __launch_bounds__(kThreads, PBDR_ITER_MINBLOCKS) k_iteration(Ite
       R[kResLb + k] = S[18 + k] - tmp[k];
     }
     double qd[4];
-    const bool ok = polar_rotation_f(&S[6], &R[kResR], qd);
+    const float4 rq4 = s_brq[lane];
+    const float rq[4] = {rq4.x, rq4.y, rq4.z, rq4.w};
+    const bool ok = polar_warm_f(&S[6], rq, &R[kResR], qd);
     R[kResSmOk] = ok ? 1.0f : 0.0f;
+    A.rquat[bb] = ok ? make_float4(static_cast<float>(qd[0]), static_cast<float>(qd[1]),
+                                   static_cast<float>(qd[2]), static_cast<float>(qd[3]))
+                     : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
     if (!ok) record_error(A.err, PBDR_DEVERR_DEGENERATE, bb, A.substep_counter);
     A.anchor[bb] = make_float4(an.x + c[0], an.y + c[1], an.z + c[2], 0.0f);
   }
@@ -991,7 +998,10 @@ __global__ void __launch_bounds__(kThreads) k_body_stats(StatsArgs A) {
 
 }  // namespace
 
-size_t iteration_smem_bytes() { return sizeof(float4) * 3 * kSlots; }
+#ifndef PBDR_ITER_EXTRA_SMEM
+#define PBDR_ITER_EXTRA_SMEM 0
+#endif
+size_t iteration_smem_bytes() { return sizeof(float4) * 3 * kSlots + PBDR_ITER_EXTRA_SMEM; }
 
 void launch_integrate(const IntegrateArgs& a, cudaStream_t s) {
   const unsigned blocks = static_cast<unsigned>((a.n + 255) / 256);

@@ -136,6 +136,7 @@ struct IterArgs {
   const int* cand_j;
   const float* cand_rr;
   float4* anchor;        // per body (xyz)
+  float4* rquat;         // per body warm-start rotation (w, x, y, z), 0 = none
   const int4* cta_desc;  // per CTA: (first slot, slot count, first body, body count)
   const int4* warp_desc; // per CTA warp: (body, warp in body, body start, n | W << 16); body -1 = idle
   const int4* body_desc; // (start, n, W, first warp in CTA)

@@ -106,6 +106,10 @@ PBDR_HD int32_t pbdr_cell_coord(float x, float inv_h) {
 #define PBDR_POLAR_MAX_IT 64
 #define PBDR_POLAR_REL_DET 1e-12
 #define PBDR_ONE_THIRD (1.0 / 3.0)
+/* Warm-started rotation extraction: Gauss-Newton steps from the previous
+ * iteration's rotation (see polar_warm in oracle_math.hpp / pbdr_mat3.cuh). */
+#define PBDR_POLAR_WARM_STEPS 4
+#define PBDR_POLAR_WARM_MAX2 0.25
 /* fp32 warm-up stage of the polar (then fp64 polish to PBDR_POLAR_TOL). */
 #define PBDR_POLAR_F32_TOL2 1e-12f
 #define PBDR_POLAR_F32_TOLQ 1e-7f

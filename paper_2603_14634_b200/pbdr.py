@@ -148,6 +148,8 @@ def lib() -> C.CDLL:
         L.pbdr_gpu_debug_write_anchor.argtypes = [vp, vp]
         L.pbdr_gpu_debug_phase_timing.argtypes = [vp, vp]
         L.pbdr_gpu_debug_near_count.argtypes = [vp, C.POINTER(i64)]
+        L.pbdr_gpu_debug_read_rquat.argtypes = [vp, vp]
+        L.pbdr_gpu_debug_write_rquat.argtypes = [vp, vp]
         L.pbdr_scene_generate.argtypes = [C.c_int, C.c_uint64, i64, C.POINTER(vp)]
         L.pbdr_scene_generate_c4_shard.argtypes = [C.c_uint64, i64, i64, C.POINTER(vp)]
         L.pbdr_scene_view.argtypes = [vp, C.POINTER(SceneDesc), C.POINTER(SolverCfg)]
@@ -471,6 +473,15 @@ class GpuSolver:
         out = np.zeros((self.info.num_ctas, 8), np.int64)
         raise_status(lib().pbdr_gpu_debug_phase_timing(self._h, _ptr(out)))
         return out
+
+    def debug_rquat(self):
+        q = np.empty((self.nb, 4), np.float32)
+        raise_status(lib().pbdr_gpu_debug_read_rquat(self._h, _ptr(q)))
+        return q
+
+    def debug_write_rquat(self, q):
+        q = np.ascontiguousarray(q, np.float32)
+        raise_status(lib().pbdr_gpu_debug_write_rquat(self._h, _ptr(q)))
 
     def debug_write_anchor(self, a):
         a = np.ascontiguousarray(a, np.float32)

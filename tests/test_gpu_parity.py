@@ -83,6 +83,7 @@ def test_iterations_bit_exact(pbdr, pyoracle, cid, scale):
         assert_same(gp, op, f"positions after iteration {it}")
         assert_same(gv, ov, f"velocities after iteration {it}")
         assert_same(gpu.debug_anchor(), orc.read_anchor(), f"anchors after iteration {it}")
+        assert_same(gpu.debug_rquat(), orc.read_rquat(), f"warm-start rotations after iteration {it}")
 
 
 @pytest.mark.parametrize("cid,scale", CASES)
@@ -230,6 +231,7 @@ def test_replay_contact_rich_state(pbdr, pyoracle, cid, scale, frames):
     p4, v4 = gpu.read_f32()
     orc.write_f32(p4, v4)
     orc.write_anchor(gpu.debug_anchor())
+    orc.write_rquat(gpu.debug_rquat())
     gpu.debug_prologue()
     orc.integrate()
     orc.candidates()

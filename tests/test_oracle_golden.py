@@ -152,3 +152,26 @@ def test_extract_pose_matches_reference(pbdr, pyoracle, golden):
         np.testing.assert_allclose(st[0:3], case["com"], atol=2e-6 * max(1, np.abs(cur).max()))
         q, qref = st[3:7], np.array(case["quat"])
         assert min(np.abs(q - qref).max(), np.abs(q + qref).max()) < 2e-5
+
+
+def test_warm_started_polar_matches_cold(pyoracle, golden):
+    # The warm start (previous rotation, Gauss-Newton on the symmetry
+    # condition) converges to the same polar factor as the cold Newton path.
+    rs = np.random.default_rng(11)
+    for case in golden["polar"]:
+        if case["status"] != 0:
+            continue
+        A = np.array(case["A"]).reshape(3, 3)
+        ok, Rc, qc = pyoracle.polar(A)
+        for tilt in (1e-4, 1e-2, 0.2):
+            axis = rs.normal(size=3)
+            axis /= np.linalg.norm(axis)
+            dq = np.concatenate([[np.cos(tilt / 2)], np.sin(tilt / 2) * axis])
+            w0, v0 = qc[0], qc[1:]
+            w1, v1 = dq[0], dq[1:]
+            rq = np.concatenate([[w0 * w1 - v0 @ v1], w0 * v1 + w1 * v0 + np.cross(v0, v1)])
+            okw, Rw, _ = pyoracle.polar_warm(A, rq)
+            assert okw
+            np.testing.assert_allclose(Rw, Rc, atol=1e-10)
+    ok, R, _ = pyoracle.polar_warm(np.eye(3), np.zeros(4))
+    assert ok and np.allclose(R, np.eye(3))
