@@ -141,10 +141,12 @@ def workload(args, rank, world):
     from paper_2603_14634_b200 import pbdr as P
     cid = args.config
     if cid == 4:
-        per_rank = args.scale if args.scale > 0 else 4096
-        g = P.GeneratedScene(4, seed=args.seed, scale=per_rank, c4_first_scene=rank * per_rank)
+        from paper_2603_14634_b200 import shard as S
+        sh = S.c4_shard(rank, world, args.scale if args.scale > 0 else 4096)
+        g = S.generate_c4_shard(sh, seed=args.seed)
         name = P.CONFIG_NAMES[4]
-        extra = {"scenes_per_gpu": per_rank, "scenes_total": per_rank * world, "parallelism": f"scene-shard x{world}"}
+        extra = {"scenes_per_gpu": sh.scenes_per_rank, "scenes_total": sh.total_scenes,
+                 "parallelism": f"scene-shard x{world} (no collective in the data path)"}
     else:
         g = P.GeneratedScene(cid, seed=args.seed, scale=args.scale)
         name = P.CONFIG_NAMES[cid]
