@@ -77,7 +77,14 @@ struct State {
   std::vector<int64_t> bstart;
   std::vector<float> bM, binvM, anchor, bforce;
   std::vector<float> rquat;  // per body: last rotation (w, x, y, z), 0 = none
+  std::vector<float> mom_acc;  // per body kPerSubstep accumulators (P, L)
+  bool per_substep = false;
+  bool any_torque = false;
+  int iter_in_substep = 0;
   std::vector<int32_t> bscene, bexempt, bprog;
+  std::vector<float> btorque;       // 3 per body
+  std::vector<int32_t> btorque_on;  // nonzero torque program
+  std::vector<float> wcom, walpha;  // 3 per body: com and alpha at the substep start
   std::vector<double> tstart, tstop;
   std::vector<Plane4> planes;
   float dt = 0, inv_dt = 0, g = 0, relax = 1, h = 0, inv_h = 0, h2 = 0;
@@ -140,16 +147,71 @@ inline void cross3(const float a[3], const float b[3], float o[3]) {
 }
 
 // ---- integrate ---------------------------
+// distribute_wrench (body.cpp:126-150): alpha = pinv(I) tau with the com and
+// inertia of X at the substep start, anchored fp32 sums in the pinned tree.
+void wrench_prepass(State& s) {
+#pragma omp parallel for num_threads(s.threads) schedule(dynamic, 8)
+  for (int32_t b = 0; b < s.nb; ++b) {
+    if (!s.btorque_on[b]) continue;
+    const int64_t start = s.bstart[b];
+    const int n = static_cast<int>(s.bstart[b + 1] - start);
+    const float a[3] = {s.anchor[3 * b], s.anchor[3 * b + 1], s.anchor[3 * b + 2]};
+    std::vector<float> vals(9 * static_cast<size_t>(n));
+    for (int q = 0; q < n; ++q) {
+      const int64_t p = start + q;
+      const float mk = s.vel[4 * p + 3];
+      const float pp[3] = {s.pos[4 * p] - a[0], s.pos[4 * p + 1] - a[1], s.pos[4 * p + 2] - a[2]};
+      const float s2 = (pp[0] * pp[0] + pp[1] * pp[1]) + pp[2] * pp[2];
+      float* o = &vals[9 * static_cast<size_t>(q)];
+      o[0] = mk * pp[0]; o[1] = mk * pp[1]; o[2] = mk * pp[2];
+      o[3] = mk * (s2 - pp[0] * pp[0]);
+      o[4] = mk * (s2 - pp[1] * pp[1]);
+      o[5] = mk * (s2 - pp[2] * pp[2]);
+      o[6] = -(mk * (pp[0] * pp[1]));
+      o[7] = -(mk * (pp[0] * pp[2]));
+      o[8] = -(mk * (pp[1] * pp[2]));
+    }
+    float S[9] = {};
+    tree_sum<9>(n, vals.data(), S);
+    const float M = s.bM[b], invM = s.binvM[b];
+    float c[3];
+    for (int k = 0; k < 3; ++k) c[k] = S[k] * invM;
+    const float Ixx = S[3] - M * (c[1] * c[1] + c[2] * c[2]);
+    const float Iyy = S[4] - M * (c[0] * c[0] + c[2] * c[2]);
+    const float Izz = S[5] - M * (c[0] * c[0] + c[1] * c[1]);
+    const float Ixy = S[6] + M * (c[0] * c[1]);
+    const float Ixz = S[7] + M * (c[0] * c[2]);
+    const float Iyz = S[8] + M * (c[1] * c[2]);
+    orc::M3 I = {{{Ixx, Ixy, Ixz}, {Ixy, Iyy, Iyz}, {Ixz, Iyz, Izz}}};
+    const double tau[3] = {s.btorque[3 * b], s.btorque[3 * b + 1], s.btorque[3 * b + 2]};
+    double al[3], nax[3];
+    const unsigned e = orc::inertia_solve(I, tau, al, nax);
+    if (e) flag(s, e, b, nax);
+    for (int k = 0; k < 3; ++k) {
+      s.wcom[3 * b + k] = a[k] + c[k];
+      s.walpha[3 * b + k] = static_cast<float>(al[k]);
+    }
+  }
+}
+
 void integrate(State& s) {
+  s.iter_in_substep = 0;
+  if (s.any_torque) wrench_prepass(s);
   const double t = static_cast<double>(s.substep_index) * s.dt_d;
 #pragma omp parallel for num_threads(s.threads) schedule(static)
   for (int64_t p = 0; p < s.n; ++p) {
     const int32_t b = s.body_of[p];
     float a[3] = {0.0f, 0.0f, s.bexempt[b] ? 0.0f : -s.g};
+    float* x = &s.pos[4 * p];
     if (s.bprog[b] && t >= s.tstart[b] && t < s.tstop[b]) {
       for (int k = 0; k < 3; ++k) a[k] = a[k] + s.bforce[3 * b + k] * s.binvM[b];
+      if (s.btorque_on[b]) {
+        const float r[3] = {x[0] - s.wcom[3 * b], x[1] - s.wcom[3 * b + 1], x[2] - s.wcom[3 * b + 2]};
+        float ar[3];
+        cross3(&s.walpha[3 * b], r, ar);
+        for (int k = 0; k < 3; ++k) a[k] = a[k] + ar[k];
+      }
     }
-    float* x = &s.pos[4 * p];
     float* v = &s.vel[4 * p];
     float* xi = &s.init[4 * p];
     for (int k = 0; k < 3; ++k) {
@@ -285,6 +347,9 @@ struct BodyIn {
   float* rq;          // warm-start quaternion (in/out), 4 floats
   float M, invM, dt, inv_dt;
   bool incremental, linfix, angfix;
+  float* acc = nullptr;  // kPerSubstep accumulators (6 floats) or null
+  bool reset = false;    // first iteration of the substep
+  bool last = true;      // last iteration of the substep
 };
 
 struct BodyOut {
@@ -298,10 +363,14 @@ struct BodyOut {
 // Momentum enforcement (Eq. 1 then Eq. 2).
 // Inputs are the asm state (xa, va), its anchored positions pa, the per-particle
 // update dX (so c_asm = c + sum m dX / M) and the bsm momenta.
+// kPerSubstep (acc != null): the SM-induced changes (P_bsm - P_asm,
+// L_asm - L_bsm) are accumulated over the substep's iterations (acc reset at
+// iteration 0) and corrected once, in the last iteration (correct == true).
 void momentum_fix(int n, const float* m, const float* xa, const float* va, const float* pa,
                   const float* dX, const float c[3], const float Pb[3], const float Lb[3], float M,
                   float invM, float dt, bool linfix, bool angfix, float* xo, float* vo,
-                  unsigned& err, double axis[3]) {
+                  unsigned& err, double axis[3], float* acc = nullptr, bool reset = false,
+                  bool last = true) {
   std::vector<float> vals(15 * static_cast<size_t>(n));
   for (int q = 0; q < n; ++q) {
     const float mk = m[q];
@@ -333,9 +402,26 @@ void momentum_fix(int n, const float* m, const float* xa, const float* va, const
   }
   cross3(ca, Pa, tmp);
   for (int k = 0; k < 3; ++k) La[k] = SB[6 + k] - tmp[k];
-  if (linfix)
-    for (int k = 0; k < 3; ++k) dv[k] = (Pb[k] - Pa[k]) * invM;
-  if (angfix) {
+  float dP[3], dLf[3];
+  for (int k = 0; k < 3; ++k) {
+    dP[k] = Pb[k] - Pa[k];
+    dLf[k] = La[k] - Lb[k];
+  }
+  bool correct = true;
+  if (acc) {
+    for (int k = 0; k < 3; ++k) {
+      const float p0 = reset ? 0.0f : acc[k];
+      const float l0 = reset ? 0.0f : acc[3 + k];
+      acc[k] = p0 + dP[k];
+      acc[3 + k] = l0 + dLf[k];
+      dP[k] = acc[k];
+      dLf[k] = acc[3 + k];
+    }
+    correct = last;
+  }
+  if (linfix && correct)
+    for (int k = 0; k < 3; ++k) dv[k] = dP[k] * invM;
+  if (angfix && correct) {
     const float Ixx = SB[9] - M * (ca[1] * ca[1] + ca[2] * ca[2]);
     const float Iyy = SB[10] - M * (ca[0] * ca[0] + ca[2] * ca[2]);
     const float Izz = SB[11] - M * (ca[0] * ca[0] + ca[1] * ca[1]);
@@ -343,8 +429,8 @@ void momentum_fix(int n, const float* m, const float* xa, const float* va, const
     const float Ixz = SB[13] + M * (ca[0] * ca[2]);
     const float Iyz = SB[14] + M * (ca[1] * ca[2]);
     orc::M3 I = {{{Ixx, Ixy, Ixz}, {Ixy, Iyy, Iyz}, {Ixz, Iyz, Izz}}};
-    const double dL[3] = {static_cast<double>(La[0] - Lb[0]), static_cast<double>(La[1] - Lb[1]),
-                          static_cast<double>(La[2] - Lb[2])};
+    const double dL[3] = {static_cast<double>(dLf[0]), static_cast<double>(dLf[1]),
+                          static_cast<double>(dLf[2])};
     double wd[3];
     const unsigned e = orc::inertia_solve(I, dL, wd, axis);
     err |= e;
@@ -446,7 +532,7 @@ void body_iteration(const BodyIn& in, BodyOut& out) {
   }
   if (in.linfix || in.angfix) {
     momentum_fix(n, in.m, xa.data(), va.data(), pa.data(), dXv.data(), c, Pb, Lb, in.M, in.invM,
-                 in.dt, in.linfix, in.angfix, out.x, out.v, out.err, out.axis);
+                 in.dt, in.linfix, in.angfix, out.x, out.v, out.err, out.axis, in.acc, in.reset, in.last);
   } else {
     std::memcpy(out.x, xa.data(), sizeof(float) * 3 * n);
     std::memcpy(out.v, va.data(), sizeof(float) * 3 * n);
@@ -485,6 +571,11 @@ void iteration(State& s) {
     BodyIn in{n, x.data(), v.data(), m.data(), q0.data(), dc.data(), init.data(),
               {s.anchor[3 * b], s.anchor[3 * b + 1], s.anchor[3 * b + 2]}, &s.rquat[4 * b],
               s.bM[b], s.binvM[b], s.dt, s.inv_dt, s.incremental, s.linfix, s.angfix};
+    if (s.per_substep) {
+      in.acc = &s.mom_acc[6 * b];
+      in.reset = s.iter_in_substep == 0;
+      in.last = s.iter_in_substep == s.iters - 1;
+    }
     BodyOut out{xo.data(), vo.data(), {0, 0, 0}};
     body_iteration(in, out);
     if (out.err) flag(s, out.err, b, out.axis);
@@ -497,6 +588,7 @@ void iteration(State& s) {
     }
     for (int k = 0; k < 3; ++k) s.anchor[3 * b + k] = in.a[k] + out.c[k];
   }
+  ++s.iter_in_substep;
 }
 
 // ---- per-body trajectory sample (body.cpp:72-83, 103-124) --------------------
@@ -583,7 +675,12 @@ int oracle_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* cfg, int thre
   s->binvM.resize(s->nb);
   s->anchor.resize(3 * s->nb);
   s->rquat.assign(4 * s->nb, 0.0f);
+  s->mom_acc.assign(6 * s->nb, 0.0f);
   s->bforce.assign(3 * s->nb, 0.0f);
+  s->btorque.assign(3 * s->nb, 0.0f);
+  s->btorque_on.assign(s->nb, 0);
+  s->wcom.assign(3 * s->nb, 0.0f);
+  s->walpha.assign(3 * s->nb, 0.0f);
   s->bscene.resize(s->nb);
   s->bexempt.assign(s->nb, 0);
   s->bprog.assign(s->nb, 0);
@@ -618,7 +715,12 @@ int oracle_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* cfg, int thre
       s->bprog[b] = 1;
       s->tstart[b] = pr.t_start;
       s->tstop[b] = pr.t_stop;
-      for (int c = 0; c < 3; ++c) s->bforce[3 * b + c] = static_cast<float>(pr.force[c]);
+      for (int c = 0; c < 3; ++c) {
+        s->bforce[3 * b + c] = static_cast<float>(pr.force[c]);
+        s->btorque[3 * b + c] = static_cast<float>(pr.torque[c]);
+      }
+      s->btorque_on[b] = (pr.torque[0] != 0.0 || pr.torque[1] != 0.0 || pr.torque[2] != 0.0) ? 1 : 0;
+      s->any_torque = s->any_torque || s->btorque_on[b];
     }
   }
   s->bstart[s->nb] = slot;
@@ -654,6 +756,7 @@ int oracle_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* cfg, int thre
   s->incremental = cfg->velocity_update == PBDR_VELOCITY_INCREMENTAL;
   s->linfix = cfg->linear_momentum_fix != 0;
   s->angfix = cfg->angular_momentum_fix != 0;
+  s->per_substep = cfg->momentum_frequency == PBDR_MOMENTUM_PER_SUBSTEP;
   s->h = static_cast<float>(2.0 * rmax);
   s->inv_h = 1.0f / s->h;
   s->h2 = s->h * s->h;

@@ -44,6 +44,12 @@ struct pbdr_handle {
   int4* cta_desc = nullptr;
   float4* anchor = nullptr;
   float4* rquat = nullptr;
+  float4* mom_acc = nullptr;
+  float4* wcom = nullptr;    // torque programs: per-body com and alpha
+  float4* walpha = nullptr;
+  bool has_torque = false;
+  int per_substep = 0;
+  int debug_iter = 0;  // iteration index for the replay hook
   uint32_t* keys[2] = {nullptr, nullptr};
   uint32_t* vals[2] = {nullptr, nullptr};
   void* sort_temp = nullptr;
@@ -177,6 +183,8 @@ void enqueue_substep(pbdr_handle* h, pbdr_dev::LaunchHook* hook) {
   ia.programs = h->programs;
   ia.body_mass = h->body_mass;
   ia.key_all = h->key_all;
+  ia.wcom = h->wcom;
+  ia.walpha = h->walpha;
   ia.box_min = h->box_min;
   ia.box_max = h->box_max;
   ia.substep_counter = h->counter;
@@ -196,6 +204,24 @@ void enqueue_substep(pbdr_handle* h, pbdr_dev::LaunchHook* hook) {
   if (hook) hook->before(kHookRanges);
   launch_cell_clear(h->cells, h->keys[h->sorted_buf], h->near_count + 1, h->n, h->stream);
   if (hook) hook->after(kHookRanges);
+  if (h->has_torque) {
+    WrenchArgs wa{};
+    wa.pos = h->pos[h->cur];
+    wa.vel = h->vel;
+    wa.anchor = h->anchor;
+    wa.cta_desc = h->cta_desc;
+    wa.warp_desc = h->warp_desc;
+    wa.body_mass = h->body_mass;
+    wa.body_desc = h->body_desc;
+    wa.programs = h->programs;
+    wa.wcom = h->wcom;
+    wa.walpha = h->walpha;
+    wa.err = h->err;
+    wa.substep_counter = h->counter;
+    if (hook) hook->before(kHookIntegrate);
+    launch_wrench(wa, h->ctas, h->stream);
+    if (hook) hook->after(kHookIntegrate);
+  }
   if (hook) hook->before(kHookIntegrate);
   launch_integrate(ia, h->stream);
   if (hook) hook->after(kHookIntegrate);
@@ -294,7 +320,7 @@ void enqueue_substep(pbdr_handle* h, pbdr_dev::LaunchHook* hook) {
   if (hook) hook->after(kHookNeighbours);
 }
 
-void enqueue_iteration(pbdr_handle* h, pbdr_dev::LaunchHook* hook) {
+void enqueue_iteration(pbdr_handle* h, int iter_index, pbdr_dev::LaunchHook* hook) {
   using namespace pbdr_dev;
   IterArgs it{};
   it.pos_in = h->pos[h->cur];
@@ -307,6 +333,10 @@ void enqueue_iteration(pbdr_handle* h, pbdr_dev::LaunchHook* hook) {
   it.cand_rr = h->cand_rr;
   it.anchor = h->anchor;
   it.rquat = h->rquat;
+  it.per_substep = h->per_substep;
+  it.iter_index = iter_index;
+  it.last_iter = iter_index == h->iters - 1;
+  it.mom_acc = h->mom_acc;
   it.cta_desc = h->cta_desc;
   it.warp_desc = h->warp_desc;
   it.body_desc = h->body_desc;
@@ -331,7 +361,7 @@ void enqueue_iteration(pbdr_handle* h, pbdr_dev::LaunchHook* hook) {
 void enqueue_substeps(pbdr_handle* h, int64_t count, pbdr_dev::LaunchHook* hook) {
   for (int64_t s = 0; s < count; ++s) {
     enqueue_substep(h, hook);
-    for (int i = 0; i < h->iters; ++i) enqueue_iteration(h, hook);
+    for (int i = 0; i < h->iters; ++i) enqueue_iteration(h, i, hook);
   }
 }
 
@@ -397,9 +427,9 @@ int validate(const pbdr_scene_desc* d, const pbdr_solver_cfg* c) {
   if (c->substeps < 1) return set_config_error("substeps", "must be >= 1");
   if (c->solver_iterations < 1) return set_config_error("solver_iterations", "must be >= 1");
   if (!std::isfinite(c->gravity)) return set_config_error("gravity", "must be finite");
-  if (c->momentum_frequency != PBDR_MOMENTUM_PER_ITERATION)
-    return set_config_error("momentum_frequency",
-                            "kPerSubstep is not implemented on the GPU path yet");
+  if (c->momentum_frequency != PBDR_MOMENTUM_PER_ITERATION &&
+      c->momentum_frequency != PBDR_MOMENTUM_PER_SUBSTEP)
+    return set_config_error("momentum_frequency", "unknown value");
   if (c->velocity_update != PBDR_VELOCITY_LEGACY && c->velocity_update != PBDR_VELOCITY_INCREMENTAL)
     return set_config_error("velocity_update", "unknown mode");
   if (d->num_particles <= 0) return set_config_error("particles", "scene has no particles");
@@ -409,14 +439,6 @@ int validate(const pbdr_scene_desc* d, const pbdr_solver_cfg* c) {
   if (!(d->contact_relaxation >= 0.0)) return set_config_error("contact_relaxation", "must be >= 0");
   const int planes = (d->has_ground ? 1 : 0) + std::max(0, d->num_walls);
   if (planes > PBDR_MAX_PLANES) return set_config_error("walls", "at most 8 planes (ground + walls)");
-  if (d->programs) {
-    for (int32_t b = 0; b < d->num_bodies; ++b) {
-      const pbdr_force_program& p = d->programs[b];
-      if (p.torque[0] != 0.0 || p.torque[1] != 0.0 || p.torque[2] != 0.0)
-        return set_config_error("programs.torque",
-                                "torque programs are not implemented on the GPU path yet");
-    }
-  }
   return PBDR_OK;
 }
 
@@ -526,7 +548,12 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
       bp.fx = static_cast<float>(p.force[0]);
       bp.fy = static_cast<float>(p.force[1]);
       bp.fz = static_cast<float>(p.force[2]);
-      bp.flags = 1 | (p.gravity_exempt ? 2 : 0);
+      bp.tx = static_cast<float>(p.torque[0]);
+      bp.ty = static_cast<float>(p.torque[1]);
+      bp.tz = static_cast<float>(p.torque[2]);
+      const bool torque = p.torque[0] != 0.0 || p.torque[1] != 0.0 || p.torque[2] != 0.0;
+      bp.flags = 1 | (p.gravity_exempt ? 2 : 0) | (torque ? 4 : 0);
+      h->has_torque = h->has_torque || torque;
       bp.t_start = p.t_start;
       bp.t_stop = p.t_stop;
     }
@@ -550,6 +577,7 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
   h->incremental = c->velocity_update == PBDR_VELOCITY_INCREMENTAL;
   h->linfix = c->linear_momentum_fix != 0;
   h->angfix = c->angular_momentum_fix != 0;
+  h->per_substep = c->momentum_frequency == PBDR_MOMENTUM_PER_SUBSTEP;
   h->h = static_cast<float>(2.0 * rmax);
   h->inv_h = 1.0f / h->h;
   h->h2 = h->h * h->h;
@@ -595,6 +623,9 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
   rc |= dalloc(h, &h->cta_desc, cdesc.size());
   rc |= dalloc(h, &h->anchor, nb);
   rc |= dalloc(h, &h->rquat, nb);
+  rc |= dalloc(h, &h->mom_acc, 2 * static_cast<size_t>(nb));
+  rc |= dalloc(h, &h->wcom, nb);
+  rc |= dalloc(h, &h->walpha, nb);
   rc |= dalloc(h, &h->keys[0], n);
   rc |= dalloc(h, &h->keys[1], n);
   rc |= dalloc(h, &h->vals[0], n);
@@ -679,7 +710,8 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
     return code;
   }
   h->launches_per_frame = static_cast<int64_t>(h->substeps) *
-                          (1 + 1 + 1 + 2 + h->bpasses + 2 + 3 + 2 + h->passes + 1 + 1 + h->iters);
+                          ((h->has_torque ? 1 : 0) + 1 + 1 + 1 + 2 + h->bpasses + 2 + 3 + 2 + h->passes + 1 + 1 +
+                           h->iters);
   *out = h;
   return PBDR_OK;
 }
@@ -861,6 +893,7 @@ int pbdr_gpu_debug_prologue(pbdr_handle* h) {
   if (!h) return set_error(PBDR_ERR_GENERIC, "null handle");
   PBDR_CUDA(cudaSetDevice(h->device));
   enqueue_substep(h, nullptr);
+  h->debug_iter = 0;
   PBDR_CUDA(cudaGetLastError());
   return check_errors(h);
 }
@@ -868,7 +901,8 @@ int pbdr_gpu_debug_prologue(pbdr_handle* h) {
 int pbdr_gpu_debug_iteration(pbdr_handle* h, int) {
   if (!h) return set_error(PBDR_ERR_GENERIC, "null handle");
   PBDR_CUDA(cudaSetDevice(h->device));
-  enqueue_iteration(h, nullptr);
+  enqueue_iteration(h, h->debug_iter % std::max(1, h->iters), nullptr);
+  ++h->debug_iter;
   PBDR_CUDA(cudaGetLastError());
   return check_errors(h);
 }
@@ -886,7 +920,7 @@ int pbdr_gpu_debug_phase_timing(pbdr_handle* h, long long* out) {
   }
   PBDR_CUDA(cudaMemsetAsync(h->timing_buf, 0, sizeof(long long) * 8 * h->ctas, h->stream));
   h->timing = h->timing_buf;  // only this launch is instrumented
-  enqueue_iteration(h, nullptr);
+  enqueue_iteration(h, 0, nullptr);
   h->timing = nullptr;
   PBDR_CUDA(cudaMemcpyAsync(out, h->timing_buf, sizeof(long long) * 8 * h->ctas, cudaMemcpyDeviceToHost,
                             h->stream));

@@ -117,13 +117,24 @@ __global__ void __launch_bounds__(256) k_integrate_key(IntegrateArgs A) {
     const double t = static_cast<double>(*A.substep_counter) * A.dt_d;
     const BodyProgram pr = A.programs[b];
     float a[3] = {0.0f, 0.0f, (pr.flags & 2) ? 0.0f : -A.gravity};
+    const float4 x = A.pos[p];
     if ((pr.flags & 1) && t >= pr.t_start && t < pr.t_stop) {
       const float invM = A.body_mass[b].y;
       a[0] = a[0] + pr.fx * invM;
       a[1] = a[1] + pr.fy * invM;
       a[2] = a[2] + pr.fz * invM;
+      if (pr.flags & 4) {
+        const float4 c = A.wcom[b];
+        const float4 al = A.walpha[b];
+        const float r[3] = {x.x - c.x, x.y - c.y, x.z - c.z};
+        const float alv[3] = {al.x, al.y, al.z};
+        float ar[3];
+        cross3(alv, r, ar);
+        a[0] = a[0] + ar[0];
+        a[1] = a[1] + ar[1];
+        a[2] = a[2] + ar[2];
+      }
     }
-    const float4 x = A.pos[p];
     const float4 v = A.vel[p];
     A.init[p] = make_float4(x.x, x.y, x.z, 0.0f);
     float4 vn;
@@ -830,10 +841,33 @@ __global__ void __launch_bounds__(kThreads, PBDR_ITER_MINBLOCKS) k_iteration(Ite
     cross3(ca, Pa, tmp);
 #pragma unroll
     for (int k = 0; k < 3; ++k) La[k] = S[6 + k] - tmp[k];
-    if (A.linfix)
+    // SM-induced momentum change of this iteration (P_bsm - P_asm, L_asm - L_bsm).
+    float dP[3], dL[3];
 #pragma unroll
-      for (int k = 0; k < 3; ++k) dv[k] = (R[kResPb + k] - Pa[k]) * invM;
-    if (A.angfix) {
+    for (int k = 0; k < 3; ++k) {
+      dP[k] = R[kResPb + k] - Pa[k];
+      dL[k] = La[k] - R[kResLb + k];
+    }
+    bool correct = true;
+    if (A.per_substep) {
+      // kPerSubstep: accumulate over the substep's iterations, correct once.
+      float4 aP = make_float4(0.0f, 0.0f, 0.0f, 0.0f), aL = aP;
+      if (A.iter_index > 0) {
+        aP = A.mom_acc[2 * bb];
+        aL = A.mom_acc[2 * bb + 1];
+      }
+      aP.x = aP.x + dP[0]; aP.y = aP.y + dP[1]; aP.z = aP.z + dP[2];
+      aL.x = aL.x + dL[0]; aL.y = aL.y + dL[1]; aL.z = aL.z + dL[2];
+      A.mom_acc[2 * bb] = aP;
+      A.mom_acc[2 * bb + 1] = aL;
+      dP[0] = aP.x; dP[1] = aP.y; dP[2] = aP.z;
+      dL[0] = aL.x; dL[1] = aL.y; dL[2] = aL.z;
+      correct = A.last_iter != 0;
+    }
+    if (A.linfix && correct)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) dv[k] = dP[k] * invM;
+    if (A.angfix && correct) {
       float If[6];
       If[0] = S[9] - M * (ca[1] * ca[1] + ca[2] * ca[2]);
       If[1] = S[10] - M * (ca[0] * ca[0] + ca[2] * ca[2]);
@@ -841,7 +875,6 @@ __global__ void __launch_bounds__(kThreads, PBDR_ITER_MINBLOCKS) k_iteration(Ite
       If[3] = S[12] + M * (ca[0] * ca[1]);
       If[4] = S[13] + M * (ca[0] * ca[2]);
       If[5] = S[14] + M * (ca[1] * ca[2]);
-      const float dL[3] = {La[0] - R[kResLb], La[1] - R[kResLb + 1], La[2] - R[kResLb + 2]};
       double nax[3];
       const unsigned e = inertia_solve_f(If, dL, om, nax);
       if (e) record_error(A.err, e, bb, A.substep_counter, nax);
@@ -996,6 +1029,85 @@ __global__ void __launch_bounds__(kThreads) k_body_stats(StatsArgs A) {
   for (int k = 0; k < 4; ++k) o[3 + k] = qd[k];
 }
 
+// ---------------------------------------------------------------------------
+// Torque programs: per-body com, inertia and alpha = pinv(I) tau of X at the
+// substep start (distribute_wrench, body.cpp:126-150). Same reduction tree as
+// every body sum (pbdr_pinned.h); the oracle mirrors it (integrate()).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_body_wrench(WrenchArgs A) {
+  __shared__ float s_part[kWarps][9];
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int4 cd = A.cta_desc[blockIdx.x];
+  const int4 wd = A.warp_desc[blockIdx.x * kWarps + warp];
+  const int b = wd.x;
+  const int wi = wd.y;
+  const bool live = b >= 0 && (A.programs[b].flags & 4);
+  float acc[9];
+#pragma unroll
+  for (int f = 0; f < 9; ++f) acc[f] = 0.0f;
+  if (live) {
+    const int start = wd.z, n = wd.w & 0xFFFF, W = wd.w >> 16;
+    const float4 an = A.anchor[b];
+    const float a[3] = {an.x, an.y, an.z};
+#pragma unroll
+    for (int k = 0; k < PBDR_KP; ++k) {
+      const int q = k * 32 * W + wi * 32 + lane;
+      if (q >= n) continue;
+      const int64_t p = start + q;
+      const float4 x4 = A.pos[p];
+      const float mk = A.vel[p].w;
+      const float pp[3] = {x4.x - a[0], x4.y - a[1], x4.z - a[2]};
+      const float s2 = (pp[0] * pp[0] + pp[1] * pp[1]) + pp[2] * pp[2];
+      acc[0] = acc[0] + mk * pp[0];
+      acc[1] = acc[1] + mk * pp[1];
+      acc[2] = acc[2] + mk * pp[2];
+      acc[3] = acc[3] + mk * (s2 - pp[0] * pp[0]);
+      acc[4] = acc[4] + mk * (s2 - pp[1] * pp[1]);
+      acc[5] = acc[5] + mk * (s2 - pp[2] * pp[2]);
+      acc[6] = acc[6] + -(mk * (pp[0] * pp[1]));
+      acc[7] = acc[7] + -(mk * (pp[0] * pp[2]));
+      acc[8] = acc[8] + -(mk * (pp[1] * pp[2]));
+    }
+    warp_butterfly<9>(acc);
+    if (lane == 0)
+#pragma unroll
+      for (int f = 0; f < 9; ++f) s_part[warp][f] = acc[f];
+  }
+  __syncthreads();
+  if (!(warp == 0 && lane < cd.w)) return;
+  const int bb = cd.z + lane;
+  const BodyProgram pr = A.programs[bb];
+  if (!(pr.flags & 4)) return;
+  const int4 bd = A.body_desc[bb];
+  float S[9];
+#pragma unroll
+  for (int f = 0; f < 9; ++f) S[f] = s_part[bd.w][f];
+  for (int u = 1; u < bd.z; ++u)
+#pragma unroll
+    for (int f = 0; f < 9; ++f) S[f] = S[f] + s_part[bd.w + u][f];
+  const float2 mass = A.body_mass[bb];
+  const float M = mass.x, invM = mass.y;
+  const float4 an = A.anchor[bb];
+  float c[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) c[k] = S[k] * invM;
+  float If[6];
+  If[0] = S[3] - M * (c[1] * c[1] + c[2] * c[2]);
+  If[1] = S[4] - M * (c[0] * c[0] + c[2] * c[2]);
+  If[2] = S[5] - M * (c[0] * c[0] + c[1] * c[1]);
+  If[3] = S[6] + M * (c[0] * c[1]);
+  If[4] = S[7] + M * (c[0] * c[2]);
+  If[5] = S[8] + M * (c[1] * c[2]);
+  const float tau[3] = {pr.tx, pr.ty, pr.tz};
+  float al[3];
+  double nax[3];
+  const unsigned e = inertia_solve_f(If, tau, al, nax);
+  if (e) record_error(A.err, e, bb, A.substep_counter, nax);
+  A.wcom[bb] = make_float4(an.x + c[0], an.y + c[1], an.z + c[2], 0.0f);
+  A.walpha[bb] = make_float4(al[0], al[1], al[2], 0.0f);
+}
+
 }  // namespace
 
 #ifndef PBDR_ITER_EXTRA_SMEM
@@ -1048,6 +1160,10 @@ cudaError_t prepare_iteration_kernel() {
 
 void launch_iteration(const IterArgs& a, int ctas, cudaStream_t s) {
   k_iteration<<<ctas, kThreads, iteration_smem_bytes(), s>>>(a);
+}
+
+void launch_wrench(const WrenchArgs& a, int ctas, cudaStream_t s) {
+  k_body_wrench<<<ctas, kThreads, 0, s>>>(a);
 }
 
 void launch_stats(const StatsArgs& a, int ctas, cudaStream_t s) {

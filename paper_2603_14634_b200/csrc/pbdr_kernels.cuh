@@ -24,10 +24,31 @@ struct DevError {
   double axis[3];
 };
 
-struct BodyProgram {  // ForceProgram (scene.hpp:53-61), fp32 force + window
+struct BodyProgram {  // ForceProgram (scene.hpp:53-61), fp32 force/torque + window
   float fx, fy, fz;
-  int flags;  // bit0: has program, bit1: gravity exempt
+  int flags;  // bit0: has program, bit1: gravity exempt, bit2: nonzero torque
+  float tx, ty, tz;
+  int pad;
   double t_start, t_stop;
+};
+
+// distribute_wrench (body.cpp:126-150) on the device: per body with a torque
+// program, the com c and inertia I of X at the substep start (anchored fp32
+// tree sums, parallel axis) and alpha = pinv(I) tau; integrate then adds
+// alpha x (x - c) to the acceleration.
+struct WrenchArgs {
+  const float4* pos;
+  const float4* vel;  // .w = mass
+  const float4* anchor;
+  const int4* cta_desc;
+  const int4* warp_desc;
+  const float2* body_mass;
+  const int4* body_desc;
+  const BodyProgram* programs;
+  float4* wcom;    // per body: com (xyz)
+  float4* walpha;  // per body: alpha (xyz)
+  DevError* err;
+  const long long* substep_counter;
 };
 
 struct IntegrateArgs {
@@ -39,6 +60,8 @@ struct IntegrateArgs {
   const BodyProgram* programs;  // per body
   const float2* body_mass;      // (M, 1/M)
   uint32_t* key_all;  // [n] cell key of every particle (slot order)
+  const float4* wcom;    // torque programs: per-body com and alpha (or null)
+  const float4* walpha;
   uint32_t* box_min;  // per body 3 x order-preserving uint of the min corner of X~
   uint32_t* box_max;
   const long long* substep_counter;
@@ -147,6 +170,10 @@ struct IterArgs {
   Planes planes;
   float dt, inv_dt, relax;
   int incremental, linfix, angfix;
+  int per_substep;    // MomentumFrequency::kPerSubstep
+  int iter_index;     // iteration within the substep
+  int last_iter;      // iteration_index == solver_iterations - 1
+  float4* mom_acc;    // per body (P, L) accumulators for kPerSubstep
   long long* timing;  // optional per-CTA phase clocks (debug), else null
 };
 
@@ -175,5 +202,6 @@ size_t iteration_smem_bytes();
 cudaError_t prepare_iteration_kernel();
 void launch_iteration(const IterArgs& a, int ctas, cudaStream_t s);
 void launch_stats(const StatsArgs& a, int ctas, cudaStream_t s);
+void launch_wrench(const WrenchArgs& a, int ctas, cudaStream_t s);
 
 }  // namespace pbdr_dev

@@ -305,6 +305,28 @@ def rigid_body_arrays(centers_list, radius, masses, velocities=None):
                 total_mass=np.array(tm), rest_com=np.array(rc))
 
 
+def scene_with_programs(src, programs) -> "ArrayScene":
+    """Copy of a scene (GeneratedScene or ArrayScene) with per-body ForcePrograms
+    attached (scene.hpp:53-61: Scene::programs, one per body)."""
+    d = src.desc
+    n, nb = int(d.num_particles), int(d.num_bodies)
+
+    def arr(name, count, dtype=np.float64):
+        ptr = getattr(d, name)
+        return np.ctypeslib.as_array(ptr, shape=(count,)).astype(dtype, copy=True) if count else np.zeros(0, dtype)
+
+    walls = [d.walls[i] for i in range(d.num_walls)] if d.num_walls else ()
+    body_scene = arr("body_scene", nb, np.int32) if bool(d.body_scene) else None
+    return ArrayScene(position=arr("position", 3 * n), velocity=arr("velocity", 3 * n),
+                      inv_mass=arr("inv_mass", n), radius=arr("radius", n),
+                      body_offsets=arr("body_offsets", nb + 1, np.int64),
+                      rest_offsets=arr("rest_offsets", 3 * n), total_mass=arr("total_mass", nb),
+                      rest_com=arr("rest_com", 3 * nb), body_indices=arr("body_indices", n, np.int32),
+                      body_id=arr("body_id", n, np.int32), ground=d.ground, has_ground=bool(d.has_ground),
+                      contact_relaxation=d.contact_relaxation, walls=walls, body_scene=body_scene,
+                      programs=list(programs))
+
+
 class GeneratedScene:
     """One of the five BASELINE.json configs, built by the library's host generator."""
 

@@ -119,13 +119,15 @@ def test_odd_iteration_count_parity(pbdr, pyoracle):
     assert np.array_equal(gpu.read_f32()[0], orc.read_f32()[0])
 
 
-@pytest.mark.parametrize("variant", ["pbd", "linear_only", "angular_only", "legacy_fixed"])
+@pytest.mark.parametrize("variant", ["pbd", "linear_only", "angular_only", "legacy_fixed", "per_substep"])
 def test_solver_variants_bit_exact(pbdr, pyoracle, variant):
-    # SolverConfig::pbd() and the Table IV ablations (scene.hpp:22-24, 33-39).
+    # SolverConfig::pbd(), the Table IV ablations and MomentumFrequency
+    # (scene.hpp:15, 22-25, 33-39).
     cfg = {"pbd": P.pbd_cfg(frame_rate=240.0),
            "linear_only": P.solver_cfg(frame_rate=240.0, angular_momentum_fix=False),
            "angular_only": P.solver_cfg(frame_rate=240.0, linear_momentum_fix=False),
-           "legacy_fixed": P.solver_cfg(frame_rate=240.0, velocity_update=0)}[variant]
+           "legacy_fixed": P.solver_cfg(frame_rate=240.0, velocity_update=0),
+           "per_substep": P.solver_cfg(frame_rate=240.0, momentum_frequency=1)}[variant]
     g = P.GeneratedScene(2)
     gpu = P.GpuSolver(g.desc, cfg)
     orc = pyoracle.Oracle(g.desc, cfg)
@@ -135,6 +137,43 @@ def test_solver_variants_bit_exact(pbdr, pyoracle, variant):
     op, ov = orc.read_f32()
     assert_same(gp, op, variant + " positions")
     assert_same(gv, ov, variant + " velocities")
+
+
+def _programs(nb, seed=3):
+    # Mix of force-only, torque-only, force+torque, windowed and gravity-exempt
+    # programs (scene.hpp:53-61); bodies with no wrench keep a null program.
+    rng = np.random.default_rng(seed)
+    out = []
+    for b in range(nb):
+        kind = b % 5
+        F = tuple(rng.uniform(-5, 5, 3)) if kind in (1, 3) else (0.0, 0.0, 0.0)
+        tau = tuple(rng.uniform(-0.05, 0.05, 3)) if kind in (2, 3, 4) else (0.0, 0.0, 0.0)
+        t0, t1 = (0.002, 0.006) if kind == 4 else (0.0, float("inf"))
+        out.append(P.ForceProgram(F, tau, t0, t1, int(kind == 2), 0))
+    return out
+
+
+def test_force_torque_programs_bit_exact(pbdr, pyoracle):
+    # External wrench programs on the GPU path:
+    # force at the com plus torque distributed as m_p * (I^-1 tau) x r_p
+    # (body.cpp:126-150), inside [t_start, t_stop), gravity_exempt bodies.
+    g = P.GeneratedScene(2)
+    sc = P.scene_with_programs(g, _programs(g.desc.num_bodies))
+    cfg = P.solver_cfg(frame_rate=240.0)
+    gpu = P.GpuSolver(sc.desc, cfg)
+    orc = pyoracle.Oracle(sc.desc, cfg)
+    gpu.debug_prologue()
+    orc.integrate()
+    assert_same(gpu.read_f32()[1], orc.read_f32()[1], "velocities after the wrench integrate")
+    gpu = P.GpuSolver(sc.desc, cfg)
+    orc = pyoracle.Oracle(sc.desc, cfg)
+    gpu.step_frames(3)
+    assert orc.step(3 * cfg.substeps) == 0
+    gp, gv = gpu.read_f32()
+    op, ov = orc.read_f32()
+    assert_same(gp, op, "positions")
+    assert_same(gv, ov, "velocities")
+    assert_same(gpu.read_bodies(), orc.body_stats(), "body stats")
 
 
 @pytest.mark.slow
