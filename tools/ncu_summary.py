@@ -14,18 +14,26 @@ def launches(path, out):
     rows = list(csv.reader(open(path)))
     start = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
     hdr = rows[start]
-    ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
-    tot, cnt = defaultdict(float), defaultdict(int)
+    ki, mi, vi, ui = (hdr.index("Kernel Name"), hdr.index("Metric Name"), hdr.index("Metric Value"),
+                      hdr.index("Metric Unit"))
+    tot, cnt, dram = defaultdict(float), defaultdict(int), defaultdict(float)
+    scale_t = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}
+    scale_b = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
     for r in rows[start + 1:]:
         name = r[ki].split("(")[0].split("::")[-1]
         v = float(r[vi].replace(",", ""))
-        v *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}.get(r[ui], 1.0)
-        tot[name] += v
-        cnt[name] += 1
+        if r[mi] == "gpu__time_duration.sum":
+            tot[name] += v * scale_t.get(r[ui], 1.0)
+            cnt[name] += 1
+        elif r[mi].startswith("dram__bytes"):
+            dram[name] += v * scale_b.get(r[ui], 1.0)
     s = sum(tot.values())
-    lines = ["| kernel | launches | total us | avg us | share |", "|---|---|---|---|---|"]
+    lines = ["| kernel | launches | total us | avg us | share | DRAM MB / launch | DRAM GB/s |",
+             "|---|---|---|---|---|---|---|"]
     for k in sorted(tot, key=lambda k: -tot[k]):
-        lines.append(f"| {k} | {cnt[k]} | {tot[k]:.1f} | {tot[k] / cnt[k]:.2f} | {tot[k] / s:.3f} |")
+        mb = dram[k] / cnt[k] / 1e6 if k in dram else float("nan")
+        gbs = dram[k] / (tot[k] * 1e-6) / 1e9 if k in dram and tot[k] > 0 else float("nan")
+        lines.append(f"| {k} | {cnt[k]} | {tot[k]:.1f} | {tot[k] / cnt[k]:.2f} | {tot[k] / s:.3f} | {mb:.1f} | {gbs:.0f} |")
     open(out, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
 
