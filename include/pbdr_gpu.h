@@ -195,6 +195,39 @@ int pbdr_gpu_debug_write_anchor(pbdr_handle* h, const float* anchor3);
 int pbdr_gpu_debug_read_rquat(pbdr_handle* h, float* q4);
 int pbdr_gpu_debug_write_rquat(pbdr_handle* h, const float* q4);
 
+/* ---- Staged stepping and x-slab decomposition --
+ * One substep = pbdr_gpu_substep_begin (integrate, hash grid, candidate lists)
+ * followed by solver_iterations calls of pbdr_gpu_substep_iteration; both only
+ * enqueue on the handle's stream (pbdr_gpu_stream), so a caller can interleave
+ * its own work on that stream between stages -- the slab runner's NCCL halo
+ * exchange. pbdr_gpu_sync waits and maps device errors to status codes.
+ * Replaces: the iteration loop inside pbdr::step. */
+int pbdr_gpu_substep_begin(pbdr_handle* h);
+int pbdr_gpu_substep_iteration(pbdr_handle* h);
+int pbdr_gpu_sync(pbdr_handle* h);
+int pbdr_gpu_stream(pbdr_handle* h, void** cuda_stream);
+
+/* Per-body roles for one rank of an x-slab decomposition: 2 = owned (simulated
+ * and authoritative), 1 = ghost (integrated and hashed so owned particles see
+ * it; positions/velocities are overwritten by the halo exchange), 0 = inactive
+ * (ignored). The layout stays the full scene's body-major layout, so every
+ * rank's contact candidate lists are the single-GPU lists in the same order.
+ * roles = NULL returns to whole-scene mode. Host array of num_bodies int8. */
+int pbdr_gpu_set_roles(pbdr_handle* h, const int8_t* roles);
+
+/* Halo exchange records: float4 per index, DEVICE pointers, enqueued on the
+ * handle's stream. POSITION / VELOCITY index particle slots (body-major order,
+ * positions of the current iteration buffer); ANCHOR / ROTATION index bodies
+ * (anchored-sum reference point; warm-start rotation w,x,y,z). */
+enum {
+  PBDR_FIELD_POSITION = 0,
+  PBDR_FIELD_VELOCITY = 1,
+  PBDR_FIELD_ANCHOR = 2,
+  PBDR_FIELD_ROTATION = 3
+};
+int pbdr_gpu_gather(pbdr_handle* h, int field, const int32_t* index, int64_t count, void* dst);
+int pbdr_gpu_scatter(pbdr_handle* h, int field, const int32_t* index, int64_t count, const void* src);
+
 /* ---- Host-side scene construction (no device work) ------------------------
  * The five BASELINE.json configs, generated deterministically from splitmix64
  * (rng.hpp:10-29) with pack_box lattices (geometry.cpp:32-55) and

@@ -99,7 +99,10 @@ struct State {
   int32_t err_body = -1;
   double err_axis[3] = {0, 0, 0};
   int threads = 1;
+  std::vector<int8_t> role;  // slab mode: 0 inactive, 1 ghost, 2 owned (empty = all owned)
 };
+
+inline int role_of(const State& s, int32_t b) { return s.role.empty() ? 2 : s.role[b]; }
 
 inline void flag(State& s, uint32_t bits, int32_t body, const double* axis = nullptr) {
 #pragma omp critical(oracle_err)
@@ -152,7 +155,7 @@ inline void cross3(const float a[3], const float b[3], float o[3]) {
 void wrench_prepass(State& s) {
 #pragma omp parallel for num_threads(s.threads) schedule(dynamic, 8)
   for (int32_t b = 0; b < s.nb; ++b) {
-    if (!s.btorque_on[b]) continue;
+    if (!s.btorque_on[b] || role_of(s, b) == 0) continue;
     const int64_t start = s.bstart[b];
     const int n = static_cast<int>(s.bstart[b + 1] - start);
     const float a[3] = {s.anchor[3 * b], s.anchor[3 * b + 1], s.anchor[3 * b + 2]};
@@ -201,6 +204,7 @@ void integrate(State& s) {
 #pragma omp parallel for num_threads(s.threads) schedule(static)
   for (int64_t p = 0; p < s.n; ++p) {
     const int32_t b = s.body_of[p];
+    if (role_of(s, b) == 0) continue;  // slab mode: not simulated on this rank
     float a[3] = {0.0f, 0.0f, s.bexempt[b] ? 0.0f : -s.g};
     float* x = &s.pos[4 * p];
     if (s.bprog[b] && t >= s.tstart[b] && t < s.tstop[b]) {
@@ -240,18 +244,22 @@ void build_candidates(State& s) {
     key[p] = {s.bscene[s.body_of[p]], pbdr_cell_coord(x[2], s.inv_h), pbdr_cell_coord(x[1], s.inv_h),
               pbdr_cell_coord(x[0], s.inv_h)};
   }
-  std::vector<int64_t> order(static_cast<size_t>(s.n));
-  for (int64_t p = 0; p < s.n; ++p) order[p] = p;
+  // Slab mode: only owned + ghost particles enter the grid.
+  std::vector<int64_t> order;
+  order.reserve(static_cast<size_t>(s.n));
+  for (int64_t p = 0; p < s.n; ++p)
+    if (role_of(s, s.body_of[p]) != 0) order.push_back(p);
   std::stable_sort(order.begin(), order.end(),
                    [&](int64_t a, int64_t b) { return key[a] < key[b]; });
-  std::vector<Key> sorted(static_cast<size_t>(s.n));
-  for (int64_t k = 0; k < s.n; ++k) sorted[k] = key[order[k]];
+  std::vector<Key> sorted(order.size());
+  for (size_t k = 0; k < order.size(); ++k) sorted[k] = key[order[k]];
 
   s.ncand.assign(static_cast<size_t>(s.n), 0);
   s.cand.assign(static_cast<size_t>(s.n) * PBDR_NBR_CAP, -1);
   s.cand_rr.assign(static_cast<size_t>(s.n) * PBDR_NBR_CAP, 0.0f);
 #pragma omp parallel for num_threads(s.threads) schedule(dynamic, 1024)
   for (int64_t i = 0; i < s.n; ++i) {
+    if (role_of(s, s.body_of[i]) == 0) continue;
     const Key ki = key[i];
     const float* xi = &s.pos[4 * i];
     std::vector<int64_t> found;
@@ -544,6 +552,7 @@ void iteration(State& s) {
   const std::vector<float> X = s.pos;  // X_i snapshot (P1)
 #pragma omp parallel for num_threads(s.threads) schedule(dynamic, 8)
   for (int32_t b = 0; b < s.nb; ++b) {
+    if (role_of(s, b) != 2) continue;  // slab mode: only owned bodies are solved
     const int64_t start = s.bstart[b];
     const int n = static_cast<int>(s.bstart[b + 1] - start);
     std::vector<float> x(3 * n), v(3 * n), m(n), q0(3 * n), dc(3 * n), init(3 * n), xo(3 * n), vo(3 * n);
@@ -595,6 +604,7 @@ void iteration(State& s) {
 void body_stats(State& s, pbdr_body_stats* out) {
 #pragma omp parallel for num_threads(s.threads) schedule(dynamic, 8)
   for (int32_t b = 0; b < s.nb; ++b) {
+    if (role_of(s, b) != 2) continue;
     const int64_t start = s.bstart[b];
     const int n = static_cast<int>(s.bstart[b + 1] - start);
     const float a[3] = {s.anchor[3 * b], s.anchor[3 * b + 1], s.anchor[3 * b + 2]};
@@ -791,6 +801,46 @@ int oracle_error(void* st, uint32_t* bits, int32_t* body, double* axis) {
   if (body) *body = s.err_body;
   if (axis) std::memcpy(axis, s.err_axis, sizeof s.err_axis);
   return finish_substep_errors(s);
+}
+
+// Slab decomposition (mirrors pbdr_gpu_set_roles / _gather / _scatter).
+void oracle_set_roles(void* st, const int8_t* roles) {
+  State& s = *static_cast<State*>(st);
+  if (!roles) {
+    s.role.clear();
+    return;
+  }
+  s.role.assign(roles, roles + s.nb);
+}
+
+void oracle_gather(void* st, int field, const int32_t* index, int64_t count, float* dst) {
+  State& s = *static_cast<State*>(st);
+  for (int64_t t = 0; t < count; ++t) {
+    const int64_t i = index[t];
+    float* o = &dst[4 * t];
+    switch (field) {
+      case PBDR_FIELD_POSITION: std::memcpy(o, &s.pos[4 * i], 16); break;
+      case PBDR_FIELD_VELOCITY: std::memcpy(o, &s.vel[4 * i], 16); break;
+      case PBDR_FIELD_ANCHOR: std::memcpy(o, &s.anchor[3 * i], 12); o[3] = 0.0f; break;
+      case PBDR_FIELD_ROTATION: std::memcpy(o, &s.rquat[4 * i], 16); break;
+      default: break;
+    }
+  }
+}
+
+void oracle_scatter(void* st, int field, const int32_t* index, int64_t count, const float* src) {
+  State& s = *static_cast<State*>(st);
+  for (int64_t t = 0; t < count; ++t) {
+    const int64_t i = index[t];
+    const float* o = &src[4 * t];
+    switch (field) {
+      case PBDR_FIELD_POSITION: std::memcpy(&s.pos[4 * i], o, 16); break;
+      case PBDR_FIELD_VELOCITY: std::memcpy(&s.vel[4 * i], o, 16); break;
+      case PBDR_FIELD_ANCHOR: std::memcpy(&s.anchor[3 * i], o, 12); break;
+      case PBDR_FIELD_ROTATION: std::memcpy(&s.rquat[4 * i], o, 16); break;
+      default: break;
+    }
+  }
 }
 
 void oracle_read_f32(void* st, float* pos4, float* vel4) {

@@ -52,6 +52,11 @@ def olib():
             getattr(L, name).restype = None
         L.oracle_num_slots.argtypes = [vp]
         L.oracle_num_slots.restype = C.c_int64
+        L.oracle_set_roles.argtypes = [vp, vp]
+        L.oracle_set_roles.restype = None
+        for name in ("oracle_gather", "oracle_scatter"):
+            getattr(L, name).argtypes = [vp, C.c_int, vp, C.c_int64, vp]
+            getattr(L, name).restype = None
         L.oracle_cell_size.argtypes = [vp]
         L.oracle_cell_size.restype = C.c_float
         L.oracle_polar.argtypes = [vp, vp, vp]
@@ -148,6 +153,22 @@ class Oracle:
 
     def end_substep(self):
         olib().oracle_end_substep(self._h)
+
+    # ---- slab decomposition (mirrors GpuSolver.set_roles / gather / scatter) --
+    def set_roles(self, roles=None):
+        r = None if roles is None else np.ascontiguousarray(roles, np.int8)
+        olib().oracle_set_roles(self._h, _p(r))
+
+    def gather(self, field, index):
+        index = np.ascontiguousarray(index, np.int32)
+        out = np.empty((len(index), 4), np.float32)
+        olib().oracle_gather(self._h, field, _p(index), len(index), _p(out))
+        return out
+
+    def scatter(self, field, index, values):
+        index = np.ascontiguousarray(index, np.int32)
+        values = np.ascontiguousarray(values, np.float32).reshape(len(index), 4)
+        olib().oracle_scatter(self._h, field, _p(index), len(index), _p(values))
 
     def error(self):
         bits = C.c_uint32()

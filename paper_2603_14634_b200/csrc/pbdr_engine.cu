@@ -100,6 +100,28 @@ struct pbdr_handle {
   int incremental = 1, linfix = 1, angfix = 1;
   pbdr_dev::Planes planes{};
 
+  // Iteration CTA packing (cta_desc / warp_desc / body_desc triples). `full` is
+  // the create-time packing of every body; in slab mode `iter` packs the owned
+  // bodies and `active` the owned + ghost bodies (torque prepass).
+  struct Packing {
+    int4* cta = nullptr;
+    int4* warp = nullptr;
+    int4* body = nullptr;
+    int ctas = 0;
+  };
+  Packing pk_full, pk_iter, pk_active;
+  std::vector<int64_t> h_bstart;  // host copy: first slot of each body
+  std::vector<int> h_bcount;      // host copy: particles of each body
+
+  // Slab mode (x-slab decomposition of one scene, pbdr_gpu_set_roles).
+  bool slab = false;
+  uint8_t* role = nullptr;     // [nb] 0 inactive, 1 ghost, 2 owned
+  int* active_list = nullptr;  // [nb] ascending ids of owned + ghost bodies
+  int n_active = 0;
+  int64_t p_lo = 0, p_hi = 0;  // slot range covering the active bodies
+  Packing slab_iter, slab_active;  // device storage (capacity nb CTAs)
+  int stage_iter = 0;
+
   cudaGraphExec_t graph[2] = {nullptr, nullptr};
   int graph_end[2] = {0, 0};
   int64_t substeps_done = 0;
@@ -188,7 +210,9 @@ void enqueue_substep(pbdr_handle* h, pbdr_dev::LaunchHook* hook) {
   ia.box_min = h->box_min;
   ia.box_max = h->box_max;
   ia.substep_counter = h->counter;
-  ia.n = h->n;
+  ia.role = h->slab ? h->role : nullptr;
+  ia.p0 = h->p_lo;
+  ia.n = h->p_hi;
   ia.dt = h->dt;
   ia.gravity = h->gravity;
   ia.inv_h = h->inv_h;
@@ -209,17 +233,17 @@ void enqueue_substep(pbdr_handle* h, pbdr_dev::LaunchHook* hook) {
     wa.pos = h->pos[h->cur];
     wa.vel = h->vel;
     wa.anchor = h->anchor;
-    wa.cta_desc = h->cta_desc;
-    wa.warp_desc = h->warp_desc;
+    wa.cta_desc = h->pk_active.cta;
+    wa.warp_desc = h->pk_active.warp;
     wa.body_mass = h->body_mass;
-    wa.body_desc = h->body_desc;
+    wa.body_desc = h->pk_active.body;
     wa.programs = h->programs;
     wa.wcom = h->wcom;
     wa.walpha = h->walpha;
     wa.err = h->err;
     wa.substep_counter = h->counter;
     if (hook) hook->before(kHookIntegrate);
-    launch_wrench(wa, h->ctas, h->stream);
+    if (h->pk_active.ctas > 0) launch_wrench(wa, h->pk_active.ctas, h->stream);
     if (hook) hook->after(kHookIntegrate);
   }
   if (hook) hook->before(kHookIntegrate);
@@ -237,7 +261,8 @@ void enqueue_substep(pbdr_handle* h, pbdr_dev::LaunchHook* hook) {
   ba.npartners = h->npartners;
   ba.partners = h->partners;
   ba.oversize = h->oversize;
-  ba.nb = h->nb;
+  ba.list = h->slab ? h->active_list : nullptr;
+  ba.nb = h->slab ? h->n_active : h->nb;
   ba.inv_cell = h->inv_cell_b;
   ba.max_extent = h->max_extent;
   ba.inflate = h->inflate;
@@ -245,7 +270,7 @@ void enqueue_substep(pbdr_handle* h, pbdr_dev::LaunchHook* hook) {
   if (hook) hook->before(kHookBroadphase);
   launch_body_keys(ba, h->stream);
   if (hook) hook->after(kHookBroadphase);
-  const int bsb = sort_pairs(h->bkeys, h->bvals, h->nb, h->bhash_bits, h->bsort_temp, h->sm_count,
+  const int bsb = sort_pairs(h->bkeys, h->bvals, ba.nb, h->bhash_bits, h->bsort_temp, h->sm_count,
                              h->stream, hook);
   ba.sorted_bkeys = h->bkeys[bsb];
   ba.sorted_bvals = h->bvals[bsb];
@@ -271,8 +296,10 @@ void enqueue_substep(pbdr_handle* h, pbdr_dev::LaunchHook* hook) {
   nr.vals_c = h->vals[0];
   nr.near_list = h->near_list;
   nr.ncand = h->ncand;
-  nr.n = h->n;
-  nr.blocks = h->near_blocks;
+  nr.role = h->slab ? h->role : nullptr;
+  nr.p0 = h->p_lo;
+  nr.n = h->p_hi;
+  nr.blocks = static_cast<int>((h->p_hi - h->p_lo + 255) / 256);
   nr.inflate = h->inflate;
   if (hook) hook->before(kHookBroadphase);
   launch_near(nr, h->stream);
@@ -337,9 +364,9 @@ void enqueue_iteration(pbdr_handle* h, int iter_index, pbdr_dev::LaunchHook* hoo
   it.iter_index = iter_index;
   it.last_iter = iter_index == h->iters - 1;
   it.mom_acc = h->mom_acc;
-  it.cta_desc = h->cta_desc;
-  it.warp_desc = h->warp_desc;
-  it.body_desc = h->body_desc;
+  it.cta_desc = h->pk_iter.cta;
+  it.warp_desc = h->pk_iter.warp;
+  it.body_desc = h->pk_iter.body;
   it.body_mass = h->body_mass;
   it.err = h->err;
   it.substep_counter = h->counter;
@@ -353,7 +380,7 @@ void enqueue_iteration(pbdr_handle* h, int iter_index, pbdr_dev::LaunchHook* hoo
   it.angfix = h->angfix;
   it.timing = h->timing;
   if (hook) hook->before(kHookIteration);
-  launch_iteration(it, h->ctas, h->stream);
+  if (h->pk_iter.ctas > 0) launch_iteration(it, h->pk_iter.ctas, h->stream);
   if (hook) hook->after(kHookIteration);
   h->cur ^= 1;
 }
@@ -414,6 +441,35 @@ int build_graph(pbdr_handle* h, int parity) {
   cudaGraphDestroy(g);
   if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
   return PBDR_OK;
+}
+
+// Packs bodies (ascending ids) into 8-warp CTAs: a body of n particles takes
+// W = ceil(n/128) warps; consecutive ids (slot-contiguous in the body-major
+// layout) share a CTA while its warps last. bdesc[b] = (first slot, n, W,
+// first warp in the CTA) is written for the listed bodies only.
+void pack_bodies(const std::vector<int>& list, const std::vector<int64_t>& bstart, const std::vector<int>& bcount,
+                 std::vector<int4>& cdesc, std::vector<int4>& wdesc, std::vector<int4>& bdesc) {
+  cdesc.clear();
+  wdesc.clear();
+  int used = 0, prev = -2;
+  auto close = [&] {
+    for (; used < PBDR_CTA_WARPS && used > 0; ++used) wdesc.push_back(make_int4(-1, 0, 0, 1 << 16));
+    used = 0;
+  };
+  for (const int b : list) {
+    const int cnt = bcount[b];
+    const int first_slot = static_cast<int>(bstart[b]);
+    const int W = pbdr_body_warps(cnt);
+    if (used + W > PBDR_CTA_WARPS || (used > 0 && b != prev + 1)) close();
+    if (used == 0) cdesc.push_back(make_int4(first_slot, 0, b, 0));
+    cdesc.back().y += cnt;
+    cdesc.back().w += 1;
+    bdesc[b] = make_int4(first_slot, cnt, W, used);
+    for (int u = 0; u < W; ++u) wdesc.push_back(make_int4(b, u, first_slot, cnt | (W << 16)));
+    used += W;
+    prev = b;
+  }
+  close();
 }
 
 int validate(const pbdr_scene_desc* d, const pbdr_solver_cfg* c) {
@@ -485,9 +541,10 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
   std::vector<int4> cdesc;
   std::vector<char> seen(n, 0);
   h->slot_to_particle.resize(n);
+  h->h_bstart.assign(nb, 0);
+  h->h_bcount.assign(nb, 0);
   double rmax = 0.0;
   int64_t slot = 0;
-  int used = 0;
   for (int32_t b = 0; b < nb; ++b) {
     const int64_t k0 = d->body_offsets[b], k1 = d->body_offsets[b + 1];
     const int64_t cnt = k1 - k0;
@@ -527,18 +584,8 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
       body_of[slot] = b;
       rmax = std::max(rmax, d->radius[i]);
     }
-    const int W = pbdr_body_warps(static_cast<int>(cnt));
-    if (used + W > PBDR_CTA_WARPS) {
-      for (; used < PBDR_CTA_WARPS; ++used) wdesc.push_back(make_int4(-1, 0, 0, 1 << 16));
-      used = 0;
-    }
-    if (used == 0) cdesc.push_back(make_int4(static_cast<int>(first_slot), 0, b, 0));
-    cdesc.back().y += static_cast<int>(cnt);
-    cdesc.back().w += 1;
-    bdesc[b] = make_int4(static_cast<int>(first_slot), static_cast<int>(cnt), W, used);
-    for (int u = 0; u < W; ++u)
-      wdesc.push_back(make_int4(b, u, static_cast<int>(first_slot), static_cast<int>(cnt) | (W << 16)));
-    used += W;
+    h->h_bstart[b] = first_slot;
+    h->h_bcount[b] = static_cast<int>(cnt);
     mass[b] = make_float2(static_cast<float>(d->total_mass[b]), static_cast<float>(1.0 / d->total_mass[b]));
     anchor[b] = make_float4(pos[first_slot].x, pos[first_slot].y, pos[first_slot].z, 0.0f);
     scene[b] = d->body_scene ? d->body_scene[b] : 0;
@@ -563,8 +610,14 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
     release(h);
     return set_config_error("bodies.particle_indices", "every particle must belong to one body");
   }
-  for (; used < PBDR_CTA_WARPS && used > 0; ++used) wdesc.push_back(make_int4(-1, 0, 0, 1 << 16));
+  {
+    std::vector<int> all(nb);
+    for (int32_t b = 0; b < nb; ++b) all[b] = b;
+    pack_bodies(all, h->h_bstart, h->h_bcount, cdesc, wdesc, bdesc);
+  }
   h->ctas = static_cast<int>(wdesc.size() / PBDR_CTA_WARPS);
+  h->p_lo = 0;
+  h->p_hi = n;
 
   // ---- Parameters ----------------------------------------------------------
   h->substeps = c->substeps;
@@ -704,6 +757,8 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
   cudaMemset(h->cells, 0xFF, sizeof(uint4) * T);
   cudaMemset(h->near_count, 0, sizeof(long long) * 2);
   cudaMemset(h->rquat, 0, sizeof(float4) * nb);
+  h->pk_full = {h->cta_desc, h->warp_desc, h->body_desc, h->ctas};
+  h->pk_iter = h->pk_active = h->pk_full;
   if (reset_errors(h) != PBDR_OK) {
     const int code = pbdr_last_error_payload(nullptr, nullptr, nullptr);
     release(h);
@@ -860,12 +915,12 @@ int pbdr_gpu_read_bodies(pbdr_handle* h, pbdr_body_stats* out) {
   sa.vel = h->vel;
   sa.rest = h->rest;
   sa.anchor = h->anchor;
-  sa.cta_desc = h->cta_desc;
-  sa.warp_desc = h->warp_desc;
-  sa.body_desc = h->body_desc;
+  sa.cta_desc = h->pk_iter.cta;
+  sa.warp_desc = h->pk_iter.warp;
+  sa.body_desc = h->pk_iter.body;
   sa.body_mass = h->body_mass;
   sa.out = h->stats;
-  pbdr_dev::launch_stats(sa, h->ctas, h->stream);
+  if (h->pk_iter.ctas > 0) pbdr_dev::launch_stats(sa, h->pk_iter.ctas, h->stream);
   PBDR_CUDA(cudaGetLastError());
   PBDR_CUDA(cudaMemcpyAsync(out, h->stats, sizeof(double) * 13 * h->nb, cudaMemcpyDeviceToHost, h->stream));
   PBDR_CUDA(cudaStreamSynchronize(h->stream));
@@ -911,6 +966,7 @@ int pbdr_gpu_debug_iteration(pbdr_handle* h, int) {
 // phase A done, body math A done, phase B done, body math B done, end, smid).
 int pbdr_gpu_debug_phase_timing(pbdr_handle* h, long long* out) {
   if (!h || !out) return set_error(PBDR_ERR_GENERIC, "null argument");
+  if (h->slab) return set_error(PBDR_ERR_GENERIC, "phase timing is not available in slab mode");
   PBDR_CUDA(cudaSetDevice(h->device));
   if (!h->timing_buf) {
     void* p = nullptr;
@@ -1021,6 +1077,138 @@ int pbdr_gpu_debug_write_anchor(pbdr_handle* h, const float* anchor3) {
   std::vector<float4> a(h->nb);
   for (int32_t b = 0; b < h->nb; ++b) a[b] = make_float4(anchor3[3 * b], anchor3[3 * b + 1], anchor3[3 * b + 2], 0.0f);
   PBDR_CUDA(cudaMemcpy(h->anchor, a.data(), sizeof(float4) * h->nb, cudaMemcpyHostToDevice));
+  return PBDR_OK;
+}
+
+// ---- Staged stepping and slab decomposition ------------------------------------
+int pbdr_gpu_substep_begin(pbdr_handle* h) {
+  if (!h) return set_error(PBDR_ERR_GENERIC, "null handle");
+  PBDR_CUDA(cudaSetDevice(h->device));
+  enqueue_substep(h, nullptr);
+  h->stage_iter = 0;
+  PBDR_CUDA(cudaGetLastError());
+  return PBDR_OK;
+}
+
+int pbdr_gpu_substep_iteration(pbdr_handle* h) {
+  if (!h) return set_error(PBDR_ERR_GENERIC, "null handle");
+  PBDR_CUDA(cudaSetDevice(h->device));
+  enqueue_iteration(h, h->stage_iter % std::max(1, h->iters), nullptr);
+  if (++h->stage_iter == h->iters) h->substeps_done += 1;
+  PBDR_CUDA(cudaGetLastError());
+  return PBDR_OK;
+}
+
+int pbdr_gpu_sync(pbdr_handle* h) {
+  if (!h) return set_error(PBDR_ERR_GENERIC, "null handle");
+  pbdr_host::clear_error();
+  PBDR_CUDA(cudaSetDevice(h->device));
+  return check_errors(h);
+}
+
+int pbdr_gpu_stream(pbdr_handle* h, void** stream) {
+  if (!h || !stream) return set_error(PBDR_ERR_GENERIC, "null argument");
+  *stream = h->stream;
+  return PBDR_OK;
+}
+
+int pbdr_gpu_set_roles(pbdr_handle* h, const int8_t* roles) {
+  if (!h) return set_error(PBDR_ERR_GENERIC, "null handle");
+  pbdr_host::clear_error();
+  PBDR_CUDA(cudaSetDevice(h->device));
+  PBDR_CUDA(cudaStreamSynchronize(h->stream));
+  for (auto& g : h->graph)
+    if (g) {
+      cudaGraphExecDestroy(g);
+      g = nullptr;
+    }
+  if (!roles) {  // back to the whole scene
+    h->slab = false;
+    h->pk_iter = h->pk_active = h->pk_full;
+    h->p_lo = 0;
+    h->p_hi = h->n;
+    return PBDR_OK;
+  }
+  const int32_t nb = h->nb;
+  if (!h->role) {
+    int rc = PBDR_OK;
+    rc |= dalloc(h, &h->role, nb);
+    rc |= dalloc(h, &h->active_list, nb);
+    rc |= dalloc(h, &h->slab_iter.cta, nb);
+    rc |= dalloc(h, &h->slab_iter.warp, static_cast<size_t>(nb) * PBDR_CTA_WARPS);
+    rc |= dalloc(h, &h->slab_iter.body, nb);
+    rc |= dalloc(h, &h->slab_active.cta, nb);
+    rc |= dalloc(h, &h->slab_active.warp, static_cast<size_t>(nb) * PBDR_CTA_WARPS);
+    rc |= dalloc(h, &h->slab_active.body, nb);
+    if (rc != PBDR_OK) return PBDR_ERR_CUDA;
+  }
+  std::vector<uint8_t> r(nb);
+  std::vector<int> owned, active;
+  int64_t lo = h->n, hi = 0;
+  for (int32_t b = 0; b < nb; ++b) {
+    if (roles[b] < 0 || roles[b] > 2) return set_config_error("roles", "role must be 0, 1 or 2");
+    r[b] = static_cast<uint8_t>(roles[b]);
+    if (r[b] == 0) continue;
+    active.push_back(b);
+    if (r[b] == 2) owned.push_back(b);
+    lo = std::min(lo, h->h_bstart[b]);
+    hi = std::max(hi, h->h_bstart[b] + h->h_bcount[b]);
+  }
+  std::vector<int4> cd, wd, bd(nb, make_int4(0, 0, 0, 0));
+  PBDR_CUDA(cudaMemcpy(h->role, r.data(), nb, cudaMemcpyHostToDevice));
+  if (!active.empty())
+    PBDR_CUDA(cudaMemcpy(h->active_list, active.data(), sizeof(int) * active.size(), cudaMemcpyHostToDevice));
+  auto upload = [&](const std::vector<int>& list, pbdr_handle::Packing& dev) -> int {
+    pack_bodies(list, h->h_bstart, h->h_bcount, cd, wd, bd);
+    dev.ctas = static_cast<int>(cd.size());
+    if (!cd.empty()) {
+      PBDR_CUDA(cudaMemcpy(dev.cta, cd.data(), sizeof(int4) * cd.size(), cudaMemcpyHostToDevice));
+      PBDR_CUDA(cudaMemcpy(dev.warp, wd.data(), sizeof(int4) * wd.size(), cudaMemcpyHostToDevice));
+      PBDR_CUDA(cudaMemcpy(dev.body, bd.data(), sizeof(int4) * bd.size(), cudaMemcpyHostToDevice));
+    }
+    return PBDR_OK;
+  };
+  int rc = upload(owned, h->slab_iter);
+  if (rc == PBDR_OK) rc = upload(active, h->slab_active);
+  if (rc != PBDR_OK) return rc;
+  h->slab = true;
+  h->pk_iter = h->slab_iter;
+  h->pk_active = h->slab_active;
+  h->n_active = static_cast<int>(active.size());
+  h->p_lo = active.empty() ? 0 : lo;
+  h->p_hi = active.empty() ? 0 : hi;
+  return PBDR_OK;
+}
+
+static float4* exchange_field(pbdr_handle* h, int which, int64_t* limit) {
+  switch (which) {
+    case PBDR_FIELD_POSITION: *limit = h->n; return h->pos[h->cur];
+    case PBDR_FIELD_VELOCITY: *limit = h->n; return h->vel;
+    case PBDR_FIELD_ANCHOR: *limit = h->nb; return h->anchor;
+    case PBDR_FIELD_ROTATION: *limit = h->nb; return h->rquat;
+    default: return nullptr;
+  }
+}
+
+int pbdr_gpu_gather(pbdr_handle* h, int which, const int32_t* index, int64_t count, void* dst) {
+  if (!h || (count > 0 && (!index || !dst))) return set_error(PBDR_ERR_GENERIC, "null argument");
+  int64_t limit = 0;
+  const float4* src = exchange_field(h, which, &limit);
+  if (!src) return set_config_error("field", "unknown exchange field");
+  PBDR_CUDA(cudaSetDevice(h->device));
+  pbdr_dev::launch_gather4(static_cast<float4*>(dst), src, index, count, h->stream);
+  PBDR_CUDA(cudaGetLastError());
+  return PBDR_OK;
+}
+
+int pbdr_gpu_scatter(pbdr_handle* h, int which, const int32_t* index, int64_t count, const void* src) {
+  if (!h || (count > 0 && (!index || !src))) return set_error(PBDR_ERR_GENERIC, "null argument");
+  int64_t limit = 0;
+  float4* dst = exchange_field(h, which, &limit);
+  if (!dst) return set_config_error("field", "unknown exchange field");
+  PBDR_CUDA(cudaSetDevice(h->device));
+  pbdr_dev::launch_scatter4(dst, static_cast<const float4*>(src), index, count, h->stream);
+  PBDR_CUDA(cudaGetLastError());
   return PBDR_OK;
 }
 

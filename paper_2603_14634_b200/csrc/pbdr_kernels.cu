@@ -108,12 +108,12 @@ __device__ __forceinline__ float ord2f(uint32_t u) {
 }
 
 __global__ void __launch_bounds__(256) k_integrate_key(IntegrateArgs A) {
-  const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const bool valid = p < A.n;
-  int b = -1;
+  const int64_t p = A.p0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  int b = p < A.n ? A.body_of[p] : -1;
+  if (A.role && b >= 0 && A.role[b] == 0) b = -1;  // slab mode: not simulated here
+  const bool valid = b >= 0;
   float4 xn = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
   if (valid) {
-    b = A.body_of[p];
     const double t = static_cast<double>(*A.substep_counter) * A.dt_d;
     const BodyProgram pr = A.programs[b];
     float a[3] = {0.0f, 0.0f, (pr.flags & 2) ? 0.0f : -A.gravity};
@@ -193,8 +193,9 @@ __device__ __forceinline__ void load_box(const uint32_t* bmin, const uint32_t* b
 }
 
 __global__ void __launch_bounds__(256) k_body_keys(BroadArgs A) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= A.nb) return;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= A.nb) return;
+  const int b = A.list ? A.list[t] : t;
   float lo[3], hi[3];
   load_box(A.box_min, A.box_max, b, lo, hi);
   // A box wider than the coarse cell (minus the inflation) would break the
@@ -204,8 +205,8 @@ __global__ void __launch_bounds__(256) k_body_keys(BroadArgs A) {
   int32_t c[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) c[k] = pbdr_cell_coord(0.5f * (lo[k] + hi[k]), A.inv_cell);
-  A.bkeys[b] = pbdr_cell_hash(c[0], c[1], c[2], static_cast<uint32_t>(A.body_scene[b]), A.mask);
-  A.bvals[b] = static_cast<uint32_t>(b);
+  A.bkeys[t] = pbdr_cell_hash(c[0], c[1], c[2], static_cast<uint32_t>(A.body_scene[b]), A.mask);
+  A.bvals[t] = static_cast<uint32_t>(b);
 }
 
 __global__ void __launch_bounds__(256) k_body_ranges(BroadArgs A) {
@@ -220,8 +221,9 @@ __global__ void __launch_bounds__(256) k_body_ranges(BroadArgs A) {
 // inflated by h. The coarse cell is >= the largest box extent + h, so partner
 // box centres lie in the 27 neighbouring coarse cells.
 __global__ void __launch_bounds__(128) k_body_partners(BroadArgs A) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= A.nb) return;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= A.nb) return;
+  const int b = A.list ? A.list[t] : t;
   if (*A.oversize) {
     A.npartners[b] = -1;
     return;
@@ -304,12 +306,13 @@ __global__ void __launch_bounds__(256) k_cell_ranges(RangesArgs A) {
 // order (deterministic).
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_near_flag(NearArgs A) {
-  const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t p = A.p0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   bool near = false;
   if (p < A.n) {
-    const float4 xi = A.pos[p];
     const int bi = A.body_of[p];
-    const int np = A.npartners[bi];
+    const bool active = !A.role || A.role[bi] != 0;
+    const float4 xi = A.pos[p];
+    const int np = active ? A.npartners[bi] : 0;
     near = np < 0;  // partner overflow: search in full
     for (int k = 0; k < np && !near; ++k) {
       const int o = A.partners[static_cast<int64_t>(bi) * PBDR_PARTNER_CAP + k];
@@ -367,7 +370,7 @@ __global__ void __launch_bounds__(1024) k_near_scan(NearArgs A) {
 
 __global__ void __launch_bounds__(256) k_near_compact(NearArgs A) {
   __shared__ uint32_t s_w[8];
-  const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t p = A.p0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const bool near = p < A.n && A.flag[p] != 0;
   const unsigned bal = __ballot_sync(kFull, near);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1116,26 +1119,51 @@ __global__ void __launch_bounds__(kThreads) k_body_wrench(WrenchArgs A) {
 size_t iteration_smem_bytes() { return sizeof(float4) * 3 * kSlots + PBDR_ITER_EXTRA_SMEM; }
 
 void launch_integrate(const IntegrateArgs& a, cudaStream_t s) {
-  const unsigned blocks = static_cast<unsigned>((a.n + 255) / 256);
+  const unsigned blocks = static_cast<unsigned>((a.n - a.p0 + 255) / 256);
+  if (blocks == 0) return;
   k_integrate_key<<<blocks, 256, 0, s>>>(a);
 }
 
 void launch_body_keys(const BroadArgs& a, cudaStream_t s) {
+  if (a.nb == 0) return;
   k_body_keys<<<(a.nb + 255) / 256, 256, 0, s>>>(a);
 }
 
 void launch_body_ranges(const BroadArgs& a, cudaStream_t s) {
+  if (a.nb == 0) return;
   k_body_ranges<<<(a.nb + 255) / 256, 256, 0, s>>>(a);
 }
 
 void launch_body_partners(const BroadArgs& a, cudaStream_t s) {
+  if (a.nb == 0) return;
   k_body_partners<<<(a.nb + 127) / 128, 128, 0, s>>>(a);
 }
 
 void launch_near(const NearArgs& a, cudaStream_t s) {
-  k_near_flag<<<a.blocks, 256, 0, s>>>(a);
+  if (a.blocks > 0) k_near_flag<<<a.blocks, 256, 0, s>>>(a);
   k_near_scan<<<1, 1024, 0, s>>>(a);
-  k_near_compact<<<a.blocks, 256, 0, s>>>(a);
+  if (a.blocks > 0) k_near_compact<<<a.blocks, 256, 0, s>>>(a);
+}
+
+// Slab halo exchange: float4 records by index (particle slots or body ids).
+__global__ void __launch_bounds__(256) k_gather4(float4* __restrict__ dst, const float4* __restrict__ src,
+                                                 const int* __restrict__ idx, int64_t count) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t < count) dst[t] = src[idx[t]];
+}
+
+__global__ void __launch_bounds__(256) k_scatter4(float4* __restrict__ dst, const float4* __restrict__ src,
+                                                  const int* __restrict__ idx, int64_t count) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t < count) dst[idx[t]] = src[t];
+}
+
+void launch_gather4(float4* dst, const float4* src, const int* idx, int64_t count, cudaStream_t s) {
+  if (count > 0) k_gather4<<<static_cast<unsigned>((count + 255) / 256), 256, 0, s>>>(dst, src, idx, count);
+}
+
+void launch_scatter4(float4* dst, const float4* src, const int* idx, int64_t count, cudaStream_t s) {
+  if (count > 0) k_scatter4<<<static_cast<unsigned>((count + 255) / 256), 256, 0, s>>>(dst, src, idx, count);
 }
 
 void launch_cell_clear(uint4* cells, const uint32_t* prev_keys, const long long* prev_count, int64_t n_max,

@@ -65,7 +65,9 @@ struct IntegrateArgs {
   uint32_t* box_min;  // per body 3 x order-preserving uint of the min corner of X~
   uint32_t* box_max;
   const long long* substep_counter;
-  int64_t n;
+  const uint8_t* role;  // slab mode: per-body role (0 inactive, 1 ghost, 2 owned), else null
+  int64_t p0;           // first slot of the launch range (slab mode: active range)
+  int64_t n;            // end of the launch range
   float dt, gravity, inv_h;
   double dt_d;
   uint32_t mask;
@@ -86,7 +88,8 @@ struct BroadArgs {
   int* npartners;      // [nb], -1 = overflow (search every particle of the body)
   int* partners;       // [nb * PBDR_PARTNER_CAP]
   unsigned* oversize;  // set when a body box exceeds max_extent (disables the skip)
-  int nb;
+  const int* list;     // slab mode: the active bodies (ascending), else null (all bodies)
+  int nb;              // bodies in the list (all bodies when list is null)
   float inv_cell;      // 1 / coarse cell
   float max_extent;    // coarse cell - inflation: the largest box the grid guarantees
   float inflate;       // h, slightly enlarged
@@ -112,7 +115,9 @@ struct NearArgs {
   uint32_t* vals_c;       // compacted slots (sort input)
   int* near_list;         // compacted slots (slot order)
   int* ncand;             // zeroed for particles that are not near
-  int64_t n;
+  const uint8_t* role;    // slab mode: inactive bodies' particles are never near
+  int64_t p0;             // first slot of the range (slab mode: active range)
+  int64_t n;              // end of the range
   int blocks;
   float inflate;
 };
@@ -193,6 +198,8 @@ void launch_integrate(const IntegrateArgs& a, cudaStream_t s);
 void launch_body_keys(const BroadArgs& a, cudaStream_t s);
 void launch_body_ranges(const BroadArgs& a, cudaStream_t s);
 void launch_body_partners(const BroadArgs& a, cudaStream_t s);
+void launch_gather4(float4* dst, const float4* src, const int* idx, int64_t count, cudaStream_t s);
+void launch_scatter4(float4* dst, const float4* src, const int* idx, int64_t count, cudaStream_t s);
 void launch_near(const NearArgs& a, cudaStream_t s);
 void launch_cell_clear(uint4* cells, const uint32_t* prev_keys, const long long* prev_count, int64_t n_max,
                        cudaStream_t s);

@@ -306,6 +306,7 @@ struct CubeGridSpec {
   double vmax; // linear velocity U[-vmax, vmax]^3
   double wmax; // angular velocity U[-wmax, wmax]^3 (0 = none)
   double max_tilt = 0.0;  // > 0: rotation by angle U[0, max_tilt] about a uniform axis
+  bool x_major = false;   // body order: x slowest (x-slabs are contiguous body ranges)
 };
 
 // Rotation by angle U[0, max_angle] about a uniformly distributed axis (three
@@ -327,9 +328,19 @@ static int64_t gen_cube_grid(GeneratedScene& s, SplitMix& rng, const CubeGridSpe
   const std::vector<V3> lat = lattice_box(hh, hh, hh, g.n, g.n, g.n, &r);
   HullGrid grid(0.5);
   int64_t forced = 0;
-  for (int k = 0; k < g.gz; ++k)
-    for (int j = 0; j < g.gy; ++j)
-      for (int i = 0; i < g.gx; ++i) {
+  const int64_t cells = static_cast<int64_t>(g.gx) * g.gy * g.gz;
+  for (int64_t t = 0; t < cells; ++t) {
+      int i, j, k;
+      if (g.x_major) {
+        k = static_cast<int>(t % g.gz);
+        j = static_cast<int>((t / g.gz) % g.gy);
+        i = static_cast<int>(t / (static_cast<int64_t>(g.gz) * g.gy));
+      } else {
+        i = static_cast<int>(t % g.gx);
+        j = static_cast<int>((t / g.gx) % g.gy);
+        k = static_cast<int>(t / (static_cast<int64_t>(g.gx) * g.gy));
+      }
+      {
         const V3 base = {g.origin.x + g.pitch * i, g.origin.y + g.pitch * j, g.origin.z + g.pitch * k};
         Rot R{};
         V3 c{};
@@ -346,6 +357,7 @@ static int64_t gen_cube_grid(GeneratedScene& s, SplitMix& rng, const CubeGridSpe
         const V3 w = g.wmax > 0 ? uniform_box(rng, -g.wmax, g.wmax) : V3{0, 0, 0};
         add_body(s, lat, r, g.mass, R, c, v, w, scene_id);
       }
+  }
   return forced;
 }
 
@@ -417,11 +429,13 @@ static void gen_c4(GeneratedScene& s, uint64_t seed, int64_t ns, int64_t first_s
 // take uniformly random orientations at pitch 0.2 without overlapping, so the
 // orientation is a seeded tilt of U[0, 0.07] rad about a uniform axis and the
 // jitter is U[-0.01,0.01]^3 -- together provably overlap-free.
+// Bodies are numbered x-major, so an x-slab (slab.py) is a contiguous range of
+// bodies and slots up to migrations.
 static void gen_c5(GeneratedScene& s, uint64_t seed, int64_t gx) {
   SplitMix rng(seed);
   const int g = static_cast<int>(gx);
   const double half = 0.5 * 0.2 * (g - 1);
-  CubeGridSpec spec{g, g, std::max(1, g / 2), 0.2, {-half, -half, 0.2}, 0.01, 8, 1.0, 0.5, 0.0, 0.07};
+  CubeGridSpec spec{g, g, std::max(1, g / 2), 0.2, {-half, -half, 0.2}, 0.01, 8, 1.0, 0.5, 0.0, 0.07, true};
   s.forced_overlaps = gen_cube_grid(s, rng, spec, 0);
   s.frames = 100;
 }

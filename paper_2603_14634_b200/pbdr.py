@@ -113,6 +113,9 @@ class Info(C.Structure):
 _lib = None
 
 
+FIELD_POSITION, FIELD_VELOCITY, FIELD_ANCHOR, FIELD_ROTATION = 0, 1, 2, 3
+
+
 def lib() -> C.CDLL:
     """Loads the in-tree CUDA library; raises loudly when it has not been built."""
     global _lib
@@ -150,6 +153,12 @@ def lib() -> C.CDLL:
         L.pbdr_gpu_debug_near_count.argtypes = [vp, C.POINTER(i64)]
         L.pbdr_gpu_debug_read_rquat.argtypes = [vp, vp]
         L.pbdr_gpu_debug_write_rquat.argtypes = [vp, vp]
+        for name in ("pbdr_gpu_substep_begin", "pbdr_gpu_substep_iteration", "pbdr_gpu_sync"):
+            getattr(L, name).argtypes = [vp]
+        L.pbdr_gpu_stream.argtypes = [vp, C.POINTER(vp)]
+        L.pbdr_gpu_set_roles.argtypes = [vp, vp]
+        for name in ("pbdr_gpu_gather", "pbdr_gpu_scatter"):
+            getattr(L, name).argtypes = [vp, C.c_int, vp, i64, vp]
         L.pbdr_scene_generate.argtypes = [C.c_int, C.c_uint64, i64, C.POINTER(vp)]
         L.pbdr_scene_generate_c4_shard.argtypes = [C.c_uint64, i64, i64, C.POINTER(vp)]
         L.pbdr_scene_view.argtypes = [vp, C.POINTER(SceneDesc), C.POINTER(SolverCfg)]
@@ -415,6 +424,32 @@ class GpuSolver:
 
     def step_frames(self, frames: int = 1):
         raise_status(lib().pbdr_gpu_step_frames(self._h, frames))
+
+    # ---- staged stepping / x-slab decomposition (include/pbdr_gpu.h) ----------
+    def substep_begin(self):
+        raise_status(lib().pbdr_gpu_substep_begin(self._h))
+
+    def substep_iteration(self):
+        raise_status(lib().pbdr_gpu_substep_iteration(self._h))
+
+    def sync(self):
+        raise_status(lib().pbdr_gpu_sync(self._h))
+
+    def stream_handle(self) -> int:
+        s = C.c_void_p()
+        raise_status(lib().pbdr_gpu_stream(self._h, C.byref(s)))
+        return s.value or 0
+
+    def set_roles(self, roles=None):
+        r = None if roles is None else np.ascontiguousarray(roles, np.int8)
+        raise_status(lib().pbdr_gpu_set_roles(self._h, None if r is None else r.ctypes.data_as(C.c_void_p)))
+
+    def gather_dev(self, field: int, index_ptr: int, count: int, dst_ptr: int):
+        """float4 records by index, device pointers, enqueued on the handle's stream."""
+        raise_status(lib().pbdr_gpu_gather(self._h, field, C.c_void_p(index_ptr), count, C.c_void_p(dst_ptr)))
+
+    def scatter_dev(self, field: int, index_ptr: int, count: int, src_ptr: int):
+        raise_status(lib().pbdr_gpu_scatter(self._h, field, C.c_void_p(index_ptr), count, C.c_void_p(src_ptr)))
 
     def time_frames(self, frames: int) -> float:
         ms = C.c_float()
