@@ -10,8 +10,11 @@ Default workload (N=1): config 4 (BASELINE.json configs[3]) -- 4096 batched
 independent scenes of 16 cubes (14,155,776 particles), the largest config the
 metric's 1/2/4/8-GPU scaling is quoted on that shards with no communication.
 Under torchrun each rank simulates its own 4096 scenes (weak scaling). Other
-configs: --config 1..5 (C5 at N=1 is the single giant scene; its x-slab halo
-exchange is not built yet, so --config 5 runs replicas under torchrun).
+configs: --config 1..5. --config 5 under torchrun runs the single giant scene
+split into x-slabs (paper_2603_14634_b200/slab.py): each rank owns the bodies
+whose com lies in its slab, ghosts are refreshed over NCCL after every
+iteration, bodies migrate at frame boundaries (strong scaling: the scene is
+fixed as N grows). C1-C3 run replicas under torchrun.
 
 --impl reference times the oracle restatement of the reference's CPU solver
 (the reference's own solver.cpp is absent from /root/reference, so the port is
@@ -216,11 +219,81 @@ def reference_arm(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def slab_bench(args, rank, world, local):
+    """Config 5 split into x-slabs across the ranks (one scene, NCCL halo)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2603_14634_b200 import pbdr as P
+    from paper_2603_14634_b200 import slab as S
+
+    g = P.GeneratedScene(5, seed=args.seed, scale=args.scale)
+    nb = g.desc.num_bodies
+    off = g.array("body_offsets", nb + 1, np.int64)
+    rho, h = S.body_reach(g.array("rest_offsets", 3 * g.num_particles), off, g.array("radius", g.num_particles))
+    solver = P.GpuSolver(g.desc, g.cfg, device=local)
+    eng = S.GpuEngine(solver, g.cfg)
+    run = S.SlabRunner(eng, rank, world, S.TorchComm(), off, rho=rho, h=h, margin=0.1)
+    run.start()
+    run.step_frames(max(3, args.warmup))
+    dist.barrier()
+    torch.cuda.synchronize(local)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        ev0.record(eng.stream)
+        run.step_frames(args.steps)
+        ev1.record(eng.stream)
+        ev1.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    dist.barrier()
+    t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    n_total = solver.n
+    subs = g.cfg.substeps
+    value = n_total * subs * args.steps / (ms_max / 1e3)
+    owned = torch.tensor([sum(int(run.bcount[b]) for b in run.owned)], dtype=torch.int64, device=f"cuda:{local}")
+    owned_max = owned.clone()
+    dist.all_reduce(owned_max, op=dist.ReduceOp.MAX)
+    ghosts = sum(len(v) for v in run.plan.recv_bodies.values())
+    peak, peak_src = measured_peak()
+    if rank == 0:
+        line = {
+            "metric": "particle-substeps/s", "value": value, "unit": "particle-substeps/s", "n_gpus": world,
+            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded BASELINE.json config 5, host generator)",
+            "config": {"workload": P.CONFIG_NAMES[5], "particles_total": n_total, "bodies_total": nb,
+                       "substeps_per_step": subs, "iterations": g.cfg.solver_iterations,
+                       "parallelism": f"x-slab x{world}, NCCL halo after every iteration, migration per frame",
+                       "max_owned_particles_per_gpu": int(owned_max.item()), "ghost_bodies_rank0": ghosts,
+                       "ghost_band_m": run.geo.ghost_band,
+                       "l2": "inputs larger than L2"},
+            "roofline": {"bound": "hbm", "achieved": (value / world) * BYTES_PER_SUBSTEP / 1e9, "peak": peak,
+                         "unit": "GB/s", "frac": (value / world) * BYTES_PER_SUBSTEP / (peak * 1e9),
+                         "traffic": None, "kernel": "whole substep (per GPU)", "peak_source": peak_src},
+            "cpu_baseline": None,
+            "e2e": None,
+            "gpu_launches": int(solver.info.launches_per_frame * args.steps),
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    solver.close()
+    dist.destroy_process_group()
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
     if args.impl == "reference":
         reference_arm(args, rank, world)
+        return
+    if args.config == 5 and world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        slab_bench(args, rank, world, local)
         return
 
     import torch
