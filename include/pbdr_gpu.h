@@ -195,6 +195,18 @@ int pbdr_gpu_debug_write_anchor(pbdr_handle* h, const float* anchor3);
 int pbdr_gpu_debug_read_rquat(pbdr_handle* h, float* q4);
 int pbdr_gpu_debug_write_rquat(pbdr_handle* h, const float* q4);
 
+/* ---- Trajectory emission ------------------------
+ * When enabled, every frame stepped by pbdr_gpu_step_frames / _time_frames
+ * appends one pbdr_body_stats per body (com, orientation vs rest, P, L; the
+ * same numbers as pbdr_gpu_read_bodies at that frame) to a device ring of
+ * `capacity_frames` frames -- one extra launch per frame, no host sync. Drain
+ * copies the pending frames (oldest first; out: frames x num_bodies x 13
+ * doubles, t: frames seconds) and empties the ring; a full ring makes the next
+ * step return an error. capacity 0 disables emission. In slab mode only the
+ * owned bodies' records are written. */
+int pbdr_gpu_trajectory_enable(pbdr_handle* h, int64_t capacity_frames);
+int pbdr_gpu_trajectory_drain(pbdr_handle* h, double* out, double* t, int64_t max_frames, int64_t* frames);
+
 /* ---- Staged stepping and x-slab decomposition --
  * One substep = pbdr_gpu_substep_begin (integrate, hash grid, candidate lists)
  * followed by solver_iterations calls of pbdr_gpu_substep_iteration; both only

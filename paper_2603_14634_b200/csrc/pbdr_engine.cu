@@ -122,6 +122,13 @@ struct pbdr_handle {
   Packing slab_iter, slab_active;  // device storage (capacity nb CTAs)
   int stage_iter = 0;
 
+  // Trajectory emission: per frame, per owned body, the 13-double
+  // sample of pbdr_body_stats into a device ring drained by the host.
+  double* traj = nullptr;
+  int64_t traj_cap = 0;      // frames the ring holds
+  int64_t traj_pending = 0;  // frames written since the last drain
+  std::vector<double> traj_t;  // time stamp of each pending frame
+
   cudaGraphExec_t graph[2] = {nullptr, nullptr};
   int graph_end[2] = {0, 0};
   int64_t substeps_done = 0;
@@ -783,6 +790,20 @@ int pbdr_gpu_step(pbdr_handle* h, int64_t substeps) {
   return check_errors(h);
 }
 
+static void enqueue_stats(pbdr_handle* h, double* out) {
+  pbdr_dev::StatsArgs sa{};
+  sa.pos = h->pos[h->cur];
+  sa.vel = h->vel;
+  sa.rest = h->rest;
+  sa.anchor = h->anchor;
+  sa.cta_desc = h->pk_iter.cta;
+  sa.warp_desc = h->pk_iter.warp;
+  sa.body_desc = h->pk_iter.body;
+  sa.body_mass = h->body_mass;
+  sa.out = out;
+  if (h->pk_iter.ctas > 0) pbdr_dev::launch_stats(sa, h->pk_iter.ctas, h->stream);
+}
+
 static int step_frames_async(pbdr_handle* h, int64_t frames) {
   for (int64_t f = 0; f < frames; ++f) {
     const int parity = h->cur;
@@ -790,9 +811,16 @@ static int step_frames_async(pbdr_handle* h, int64_t frames) {
       const int rc = build_graph(h, parity);
       if (rc != PBDR_OK) return rc;
     }
+    if (h->traj && h->traj_pending == h->traj_cap)
+      return set_error(PBDR_ERR_GENERIC, "trajectory ring full: drain it (pbdr_gpu_trajectory_drain)");
     PBDR_CUDA(cudaGraphLaunch(h->graph[parity], h->stream));
     h->cur = h->graph_end[parity];
     h->substeps_done += h->substeps;
+    if (h->traj) {
+      enqueue_stats(h, h->traj + h->traj_pending * static_cast<int64_t>(h->nb) * 13);
+      h->traj_t.push_back(static_cast<double>(h->substeps_done) * h->dt_d);
+      ++h->traj_pending;
+    }
   }
   return PBDR_OK;
 }
@@ -910,17 +938,7 @@ int pbdr_gpu_read_bodies(pbdr_handle* h, pbdr_body_stats* out) {
   if (!h || !out) return set_error(PBDR_ERR_GENERIC, "null argument");
   static_assert(sizeof(pbdr_body_stats) == 13 * sizeof(double), "stats layout");
   PBDR_CUDA(cudaSetDevice(h->device));
-  pbdr_dev::StatsArgs sa{};
-  sa.pos = h->pos[h->cur];
-  sa.vel = h->vel;
-  sa.rest = h->rest;
-  sa.anchor = h->anchor;
-  sa.cta_desc = h->pk_iter.cta;
-  sa.warp_desc = h->pk_iter.warp;
-  sa.body_desc = h->pk_iter.body;
-  sa.body_mass = h->body_mass;
-  sa.out = h->stats;
-  if (h->pk_iter.ctas > 0) pbdr_dev::launch_stats(sa, h->pk_iter.ctas, h->stream);
+  enqueue_stats(h, h->stats);
   PBDR_CUDA(cudaGetLastError());
   PBDR_CUDA(cudaMemcpyAsync(out, h->stats, sizeof(double) * 13 * h->nb, cudaMemcpyDeviceToHost, h->stream));
   PBDR_CUDA(cudaStreamSynchronize(h->stream));
@@ -1077,6 +1095,43 @@ int pbdr_gpu_debug_write_anchor(pbdr_handle* h, const float* anchor3) {
   std::vector<float4> a(h->nb);
   for (int32_t b = 0; b < h->nb; ++b) a[b] = make_float4(anchor3[3 * b], anchor3[3 * b + 1], anchor3[3 * b + 2], 0.0f);
   PBDR_CUDA(cudaMemcpy(h->anchor, a.data(), sizeof(float4) * h->nb, cudaMemcpyHostToDevice));
+  return PBDR_OK;
+}
+
+// ---- Trajectory emission -----------------------------------------------------
+int pbdr_gpu_trajectory_enable(pbdr_handle* h, int64_t capacity_frames) {
+  if (!h) return set_error(PBDR_ERR_GENERIC, "null handle");
+  PBDR_CUDA(cudaSetDevice(h->device));
+  PBDR_CUDA(cudaStreamSynchronize(h->stream));
+  if (h->traj) {
+    cudaFree(h->traj);
+    h->allocations.erase(std::find(h->allocations.begin(), h->allocations.end(), static_cast<void*>(h->traj)));
+    h->traj = nullptr;
+  }
+  h->traj_cap = 0;
+  h->traj_pending = 0;
+  h->traj_t.clear();
+  if (capacity_frames <= 0) return PBDR_OK;
+  const int rc = dalloc(h, &h->traj, static_cast<size_t>(capacity_frames) * h->nb * 13);
+  if (rc != PBDR_OK) return rc;
+  h->traj_cap = capacity_frames;
+  return PBDR_OK;
+}
+
+int pbdr_gpu_trajectory_drain(pbdr_handle* h, double* out, double* t, int64_t max_frames, int64_t* frames) {
+  if (!h || !frames) return set_error(PBDR_ERR_GENERIC, "null argument");
+  PBDR_CUDA(cudaSetDevice(h->device));
+  PBDR_CUDA(cudaStreamSynchronize(h->stream));
+  const int64_t k = std::min(h->traj_pending, max_frames);
+  if (k < h->traj_pending)
+    return set_error(PBDR_ERR_GENERIC, "trajectory drain: output holds fewer frames than pending");
+  if (k > 0 && out)
+    PBDR_CUDA(cudaMemcpy(out, h->traj, sizeof(double) * 13 * h->nb * k, cudaMemcpyDeviceToHost));
+  if (t)
+    for (int64_t f = 0; f < k; ++f) t[f] = h->traj_t[f];
+  *frames = k;
+  h->traj_pending = 0;
+  h->traj_t.clear();
   return PBDR_OK;
 }
 

@@ -156,6 +156,8 @@ def lib() -> C.CDLL:
         for name in ("pbdr_gpu_substep_begin", "pbdr_gpu_substep_iteration", "pbdr_gpu_sync"):
             getattr(L, name).argtypes = [vp]
         L.pbdr_gpu_stream.argtypes = [vp, C.POINTER(vp)]
+        L.pbdr_gpu_trajectory_enable.argtypes = [vp, i64]
+        L.pbdr_gpu_trajectory_drain.argtypes = [vp, vp, vp, i64, C.POINTER(i64)]
         L.pbdr_gpu_set_roles.argtypes = [vp, vp]
         for name in ("pbdr_gpu_gather", "pbdr_gpu_scatter"):
             getattr(L, name).argtypes = [vp, C.c_int, vp, i64, vp]
@@ -424,6 +426,20 @@ class GpuSolver:
 
     def step_frames(self, frames: int = 1):
         raise_status(lib().pbdr_gpu_step_frames(self._h, frames))
+
+    # ---- trajectory emission ------------------------------------
+    def enable_trajectory(self, capacity_frames: int):
+        self._traj_cap = capacity_frames
+        raise_status(lib().pbdr_gpu_trajectory_enable(self._h, capacity_frames))
+
+    def drain_trajectory(self):
+        """(t[frames], stats[frames, num_bodies, 13]) of the frames since the last drain."""
+        cap = getattr(self, "_traj_cap", 0)
+        out = np.zeros((cap, self.nb, 13), np.float64)
+        t = np.zeros(cap, np.float64)
+        k = C.c_int64()
+        raise_status(lib().pbdr_gpu_trajectory_drain(self._h, _ptr(out), _ptr(t), cap, C.byref(k)))
+        return t[:k.value].copy(), out[:k.value].copy()
 
     # ---- staged stepping / x-slab decomposition (include/pbdr_gpu.h) ----------
     def substep_begin(self):
