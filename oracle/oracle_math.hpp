@@ -144,6 +144,25 @@ inline M3 quat_to(const double q[4]) {
   return r;
 }
 
+// |q|^2 R(q) for a non-unit quaternion (homogeneous form).
+inline M3 quat_to_h(const double q[4]) {
+  const double w = q[0], x = q[1], y = q[2], z = q[3];
+  const double w2 = w * w, xx = x * x, yy = y * y, zz = z * z;
+  const double xy = x * y, xz = x * z, yz = y * z;
+  const double wx = w * x, wy = w * y, wz = w * z;
+  M3 r;
+  r.a[0][0] = (w2 + xx) - (yy + zz);
+  r.a[0][1] = 2.0 * (xy - wz);
+  r.a[0][2] = 2.0 * (xz + wy);
+  r.a[1][0] = 2.0 * (xy + wz);
+  r.a[1][1] = (w2 + yy) - (xx + zz);
+  r.a[1][2] = 2.0 * (yz - wx);
+  r.a[2][0] = 2.0 * (xz - wy);
+  r.a[2][1] = 2.0 * (yz + wx);
+  r.a[2][2] = (w2 + zz) - (xx + yy);
+  return r;
+}
+
 inline double frob2(const M3& m) {
   double s = 0.0;
   for (int i = 0; i < 3; ++i)
@@ -303,14 +322,11 @@ inline bool polar_warm(const M3& A, const float rq[4], M3& R, double q[4]) {
   const double c3 = frob2(A) * PBDR_ONE_THIRD;
   if (!(d0 > 0.0) || d0 * d0 <= (PBDR_POLAR_REL_DET * PBDR_POLAR_REL_DET) * ((c3 * c3) * c3)) return false;
   if (rq[0] != 0.0f || rq[1] != 0.0f || rq[2] != 0.0f || rq[3] != 0.0f) {
+    // Homogeneous iterate: qc is not renormalised between steps; R0 below is
+    // |qc|^2 R(qc), and the step h is invariant under that uniform scale.
     double qc[4] = {rq[0], rq[1], rq[2], rq[3]};
-    {
-      const double n = std::sqrt(((qc[0] * qc[0] + qc[1] * qc[1]) + qc[2] * qc[2]) + qc[3] * qc[3]);
-      const double in = 1.0 / n;
-      for (int k = 0; k < 4; ++k) qc[k] = qc[k] * in;
-    }
     for (int step = 0; step < PBDR_POLAR_WARM_STEPS; ++step) {
-      const M3 R0 = quat_to(qc);
+      const M3 R0 = quat_to_h(qc);
       double B[3][3];
       for (int i = 0; i < 3; ++i)
         for (int j = 0; j < 3; ++j)
@@ -344,14 +360,14 @@ inline bool polar_warm(const M3& A, const float rq[4], M3& R, double q[4]) {
       qn[1] = (qc[0] * h[0] + qc[1]) + (qc[2] * h[2] - qc[3] * h[1]);
       qn[2] = (qc[0] * h[1] + qc[2]) + (qc[3] * h[0] - qc[1] * h[2]);
       qn[3] = (qc[0] * h[2] + qc[3]) + (qc[1] * h[1] - qc[2] * h[0]);
-      const double n = std::sqrt(((qn[0] * qn[0] + qn[1] * qn[1]) + qn[2] * qn[2]) + qn[3] * qn[3]);
-      const double in = 1.0 / n;
-      for (int k = 0; k < 4; ++k) qc[k] = qn[k] * in;
-      if (ww <= PBDR_POLAR_TOLQ) {
-        for (int k = 0; k < 4; ++k) q[k] = qc[k];
-        R = quat_to(qc);
+      if (ww <= PBDR_POLAR_WARM_TOLQ) {
+        const double n = std::sqrt(((qn[0] * qn[0] + qn[1] * qn[1]) + qn[2] * qn[2]) + qn[3] * qn[3]);
+        const double in = 1.0 / n;
+        for (int k = 0; k < 4; ++k) q[k] = qn[k] * in;
+        R = quat_to(q);
         return true;
       }
+      for (int k = 0; k < 4; ++k) qc[k] = qn[k];
     }
   }
   return polar_rotation(A, R, q);

@@ -61,6 +61,42 @@ __device__ __forceinline__ void warp_butterfly(float (&acc)[F]) {
     for (int f = 0; f < F; ++f) acc[f] = acc[f] + __shfl_xor_sync(kFull, acc[f], off);
 }
 
+// Same reduction tree as warp_butterfly (xor offsets 16, 8, 4, 2, 1; every add
+// combines the partial sums of lanes l and l^off), computed by recursive
+// halving: at each offset a lane keeps half of the remaining fields and
+// exchanges the other half, so F fields cost ~P-1 shuffles instead of 5F
+// (P = F rounded up to a power of two). On return lane l holds the total of
+// field l * P / 32 (every lane of a group of 32/P holds the same value);
+// the totals are bit-identical to warp_butterfly's (IEEE add is commutative).
+template <int F>
+__device__ __forceinline__ float warp_reduce_scatter(const float (&acc)[F]) {
+  constexpr int P = F <= 1 ? 1 : F <= 2 ? 2 : F <= 4 ? 4 : F <= 8 ? 8 : F <= 16 ? 16 : 32;
+  static_assert(F <= 32, "at most 32 fields");
+  const int lane = threadIdx.x & 31;
+  float v[P];
+#pragma unroll
+  for (int f = 0; f < P; ++f) v[f] = f < F ? acc[f] : 0.0f;
+  int c = P;
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) {
+    if (c > 1) {
+      const bool up = (lane & off) != 0;
+      const int h = c / 2;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        if (k >= h) break;
+        const float send = up ? v[k] : v[h + k];
+        const float keep = up ? v[h + k] : v[k];
+        v[k] = keep + __shfl_xor_sync(kFull, send, off);
+      }
+      c = h;
+    } else {
+      v[0] = v[0] + __shfl_xor_sync(kFull, v[0], off);
+    }
+  }
+  return v[0];
+}
+
 // ---- TMA bulk staging (cp.async.bulk + mbarrier) ---------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -493,6 +529,54 @@ __global__ void __launch_bounds__(128) k_neighbours(NeighbourArgs A) {
 // k < 4. Warp 0 runs the per-body fp64 math for all bodies of the CTA, one
 // lane per body.
 // ---------------------------------------------------------------------------
+// One particle-particle contact of particle i (slot p, X_i = x, inverse mass
+// w) against candidate j: Jacobi delta accumulated into dPP.
+__device__ __forceinline__ void pp_contact(const float x[3], float w, int64_t p, float4 xj, int j, float rr,
+                                           float relax, float dPP[3]) {
+  const float e[3] = {x[0] - xj.x, x[1] - xj.y, x[2] - xj.z};
+  const float d2 = (e[0] * e[0] + e[1] * e[1]) + e[2] * e[2];
+  if (d2 < rr * rr) {
+    const float dist = sqrtf(d2);
+    float nrm[3];
+    if (dist > PBDR_COINCIDENT_EPS) {
+      const float inv = 1.0f / dist;
+      nrm[0] = e[0] * inv; nrm[1] = e[1] * inv; nrm[2] = e[2] * inv;
+    } else {
+      nrm[0] = p < j ? 1.0f : -1.0f; nrm[1] = 0.0f; nrm[2] = 0.0f;
+    }
+    const float C = dist - rr;
+    const float kk = (relax * (w / (w + xj.w))) * C;
+    dPP[0] = dPP[0] - kk * nrm[0];
+    dPP[1] = dPP[1] - kk * nrm[1];
+    dPP[2] = dPP[2] - kk * nrm[2];
+  }
+}
+
+#ifndef PBDR_STAGE_INIT
+#define PBDR_STAGE_INIT 0
+#endif
+#ifndef PBDR_FLAT_CAND
+#define PBDR_FLAT_CAND 0
+#endif
+// Per-body math of the CTA's bodies: one lane per body on warp 0, or (per-warp
+// mode) lane 0 of warp b for body b, so the bodies' fp64 chains issue from
+// different warps / SM sub-partitions instead of sharing one warp.
+#ifndef PBDR_MATH_PER_WARP
+#define PBDR_MATH_PER_WARP 0
+#endif
+#if PBDR_MATH_PER_WARP
+#define PBDR_MATH_ACTIVE (lane == 0 && warp < cd.w)
+#define PBDR_MATH_BODY warp
+#else
+#define PBDR_MATH_ACTIVE (warp == 0 && lane < cd.w)
+#define PBDR_MATH_BODY lane
+#endif
+#if PBDR_STAGE_INIT
+#define PBDR_INIT_AT(gslot, sslot) s_init[(sslot)]
+#else
+#define PBDR_INIT_AT(gslot, sslot) A.init[(gslot)]
+#endif
+
 constexpr int kResF = 32;
 enum ResSlot {
   kResC = 0,      // c (3), anchor-relative com of X_i
@@ -510,7 +594,7 @@ enum ResSlot {
 #define PBDR_ITER_MINBLOCKS 3
 #endif
 __global__ void __launch_bounds__(kThreads, PBDR_ITER_MINBLOCKS) k_iteration(IterArgs A) {
-  extern __shared__ float4 s_stage[];  // pos | vel | rest, kSlots each
+  extern __shared__ float4 s_stage[];  // pos | vel | rest [| init], kSlots each
   __shared__ float s_part[kWarps][21];
   __shared__ float s_res[kWarps][kResF];
   __shared__ __align__(8) uint64_t s_bar;
@@ -518,6 +602,9 @@ __global__ void __launch_bounds__(kThreads, PBDR_ITER_MINBLOCKS) k_iteration(Ite
   float4* s_pos = s_stage;
   float4* s_vel = s_stage + kSlots;
   float4* s_rest = s_stage + 2 * kSlots;
+#if PBDR_STAGE_INIT
+  float4* s_init = s_stage + 3 * kSlots;
+#endif
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -527,7 +614,12 @@ __global__ void __launch_bounds__(kThreads, PBDR_ITER_MINBLOCKS) k_iteration(Ite
   if (threadIdx.x == 0) {
     mbar_init(&s_bar, 1);
     const uint32_t bytes = static_cast<uint32_t>(cd.y) * 16u;
+#if PBDR_STAGE_INIT
+    mbar_expect_tx(&s_bar, 4u * bytes);
+    bulk_g2s(s_init, A.init + first, bytes, &s_bar);
+#else
     mbar_expect_tx(&s_bar, 3u * bytes);
+#endif
     bulk_g2s(s_pos, A.pos_in + first, bytes, &s_bar);
     bulk_g2s(s_vel, A.vel + first, bytes, &s_bar);
     bulk_g2s(s_rest, A.rest + first, bytes, &s_bar);
@@ -583,8 +675,45 @@ __global__ void __launch_bounds__(kThreads, PBDR_ITER_MINBLOCKS) k_iteration(Ite
 #pragma unroll
   for (int f = 0; f < 21; ++f) acc[f] = 0.0f;
 #pragma unroll
+  for (int k = 0; k < PBDR_KP; ++k) dX[k][0] = dX[k][1] = dX[k][2] = 0.0f;
+#if PBDR_FLAT_CAND
+  // Particle-particle deltas first, candidate rank c outermost: the loads of
+  // the lane's KP particles for one rank are independent and overlap. Per
+  // particle the sum still runs over c ascending from +0.
+  {
+    int cmax = 0;
+#pragma unroll
+    for (int k = 0; k < PBDR_KP; ++k) cmax = max(cmax, ncs[k]);
+    for (int c = 0; c < cmax; ++c) {
+      int jj[PBDR_KP];
+      float rr[PBDR_KP];
+      float4 xj[PBDR_KP];
+#pragma unroll
+      for (int k = 0; k < PBDR_KP; ++k) {
+        const int64_t p = start + k * 32 * W + wi * 32 + lane;
+        jj[k] = 0;
+        rr[k] = 0.0f;
+        if (c < ncs[k]) {
+          jj[k] = A.cand_j[static_cast<int64_t>(c) * A.n + p];
+          rr[k] = A.cand_rr[static_cast<int64_t>(c) * A.n + p];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < PBDR_KP; ++k)
+        if (c < ncs[k]) xj[k] = A.pos_in[jj[k]];
+#pragma unroll
+      for (int k = 0; k < PBDR_KP; ++k) {
+        if (!(c < ncs[k])) continue;
+        const int q = k * 32 * W + wi * 32 + lane;
+        const float4 x4 = s_pos[off + q];
+        const float x[3] = {x4.x, x4.y, x4.z};
+        pp_contact(x, x4.w, start + q, xj[k], jj[k], rr[k], A.relax, dX[k]);
+      }
+    }
+  }
+#endif
+#pragma unroll
   for (int k = 0; k < PBDR_KP; ++k) {
-    dX[k][0] = dX[k][1] = dX[k][2] = 0.0f;
     const int q = k * 32 * W + wi * 32 + lane;
     if (!(live && q < n)) continue;
     const int64_t p = start + q;
@@ -606,7 +735,7 @@ __global__ void __launch_bounds__(kThreads, PBDR_ITER_MINBLOCKS) k_iteration(Ite
         dPG[2] = dPG[2] + push * Pn[2];
         const float mu = A.planes.mu[pl];
         if (mu > 0.0f) {
-          const float4 xi = A.init[p];
+          const float4 xi = PBDR_INIT_AT(p, off + q);
           const float t[3] = {x[0] - xi.x, x[1] - xi.y, x[2] - xi.z};
           const float tn = (t[0] * Pn[0] + t[1] * Pn[1]) + t[2] * Pn[2];
           const float tt[3] = {t[0] - tn * Pn[0], t[1] - tn * Pn[1], t[2] - tn * Pn[2]};
@@ -628,30 +757,22 @@ __global__ void __launch_bounds__(kThreads, PBDR_ITER_MINBLOCKS) k_iteration(Ite
         }
       }
     }
+#if PBDR_FLAT_CAND
+    float dPP[3] = {dX[k][0], dX[k][1], dX[k][2]};  // candidates summed before this loop
+#else
     float dPP[3] = {0.0f, 0.0f, 0.0f};
+#ifdef PBDR_DIAG_NO_PP
+    const int nc = 0;  // diagnostic build only
+#else
     const int nc = ncs[k];
+#endif
     for (int c = 0; c < nc; ++c) {
       const int j = A.cand_j[static_cast<int64_t>(c) * A.n + p];
       const float rr = A.cand_rr[static_cast<int64_t>(c) * A.n + p];
       const float4 xj = A.pos_in[j];
-      const float e[3] = {x[0] - xj.x, x[1] - xj.y, x[2] - xj.z};
-      const float d2 = (e[0] * e[0] + e[1] * e[1]) + e[2] * e[2];
-      if (d2 < rr * rr) {
-        const float dist = sqrtf(d2);
-        float nrm[3];
-        if (dist > PBDR_COINCIDENT_EPS) {
-          const float inv = 1.0f / dist;
-          nrm[0] = e[0] * inv; nrm[1] = e[1] * inv; nrm[2] = e[2] * inv;
-        } else {
-          nrm[0] = p < j ? 1.0f : -1.0f; nrm[1] = 0.0f; nrm[2] = 0.0f;
-        }
-        const float C = dist - rr;
-        const float kk = (A.relax * (x4.w / (x4.w + xj.w))) * C;
-        dPP[0] = dPP[0] - kk * nrm[0];
-        dPP[1] = dPP[1] - kk * nrm[1];
-        dPP[2] = dPP[2] - kk * nrm[2];
-      }
+      pp_contact(x, x4.w, p, xj, j, rr, A.relax, dPP);
     }
+#endif
     const float v[3] = {v4.x, v4.y, v4.z};
     const float q0[3] = {r4.x, r4.y, r4.z};
     float pp[3], pb[3], mp[3], mvb[3], kb[3];
@@ -683,20 +804,18 @@ __global__ void __launch_bounds__(kThreads, PBDR_ITER_MINBLOCKS) k_iteration(Ite
     acc[20] = acc[20] + kb[2];
   }
   if (live) {
-    warp_butterfly<21>(acc);
-    if (lane == 0)
-#pragma unroll
-      for (int f = 0; f < 21; ++f) s_part[warp][f] = acc[f];
+    const float tot = warp_reduce_scatter<21>(acc);  // lane f: total of field f
+    if (lane < 21) s_part[warp][lane] = tot;
   }
   __syncthreads();
   if (tm && threadIdx.x == 0) tm[2] = clock64();
 
   // ---- per-body math A (warp 0, lane = body of the CTA) ---------------------
-  if (warp == 0 && lane < cd.w) {
-    const int bb = cd.z + lane;
-    const float4 an = s_banc[lane];
-    const float invM = s_binv[lane];
-    const int2 bw = s_bw[lane];
+  if (PBDR_MATH_ACTIVE) {
+    const int bb = cd.z + PBDR_MATH_BODY;
+    const float4 an = s_banc[PBDR_MATH_BODY];
+    const float invM = s_binv[PBDR_MATH_BODY];
+    const int2 bw = s_bw[PBDR_MATH_BODY];
     const int fw = bw.x;
     float S[21];
 #pragma unroll
@@ -716,7 +835,7 @@ __global__ void __launch_bounds__(kThreads, PBDR_ITER_MINBLOCKS) k_iteration(Ite
       Pb[k] = S[15 + k];
     }
     cross3(cb, Pb, tmp);
-    float* R = &s_res[lane][0];
+    float* R = &s_res[PBDR_MATH_BODY][0];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       R[kResC + k] = c[k];
@@ -724,9 +843,15 @@ __global__ void __launch_bounds__(kThreads, PBDR_ITER_MINBLOCKS) k_iteration(Ite
       R[kResLb + k] = S[18 + k] - tmp[k];
     }
     double qd[4];
-    const float4 rq4 = s_brq[lane];
+    const float4 rq4 = s_brq[PBDR_MATH_BODY];
     const float rq[4] = {rq4.x, rq4.y, rq4.z, rq4.w};
+#ifdef PBDR_DIAG_NO_POLAR
+    bool ok = true;  // diagnostic build only: identity rotation
+    for (int f = 0; f < 9; ++f) R[kResR + f] = (f % 4 == 0) ? 1.0f : 0.0f;
+    qd[0] = 1.0; qd[1] = qd[2] = qd[3] = 0.0;
+#else
     const bool ok = polar_warm_f(&S[6], rq, &R[kResR], qd);
+#endif
     R[kResSmOk] = ok ? 1.0f : 0.0f;
     A.rquat[bb] = ok ? make_float4(static_cast<float>(qd[0]), static_cast<float>(qd[1]),
                                    static_cast<float>(qd[2]), static_cast<float>(qd[3]))
@@ -761,7 +886,7 @@ __global__ void __launch_bounds__(kThreads, PBDR_ITER_MINBLOCKS) k_iteration(Ite
       const float q0[3] = {r4.x, r4.y, r4.z};
       float xi[3] = {0.0f, 0.0f, 0.0f};
       if (!A.incremental) {
-        const float4 i4 = A.init[start + q];
+        const float4 i4 = PBDR_INIT_AT(start + q, off + q);
         xi[0] = i4.x; xi[1] = i4.y; xi[2] = i4.z;
       }
       float xa[3], va[3], pa[3];
@@ -809,19 +934,17 @@ __global__ void __launch_bounds__(kThreads, PBDR_ITER_MINBLOCKS) k_iteration(Ite
   if (!fixes) return;
 
   if (live) {
-    warp_butterfly<15>(accB);
-    if (lane == 0)
-#pragma unroll
-      for (int f = 0; f < 15; ++f) s_part[warp][f] = accB[f];
+    const float tot = warp_reduce_scatter<15>(accB);  // lanes 2f, 2f+1: field f
+    if ((lane & 1) == 0 && (lane >> 1) < 15) s_part[warp][lane >> 1] = tot;
   }
   __syncthreads();
   if (tm && threadIdx.x == 0) tm[4] = clock64();
 
   // ---- per-body math B: momentum corrections -------------------------------
-  if (warp == 0 && lane < cd.w) {
-    const int bb = cd.z + lane;
-    const float2 mass = make_float2(s_banc[lane].w, s_binv[lane]);
-    const int2 bw = s_bw[lane];
+  if (PBDR_MATH_ACTIVE) {
+    const int bb = cd.z + PBDR_MATH_BODY;
+    const float2 mass = make_float2(s_banc[PBDR_MATH_BODY].w, s_binv[PBDR_MATH_BODY]);
+    const int2 bw = s_bw[PBDR_MATH_BODY];
     const int fw = bw.x;
     float S[15];
 #pragma unroll
@@ -833,7 +956,7 @@ __global__ void __launch_bounds__(kThreads, PBDR_ITER_MINBLOCKS) k_iteration(Ite
 #pragma unroll
     for (int f = 0; f < 15; ++f) finite = finite && isfinite(S[f]);
     if (!finite) record_error(A.err, PBDR_DEVERR_NONFINITE, bb, A.substep_counter);
-    float* R = &s_res[lane][0];
+    float* R = &s_res[PBDR_MATH_BODY][0];
     const float M = mass.x, invM = mass.y;
     float ca[3], Pa[3], La[3], tmp[3], dv[3] = {0.0f, 0.0f, 0.0f}, om[3] = {0.0f, 0.0f, 0.0f};
 #pragma unroll
@@ -879,7 +1002,12 @@ __global__ void __launch_bounds__(kThreads, PBDR_ITER_MINBLOCKS) k_iteration(Ite
       If[4] = S[13] + M * (ca[0] * ca[2]);
       If[5] = S[14] + M * (ca[1] * ca[2]);
       double nax[3];
+#ifdef PBDR_DIAG_NO_INERTIA
+      const unsigned e = 0;  // diagnostic build only
+      om[0] = dL[0] * If[0]; om[1] = dL[1] * If[1]; om[2] = dL[2] * If[2];
+#else
       const unsigned e = inertia_solve_f(If, dL, om, nax);
+#endif
       if (e) record_error(A.err, e, bb, A.substep_counter, nax);
     }
 #pragma unroll
@@ -909,7 +1037,7 @@ __global__ void __launch_bounds__(kThreads, PBDR_ITER_MINBLOCKS) k_iteration(Ite
     const float4 v4 = s_vel[off + q];
     float xi[3] = {0.0f, 0.0f, 0.0f};
     if (!A.incremental) {
-      const float4 i4 = A.init[start + q];
+      const float4 i4 = PBDR_INIT_AT(start + q, off + q);
       xi[0] = i4.x; xi[1] = i4.y; xi[2] = i4.z;
     }
     const float x[3] = {x4.x, x4.y, x4.z};
@@ -1116,7 +1244,7 @@ __global__ void __launch_bounds__(kThreads) k_body_wrench(WrenchArgs A) {
 #ifndef PBDR_ITER_EXTRA_SMEM
 #define PBDR_ITER_EXTRA_SMEM 0
 #endif
-size_t iteration_smem_bytes() { return sizeof(float4) * 3 * kSlots + PBDR_ITER_EXTRA_SMEM; }
+size_t iteration_smem_bytes() { return sizeof(float4) * (PBDR_STAGE_INIT ? 4 : 3) * kSlots + PBDR_ITER_EXTRA_SMEM; }
 
 void launch_integrate(const IntegrateArgs& a, cudaStream_t s) {
   const unsigned blocks = static_cast<unsigned>((a.n - a.p0 + 255) / 256);
@@ -1182,8 +1310,14 @@ void launch_neighbours(const NeighbourArgs& a, cudaStream_t s) {
 }
 
 cudaError_t prepare_iteration_kernel() {
-  return cudaFuncSetAttribute(k_iteration, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              static_cast<int>(iteration_smem_bytes()));
+  cudaError_t e = cudaFuncSetAttribute(k_iteration, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(iteration_smem_bytes()));
+  if (e != cudaSuccess) return e;
+#ifdef PBDR_ITER_CARVEOUT
+  return cudaFuncSetAttribute(k_iteration, cudaFuncAttributePreferredSharedMemoryCarveout, PBDR_ITER_CARVEOUT);
+#else
+  return cudaSuccess;
+#endif
 }
 
 void launch_iteration(const IterArgs& a, int ctas, cudaStream_t s) {

@@ -110,6 +110,12 @@ PBDR_HD int32_t pbdr_cell_coord(float x, float inv_h) {
  * iteration's rotation (see polar_warm in oracle_math.hpp / pbdr_mat3.cuh). */
 #define PBDR_POLAR_WARM_STEPS 4
 #define PBDR_POLAR_WARM_MAX2 0.25
+/* A Gauss-Newton step of squared size <= 1e-10 (|w| <= 1e-5 rad) is the last:
+ * the step is quadratically convergent, so the rotation it returns is within
+ * O(|w|^2) ~ 1e-10 rad of the polar factor -- below the reference polar's own
+ * 1e-9 tolerance and three orders below fp32 particle resolution. Most
+ * iterations after the first of a substep need one step. */
+#define PBDR_POLAR_WARM_TOLQ 1e-10
 /* fp32 warm-up stage of the polar (then fp64 polish to PBDR_POLAR_TOL). */
 #define PBDR_POLAR_F32_TOL2 1e-12f
 #define PBDR_POLAR_F32_TOLQ 1e-7f
