@@ -317,10 +317,10 @@ inline bool polar_rotation(const M3& A, M3& R, double q[4]) {
 // singular solve, or 4 steps without convergence fall back to the cold
 // two-stage Newton polar. The result is the same polar factor to 1e-12.
 inline bool polar_warm(const M3& A, const float rq[4], M3& R, double q[4]) {
-  if (!finite3(A)) return false;
   const double d0 = det3(A);
   const double c3 = frob2(A) * PBDR_ONE_THIRD;
-  if (!(d0 > 0.0) || d0 * d0 <= (PBDR_POLAR_REL_DET * PBDR_POLAR_REL_DET) * ((c3 * c3) * c3)) return false;
+  const bool bad =
+      !finite3(A) || !(d0 > 0.0) || d0 * d0 <= (PBDR_POLAR_REL_DET * PBDR_POLAR_REL_DET) * ((c3 * c3) * c3);
   if (rq[0] != 0.0f || rq[1] != 0.0f || rq[2] != 0.0f || rq[3] != 0.0f) {
     // Homogeneous iterate: qc is not renormalised between steps; R0 below is
     // |qc|^2 R(qc), and the step h is invariant under that uniform scale.
@@ -361,15 +361,20 @@ inline bool polar_warm(const M3& A, const float rq[4], M3& R, double q[4]) {
       qn[2] = (qc[0] * h[1] + qc[2]) + (qc[3] * h[0] - qc[1] * h[2]);
       qn[3] = (qc[0] * h[2] + qc[3]) + (qc[1] * h[1] - qc[2] * h[0]);
       if (ww <= PBDR_POLAR_WARM_TOLQ) {
-        const double n = std::sqrt(((qn[0] * qn[0] + qn[1] * qn[1]) + qn[2] * qn[2]) + qn[3] * qn[3]);
-        const double in = 1.0 / n;
-        for (int k = 0; k < 4; ++k) q[k] = qn[k] * in;
-        R = quat_to(q);
+        if (bad) return false;
+        const double n2 = ((qn[0] * qn[0] + qn[1] * qn[1]) + qn[2] * qn[2]) + qn[3] * qn[3];
+        const double r = 1.0 / n2;
+        const double s = 1.5 - 0.5 * n2;
+        R = quat_to_h(qn);
+        for (int i = 0; i < 3; ++i)
+          for (int j = 0; j < 3; ++j) R.a[i][j] = R.a[i][j] * r;
+        for (int k = 0; k < 4; ++k) q[k] = qn[k] * s;
         return true;
       }
       for (int k = 0; k < 4; ++k) qc[k] = qn[k];
     }
   }
+  if (bad) return false;
   return polar_rotation(A, R, q);
 }
 

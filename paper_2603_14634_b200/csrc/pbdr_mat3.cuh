@@ -124,6 +124,24 @@ __device__ __forceinline__ void d3_quat_to(const double q[4], float R[9]) {
   R[8] = static_cast<float>(1.0 - 2.0 * (xx + yy));
 }
 
+// R = r * |q|^2 R(q) (homogeneous form; r = 1/|q|^2 gives the rotation of a
+// non-unit q), rounded to float.
+__device__ __forceinline__ void d3_quat_to_h(const double q[4], double r, float R[9]) {
+  const double w = q[0], x = q[1], y = q[2], z = q[3];
+  const double w2 = w * w, xx = x * x, yy = y * y, zz = z * z;
+  const double xy = x * y, xz = x * z, yz = y * z;
+  const double wx = w * x, wy = w * y, wz = w * z;
+  R[0] = static_cast<float>(((w2 + xx) - (yy + zz)) * r);
+  R[1] = static_cast<float>((2.0 * (xy - wz)) * r);
+  R[2] = static_cast<float>((2.0 * (xz + wy)) * r);
+  R[3] = static_cast<float>((2.0 * (xy + wz)) * r);
+  R[4] = static_cast<float>(((w2 + yy) - (xx + zz)) * r);
+  R[5] = static_cast<float>((2.0 * (yz - wx)) * r);
+  R[6] = static_cast<float>((2.0 * (xz - wy)) * r);
+  R[7] = static_cast<float>((2.0 * (yz + wx)) * r);
+  R[8] = static_cast<float>(((w2 + zz) - (xx + yy)) * r);
+}
+
 __device__ __forceinline__ double d3_frob2(const D3& m) {
   double s = 0.0;
 #pragma unroll
@@ -313,10 +331,12 @@ bool polar_warm_f(const float Af[9], const float rq[4], float R[9], double q[4])
     A.a[i / 3][i % 3] = static_cast<double>(Af[i]);
     finite = finite && isfinite(Af[i]);
   }
-  if (!finite) return false;
+  // Degeneracy is decided here but only acted on at the exits, so the checks
+  // overlap the first Gauss-Newton step instead of preceding it.
   const double d0 = d3_det(A);
   const double c3 = d3_frob2(A) * PBDR_ONE_THIRD;
-  if (!(d0 > 0.0) || d0 * d0 <= (PBDR_POLAR_REL_DET * PBDR_POLAR_REL_DET) * ((c3 * c3) * c3)) return false;
+  const bool bad =
+      !finite || !(d0 > 0.0) || d0 * d0 <= (PBDR_POLAR_REL_DET * PBDR_POLAR_REL_DET) * ((c3 * c3) * c3);
   if (rq[0] != 0.0f || rq[1] != 0.0f || rq[2] != 0.0f || rq[3] != 0.0f) {
     // Homogeneous iterate (mirrors oracle polar_warm): qc is not renormalised
     // between steps; R0 = |qc|^2 R(qc) and the step h is scale invariant.
@@ -374,17 +394,22 @@ bool polar_warm_f(const float Af[9], const float rq[4], float R[9], double q[4])
       qn[2] = (qc[0] * h[1] + qc[2]) + (qc[3] * h[0] - qc[1] * h[2]);
       qn[3] = (qc[0] * h[2] + qc[3]) + (qc[1] * h[1] - qc[2] * h[0]);
       if (ww <= PBDR_POLAR_WARM_TOLQ) {
-        const double n = sqrt(((qn[0] * qn[0] + qn[1] * qn[1]) + qn[2] * qn[2]) + qn[3] * qn[3]);
-        const double in = 1.0 / n;
+        if (bad) return false;
+        // R = |qn|^-2 (homogeneous rotation of qn); the stored quaternion gets
+        // one Newton step of 1/sqrt from |qn|^2 ~ 1 (error O((|qn|^2 - 1)^2)).
+        const double n2 = ((qn[0] * qn[0] + qn[1] * qn[1]) + qn[2] * qn[2]) + qn[3] * qn[3];
+        const double r = 1.0 / n2;
+        const double s = 1.5 - 0.5 * n2;
+        d3_quat_to_h(qn, r, R);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) q[k] = qn[k] * in;
-        d3_quat_to(q, R);
+        for (int k = 0; k < 4; ++k) q[k] = qn[k] * s;
         return true;
       }
 #pragma unroll
       for (int k = 0; k < 4; ++k) qc[k] = qn[k];
     }
   }
+  if (bad) return false;
   return polar_rotation_f(Af, R, q);
 }
 
