@@ -180,6 +180,7 @@ struct IterArgs {
   int last_iter;      // iteration_index == solver_iterations - 1
   float4* mom_acc;    // per body (P, L) accumulators for kPerSubstep
   long long* timing;  // optional per-CTA phase clocks (debug), else null
+  int ntiles;         // packed CTAs (tiles) of this launch; set by launch_iteration
 };
 
 struct StatsArgs {
