@@ -48,6 +48,7 @@ struct pbdr_handle {
   float4* wcom = nullptr;    // torque programs: per-body com and alpha
   float4* walpha = nullptr;
   bool has_torque = false;
+  bool has_programs = false;  // any body with a ForceProgram
   int per_substep = 0;
   int debug_iter = 0;  // iteration index for the replay hook
   uint32_t* keys[2] = {nullptr, nullptr};
@@ -218,6 +219,7 @@ void enqueue_substep(pbdr_handle* h, pbdr_dev::LaunchHook* hook) {
   ia.box_max = h->box_max;
   ia.substep_counter = h->counter;
   ia.role = h->slab ? h->role : nullptr;
+  ia.has_programs = h->has_programs ? 1 : 0;
   ia.p0 = h->p_lo;
   ia.n = h->p_hi;
   ia.dt = h->dt;
@@ -607,6 +609,7 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
       bp.tz = static_cast<float>(p.torque[2]);
       const bool torque = p.torque[0] != 0.0 || p.torque[1] != 0.0 || p.torque[2] != 0.0;
       bp.flags = 1 | (p.gravity_exempt ? 2 : 0) | (torque ? 4 : 0);
+      h->has_programs = true;
       h->has_torque = h->has_torque || torque;
       bp.t_start = p.t_start;
       bp.t_stop = p.t_stop;

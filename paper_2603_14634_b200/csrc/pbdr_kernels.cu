@@ -114,12 +114,69 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                : "memory");
 }
 
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+__device__ __forceinline__ __attribute__((unused)) void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
           smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+
+// L2 residency hints: descriptors and per-body tables are tiny and re-read by
+// every launch, while particle state streams through (>> 126 MB L2). Keep the
+// former (evict_last), stream the latter (evict_first on the bulk copies).
+#ifndef PBDR_L2_HINTS
+#define PBDR_L2_HINTS 1
+#endif
+template <typename T>
+__device__ __forceinline__ T ld_keep_nc(const T* p) {
+#if PBDR_L2_HINTS
+  static_assert(sizeof(T) == 16 || sizeof(T) == 8, "vector loads only");
+  T v;
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  if constexpr (sizeof(T) == 16) {
+    uint32_t* r = reinterpret_cast<uint32_t*>(&v);
+    asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "l"(p), "l"(pol));
+  } else {
+    uint32_t* r = reinterpret_cast<uint32_t*>(&v);
+    asm volatile("ld.global.nc.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;" : "=r"(r[0]), "=r"(r[1]) : "l"(p), "l"(pol));
+  }
+  return v;
+#else
+  return *p;
+#endif
+}
+
+template <typename T>
+__device__ __forceinline__ T ld_keep(const T* p) {  // coherent (data this kernel also writes)
+#if PBDR_L2_HINTS
+  static_assert(sizeof(T) == 16, "float4 only");
+  T v;
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  uint32_t* r = reinterpret_cast<uint32_t*>(&v);
+  asm volatile("ld.global.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "l"(p), "l"(pol));
+  return v;
+#else
+  return *p;
+#endif
+}
+
+__device__ __forceinline__ void bulk_g2s_stream(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+#if PBDR_L2_HINTS
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+#else
+  bulk_g2s(dst, src, bytes, bar);
+#endif
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
@@ -152,10 +209,11 @@ __global__ void __launch_bounds__(256) k_integrate_key(IntegrateArgs A) {
   const bool valid = b >= 0;
   float4 xn = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
   if (valid) {
-    const double t = static_cast<double>(*A.substep_counter) * A.dt_d;
-    const BodyProgram pr = A.programs[b];
-    float a[3] = {0.0f, 0.0f, (pr.flags & 2) ? 0.0f : -A.gravity};
     const float4 x = A.pos[p];
+    BodyProgram pr{};
+    if (A.has_programs) pr = A.programs[b];  // scenes without programs skip the 48-B record
+    float a[3] = {0.0f, 0.0f, (pr.flags & 2) ? 0.0f : -A.gravity};
+    const double t = static_cast<double>(*A.substep_counter) * A.dt_d;
     if ((pr.flags & 1) && t >= pr.t_start && t < pr.t_stop) {
       const float invM = A.body_mass[b].y;
       a[0] = a[0] + pr.fx * invM;
@@ -257,13 +315,18 @@ __global__ void __launch_bounds__(256) k_body_ranges(BroadArgs A) {
 
 // Partners of body b: other bodies of its scene whose box overlaps b's box
 // inflated by h. The coarse cell is >= the largest box extent + h, so partner
-// box centres lie in the 27 neighbouring coarse cells.
-__global__ void __launch_bounds__(128) k_body_partners(BroadArgs A) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= A.nb) return;
+// box centres lie in the 27 neighbouring coarse cells. One warp per body:
+// lane t < 27 scans coarse cell t (lanes whose cells hash to the same bucket
+// scan it once), hits are compacted with ballots. The partner list is only
+// used as a set (near filter), so its order is immaterial; overflow (more than
+// PBDR_PARTNER_CAP partners) marks the body for a full search.
+__global__ void __launch_bounds__(256) k_body_partners(BroadArgs A) {
+  const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= A.nb) return;  // warp-uniform
   const int b = A.list ? A.list[t] : t;
   if (*A.oversize) {
-    A.npartners[b] = -1;
+    if (lane == 0) A.npartners[b] = -1;
     return;
   }
   float lo[3], hi[3];
@@ -276,36 +339,42 @@ __global__ void __launch_bounds__(128) k_body_partners(BroadArgs A) {
     lo[k] = lo[k] - (A.inflate + fabsf(lo[k]) * 1e-6f);
     hi[k] = hi[k] + (A.inflate + fabsf(hi[k]) * 1e-6f);
   }
-  int count = 0;
-  bool overflow = false;
-  uint32_t visited[27];
-#pragma unroll
-  for (int t = 0; t < 27; ++t) {
-    const uint32_t key = pbdr_cell_hash(c[0] + t % 3 - 1, c[1] + (t / 3) % 3 - 1, c[2] + t / 9 - 1,
-                                        static_cast<uint32_t>(sb), A.mask);
-    bool dup = false;
-#pragma unroll
-    for (int u = 0; u < t; ++u) dup = dup || visited[u] == key;
-    visited[t] = key;
-    if (dup) continue;
-    const uint2 e = A.bcells[key];
-    if (e.x == kEmpty) continue;
-    for (uint32_t s = e.x; s < e.y; ++s) {
-      const int o = static_cast<int>(A.sorted_bvals[s]);
-      if (o == b || A.body_scene[o] != sb) continue;
-      float olo[3], ohi[3];
-      load_box(A.box_min, A.box_max, o, olo, ohi);
-      if (olo[0] > hi[0] || ohi[0] < lo[0] || olo[1] > hi[1] || ohi[1] < lo[1] || olo[2] > hi[2] ||
-          ohi[2] < lo[2])
-        continue;
-      if (count < PBDR_PARTNER_CAP)
-        A.partners[static_cast<int64_t>(b) * PBDR_PARTNER_CAP + count] = o;
-      else
-        overflow = true;
-      ++count;
+  uint32_t key = 0xFFFFFFFFu;
+  if (lane < 27)
+    key = pbdr_cell_hash(c[0] + lane % 3 - 1, c[1] + (lane / 3) % 3 - 1, c[2] + lane / 9 - 1,
+                         static_cast<uint32_t>(sb), A.mask);
+  const unsigned same = __match_any_sync(kFull, key);
+  const bool owner = lane < 27 && (__ffs(same) - 1) == lane;  // lowest lane of its bucket
+  uint32_t s = 0, e = 0;
+  if (owner) {
+    const uint2 r = A.bcells[key];
+    if (r.x != kEmpty) {
+      s = r.x;
+      e = r.y;
     }
   }
-  A.npartners[b] = overflow ? -1 : count;
+  int count = 0;
+  while (__any_sync(kFull, s < e)) {
+    bool hit = false;
+    int o = -1;
+    if (s < e) {
+      o = static_cast<int>(A.sorted_bvals[s]);
+      ++s;
+      if (o != b && A.body_scene[o] == sb) {
+        float olo[3], ohi[3];
+        load_box(A.box_min, A.box_max, o, olo, ohi);
+        hit = !(olo[0] > hi[0] || ohi[0] < lo[0] || olo[1] > hi[1] || ohi[1] < lo[1] || olo[2] > hi[2] ||
+                ohi[2] < lo[2]);
+      }
+    }
+    const unsigned m = __ballot_sync(kFull, hit);
+    if (hit) {
+      const int slot = count + __popc(m & ((1u << lane) - 1u));
+      if (slot < PBDR_PARTNER_CAP) A.partners[static_cast<int64_t>(b) * PBDR_PARTNER_CAP + slot] = o;
+    }
+    count += __popc(m);
+  }
+  if (lane == 0) A.npartners[b] = count > PBDR_PARTNER_CAP ? -1 : count;
 }
 
 // ---------------------------------------------------------------------------
@@ -379,6 +448,7 @@ __global__ void __launch_bounds__(1024) k_near_scan(NearArgs A) {
   const int lo = t * per;
   const int hi = min(A.blocks, lo + per);
   uint32_t sum = 0;
+#pragma unroll 8
   for (int b = lo; b < hi; ++b) sum += A.block_count[b];
   uint32_t incl = sum;
 #pragma unroll
@@ -399,9 +469,11 @@ __global__ void __launch_bounds__(1024) k_near_scan(NearArgs A) {
   }
   __syncthreads();
   uint32_t run = incl - sum + ((t >> 5) ? s_warp[(t >> 5) - 1] : 0u);
+#pragma unroll 8
   for (int b = lo; b < hi; ++b) {
+    const uint32_t c = A.block_count[b];
     A.block_off[b] = run;
-    run += A.block_count[b];
+    run += c;
   }
   if (t == 1023) *A.count = static_cast<long long>(run);
 }
@@ -573,6 +645,14 @@ __device__ __forceinline__ void pp_contact(const float x[3], float w, int64_t p,
 #define PBDR_MATH_ACTIVE (warp == 0 && lane < cd.w)
 #define PBDR_MATH_BODY lane
 #endif
+#ifndef PBDR_STAGE_REST
+#define PBDR_STAGE_REST 1
+#endif
+#if PBDR_STAGE_REST
+#define PBDR_REST_AT(gslot, sslot) s_rest[(sslot)]
+#else
+#define PBDR_REST_AT(gslot, sslot) __ldg(&A.rest[(gslot)])
+#endif
 #if PBDR_STAGE_INIT
 #define PBDR_INIT_AT(gslot, sslot) s_init[(sslot)]
 #else
@@ -617,22 +697,23 @@ __global__ void __launch_bounds__(kThreads, PBDR_ITER_MINBLOCKS) k_iteration(Ite
   __shared__ float s_binv[kWarps];   // 1/M
   __shared__ float4 s_brq[kWarps];   // warm-start rotation (w, x, y, z)
   const bool fixes = A.linfix || A.angfix;
+  const long long t_entry = A.timing ? clock64() : 0;  // phase clocks (debug launches only)
   if (threadIdx.x == 0) mbar_init(&s_bar, 1);
 
   // Tiles (packed CTAs of whole bodies) are walked with a grid stride; the
   // next tile's descriptors are loaded one tile ahead, so a tile starts with
   // the bulk copies and the body-table loads instead of a descriptor chain.
   int tile = blockIdx.x;
-  int4 cd_n = A.cta_desc[tile];
-  int4 wd_n = A.warp_desc[tile * kWarps + warp];
+  int4 cd_n = ld_keep_nc(&A.cta_desc[tile]);
+  int4 wd_n = ld_keep_nc(&A.warp_desc[tile * kWarps + warp]);
   for (uint32_t it_parity = 0; tile < A.ntiles; tile += gridDim.x, it_parity ^= 1u) {
   const int4 cd = cd_n;  // first slot, slot count, first body, bodies
   const int4 wd = wd_n;
   {
     const int tn = tile + static_cast<int>(gridDim.x);
     if (tn < A.ntiles) {
-      cd_n = A.cta_desc[tn];
-      wd_n = A.warp_desc[tn * kWarps + warp];
+      cd_n = ld_keep_nc(&A.cta_desc[tn]);
+      wd_n = ld_keep_nc(&A.warp_desc[tn * kWarps + warp]);
     }
   }
   const int first = cd.x;
@@ -643,22 +724,25 @@ __global__ void __launch_bounds__(kThreads, PBDR_ITER_MINBLOCKS) k_iteration(Ite
     mbar_expect_tx(&s_bar, 4u * bytes);
     bulk_g2s(s_init, A.init + first, bytes, &s_bar);
 #else
-    mbar_expect_tx(&s_bar, 3u * bytes);
+    mbar_expect_tx(&s_bar, (PBDR_STAGE_REST ? 3u : 2u) * bytes);
 #endif
-    bulk_g2s(s_pos, A.pos_in + first, bytes, &s_bar);
-    bulk_g2s(s_vel, A.vel + first, bytes, &s_bar);
-    bulk_g2s(s_rest, A.rest + first, bytes, &s_bar);
+    bulk_g2s_stream(s_pos, A.pos_in + first, bytes, &s_bar);
+    bulk_g2s_stream(s_vel, A.vel + first, bytes, &s_bar);
+    if (PBDR_STAGE_REST) bulk_g2s_stream(s_rest, A.rest + first, bytes, &s_bar);
+#ifdef PBDR_DIAG_TMAISSUE
+    if (A.timing) A.timing[8 * static_cast<int64_t>(tile) + 7] = clock64();
+#endif
   }
 
   if (warp == 0 && lane < cd.w) {
     const int bb = cd.z + lane;
-    const int4 bdb = A.body_desc[bb];
-    const float4 an = A.anchor[bb];
-    const float2 mass = A.body_mass[bb];
+    const int4 bdb = ld_keep_nc(&A.body_desc[bb]);
+    const float4 an = ld_keep(&A.anchor[bb]);
+    const float2 mass = ld_keep_nc(&A.body_mass[bb]);
     s_banc[lane] = make_float4(an.x, an.y, an.z, mass.x);
     s_binv[lane] = mass.y;
     s_bw[lane] = make_int2(bdb.w, bdb.z);
-    s_brq[lane] = A.rquat[bb];
+    s_brq[lane] = ld_keep(&A.rquat[bb]);
   }
 
   const int b = wd.x;
@@ -675,7 +759,7 @@ __global__ void __launch_bounds__(kThreads, PBDR_ITER_MINBLOCKS) k_iteration(Ite
   const int off = start - first;
 
   long long* tm = A.timing ? A.timing + 8 * static_cast<int64_t>(tile) : nullptr;
-  if (tm && threadIdx.x == 0) tm[0] = clock64();
+  if (tm && threadIdx.x == 0) tm[0] = t_entry;  // CTA entry: stage = descriptors + table + bulk copies
   __syncthreads();  // barrier initialised, per-body table filled
   float a[3];
   {
@@ -736,7 +820,7 @@ __global__ void __launch_bounds__(kThreads, PBDR_ITER_MINBLOCKS) k_iteration(Ite
     const int64_t p = start + q;
     const float4 x4 = s_pos[off + q];
     const float4 v4 = s_vel[off + q];
-    const float4 r4 = s_rest[off + q];
+    const float4 r4 = PBDR_REST_AT(start + q, off + q);
     const float x[3] = {x4.x, x4.y, x4.z};
     const float m = v4.w;
 
@@ -897,7 +981,7 @@ __global__ void __launch_bounds__(kThreads, PBDR_ITER_MINBLOCKS) k_iteration(Ite
       if (!(q < n)) continue;
       const float4 x4 = s_pos[off + q];
       const float4 v4 = s_vel[off + q];
-      const float4 r4 = s_rest[off + q];
+      const float4 r4 = PBDR_REST_AT(start + q, off + q);
       const float x[3] = {x4.x, x4.y, x4.z};
       const float v[3] = {v4.x, v4.y, v4.z};
       const float q0[3] = {r4.x, r4.y, r4.z};
@@ -1084,9 +1168,11 @@ __global__ void __launch_bounds__(kThreads, PBDR_ITER_MINBLOCKS) k_iteration(Ite
   }  // fixes
   if (tm && threadIdx.x == 0) {
     tm[6] = clock64();
+#ifndef PBDR_DIAG_TMAISSUE
     unsigned smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
     tm[7] = smid;
+#endif
   }
   __syncthreads();  // the next tile's bulk copies overwrite the staging buffers
   }  // tiles
@@ -1265,7 +1351,9 @@ __global__ void __launch_bounds__(kThreads) k_body_wrench(WrenchArgs A) {
 #ifndef PBDR_ITER_EXTRA_SMEM
 #define PBDR_ITER_EXTRA_SMEM 0
 #endif
-size_t iteration_smem_bytes() { return sizeof(float4) * (PBDR_STAGE_INIT ? 4 : 3) * kSlots + PBDR_ITER_EXTRA_SMEM; }
+size_t iteration_smem_bytes() {
+  return sizeof(float4) * ((PBDR_STAGE_INIT ? 1 : 0) + (PBDR_STAGE_REST ? 1 : 0) + 2) * kSlots + PBDR_ITER_EXTRA_SMEM;
+}
 
 void launch_integrate(const IntegrateArgs& a, cudaStream_t s) {
   const unsigned blocks = static_cast<unsigned>((a.n - a.p0 + 255) / 256);
@@ -1285,7 +1373,7 @@ void launch_body_ranges(const BroadArgs& a, cudaStream_t s) {
 
 void launch_body_partners(const BroadArgs& a, cudaStream_t s) {
   if (a.nb == 0) return;
-  k_body_partners<<<(a.nb + 127) / 128, 128, 0, s>>>(a);
+  k_body_partners<<<static_cast<unsigned>((static_cast<int64_t>(a.nb) * 32 + 255) / 256), 256, 0, s>>>(a);
 }
 
 void launch_near(const NearArgs& a, cudaStream_t s) {

@@ -66,6 +66,7 @@ struct IntegrateArgs {
   uint32_t* box_max;
   const long long* substep_counter;
   const uint8_t* role;  // slab mode: per-body role (0 inactive, 1 ghost, 2 owned), else null
+  int has_programs;     // 0: no body has a ForceProgram (gravity only)
   int64_t p0;           // first slot of the launch range (slab mode: active range)
   int64_t n;            // end of the launch range
   float dt, gravity, inv_h;
