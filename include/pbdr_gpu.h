@@ -94,6 +94,8 @@ typedef struct pbdr_scene_desc {
   int32_t num_walls;          /* extra planes after the ground (config 3's container) */
   const pbdr_plane* walls;
   const int32_t* body_scene;  /* [num_bodies] independent-scene id, or NULL = all 0 */
+  int32_t tile_kp;            /* 0 = automatic tile shape; 2, 4 or 8 particles per lane
+                                 forces it (pbdr_choose_kp in csrc/pbdr_pinned.h) */
 } pbdr_scene_desc;
 
 /* Per-body trajectory sample (SPEC.md:357 trajectory hook; body.hpp:32-36
@@ -158,6 +160,7 @@ typedef struct pbdr_info {
   int32_t sm_count;
   float cell_size;            /* h = 2 r_max, fp32 */
   float dt;                   /* fp32 substep */
+  int32_t tile_kp;            /* particles per lane of the iteration tiles */
 } pbdr_info;
 int pbdr_gpu_info(pbdr_handle* h, pbdr_info* out);
 

@@ -99,6 +99,7 @@ struct State {
   int32_t err_body = -1;
   double err_axis[3] = {0, 0, 0};
   int threads = 1;
+  int kp = 2;  // tile shape of the reduction trees (pbdr_choose_kp)
   std::vector<int8_t> role;  // slab mode: 0 inactive, 1 ghost, 2 owned (empty = all owned)
 };
 
@@ -117,8 +118,8 @@ inline void flag(State& s, uint32_t bits, int32_t body, const double* axis = nul
 
 // ---- Fixed-topology body sum (pbdr_pinned.h) --------------------------------
 template <int F>
-void tree_sum(int n, const float* vals, float out[F]) {
-  const int W = pbdr_body_warps(n);
+void tree_sum(int kp, int n, const float* vals, float out[F]) {
+  const int W = pbdr_body_warps(n, kp);
   const int K = pbdr_body_slots(n, W);
   float lane[32][F], nxt[32][F];
   for (int wi = 0; wi < W; ++wi) {
@@ -175,7 +176,7 @@ void wrench_prepass(State& s) {
       o[8] = -(mk * (pp[1] * pp[2]));
     }
     float S[9] = {};
-    tree_sum<9>(n, vals.data(), S);
+    tree_sum<9>(s.kp, n, vals.data(), S);
     const float M = s.bM[b], invM = s.binvM[b];
     float c[3];
     for (int k = 0; k < 3; ++k) c[k] = S[k] * invM;
@@ -358,6 +359,7 @@ struct BodyIn {
   float* acc = nullptr;  // kPerSubstep accumulators (6 floats) or null
   bool reset = false;    // first iteration of the substep
   bool last = true;      // last iteration of the substep
+  int kp = 2;            // tile shape of the reduction tree (pbdr_choose_kp)
 };
 
 struct BodyOut {
@@ -378,7 +380,7 @@ void momentum_fix(int n, const float* m, const float* xa, const float* va, const
                   const float* dX, const float c[3], const float Pb[3], const float Lb[3], float M,
                   float invM, float dt, bool linfix, bool angfix, float* xo, float* vo,
                   unsigned& err, double axis[3], float* acc = nullptr, bool reset = false,
-                  bool last = true) {
+                  bool last = true, int kp = 2) {
   std::vector<float> vals(15 * static_cast<size_t>(n));
   for (int q = 0; q < n; ++q) {
     const float mk = m[q];
@@ -399,7 +401,7 @@ void momentum_fix(int n, const float* m, const float* xa, const float* va, const
     o[14] = -(mk * (P[1] * P[2]));
   }
   float SB[15];
-  tree_sum<15>(n, vals.data(), SB);
+  tree_sum<15>(kp, n, vals.data(), SB);
   bool fin = true;
   for (float f : SB) fin = fin && std::isfinite(f);
   if (!fin) err |= PBDR_DEVERR_NONFINITE;
@@ -488,7 +490,7 @@ void body_iteration(const BodyIn& in, BodyOut& out) {
     o[18] = kb[0]; o[19] = kb[1]; o[20] = kb[2];
   }
   float SA[21];
-  tree_sum<21>(n, valsA.data(), SA);
+  tree_sum<21>(in.kp, n, valsA.data(), SA);
   bool finite = true;
   for (float f : SA) finite = finite && std::isfinite(f);
   if (!finite) out.err |= PBDR_DEVERR_NONFINITE;
@@ -540,7 +542,8 @@ void body_iteration(const BodyIn& in, BodyOut& out) {
   }
   if (in.linfix || in.angfix) {
     momentum_fix(n, in.m, xa.data(), va.data(), pa.data(), dXv.data(), c, Pb, Lb, in.M, in.invM,
-                 in.dt, in.linfix, in.angfix, out.x, out.v, out.err, out.axis, in.acc, in.reset, in.last);
+                 in.dt, in.linfix, in.angfix, out.x, out.v, out.err, out.axis, in.acc, in.reset, in.last,
+                 in.kp);
   } else {
     std::memcpy(out.x, xa.data(), sizeof(float) * 3 * n);
     std::memcpy(out.v, va.data(), sizeof(float) * 3 * n);
@@ -580,6 +583,7 @@ void iteration(State& s) {
     BodyIn in{n, x.data(), v.data(), m.data(), q0.data(), dc.data(), init.data(),
               {s.anchor[3 * b], s.anchor[3 * b + 1], s.anchor[3 * b + 2]}, &s.rquat[4 * b],
               s.bM[b], s.binvM[b], s.dt, s.inv_dt, s.incremental, s.linfix, s.angfix};
+    in.kp = s.kp;
     if (s.per_substep) {
       in.acc = &s.mom_acc[6 * b];
       in.reset = s.iter_in_substep == 0;
@@ -630,7 +634,7 @@ void body_stats(State& s, pbdr_body_stats* out) {
       o[15] = kk[0]; o[16] = kk[1]; o[17] = kk[2];
     }
     float S[18];
-    tree_sum<18>(n, vals.data(), S);
+    tree_sum<18>(s.kp, n, vals.data(), S);
     float c[3], P[3], tmp[3];
     for (int k = 0; k < 3; ++k) {
       c[k] = S[k] * s.binvM[b];
@@ -737,6 +741,12 @@ int oracle_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* cfg, int thre
   if (slot != n) {
     delete s;
     return PBDR_ERR_CONFIG;
+  }
+  {
+    int max_body = 0;
+    for (int32_t b = 0; b < s->nb; ++b)
+      max_body = std::max(max_body, static_cast<int>(s->bstart[b + 1] - s->bstart[b]));
+    s->kp = pbdr_choose_kp(n, s->nb, max_body, d->tile_kp);
   }
   if (d->has_ground) {
     Plane4 P;
@@ -920,6 +930,7 @@ void oracle_read_candidates(void* st, int32_t* counts, int32_t* lists) {
 void oracle_body_stats(void* st, pbdr_body_stats* out) { body_stats(*static_cast<State*>(st), out); }
 
 int64_t oracle_num_slots(void* st) { return static_cast<State*>(st)->n; }
+int oracle_tile_kp(void* st) { return static_cast<State*>(st)->kp; }
 float oracle_cell_size(void* st) { return static_cast<State*>(st)->h; }
 
 }  // extern "C"

@@ -52,6 +52,8 @@ def olib():
             getattr(L, name).restype = None
         L.oracle_num_slots.argtypes = [vp]
         L.oracle_num_slots.restype = C.c_int64
+        L.oracle_tile_kp.argtypes = [vp]
+        L.oracle_tile_kp.restype = C.c_int
         L.oracle_set_roles.argtypes = [vp, vp]
         L.oracle_set_roles.restype = None
         for name in ("oracle_gather", "oracle_scatter"):
@@ -234,6 +236,10 @@ class Oracle:
         out = np.zeros((self.nb, 13))
         olib().oracle_body_stats(self._h, _p(out))
         return out
+
+    @property
+    def tile_kp(self):
+        return olib().oracle_tile_kp(self._h)
 
     @property
     def cell_size(self):

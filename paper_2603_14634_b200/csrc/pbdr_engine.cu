@@ -49,6 +49,7 @@ struct pbdr_handle {
   float4* walpha = nullptr;
   bool has_torque = false;
   bool has_programs = false;  // any body with a ForceProgram
+  int kp = 4;                 // tile shape: particles per lane (pbdr_choose_kp)
   int per_substep = 0;
   int debug_iter = 0;  // iteration index for the replay hook
   uint32_t* keys[2] = {nullptr, nullptr};
@@ -252,7 +253,7 @@ void enqueue_substep(pbdr_handle* h, pbdr_dev::LaunchHook* hook) {
     wa.err = h->err;
     wa.substep_counter = h->counter;
     if (hook) hook->before(kHookIntegrate);
-    if (h->pk_active.ctas > 0) launch_wrench(wa, h->pk_active.ctas, h->stream);
+    if (h->pk_active.ctas > 0) launch_wrench(wa, h->pk_active.ctas, h->kp, h->stream);
     if (hook) hook->after(kHookIntegrate);
   }
   if (hook) hook->before(kHookIntegrate);
@@ -389,7 +390,7 @@ void enqueue_iteration(pbdr_handle* h, int iter_index, pbdr_dev::LaunchHook* hoo
   it.angfix = h->angfix;
   it.timing = h->timing;
   if (hook) hook->before(kHookIteration);
-  if (h->pk_iter.ctas > 0) launch_iteration(it, h->pk_iter.ctas, h->stream);
+  if (h->pk_iter.ctas > 0) launch_iteration(it, h->pk_iter.ctas, h->kp, h->stream);
   if (hook) hook->after(kHookIteration);
   h->cur ^= 1;
 }
@@ -457,7 +458,7 @@ int build_graph(pbdr_handle* h, int parity) {
 // layout) share a CTA while its warps last. bdesc[b] = (first slot, n, W,
 // first warp in the CTA) is written for the listed bodies only.
 void pack_bodies(const std::vector<int>& list, const std::vector<int64_t>& bstart, const std::vector<int>& bcount,
-                 std::vector<int4>& cdesc, std::vector<int4>& wdesc, std::vector<int4>& bdesc) {
+                 int kp, std::vector<int4>& cdesc, std::vector<int4>& wdesc, std::vector<int4>& bdesc) {
   cdesc.clear();
   wdesc.clear();
   int used = 0, prev = -2;
@@ -468,7 +469,7 @@ void pack_bodies(const std::vector<int>& list, const std::vector<int64_t>& bstar
   for (const int b : list) {
     const int cnt = bcount[b];
     const int first_slot = static_cast<int>(bstart[b]);
-    const int W = pbdr_body_warps(cnt);
+    const int W = pbdr_body_warps(cnt, kp);
     if (used + W > PBDR_CTA_WARPS || (used > 0 && b != prev + 1)) close();
     if (used == 0) cdesc.push_back(make_int4(first_slot, 0, b, 0));
     cdesc.back().y += cnt;
@@ -623,7 +624,10 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
   {
     std::vector<int> all(nb);
     for (int32_t b = 0; b < nb; ++b) all[b] = b;
-    pack_bodies(all, h->h_bstart, h->h_bcount, cdesc, wdesc, bdesc);
+    int max_body = 0;
+    for (int32_t b = 0; b < nb; ++b) max_body = std::max(max_body, h->h_bcount[b]);
+    h->kp = pbdr_choose_kp(n, nb, max_body, d->tile_kp);
+    pack_bodies(all, h->h_bstart, h->h_bcount, h->kp, cdesc, wdesc, bdesc);
   }
   h->ctas = static_cast<int>(wdesc.size() / PBDR_CTA_WARPS);
   h->p_lo = 0;
@@ -804,7 +808,7 @@ static void enqueue_stats(pbdr_handle* h, double* out) {
   sa.body_desc = h->pk_iter.body;
   sa.body_mass = h->body_mass;
   sa.out = out;
-  if (h->pk_iter.ctas > 0) pbdr_dev::launch_stats(sa, h->pk_iter.ctas, h->stream);
+  if (h->pk_iter.ctas > 0) pbdr_dev::launch_stats(sa, h->pk_iter.ctas, h->kp, h->stream);
 }
 
 static int step_frames_async(pbdr_handle* h, int64_t frames) {
@@ -961,6 +965,7 @@ int pbdr_gpu_info(pbdr_handle* h, pbdr_info* o) {
   o->sm_count = h->sm_count;
   o->cell_size = h->h;
   o->dt = h->dt;
+  o->tile_kp = h->kp;
   return PBDR_OK;
 }
 
@@ -1217,7 +1222,7 @@ int pbdr_gpu_set_roles(pbdr_handle* h, const int8_t* roles) {
   if (!active.empty())
     PBDR_CUDA(cudaMemcpy(h->active_list, active.data(), sizeof(int) * active.size(), cudaMemcpyHostToDevice));
   auto upload = [&](const std::vector<int>& list, pbdr_handle::Packing& dev) -> int {
-    pack_bodies(list, h->h_bstart, h->h_bcount, cd, wd, bd);
+    pack_bodies(list, h->h_bstart, h->h_bcount, h->kp, cd, wd, bd);
     dev.ctas = static_cast<int>(cd.size());
     if (!cd.empty()) {
       PBDR_CUDA(cudaMemcpy(dev.cta, cd.data(), sizeof(int4) * cd.size(), cudaMemcpyHostToDevice));

@@ -207,10 +207,10 @@ void launch_cell_clear(uint4* cells, const uint32_t* prev_keys, const long long*
                        cudaStream_t s);
 void launch_ranges(const RangesArgs& a, cudaStream_t s);
 void launch_neighbours(const NeighbourArgs& a, cudaStream_t s);
-size_t iteration_smem_bytes();
+size_t iteration_smem_bytes(int kp);
 cudaError_t prepare_iteration_kernel();
-void launch_iteration(const IterArgs& a, int ctas, cudaStream_t s);
-void launch_stats(const StatsArgs& a, int ctas, cudaStream_t s);
-void launch_wrench(const WrenchArgs& a, int ctas, cudaStream_t s);
+void launch_iteration(const IterArgs& a, int ctas, int kp, cudaStream_t s);
+void launch_stats(const StatsArgs& a, int ctas, int kp, cudaStream_t s);
+void launch_wrench(const WrenchArgs& a, int ctas, int kp, cudaStream_t s);
 
 }  // namespace pbdr_dev

@@ -23,7 +23,8 @@
 #endif
 
 /* ---- Per-body reduction topology ---------------------------------------
- * A body with n particles is reduced by W = ceil(n / (32*KP)) warps. Lane l of
+ * A body with n particles is reduced by W = ceil(n / (32*KP)) warps (KP: the
+ * scene's tile shape, pbdr_choose_kp). Lane l of
  * warp wi owns the particles q = k*32*W + wi*32 + l for k = 0..K-1 with
  * K = ceil(n / (32*W)) (q < n). Every body sum is, in this order:
  *   1. per lane, serially over k ascending, starting from +0.0f;
@@ -33,12 +34,35 @@
  * (proj/include/pbdr/parallel.hpp:15-18, 40-63): results are independent of
  * scheduling, and the oracle reproduces the tree exactly.
  */
-#define PBDR_KP 4                 /* particles per lane per body (max)      */
+#define PBDR_KP_MAX 8             /* particles per lane per body, largest tile */
+#ifndef PBDR_CTA_WARPS
 #define PBDR_CTA_WARPS 8          /* warps per iteration CTA                */
-#define PBDR_MAX_BODY_PARTICLES (PBDR_KP * 32 * PBDR_CTA_WARPS) /* 1024    */
+#endif
+#define PBDR_MAX_BODY_PARTICLES (PBDR_KP_MAX * 32 * PBDR_CTA_WARPS) /* 2048 */
 
-PBDR_HD int pbdr_body_warps(int n) { return (n + 32 * PBDR_KP - 1) / (32 * PBDR_KP); }
+PBDR_HD int pbdr_body_warps(int n, int kp) { return (n + 32 * kp - 1) / (32 * kp); }
 PBDR_HD int pbdr_body_slots(int n, int w) { return (n + 32 * w - 1) / (32 * w); }
+
+/* Tile shape KP (particles per lane), one per scene, chosen from the scene's
+ * size (measured on B200): small scenes are latency-bound
+ * and want the most parallel layout (KP = 2); scenes of small bodies (mean
+ * <= 384 particles) run best with KP = 8 (one warp per body up to 256
+ * particles, two CTAs per SM); larger bodies with KP = 4. KP is raised until
+ * the largest body fits one CTA. `forced` (scene_desc.tile_kp) overrides. The
+ * oracle applies the same rule, so both sides reduce with the same tree. */
+PBDR_HD int pbdr_choose_kp(long long n_particles, int n_bodies, int max_body, int forced) {
+  int kp;
+  if (forced == 2 || forced == 4 || forced == 8)
+    kp = forced;
+  else if (n_particles < 131072)
+    kp = 2;
+  else if (n_particles <= 384LL * n_bodies)
+    kp = 8;
+  else
+    kp = 4;
+  while (kp < PBDR_KP_MAX && max_body > kp * 32 * PBDR_CTA_WARPS) kp *= 2;
+  return kp;
+}
 
 /* ---- Uniform hash grid ----------------------------------------------------
  * Cell edge h = 2 * max radius. Cell coordinate per axis is

@@ -94,7 +94,7 @@ class SceneDesc(C.Structure):
                 ("programs", C.POINTER(ForceProgram)), ("ground", Plane),
                 ("has_ground", C.c_int32), ("contact_relaxation", C.c_double),
                 ("num_walls", C.c_int32), ("walls", C.POINTER(Plane)),
-                ("body_scene", C.POINTER(C.c_int32))]
+                ("body_scene", C.POINTER(C.c_int32)), ("tile_kp", C.c_int32)]
 
 
 class BodyStats(C.Structure):
@@ -107,7 +107,7 @@ class Info(C.Structure):
                 ("hash_bits", C.c_int32), ("sort_passes", C.c_int32),
                 ("launches_per_frame", C.c_int64), ("device_bytes", C.c_int64),
                 ("device", C.c_int32), ("sm_count", C.c_int32), ("cell_size", C.c_float),
-                ("dt", C.c_float)]
+                ("dt", C.c_float), ("tile_kp", C.c_int32)]
 
 
 _lib = None
@@ -236,7 +236,7 @@ class ArrayScene:
     def __init__(self, position, velocity, inv_mass, radius, body_offsets, rest_offsets,
                  total_mass, rest_com, body_indices=None, body_id=None, ground=None,
                  has_ground=True, contact_relaxation=1.0, walls=(), body_scene=None,
-                 programs=None):
+                 programs=None, tile_kp=0):
         n = len(inv_mass)
         nb = len(total_mass)
         self.position = np.ascontiguousarray(position, dtype=np.float64).reshape(n, 3)
@@ -280,6 +280,7 @@ class ArrayScene:
             d.walls = C.cast(self.walls, C.POINTER(Plane))
         if self.body_scene is not None:
             d.body_scene = self.body_scene.ctypes.data_as(C.POINTER(C.c_int32))
+        d.tile_kp = tile_kp
         self.desc = d
 
     @property
@@ -335,7 +336,7 @@ def scene_with_programs(src, programs) -> "ArrayScene":
                       rest_com=arr("rest_com", 3 * nb), body_indices=arr("body_indices", n, np.int32),
                       body_id=arr("body_id", n, np.int32), ground=d.ground, has_ground=bool(d.has_ground),
                       contact_relaxation=d.contact_relaxation, walls=walls, body_scene=body_scene,
-                      programs=list(programs))
+                      programs=list(programs), tile_kp=d.tile_kp)
 
 
 class GeneratedScene:

@@ -109,3 +109,20 @@ def test_c4_shards_concatenate_to_whole(pbdr):
     s1 = P.GeneratedScene(4, seed=0, scale=3, c4_first_scene=3)
     cat = np.concatenate([s0.positions(), s1.positions()])
     assert np.array_equal(cat, whole.positions())
+
+
+def test_tile_shape_rule_host():
+    # pbdr_choose_kp (csrc/pbdr_pinned.h): small scenes -> 2, small bodies -> 8,
+    # large bodies -> 4, raised until the largest body fits one CTA; forced
+    # values win. Checked through the oracle, which applies the same rule.
+    import sys
+    import os
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle"))
+    import pyoracle
+    from paper_2603_14634_b200 import pbdr as P
+    g1 = P.GeneratedScene(1)
+    assert pyoracle.Oracle(g1.desc, g1.cfg, threads=1).tile_kp == 2
+    g1.desc.tile_kp = 8
+    assert pyoracle.Oracle(g1.desc, g1.cfg, threads=1).tile_kp == 8
+    g3 = P.GeneratedScene(3, scale=24)  # bodies up to ~1000 particles: 2 is too small
+    assert pyoracle.Oracle(g3.desc, g3.cfg, threads=1).tile_kp == 4

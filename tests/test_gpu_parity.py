@@ -98,6 +98,30 @@ def test_one_frame_matches_oracle(pbdr, pyoracle, cid, scale):
     assert_same(gpu.read_bodies(), orc.body_stats(), "body stats")
 
 
+@pytest.mark.parametrize("kp", [2, 4, 8])
+@pytest.mark.parametrize("cid,scale", [(2, 0), (3, 24), (5, 6)])
+def test_tile_shapes_bit_exact(pbdr, pyoracle, kp, cid, scale):
+    # Every tile shape (particles per lane, pbdr_choose_kp) reduces with its own
+    # pinned tree; the oracle follows the same shape, so all stay bit-exact.
+    g = P.GeneratedScene(cid, seed=0, scale=scale)
+    g.desc.tile_kp = kp
+    gpu = P.GpuSolver(g.desc, g.cfg)
+    orc = pyoracle.Oracle(g.desc, g.cfg)
+    assert gpu.info.tile_kp == orc.tile_kp >= kp
+    gpu.step_frames(2)
+    assert orc.step(2 * g.cfg.substeps) == 0
+    gp, gv = gpu.read_f32()
+    op, ov = orc.read_f32()
+    assert_same(gp, op, f"kp={kp} positions")
+    assert_same(gv, ov, f"kp={kp} velocities")
+    assert_same(gpu.read_bodies(), orc.body_stats(), f"kp={kp} body stats")
+
+
+def test_tile_shape_rule(pbdr):
+    # The measured per-scene choice.
+    assert P.GpuSolver(P.GeneratedScene(1).desc, P.solver_cfg()).info.tile_kp == 2
+
+
 def test_graph_replay_equals_direct_substeps(pbdr):
     g = P.GeneratedScene(2)
     a = P.GpuSolver(g.desc, g.cfg)
