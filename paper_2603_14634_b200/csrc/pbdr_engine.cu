@@ -778,9 +778,13 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
     release(h);
     return code;
   }
+  // Per substep: 4 memsets + cell clear + [wrench] + integrate + body keys +
+  // body sort (memset, histogram, scan, passes) + body ranges + partners +
+  // near flag / scan / compact + particle sort (memset, histogram, scan,
+  // passes) + cell ranges + neighbours + iterations.
   h->launches_per_frame = static_cast<int64_t>(h->substeps) *
-                          ((h->has_torque ? 1 : 0) + 1 + 1 + 1 + 2 + h->bpasses + 2 + 3 + 2 + h->passes + 1 + 1 +
-                           h->iters);
+                          (4 + 1 + (h->has_torque ? 1 : 0) + 1 + 1 + (3 + h->bpasses) + 2 + 3 + (3 + h->passes) +
+                           1 + 1 + h->iters);
   *out = h;
   return PBDR_OK;
 }

@@ -439,42 +439,51 @@ __global__ void __launch_bounds__(256) k_near_flag(NearArgs A) {
   if (threadIdx.x == 0) A.block_count[blockIdx.x] = static_cast<uint32_t>(cnt);
 }
 
-// One CTA of 1024 threads: exclusive scan of the per-block near counts.
+// One CTA of 1024 threads: exclusive scan of the per-block near counts, in
+// coalesced chunks of 4096 (four consecutive counts per thread).
 __global__ void __launch_bounds__(1024) k_near_scan(NearArgs A) {
   __shared__ uint32_t s_warp[32];
+  __shared__ uint32_t s_total;
   const int t = threadIdx.x;
-  const int per = (A.blocks + 1023) / 1024;
-  const int lo = t * per;
-  const int hi = min(A.blocks, lo + per);
-  uint32_t sum = 0;
-#pragma unroll 8
-  for (int b = lo; b < hi; ++b) sum += A.block_count[b];
-  uint32_t incl = sum;
+  const int lane = t & 31, warp = t >> 5;
+  uint32_t carry = 0;
+  for (int base = 0; base < A.blocks; base += 4096) {
+    const int i0 = base + 4 * t;
+    uint32_t c[4];
 #pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    const uint32_t y = __shfl_up_sync(kFull, incl, off);
-    if ((t & 31) >= off) incl += y;
-  }
-  if ((t & 31) == 31) s_warp[t >> 5] = incl;
-  __syncthreads();
-  if (t < 32) {
-    uint32_t w = s_warp[t];
+    for (int i = 0; i < 4; ++i) c[i] = (i0 + i < A.blocks) ? A.block_count[i0 + i] : 0u;
+    const uint32_t sum = (c[0] + c[1]) + (c[2] + c[3]);
+    uint32_t incl = sum;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
-      const uint32_t y = __shfl_up_sync(kFull, w, off);
-      if (t >= off) w += y;
+      const uint32_t y = __shfl_up_sync(kFull, incl, off);
+      if (lane >= off) incl += y;
     }
-    s_warp[t] = w;
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      uint32_t w = s_warp[lane];
+      uint32_t wi = w;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, wi, off);
+        if (lane >= off) wi += y;
+      }
+      s_warp[lane] = wi - w;  // exclusive warp offsets
+      if (lane == 31) s_total = wi;
+    }
+    __syncthreads();
+    uint32_t run = carry + s_warp[warp] + (incl - sum);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (i0 + i < A.blocks) {
+        A.block_off[i0 + i] = run;
+        run += c[i];
+      }
+    carry += s_total;
+    __syncthreads();  // s_warp / s_total reuse
   }
-  __syncthreads();
-  uint32_t run = incl - sum + ((t >> 5) ? s_warp[(t >> 5) - 1] : 0u);
-#pragma unroll 8
-  for (int b = lo; b < hi; ++b) {
-    const uint32_t c = A.block_count[b];
-    A.block_off[b] = run;
-    run += c;
-  }
-  if (t == 1023) *A.count = static_cast<long long>(run);
+  if (t == 0) *A.count = static_cast<long long>(carry);
 }
 
 __global__ void __launch_bounds__(256) k_near_compact(NearArgs A) {
