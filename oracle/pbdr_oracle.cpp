@@ -144,6 +144,48 @@ void tree_sum(int kp, int n, const float* vals, float out[F]) {
   }
 }
 
+// Same tree with fused first stage: per lane acc = fma(a_q, b_q, acc) over k
+// ascending (b = 1 for summed fields: fma(a, 1, acc) == a + acc exactly).
+template <int F>
+void tree_sum_fma(int kp, int n, const float* va, const float* vb, float out[F]) {
+  const int W = pbdr_body_warps(n, kp);
+  const int K = pbdr_body_slots(n, W);
+  float lane[32][F], nxt[32][F];
+  for (int wi = 0; wi < W; ++wi) {
+    for (int l = 0; l < 32; ++l) {
+      for (int f = 0; f < F; ++f) lane[l][f] = 0.0f;
+      for (int k = 0; k < K; ++k) {
+        const int q = k * 32 * W + wi * 32 + l;
+        if (q < n)
+          for (int f = 0; f < F; ++f) {
+            const size_t i = static_cast<size_t>(q) * F + f;
+            lane[l][f] = std::fmaf(va[i], vb[i], lane[l][f]);
+          }
+      }
+    }
+    for (int off = 16; off >= 1; off >>= 1) {
+      for (int l = 0; l < 32; ++l)
+        for (int f = 0; f < F; ++f) nxt[l][f] = lane[l][f] + lane[l ^ off][f];
+      std::memcpy(lane, nxt, sizeof lane);
+    }
+    if (wi == 0) {
+      for (int f = 0; f < F; ++f) out[f] = lane[0][f];
+    } else {
+      for (int f = 0; f < F; ++f) out[f] = out[f] + lane[0][f];
+    }
+  }
+}
+
+// Pinned explicit fused multiply-adds (mirrors the kernels' fmaf()).
+inline float dot3_fma(const float a[3], const float b[3]) {
+  return std::fmaf(a[2], b[2], std::fmaf(a[1], b[1], a[0] * b[0]));
+}
+inline void cross3_fma(const float a[3], const float b[3], float o[3]) {
+  o[0] = std::fmaf(a[1], b[2], -(a[2] * b[1]));
+  o[1] = std::fmaf(a[2], b[0], -(a[0] * b[2]));
+  o[2] = std::fmaf(a[0], b[1], -(a[1] * b[0]));
+}
+
 inline void cross3(const float a[3], const float b[3], float o[3]) {
   o[0] = a[1] * b[2] - a[2] * b[1];
   o[1] = a[2] * b[0] - a[0] * b[2];
@@ -300,16 +342,16 @@ void build_candidates(State& s) {
 void ground_delta(const std::vector<Plane4>& planes, float relax, const float x[3],
                   const float* xinit, float r, float dPG[3]) {
   for (const Plane4& P : planes) {
-    const float d = (((x[0] - P.p[0]) * P.n[0] + (x[1] - P.p[1]) * P.n[1]) +
-                     (x[2] - P.p[2]) * P.n[2]) - r;
+    const float xp[3] = {x[0] - P.p[0], x[1] - P.p[1], x[2] - P.p[2]};
+    const float d = dot3_fma(xp, P.n) - r;
     if (!(d < 0.0f)) continue;
     const float push = -(relax * d);
-    for (int k = 0; k < 3; ++k) dPG[k] = dPG[k] + push * P.n[k];
+    for (int k = 0; k < 3; ++k) dPG[k] = std::fmaf(push, P.n[k], dPG[k]);
     if (!(P.mu > 0.0f)) continue;
     const float t[3] = {x[0] - xinit[0], x[1] - xinit[1], x[2] - xinit[2]};
-    const float tn = (t[0] * P.n[0] + t[1] * P.n[1]) + t[2] * P.n[2];
-    const float tt[3] = {t[0] - tn * P.n[0], t[1] - tn * P.n[1], t[2] - tn * P.n[2]};
-    const float len2 = (tt[0] * tt[0] + tt[1] * tt[1]) + tt[2] * tt[2];
+    const float tn = dot3_fma(t, P.n);
+    const float tt[3] = {std::fmaf(-tn, P.n[0], t[0]), std::fmaf(-tn, P.n[1], t[1]), std::fmaf(-tn, P.n[2], t[2])};
+    const float len2 = dot3_fma(tt, tt);
     if (!(len2 > 0.0f)) continue;
     const float len = std::sqrt(len2);
     const float lim = P.mu * (-d);
@@ -317,7 +359,7 @@ void ground_delta(const std::vector<Plane4>& planes, float relax, const float x[
       for (int k = 0; k < 3; ++k) dPG[k] = dPG[k] - tt[k];
     } else {
       const float f = lim / len;
-      for (int k = 0; k < 3; ++k) dPG[k] = dPG[k] - tt[k] * f;
+      for (int k = 0; k < 3; ++k) dPG[k] = std::fmaf(-tt[k], f, dPG[k]);
     }
   }
 }
@@ -327,7 +369,7 @@ void ground_delta(const std::vector<Plane4>& planes, float relax, const float x[
 void pp_delta(const float x[3], float w, int64_t i, const float xj[3], float wj, int64_t j,
               float rr, float relax, float dPP[3]) {
   const float e[3] = {x[0] - xj[0], x[1] - xj[1], x[2] - xj[2]};
-  const float d2 = (e[0] * e[0] + e[1] * e[1]) + e[2] * e[2];
+  const float d2 = dot3_fma(e, e);
   if (!(d2 < rr * rr)) return;
   const float dist = std::sqrt(d2);
   float nrm[3];
@@ -341,7 +383,7 @@ void pp_delta(const float x[3], float w, int64_t i, const float xj[3], float wj,
   }
   const float C = dist - rr;
   const float kk = (relax * (w / (w + wj))) * C;
-  for (int k = 0; k < 3; ++k) dPP[k] = dPP[k] - kk * nrm[k];
+  for (int k = 0; k < 3; ++k) dPP[k] = std::fmaf(-kk, nrm[k], dPP[k]);
 }
 
 struct BodyIn {
@@ -381,27 +423,29 @@ void momentum_fix(int n, const float* m, const float* xa, const float* va, const
                   float invM, float dt, bool linfix, bool angfix, float* xo, float* vo,
                   unsigned& err, double axis[3], float* acc = nullptr, bool reset = false,
                   bool last = true, int kp = 2) {
-  std::vector<float> vals(15 * static_cast<size_t>(n));
+  // (a, b) per field: the tree's first stage is acc = fma(a, b, acc).
+  std::vector<float> fa(15 * static_cast<size_t>(n)), fb(15 * static_cast<size_t>(n), 1.0f);
   for (int q = 0; q < n; ++q) {
     const float mk = m[q];
     const float* P = &pa[3 * q];
     const float mva[3] = {mk * va[3 * q], mk * va[3 * q + 1], mk * va[3 * q + 2]};
     float ka[3];
-    cross3(P, mva, ka);
-    const float s2 = (P[0] * P[0] + P[1] * P[1]) + P[2] * P[2];
-    float* o = &vals[15 * static_cast<size_t>(q)];
-    o[0] = mk * dX[3 * q]; o[1] = mk * dX[3 * q + 1]; o[2] = mk * dX[3 * q + 2];
-    o[3] = mva[0]; o[4] = mva[1]; o[5] = mva[2];
-    o[6] = ka[0]; o[7] = ka[1]; o[8] = ka[2];
-    o[9] = mk * (s2 - P[0] * P[0]);
-    o[10] = mk * (s2 - P[1] * P[1]);
-    o[11] = mk * (s2 - P[2] * P[2]);
-    o[12] = -(mk * (P[0] * P[1]));
-    o[13] = -(mk * (P[0] * P[2]));
-    o[14] = -(mk * (P[1] * P[2]));
+    cross3_fma(P, mva, ka);
+    const float s2 = dot3_fma(P, P);
+    float* a = &fa[15 * static_cast<size_t>(q)];
+    float* b = &fb[15 * static_cast<size_t>(q)];
+    for (int k = 0; k < 3; ++k) {
+      a[k] = mk; b[k] = dX[3 * q + k];
+      a[3 + k] = mk; b[3 + k] = va[3 * q + k];
+      a[6 + k] = ka[k];
+      a[9 + k] = mk; b[9 + k] = std::fmaf(-P[k], P[k], s2);
+    }
+    a[12] = -mk; b[12] = P[0] * P[1];
+    a[13] = -mk; b[13] = P[0] * P[2];
+    a[14] = -mk; b[14] = P[1] * P[2];
   }
   float SB[15];
-  tree_sum<15>(kp, n, vals.data(), SB);
+  tree_sum_fma<15>(kp, n, fa.data(), fb.data(), SB);
   bool fin = true;
   for (float f : SB) fin = fin && std::isfinite(f);
   if (!fin) err |= PBDR_DEVERR_NONFINITE;
@@ -449,14 +493,10 @@ void momentum_fix(int n, const float* m, const float* xa, const float* va, const
   for (int q = 0; q < n; ++q) {
     float r[3], wr[3];
     for (int k = 0; k < 3; ++k) r[k] = pa[3 * q + k] - ca[k];
-    cross3(om, r, wr);
+    cross3_fma(om, r, wr);
     for (int k = 0; k < 3; ++k) {
-      float vv = va[3 * q + k] + dv[k];
-      vv = vv - wr[k];
-      float xx = xa[3 * q + k] + dv[k] * dt;
-      xx = xx - wr[k] * dt;
-      vo[3 * q + k] = vv;
-      xo[3 * q + k] = xx;
+      vo[3 * q + k] = (va[3 * q + k] + dv[k]) - wr[k];
+      xo[3 * q + k] = std::fmaf(-wr[k], dt, std::fmaf(dv[k], dt, xa[3 * q + k]));
     }
   }
 }
@@ -465,32 +505,38 @@ void momentum_fix(int n, const float* m, const float* xa, const float* va, const
 // its contact deltas (pinned P1-P3, P6, P7).
 void body_iteration(const BodyIn& in, BodyOut& out) {
   const int n = in.n;
-  std::vector<float> valsA(21 * static_cast<size_t>(n));
+  std::vector<float> fa(21 * static_cast<size_t>(n)), fb(21 * static_cast<size_t>(n), 1.0f);
   for (int q = 0; q < n; ++q) {
     const float* x = &in.x[3 * q];
     const float* v = &in.v[3 * q];
     const float m = in.m[q];
     const float* dc = &in.dc[3 * q];
     const float* q0 = &in.q0[3 * q];
-    float pp[3], pb[3], mp[3], mvb[3], kb[3];
+    float pp[3], pb[3], mp[3], vb[3], mvb[3], kb[3];
     for (int k = 0; k < 3; ++k) {
       pp[k] = x[k] - in.a[k];
       pb[k] = pp[k] + dc[k];
-      const float vb = v[k] + dc[k] * in.inv_dt;
+      vb[k] = std::fmaf(dc[k], in.inv_dt, v[k]);
       mp[k] = m * pp[k];
-      mvb[k] = m * vb;
+      mvb[k] = m * vb[k];
     }
-    cross3(pb, mvb, kb);
-    float* o = &valsA[21 * static_cast<size_t>(q)];
-    o[0] = mp[0]; o[1] = mp[1]; o[2] = mp[2];
-    o[3] = m * dc[0]; o[4] = m * dc[1]; o[5] = m * dc[2];
+    cross3_fma(pb, mvb, kb);
+    float* a = &fa[21 * static_cast<size_t>(q)];
+    float* b = &fb[21 * static_cast<size_t>(q)];
+    for (int k = 0; k < 3; ++k) {
+      a[k] = m; b[k] = pp[k];
+      a[3 + k] = m; b[3 + k] = dc[k];
+      a[15 + k] = m; b[15 + k] = vb[k];
+      a[18 + k] = kb[k];
+    }
     for (int rI = 0; rI < 3; ++rI)
-      for (int cI = 0; cI < 3; ++cI) o[6 + 3 * rI + cI] = mp[rI] * q0[cI];
-    o[15] = mvb[0]; o[16] = mvb[1]; o[17] = mvb[2];
-    o[18] = kb[0]; o[19] = kb[1]; o[20] = kb[2];
+      for (int cI = 0; cI < 3; ++cI) {
+        a[6 + 3 * rI + cI] = mp[rI];
+        b[6 + 3 * rI + cI] = q0[cI];
+      }
   }
   float SA[21];
-  tree_sum<21>(in.kp, n, valsA.data(), SA);
+  tree_sum_fma<21>(in.kp, n, fa.data(), fb.data(), SA);
   bool finite = true;
   for (float f : SA) finite = finite && std::isfinite(f);
   if (!finite) out.err |= PBDR_DEVERR_NONFINITE;
@@ -527,14 +573,14 @@ void body_iteration(const BodyIn& in, BodyOut& out) {
       const float pk = x[k] - in.a[k];
       float dsm = 0.0f;
       if (sm_ok) {
-        const float gk = (Rf[k][0] * q0[0] + Rf[k][1] * q0[1]) + Rf[k][2] * q0[2];
+        const float gk = dot3_fma(Rf[k], q0);
         dsm = gk - (pk - c[k]);
       }
       const float dX = dc[k] + dsm;
       dXv[3 * q + k] = dX;
       xa[3 * q + k] = x[k] + dX;
       if (in.incremental)
-        va[3 * q + k] = v[k] + dX * in.inv_dt;
+        va[3 * q + k] = std::fmaf(dX, in.inv_dt, v[k]);
       else
         va[3 * q + k] = (xa[3 * q + k] - in.init[3 * q + k]) * in.inv_dt;
       pa[3 * q + k] = pk + dX;

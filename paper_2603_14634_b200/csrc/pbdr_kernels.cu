@@ -611,12 +611,24 @@ __global__ void __launch_bounds__(128) k_neighbours(NeighbourArgs A) {
 // k < 4. Warp 0 runs the per-body fp64 math for all bodies of the CTA, one
 // lane per body.
 // ---------------------------------------------------------------------------
+// Pinned fused multiply-adds (P8): only these explicit fmaf() are
+// contracted (the library builds with --fmad=false); the oracle uses std::fmaf
+// at the same places, and IEEE fma is correctly rounded on both sides.
+__device__ __forceinline__ float dot3_fma(const float a[3], const float b[3]) {
+  return fmaf(a[2], b[2], fmaf(a[1], b[1], a[0] * b[0]));
+}
+__device__ __forceinline__ void cross3_fma(const float a[3], const float b[3], float o[3]) {
+  o[0] = fmaf(a[1], b[2], -(a[2] * b[1]));
+  o[1] = fmaf(a[2], b[0], -(a[0] * b[2]));
+  o[2] = fmaf(a[0], b[1], -(a[1] * b[0]));
+}
+
 // One particle-particle contact of particle i (slot p, X_i = x, inverse mass
 // w) against candidate j: Jacobi delta accumulated into dPP.
 __device__ __forceinline__ void pp_contact(const float x[3], float w, int64_t p, float4 xj, int j, float rr,
                                            float relax, float dPP[3]) {
   const float e[3] = {x[0] - xj.x, x[1] - xj.y, x[2] - xj.z};
-  const float d2 = (e[0] * e[0] + e[1] * e[1]) + e[2] * e[2];
+  const float d2 = dot3_fma(e, e);
   if (d2 < rr * rr) {
     const float dist = sqrtf(d2);
     float nrm[3];
@@ -628,9 +640,9 @@ __device__ __forceinline__ void pp_contact(const float x[3], float w, int64_t p,
     }
     const float C = dist - rr;
     const float kk = (relax * (w / (w + xj.w))) * C;
-    dPP[0] = dPP[0] - kk * nrm[0];
-    dPP[1] = dPP[1] - kk * nrm[1];
-    dPP[2] = dPP[2] - kk * nrm[2];
+    dPP[0] = fmaf(-kk, nrm[0], dPP[0]);
+    dPP[1] = fmaf(-kk, nrm[1], dPP[1]);
+    dPP[2] = fmaf(-kk, nrm[2], dPP[2]);
   }
 }
 
@@ -842,19 +854,20 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
     for (int pl = 0; pl < A.planes.count; ++pl) {
       const float* Pp = A.planes.p[pl];
       const float* Pn = A.planes.n[pl];
-      const float d = (((x[0] - Pp[0]) * Pn[0] + (x[1] - Pp[1]) * Pn[1]) + (x[2] - Pp[2]) * Pn[2]) - r4.w;
+      const float xp[3] = {x[0] - Pp[0], x[1] - Pp[1], x[2] - Pp[2]};
+      const float d = dot3_fma(xp, Pn) - r4.w;
       if (d < 0.0f) {
         const float push = -(A.relax * d);
-        dPG[0] = dPG[0] + push * Pn[0];
-        dPG[1] = dPG[1] + push * Pn[1];
-        dPG[2] = dPG[2] + push * Pn[2];
+        dPG[0] = fmaf(push, Pn[0], dPG[0]);
+        dPG[1] = fmaf(push, Pn[1], dPG[1]);
+        dPG[2] = fmaf(push, Pn[2], dPG[2]);
         const float mu = A.planes.mu[pl];
         if (mu > 0.0f) {
           const float4 xi = PBDR_INIT_AT(p, off + q);
           const float t[3] = {x[0] - xi.x, x[1] - xi.y, x[2] - xi.z};
-          const float tn = (t[0] * Pn[0] + t[1] * Pn[1]) + t[2] * Pn[2];
-          const float tt[3] = {t[0] - tn * Pn[0], t[1] - tn * Pn[1], t[2] - tn * Pn[2]};
-          const float len2 = (tt[0] * tt[0] + tt[1] * tt[1]) + tt[2] * tt[2];
+          const float tn = dot3_fma(t, Pn);
+          const float tt[3] = {fmaf(-tn, Pn[0], t[0]), fmaf(-tn, Pn[1], t[1]), fmaf(-tn, Pn[2], t[2])};
+          const float len2 = dot3_fma(tt, tt);
           if (len2 > 0.0f) {
             const float len = sqrtf(len2);
             const float lim = mu * (-d);
@@ -864,9 +877,9 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
               dPG[2] = dPG[2] - tt[2];
             } else {
               const float fr = lim / len;
-              dPG[0] = dPG[0] - tt[0] * fr;
-              dPG[1] = dPG[1] - tt[1] * fr;
-              dPG[2] = dPG[2] - tt[2] * fr;
+              dPG[0] = fmaf(-tt[0], fr, dPG[0]);
+              dPG[1] = fmaf(-tt[1], fr, dPG[1]);
+              dPG[2] = fmaf(-tt[2], fr, dPG[2]);
             }
           }
         }
@@ -890,33 +903,30 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
 #endif
     const float v[3] = {v4.x, v4.y, v4.z};
     const float q0[3] = {r4.x, r4.y, r4.z};
-    float pp[3], pb[3], mp[3], mvb[3], kb[3];
+    // Body sums: product fields accumulate with one fma per particle (the
+    // first stage of the pinned reduction tree), cross products are summed.
+    float pp[3], pb[3], mp[3], vb[3], mvb[3], kb[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       dX[k][c] = dPG[c] + dPP[c];
       pp[c] = x[c] - a[c];
       pb[c] = pp[c] + dX[k][c];
-      const float vb = v[c] + dX[k][c] * A.inv_dt;
+      vb[c] = fmaf(dX[k][c], A.inv_dt, v[c]);
       mp[c] = m * pp[c];
-      mvb[c] = m * vb;
+      mvb[c] = m * vb[c];
     }
-    cross3(pb, mvb, kb);
-    acc[0] = acc[0] + mp[0];
-    acc[1] = acc[1] + mp[1];
-    acc[2] = acc[2] + mp[2];
-    acc[3] = acc[3] + m * dX[k][0];
-    acc[4] = acc[4] + m * dX[k][1];
-    acc[5] = acc[5] + m * dX[k][2];
+    cross3_fma(pb, mvb, kb);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      acc[c] = fmaf(m, pp[c], acc[c]);
+      acc[3 + c] = fmaf(m, dX[k][c], acc[3 + c]);
+      acc[15 + c] = fmaf(m, vb[c], acc[15 + c]);
+      acc[18 + c] = acc[18 + c] + kb[c];
+    }
 #pragma unroll
     for (int rI = 0; rI < 3; ++rI)
 #pragma unroll
-      for (int cI = 0; cI < 3; ++cI) acc[6 + 3 * rI + cI] = acc[6 + 3 * rI + cI] + mp[rI] * q0[cI];
-    acc[15] = acc[15] + mvb[0];
-    acc[16] = acc[16] + mvb[1];
-    acc[17] = acc[17] + mvb[2];
-    acc[18] = acc[18] + kb[0];
-    acc[19] = acc[19] + kb[1];
-    acc[20] = acc[20] + kb[2];
+      for (int cI = 0; cI < 3; ++cI) acc[6 + 3 * rI + cI] = fmaf(mp[rI], q0[cI], acc[6 + 3 * rI + cI]);
   }
   if (live) {
     const float tot = warp_reduce_scatter<21>(acc);  // lane f: total of field f
@@ -1010,35 +1020,31 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
         const float pk = x[cI] - a[cI];
         float dsm = 0.0f;
         if (sm_ok) {
-          const float g = (Rf[3 * cI] * q0[0] + Rf[3 * cI + 1] * q0[1]) + Rf[3 * cI + 2] * q0[2];
+          const float Rrow[3] = {Rf[3 * cI], Rf[3 * cI + 1], Rf[3 * cI + 2]};
+          const float g = dot3_fma(Rrow, q0);
           dsm = g - (pk - c[cI]);
         }
         dX[k][cI] = dX[k][cI] + dsm;
         xa[cI] = x[cI] + dX[k][cI];
-        va[cI] = A.incremental ? v[cI] + dX[k][cI] * A.inv_dt : (xa[cI] - xi[cI]) * A.inv_dt;
+        va[cI] = A.incremental ? fmaf(dX[k][cI], A.inv_dt, v[cI]) : (xa[cI] - xi[cI]) * A.inv_dt;
         pa[cI] = pk + dX[k][cI];
       }
       if (fixes) {
         const float mk = v4.w;
         const float mva[3] = {mk * va[0], mk * va[1], mk * va[2]};
         float ka[3];
-        cross3(pa, mva, ka);
-        const float s2 = (pa[0] * pa[0] + pa[1] * pa[1]) + pa[2] * pa[2];
-        accB[0] = accB[0] + mk * dX[k][0];
-        accB[1] = accB[1] + mk * dX[k][1];
-        accB[2] = accB[2] + mk * dX[k][2];
-        accB[3] = accB[3] + mva[0];
-        accB[4] = accB[4] + mva[1];
-        accB[5] = accB[5] + mva[2];
-        accB[6] = accB[6] + ka[0];
-        accB[7] = accB[7] + ka[1];
-        accB[8] = accB[8] + ka[2];
-        accB[9] = accB[9] + mk * (s2 - pa[0] * pa[0]);
-        accB[10] = accB[10] + mk * (s2 - pa[1] * pa[1]);
-        accB[11] = accB[11] + mk * (s2 - pa[2] * pa[2]);
-        accB[12] = accB[12] + -(mk * (pa[0] * pa[1]));
-        accB[13] = accB[13] + -(mk * (pa[0] * pa[2]));
-        accB[14] = accB[14] + -(mk * (pa[1] * pa[2]));
+        cross3_fma(pa, mva, ka);
+        const float s2 = dot3_fma(pa, pa);
+#pragma unroll
+        for (int cI = 0; cI < 3; ++cI) {
+          accB[cI] = fmaf(mk, dX[k][cI], accB[cI]);
+          accB[3 + cI] = fmaf(mk, va[cI], accB[3 + cI]);
+          accB[6 + cI] = accB[6 + cI] + ka[cI];
+          accB[9 + cI] = fmaf(mk, fmaf(-pa[cI], pa[cI], s2), accB[9 + cI]);
+        }
+        accB[12] = fmaf(-mk, pa[0] * pa[1], accB[12]);
+        accB[13] = fmaf(-mk, pa[0] * pa[2], accB[13]);
+        accB[14] = fmaf(-mk, pa[1] * pa[2], accB[14]);
       } else {
         const int64_t p = start + q;
         A.pos_out[p] = make_float4(xa[0], xa[1], xa[2], x4.w);
@@ -1161,18 +1167,14 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       xa[c] = x[c] + dX[k][c];
-      va[c] = A.incremental ? v[c] + dX[k][c] * A.inv_dt : (xa[c] - xi[c]) * A.inv_dt;
+      va[c] = A.incremental ? fmaf(dX[k][c], A.inv_dt, v[c]) : (xa[c] - xi[c]) * A.inv_dt;
       r[c] = ((x[c] - a[c]) + dX[k][c]) - ca[c];
     }
-    cross3(om, r, wr);
+    cross3_fma(om, r, wr);
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-      float vv = va[c] + dv[c];
-      vv = vv - wr[c];
-      float xx = xa[c] + dv[c] * A.dt;
-      xx = xx - wr[c] * A.dt;
-      vo[c] = vv;
-      xo[c] = xx;
+      vo[c] = (va[c] + dv[c]) - wr[c];
+      xo[c] = fmaf(-wr[c], A.dt, fmaf(dv[c], A.dt, xa[c]));
     }
     const int64_t p = start + q;
     A.pos_out[p] = make_float4(xo[0], xo[1], xo[2], x4.w);
