@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -49,6 +50,7 @@ struct pbdr_handle {
   float4* walpha = nullptr;
   bool has_torque = false;
   bool has_programs = false;  // any body with a ForceProgram
+  bool broadphase = true;     // body-box filter before the hash grid (PBDR_BROADPHASE=0 disables)
   int kp = 4;                 // tile shape: particles per lane (pbdr_choose_kp)
   int per_substep = 0;
   int debug_iter = 0;  // iteration index for the replay hook
@@ -237,6 +239,7 @@ void enqueue_substep(pbdr_handle* h, pbdr_dev::LaunchHook* hook) {
   // Reset only the buckets the previous substep filled.
   if (hook) hook->before(kHookRanges);
   launch_cell_clear(h->cells, h->keys[h->sorted_buf], h->near_count + 1, h->n, h->stream);
+  launch_ncand_clear(h->ncand, h->near_list, h->near_count + 1, h->n, h->stream);
   if (hook) hook->after(kHookRanges);
   if (h->has_torque) {
     WrenchArgs wa{};
@@ -277,17 +280,19 @@ void enqueue_substep(pbdr_handle* h, pbdr_dev::LaunchHook* hook) {
   ba.max_extent = h->max_extent;
   ba.inflate = h->inflate;
   ba.mask = h->bmask;
-  if (hook) hook->before(kHookBroadphase);
-  launch_body_keys(ba, h->stream);
-  if (hook) hook->after(kHookBroadphase);
-  const int bsb = sort_pairs(h->bkeys, h->bvals, ba.nb, h->bhash_bits, h->bsort_temp, h->sm_count,
-                             h->stream, hook);
-  ba.sorted_bkeys = h->bkeys[bsb];
-  ba.sorted_bvals = h->bvals[bsb];
-  if (hook) hook->before(kHookBroadphase);
-  launch_body_ranges(ba, h->stream);
-  launch_body_partners(ba, h->stream);
-  if (hook) hook->after(kHookBroadphase, 2);
+  if (h->broadphase) {
+    if (hook) hook->before(kHookBroadphase);
+    launch_body_keys(ba, h->stream);
+    if (hook) hook->after(kHookBroadphase);
+    const int bsb = sort_pairs(h->bkeys, h->bvals, ba.nb, h->bhash_bits, h->bsort_temp, h->sm_count,
+                               h->stream, hook);
+    ba.sorted_bkeys = h->bkeys[bsb];
+    ba.sorted_bvals = h->bvals[bsb];
+    if (hook) hook->before(kHookBroadphase);
+    launch_body_ranges(ba, h->stream);
+    launch_body_partners(ba, h->stream);
+    if (hook) hook->after(kHookBroadphase, 2);
+  }
 
   // Broadphase filter: compact the near particles (slot order) into the sort input.
   NearArgs nr{};
@@ -307,6 +312,7 @@ void enqueue_substep(pbdr_handle* h, pbdr_dev::LaunchHook* hook) {
   nr.near_list = h->near_list;
   nr.ncand = h->ncand;
   nr.role = h->slab ? h->role : nullptr;
+  nr.all_near = h->broadphase ? 0 : 1;
   nr.p0 = h->p_lo;
   nr.n = h->p_hi;
   nr.blocks = static_cast<int>((h->p_hi - h->p_lo + 255) / 256);
@@ -772,6 +778,7 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
   cudaMemset(h->near_count, 0, sizeof(long long) * 2);
   cudaMemset(h->rquat, 0, sizeof(float4) * nb);
   h->pk_full = {h->cta_desc, h->warp_desc, h->body_desc, h->ctas};
+  if (const char* e = std::getenv("PBDR_BROADPHASE")) h->broadphase = std::atoi(e) != 0;
   h->pk_iter = h->pk_active = h->pk_full;
   if (reset_errors(h) != PBDR_OK) {
     const int code = pbdr_last_error_payload(nullptr, nullptr, nullptr);
@@ -783,7 +790,7 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
   // near flag / scan / compact + particle sort (memset, histogram, scan,
   // passes) + cell ranges + neighbours + iterations.
   h->launches_per_frame = static_cast<int64_t>(h->substeps) *
-                          (4 + 1 + (h->has_torque ? 1 : 0) + 1 + 1 + (3 + h->bpasses) + 2 + 3 + (3 + h->passes) +
+                          (4 + 2 + (h->has_torque ? 1 : 0) + 1 + 1 + (3 + h->bpasses) + 2 + 3 + (3 + h->passes) +
                            1 + 1 + h->iters);
   *out = h;
   return PBDR_OK;

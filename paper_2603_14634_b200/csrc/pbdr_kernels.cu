@@ -381,25 +381,26 @@ __global__ void __launch_bounds__(256) k_body_partners(BroadArgs A) {
 // every sorted entry (slots ascend within a bucket, so bodies do too).
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_cell_ranges(RangesArgs A) {
-  const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t m = *A.count;
-  if (s == 0) {
+  if (g == 0) {
     atomicAdd(reinterpret_cast<unsigned long long*>(A.substep_counter), 1ull);
     *A.prev_count = m;
   }
-  if (s >= m) return;
-  const uint32_t k = A.keys[s];
-  const int body = A.body_of[A.vals[s]];
-  A.sorted_body[s] = body;
-  // Entries of a bucket ascend by slot, hence by body: the first entry holds
-  // the bucket's smallest body, the last its largest.
-  if (s == 0 || A.keys[s - 1] != k) {
-    A.cells[k].x = static_cast<uint32_t>(s);
-    A.cells[k].z = static_cast<uint32_t>(body);
-  }
-  if (s == m - 1 || A.keys[s + 1] != k) {
-    A.cells[k].y = static_cast<uint32_t>(s + 1);
-    A.cells[k].w = static_cast<uint32_t>(body);
+  for (int64_t s = g; s < m; s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t k = A.keys[s];
+    const int body = A.body_of[A.vals[s]];
+    A.sorted_body[s] = body;
+    // Entries of a bucket ascend by slot, hence by body: the first entry holds
+    // the bucket's smallest body, the last its largest.
+    if (s == 0 || A.keys[s - 1] != k) {
+      A.cells[k].x = static_cast<uint32_t>(s);
+      A.cells[k].z = static_cast<uint32_t>(body);
+    }
+    if (s == m - 1 || A.keys[s + 1] != k) {
+      A.cells[k].y = static_cast<uint32_t>(s + 1);
+      A.cells[k].w = static_cast<uint32_t>(body);
+    }
   }
 }
 
@@ -417,9 +418,10 @@ __global__ void __launch_bounds__(256) k_near_flag(NearArgs A) {
   if (p < A.n) {
     const int bi = A.body_of[p];
     const bool active = !A.role || A.role[bi] != 0;
-    const float4 xi = A.pos[p];
-    const int np = active ? A.npartners[bi] : 0;
-    near = np < 0;  // partner overflow: search in full
+    const int np = active ? (A.all_near ? -1 : A.npartners[bi]) : 0;
+    near = np < 0;  // partner overflow (or no broadphase): search in full
+    // Bodies without partners (most of them in sparse scenes) need no position.
+    const float4 xi = np > 0 ? A.pos[p] : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
     for (int k = 0; k < np && !near; ++k) {
       const int o = A.partners[static_cast<int64_t>(bi) * PBDR_PARTNER_CAP + k];
       float lo[3], hi[3];
@@ -502,17 +504,26 @@ __global__ void __launch_bounds__(256) k_near_compact(NearArgs A) {
     A.near_list[off] = static_cast<int>(p);
     A.keys_c[off] = A.key_all[p];
     A.vals_c[off] = static_cast<uint32_t>(p);
-  } else {
-    A.ncand[p] = 0;
   }
+}
+
+// Candidate counts are only written for near particles (k_neighbours); the
+// previous substep's near particles are reset to 0 first, so every particle
+// outside the current near list reads 0 -- O(near) writes instead of O(N).
+__global__ void __launch_bounds__(256) k_ncand_clear(int* ncand, const int* prev_near, const long long* prev_count) {
+  const long long m = *prev_count;  // device-side count: grid-stride over a fixed grid
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < m;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    ncand[prev_near[t]] = 0;
 }
 
 // Resets the buckets the previous substep wrote (instead of a full memset).
 __global__ void __launch_bounds__(256) k_cell_clear(uint4* cells, const uint32_t* prev_keys,
                                                     const long long* prev_count) {
-  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t >= *prev_count) return;
-  cells[prev_keys[t]].x = kEmpty;
+  const long long m = *prev_count;
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < m;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    cells[prev_keys[t]].x = kEmpty;
 }
 
 // ---------------------------------------------------------------------------
@@ -567,9 +578,7 @@ __device__ __forceinline__ void scan_bucket(const NeighbourArgs& A, uint32_t key
   scan_range(A, e.x, e.y, bi, si, xi, cx, cy, cz, L);
 }
 
-__global__ void __launch_bounds__(128) k_neighbours(NeighbourArgs A) {
-  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t >= *A.count) return;
+__device__ __forceinline__ void neighbours_one(const NeighbourArgs& A, int64_t t) {
   const int64_t i = A.near_list[t];
   const float4 xi = A.pos[i];
   const int bi = A.body_of[i];
@@ -601,6 +610,15 @@ __global__ void __launch_bounds__(128) k_neighbours(NeighbourArgs A) {
     A.cand_j[static_cast<int64_t>(k) * A.n + i] = j;
     A.cand_rr[static_cast<int64_t>(k) * A.n + i] = ri + A.rest[j].w;
   }
+}
+
+// Grid-stride over the device-side near count (the launch is sized for the
+// worst case, so a fixed grid avoids launching N mostly-idle threads).
+__global__ void __launch_bounds__(128) k_neighbours(NeighbourArgs A) {
+  const long long m = *A.count;
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < m;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    neighbours_one(A, t);
 }
 
 // ---------------------------------------------------------------------------
@@ -1422,18 +1440,27 @@ void launch_scatter4(float4* dst, const float4* src, const int* idx, int64_t cou
   if (count > 0) k_scatter4<<<static_cast<unsigned>((count + 255) / 256), 256, 0, s>>>(dst, src, idx, count);
 }
 
+static unsigned stride_grid(int64_t n_max) {
+  const int64_t want = (n_max + 255) / 256;
+  return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(want, 148 * 16)));
+}
+
+void launch_ncand_clear(int* ncand, const int* prev_near, const long long* prev_count, int64_t n_max,
+                        cudaStream_t s) {
+  k_ncand_clear<<<stride_grid(n_max), 256, 0, s>>>(ncand, prev_near, prev_count);
+}
+
 void launch_cell_clear(uint4* cells, const uint32_t* prev_keys, const long long* prev_count, int64_t n_max,
                        cudaStream_t s) {
-  k_cell_clear<<<static_cast<unsigned>((n_max + 255) / 256), 256, 0, s>>>(cells, prev_keys, prev_count);
+  k_cell_clear<<<stride_grid(n_max), 256, 0, s>>>(cells, prev_keys, prev_count);
 }
 
 void launch_ranges(const RangesArgs& a, cudaStream_t s) {
-  const unsigned blocks = static_cast<unsigned>((a.n + 255) / 256);
-  k_cell_ranges<<<blocks, 256, 0, s>>>(a);
+  k_cell_ranges<<<stride_grid(a.n), 256, 0, s>>>(a);
 }
 
 void launch_neighbours(const NeighbourArgs& a, cudaStream_t s) {
-  const unsigned blocks = static_cast<unsigned>((a.n + 127) / 128);
+  const unsigned blocks = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((a.n + 127) / 128, 148 * 64)));
   k_neighbours<<<blocks, 128, 0, s>>>(a);
 }
 

@@ -117,6 +117,7 @@ struct NearArgs {
   int* near_list;         // compacted slots (slot order)
   int* ncand;             // zeroed for particles that are not near
   const uint8_t* role;    // slab mode: inactive bodies' particles are never near
+  int all_near;           // broadphase off: every active particle is near
   int64_t p0;             // first slot of the range (slab mode: active range)
   int64_t n;              // end of the range
   int blocks;
@@ -203,6 +204,8 @@ void launch_body_partners(const BroadArgs& a, cudaStream_t s);
 void launch_gather4(float4* dst, const float4* src, const int* idx, int64_t count, cudaStream_t s);
 void launch_scatter4(float4* dst, const float4* src, const int* idx, int64_t count, cudaStream_t s);
 void launch_near(const NearArgs& a, cudaStream_t s);
+void launch_ncand_clear(int* ncand, const int* prev_near, const long long* prev_count, int64_t n_max,
+                        cudaStream_t s);
 void launch_cell_clear(uint4* cells, const uint32_t* prev_keys, const long long* prev_count, int64_t n_max,
                        cudaStream_t s);
 void launch_ranges(const RangesArgs& a, cudaStream_t s);
