@@ -63,6 +63,7 @@ struct pbdr_handle {
   uint8_t* near_flag = nullptr;
   uint32_t* block_count = nullptr;
   uint32_t* block_off = nullptr;
+  uint32_t* scan_tiles = nullptr;  // [2 * tiles]: tile totals, tile offsets
   long long* near_count = nullptr;  // [0] current, [1] previous substep
   int* near_list = nullptr;
   int near_blocks = 0;
@@ -306,6 +307,8 @@ void enqueue_substep(pbdr_handle* h, pbdr_dev::LaunchHook* hook) {
   nr.flag = h->near_flag;
   nr.block_count = h->block_count;
   nr.block_off = h->block_off;
+  nr.tile_sum = h->scan_tiles;
+  nr.tile_off = h->scan_tiles + (h->near_blocks + 4095) / 4096 + 1;
   nr.count = h->near_count;
   nr.keys_c = h->keys[0];
   nr.vals_c = h->vals[0];
@@ -319,7 +322,7 @@ void enqueue_substep(pbdr_handle* h, pbdr_dev::LaunchHook* hook) {
   nr.inflate = h->inflate;
   if (hook) hook->before(kHookBroadphase);
   launch_near(nr, h->stream);
-  if (hook) hook->after(kHookBroadphase, 3);
+  if (hook) hook->after(kHookBroadphase, 4);
 
   const int sb = sort_pairs(h->keys, h->vals, h->n, h->hash_bits, h->sort_temp, h->sm_count,
                             h->stream, hook, h->near_count);
@@ -714,6 +717,7 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
   rc |= dalloc(h, &h->near_flag, n);
   rc |= dalloc(h, &h->block_count, h->near_blocks);
   rc |= dalloc(h, &h->block_off, h->near_blocks);
+  rc |= dalloc(h, &h->scan_tiles, 2 * (static_cast<size_t>(h->near_blocks + 4095) / 4096 + 1));
   rc |= dalloc(h, &h->near_count, 2);
   rc |= dalloc(h, &h->near_list, n);
   rc |= dalloc(h, &h->box_min, 3 * static_cast<size_t>(nb));
@@ -790,7 +794,7 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
   // near flag / scan / compact + particle sort (memset, histogram, scan,
   // passes) + cell ranges + neighbours + iterations.
   h->launches_per_frame = static_cast<int64_t>(h->substeps) *
-                          (4 + 2 + (h->has_torque ? 1 : 0) + 1 + 1 + (3 + h->bpasses) + 2 + 3 + (3 + h->passes) +
+                          (4 + 2 + (h->has_torque ? 1 : 0) + 1 + 1 + (3 + h->bpasses) + 2 + 4 + (3 + h->passes) +
                            1 + 1 + h->iters);
   *out = h;
   return PBDR_OK;

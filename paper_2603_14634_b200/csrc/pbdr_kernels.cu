@@ -441,51 +441,63 @@ __global__ void __launch_bounds__(256) k_near_flag(NearArgs A) {
   if (threadIdx.x == 0) A.block_count[blockIdx.x] = static_cast<uint32_t>(cnt);
 }
 
-// One CTA of 1024 threads: exclusive scan of the per-block near counts, in
-// coalesced chunks of 4096 (four consecutive counts per thread).
-__global__ void __launch_bounds__(1024) k_near_scan(NearArgs A) {
-  __shared__ uint32_t s_warp[32];
-  __shared__ uint32_t s_total;
-  const int t = threadIdx.x;
-  const int lane = t & 31, warp = t >> 5;
-  uint32_t carry = 0;
-  for (int base = 0; base < A.blocks; base += 4096) {
-    const int i0 = base + 4 * t;
-    uint32_t c[4];
+// Exclusive scan of the per-block near counts in two levels: k_near_scan_tiles
+// scans tiles of 4096 counts (one CTA each, four consecutive counts per
+// thread) and stores the tile totals; k_near_scan_top scans the tile totals
+// (one CTA) and writes the total. k_near_compact adds the tile offset.
+constexpr int kScanTile = 4096;
+
+__device__ __forceinline__ uint32_t block_exclusive_scan_1024(uint32_t v, uint32_t* s_warp, uint32_t* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t incl = v;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) c[i] = (i0 + i < A.blocks) ? A.block_count[i0 + i] : 0u;
-    const uint32_t sum = (c[0] + c[1]) + (c[2] + c[3]);
-    uint32_t incl = sum;
+  for (int off = 1; off < 32; off <<= 1) {
+    const uint32_t y = __shfl_up_sync(kFull, incl, off);
+    if (lane >= off) incl += y;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const uint32_t w = s_warp[lane];
+    uint32_t wi = w;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
-      const uint32_t y = __shfl_up_sync(kFull, incl, off);
-      if (lane >= off) incl += y;
+      const uint32_t y = __shfl_up_sync(kFull, wi, off);
+      if (lane >= off) wi += y;
     }
-    if (lane == 31) s_warp[warp] = incl;
-    __syncthreads();
-    if (warp == 0) {
-      uint32_t w = s_warp[lane];
-      uint32_t wi = w;
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const uint32_t y = __shfl_up_sync(kFull, wi, off);
-        if (lane >= off) wi += y;
-      }
-      s_warp[lane] = wi - w;  // exclusive warp offsets
-      if (lane == 31) s_total = wi;
-    }
-    __syncthreads();
-    uint32_t run = carry + s_warp[warp] + (incl - sum);
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      if (i0 + i < A.blocks) {
-        A.block_off[i0 + i] = run;
-        run += c[i];
-      }
-    carry += s_total;
-    __syncthreads();  // s_warp / s_total reuse
+    s_warp[lane] = wi - w;
+    if (lane == 31) *total = wi;
   }
-  if (t == 0) *A.count = static_cast<long long>(carry);
+  __syncthreads();
+  return s_warp[warp] + (incl - v);
+}
+
+__global__ void __launch_bounds__(1024) k_near_scan_tiles(NearArgs A) {
+  __shared__ uint32_t s_warp[32];
+  __shared__ uint32_t s_total;
+  const int i0 = blockIdx.x * kScanTile + 4 * threadIdx.x;
+  uint32_t c[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) c[i] = (i0 + i < A.blocks) ? A.block_count[i0 + i] : 0u;
+  const uint32_t sum = (c[0] + c[1]) + (c[2] + c[3]);
+  uint32_t run = block_exclusive_scan_1024(sum, s_warp, &s_total);
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    if (i0 + i < A.blocks) {
+      A.block_off[i0 + i] = run;
+      run += c[i];
+    }
+  if (threadIdx.x == 0) A.tile_sum[blockIdx.x] = s_total;
+}
+
+__global__ void __launch_bounds__(1024) k_near_scan_top(NearArgs A) {
+  __shared__ uint32_t s_warp[32];
+  __shared__ uint32_t s_total;
+  const int tiles = (A.blocks + kScanTile - 1) / kScanTile;  // <= 1024 (n < 2^32)
+  const uint32_t v = threadIdx.x < tiles ? A.tile_sum[threadIdx.x] : 0u;
+  const uint32_t ex = block_exclusive_scan_1024(v, s_warp, &s_total);
+  if (threadIdx.x < tiles) A.tile_off[threadIdx.x] = ex;
+  if (threadIdx.x == 0) *A.count = static_cast<long long>(s_total);
 }
 
 __global__ void __launch_bounds__(256) k_near_compact(NearArgs A) {
@@ -496,7 +508,7 @@ __global__ void __launch_bounds__(256) k_near_compact(NearArgs A) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (lane == 0) s_w[warp] = __popc(bal);
   __syncthreads();
-  uint32_t off = A.block_off[blockIdx.x];
+  uint32_t off = A.block_off[blockIdx.x] + A.tile_off[blockIdx.x / kScanTile];
   for (int w = 0; w < warp; ++w) off += s_w[w];
   off += __popc(bal & ((1u << lane) - 1u));
   if (p >= A.n) return;
@@ -1414,8 +1426,11 @@ void launch_body_partners(const BroadArgs& a, cudaStream_t s) {
 }
 
 void launch_near(const NearArgs& a, cudaStream_t s) {
-  if (a.blocks > 0) k_near_flag<<<a.blocks, 256, 0, s>>>(a);
-  k_near_scan<<<1, 1024, 0, s>>>(a);
+  if (a.blocks > 0) {
+    k_near_flag<<<a.blocks, 256, 0, s>>>(a);
+    k_near_scan_tiles<<<(a.blocks + kScanTile - 1) / kScanTile, 1024, 0, s>>>(a);
+  }
+  k_near_scan_top<<<1, 1024, 0, s>>>(a);
   if (a.blocks > 0) k_near_compact<<<a.blocks, 256, 0, s>>>(a);
 }
 

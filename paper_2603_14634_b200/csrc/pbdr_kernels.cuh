@@ -111,6 +111,8 @@ struct NearArgs {
   uint8_t* flag;          // [n]
   uint32_t* block_count;  // [blocks]
   uint32_t* block_off;    // [blocks]
+  uint32_t* tile_sum;     // [ceil(blocks / 4096)] scan tile totals
+  uint32_t* tile_off;     // [ceil(blocks / 4096)] scan tile offsets
   long long* count;       // total near particles (device)
   uint32_t* keys_c;       // compacted keys  (sort input)
   uint32_t* vals_c;       // compacted slots (sort input)
