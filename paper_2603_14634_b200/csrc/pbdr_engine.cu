@@ -60,9 +60,7 @@ struct pbdr_handle {
   uint4* cells = nullptr;
   // broadphase-filtered particle list
   uint32_t* key_all = nullptr;
-  uint8_t* near_flag = nullptr;
-  uint32_t* block_count = nullptr;
-  uint32_t* block_off = nullptr;
+  uint32_t* body_near = nullptr;   // [2 * nb]: near particles per body, scan offsets
   uint32_t* scan_tiles = nullptr;  // [2 * tiles]: tile totals, tile offsets
   long long* near_count = nullptr;  // [0] current, [1] previous substep
   int* near_list = nullptr;
@@ -298,27 +296,24 @@ void enqueue_substep(pbdr_handle* h, pbdr_dev::LaunchHook* hook) {
   // Broadphase filter: compact the near particles (slot order) into the sort input.
   NearArgs nr{};
   nr.pos = h->pos[h->cur];
-  nr.body_of = h->body_of;
+  nr.body_desc = h->pk_full.body;
   nr.box_min = h->box_min;
   nr.box_max = h->box_max;
   nr.npartners = h->npartners;
   nr.partners = h->partners;
   nr.key_all = h->key_all;
-  nr.flag = h->near_flag;
-  nr.block_count = h->block_count;
-  nr.block_off = h->block_off;
+  nr.list = h->slab ? h->active_list : nullptr;
+  nr.nbl = h->slab ? h->n_active : h->nb;
+  nr.body_near = h->body_near;
+  nr.body_off = h->body_near + h->nb;
   nr.tile_sum = h->scan_tiles;
-  nr.tile_off = h->scan_tiles + (h->near_blocks + 4095) / 4096 + 1;
+  nr.tile_off = h->scan_tiles + (h->nb + 4095) / 4096 + 1;
   nr.count = h->near_count;
   nr.keys_c = h->keys[0];
   nr.vals_c = h->vals[0];
   nr.near_list = h->near_list;
-  nr.ncand = h->ncand;
   nr.role = h->slab ? h->role : nullptr;
   nr.all_near = h->broadphase ? 0 : 1;
-  nr.p0 = h->p_lo;
-  nr.n = h->p_hi;
-  nr.blocks = static_cast<int>((h->p_hi - h->p_lo + 255) / 256);
   nr.inflate = h->inflate;
   if (hook) hook->before(kHookBroadphase);
   launch_near(nr, h->stream);
@@ -714,10 +709,8 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
   rc |= dalloc(h, &h->cells, T);
   h->near_blocks = static_cast<int>((n + 255) / 256);
   rc |= dalloc(h, &h->key_all, n);
-  rc |= dalloc(h, &h->near_flag, n);
-  rc |= dalloc(h, &h->block_count, h->near_blocks);
-  rc |= dalloc(h, &h->block_off, h->near_blocks);
-  rc |= dalloc(h, &h->scan_tiles, 2 * (static_cast<size_t>(h->near_blocks + 4095) / 4096 + 1));
+  rc |= dalloc(h, &h->body_near, 2 * static_cast<size_t>(nb));
+  rc |= dalloc(h, &h->scan_tiles, 2 * (static_cast<size_t>(nb + 4095) / 4096 + 1));
   rc |= dalloc(h, &h->near_count, 2);
   rc |= dalloc(h, &h->near_list, n);
   rc |= dalloc(h, &h->box_min, 3 * static_cast<size_t>(nb));

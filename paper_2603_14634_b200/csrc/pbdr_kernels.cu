@@ -409,44 +409,104 @@ __global__ void __launch_bounds__(256) k_cell_ranges(RangesArgs A) {
 // Broadphase filter (exact): a candidate j of particle i lies in j's body box
 // and within h of i, so i lies in the h-inflated box of a partner body. Only
 // such "near" particles enter the hash grid and search it; the others have no
-// candidates. Flags -> block counts -> exclusive scan -> compaction in slot
-// order (deterministic).
+// candidates. Per body (one warp, partner boxes held in lanes): count the near
+// particles; scan the body counts; write the near slots of each body at its
+// offset. Bodies without partners cost no particle reads; the list is in slot
+// order (bodies ascend, slots ascend within a body), so it is deterministic.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_near_flag(NearArgs A) {
-  const int64_t p = A.p0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  bool near = false;
-  if (p < A.n) {
-    const int bi = A.body_of[p];
-    const bool active = !A.role || A.role[bi] != 0;
-    const int np = active ? (A.all_near ? -1 : A.npartners[bi]) : 0;
-    near = np < 0;  // partner overflow (or no broadphase): search in full
-    // Bodies without partners (most of them in sparse scenes) need no position.
-    const float4 xi = np > 0 ? A.pos[p] : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-    for (int k = 0; k < np && !near; ++k) {
-      const int o = A.partners[static_cast<int64_t>(bi) * PBDR_PARTNER_CAP + k];
-      float lo[3], hi[3];
-      load_box(A.box_min, A.box_max, o, lo, hi);
-      const float xs[3] = {xi.x, xi.y, xi.z};
-      bool in = true;
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const float m = A.inflate + fmaxf(fabsf(lo[c]), fabsf(hi[c])) * 1e-6f;
-        in = in && xs[c] >= lo[c] - m && xs[c] <= hi[c] + m;
-      }
-      near = in;
-    }
-    A.flag[p] = near ? 1 : 0;
-  }
-  const int cnt = __syncthreads_count(near);
-  if (threadIdx.x == 0) A.block_count[blockIdx.x] = static_cast<uint32_t>(cnt);
-}
-
-// Exclusive scan of the per-block near counts in two levels: k_near_scan_tiles
-// scans tiles of 4096 counts (one CTA each, four consecutive counts per
-// thread) and stores the tile totals; k_near_scan_top scans the tile totals
-// (one CTA) and writes the total. k_near_compact adds the tile offset.
 constexpr int kScanTile = 4096;
 
+struct NearBoxes {
+  float lo[3], hi[3];  // lane k < np: partner k's box inflated by h (+ relative guard)
+};
+
+__device__ __forceinline__ int near_body_setup(const NearArgs& A, int t, int lane, int& b, int& start, int& n,
+                                               NearBoxes& bx) {
+  b = A.list ? A.list[t] : t;
+  const int4 bd = A.body_desc[b];
+  start = bd.x;
+  n = bd.y;
+  int np = A.all_near ? -1 : A.npartners[b];
+  if (A.role && A.role[b] == 0) np = 0;
+  if (np > 0 && lane < np) {
+    const int o = A.partners[static_cast<int64_t>(b) * PBDR_PARTNER_CAP + lane];
+    float lo[3], hi[3];
+    load_box(A.box_min, A.box_max, o, lo, hi);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const float m = A.inflate + fmaxf(fabsf(lo[c]), fabsf(hi[c])) * 1e-6f;
+      bx.lo[c] = lo[c] - m;
+      bx.hi[c] = hi[c] + m;
+    }
+  }
+  return np;
+}
+
+// Near test of particle slot p against the np partner boxes held by lanes.
+__device__ __forceinline__ bool near_test(const NearArgs& A, bool valid, int64_t p, int np, const NearBoxes& bx) {
+  float4 xi = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+  if (valid) xi = A.pos[p];
+  bool in_any = false;
+  for (int k = 0; k < np; ++k) {
+    float lo[3], hi[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      lo[c] = __shfl_sync(kFull, bx.lo[c], k);
+      hi[c] = __shfl_sync(kFull, bx.hi[c], k);
+    }
+    in_any = in_any || (xi.x >= lo[0] && xi.x <= hi[0] && xi.y >= lo[1] && xi.y <= hi[1] && xi.z >= lo[2] &&
+                        xi.z <= hi[2]);
+  }
+  return valid && in_any;
+}
+
+__global__ void __launch_bounds__(256) k_near_count(NearArgs A) {
+  const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= A.nbl) return;  // warp-uniform
+  int b, start, n;
+  NearBoxes bx{};
+  const int np = near_body_setup(A, t, lane, b, start, n, bx);
+  uint32_t cnt = 0;
+  if (np < 0) {
+    cnt = static_cast<uint32_t>(n);
+  } else if (np > 0) {
+    for (int base = 0; base < n; base += 32) {
+      const int q = base + lane;
+      cnt += __popc(__ballot_sync(kFull, near_test(A, q < n, start + static_cast<int64_t>(q), np, bx)));
+    }
+  }
+  if (lane == 0) A.body_near[t] = cnt;
+}
+
+__global__ void __launch_bounds__(256) k_near_write(NearArgs A) {
+  const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= A.nbl) return;
+  if (A.body_near[t] == 0u) return;  // warp-uniform
+  int b, start, n;
+  NearBoxes bx{};
+  const int np = near_body_setup(A, t, lane, b, start, n, bx);
+  uint32_t off = A.body_off[t] + A.tile_off[t / kScanTile];
+  for (int base = 0; base < n; base += 32) {
+    const int q = base + lane;
+    const int64_t p = start + static_cast<int64_t>(q);
+    const bool near = np < 0 ? q < n : near_test(A, q < n, p, np, bx);
+    const unsigned bal = __ballot_sync(kFull, near);
+    if (near) {
+      const uint32_t o = off + __popc(bal & ((1u << lane) - 1u));
+      A.near_list[o] = static_cast<int>(p);
+      A.keys_c[o] = A.key_all[p];
+      A.vals_c[o] = static_cast<uint32_t>(p);
+    }
+    off += __popc(bal);
+  }
+}
+
+// Exclusive scan of the body near counts in two levels: k_near_scan_tiles
+// scans tiles of 4096 counts (one CTA each, four consecutive counts per
+// thread) and stores the tile totals; k_near_scan_top scans the tile totals
+// (one CTA) and writes the near total; k_near_write adds the tile offset.
 __device__ __forceinline__ uint32_t block_exclusive_scan_1024(uint32_t v, uint32_t* s_warp, uint32_t* total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t incl = v;
@@ -478,13 +538,13 @@ __global__ void __launch_bounds__(1024) k_near_scan_tiles(NearArgs A) {
   const int i0 = blockIdx.x * kScanTile + 4 * threadIdx.x;
   uint32_t c[4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) c[i] = (i0 + i < A.blocks) ? A.block_count[i0 + i] : 0u;
+  for (int i = 0; i < 4; ++i) c[i] = (i0 + i < A.nbl) ? A.body_near[i0 + i] : 0u;
   const uint32_t sum = (c[0] + c[1]) + (c[2] + c[3]);
   uint32_t run = block_exclusive_scan_1024(sum, s_warp, &s_total);
 #pragma unroll
   for (int i = 0; i < 4; ++i)
-    if (i0 + i < A.blocks) {
-      A.block_off[i0 + i] = run;
+    if (i0 + i < A.nbl) {
+      A.body_off[i0 + i] = run;
       run += c[i];
     }
   if (threadIdx.x == 0) A.tile_sum[blockIdx.x] = s_total;
@@ -493,30 +553,11 @@ __global__ void __launch_bounds__(1024) k_near_scan_tiles(NearArgs A) {
 __global__ void __launch_bounds__(1024) k_near_scan_top(NearArgs A) {
   __shared__ uint32_t s_warp[32];
   __shared__ uint32_t s_total;
-  const int tiles = (A.blocks + kScanTile - 1) / kScanTile;  // <= 1024 (n < 2^32)
-  const uint32_t v = threadIdx.x < tiles ? A.tile_sum[threadIdx.x] : 0u;
+  const int tiles = (A.nbl + kScanTile - 1) / kScanTile;  // <= 1024 (bodies < 4M)
+  const uint32_t v = static_cast<int>(threadIdx.x) < tiles ? A.tile_sum[threadIdx.x] : 0u;
   const uint32_t ex = block_exclusive_scan_1024(v, s_warp, &s_total);
-  if (threadIdx.x < tiles) A.tile_off[threadIdx.x] = ex;
+  if (static_cast<int>(threadIdx.x) < tiles) A.tile_off[threadIdx.x] = ex;
   if (threadIdx.x == 0) *A.count = static_cast<long long>(s_total);
-}
-
-__global__ void __launch_bounds__(256) k_near_compact(NearArgs A) {
-  __shared__ uint32_t s_w[8];
-  const int64_t p = A.p0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const bool near = p < A.n && A.flag[p] != 0;
-  const unsigned bal = __ballot_sync(kFull, near);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (lane == 0) s_w[warp] = __popc(bal);
-  __syncthreads();
-  uint32_t off = A.block_off[blockIdx.x] + A.tile_off[blockIdx.x / kScanTile];
-  for (int w = 0; w < warp; ++w) off += s_w[w];
-  off += __popc(bal & ((1u << lane) - 1u));
-  if (p >= A.n) return;
-  if (near) {
-    A.near_list[off] = static_cast<int>(p);
-    A.keys_c[off] = A.key_all[p];
-    A.vals_c[off] = static_cast<uint32_t>(p);
-  }
 }
 
 // Candidate counts are only written for near particles (k_neighbours); the
@@ -1426,12 +1467,15 @@ void launch_body_partners(const BroadArgs& a, cudaStream_t s) {
 }
 
 void launch_near(const NearArgs& a, cudaStream_t s) {
-  if (a.blocks > 0) {
-    k_near_flag<<<a.blocks, 256, 0, s>>>(a);
-    k_near_scan_tiles<<<(a.blocks + kScanTile - 1) / kScanTile, 1024, 0, s>>>(a);
+  if (a.nbl > 0) {
+    const unsigned wblocks = static_cast<unsigned>((static_cast<int64_t>(a.nbl) * 32 + 255) / 256);
+    k_near_count<<<wblocks, 256, 0, s>>>(a);
+    k_near_scan_tiles<<<(a.nbl + kScanTile - 1) / kScanTile, 1024, 0, s>>>(a);
+    k_near_scan_top<<<1, 1024, 0, s>>>(a);
+    k_near_write<<<wblocks, 256, 0, s>>>(a);
+  } else {
+    cudaMemsetAsync(a.count, 0, sizeof(long long), s);
   }
-  k_near_scan_top<<<1, 1024, 0, s>>>(a);
-  if (a.blocks > 0) k_near_compact<<<a.blocks, 256, 0, s>>>(a);
 }
 
 // Slab halo exchange: float4 records by index (particle slots or body ids).

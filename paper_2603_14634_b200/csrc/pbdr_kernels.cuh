@@ -102,27 +102,24 @@ struct BroadArgs {
 // slot order, into the list that the hash grid is built from.
 struct NearArgs {
   const float4* pos;  // X~
-  const int* body_of;
+  const int4* body_desc;  // (first slot, n, ...) per body (whole-scene packing)
   const uint32_t* box_min;
   const uint32_t* box_max;
   const int* npartners;
   const int* partners;
   const uint32_t* key_all;
-  uint8_t* flag;          // [n]
-  uint32_t* block_count;  // [blocks]
-  uint32_t* block_off;    // [blocks]
-  uint32_t* tile_sum;     // [ceil(blocks / 4096)] scan tile totals
-  uint32_t* tile_off;     // [ceil(blocks / 4096)] scan tile offsets
+  const int* list;        // slab mode: active bodies (ascending), else null (all bodies)
+  int nbl;                // bodies to process
+  uint32_t* body_near;    // [nbl] near particles per body
+  uint32_t* body_off;     // [nbl] exclusive offsets within the scan tile
+  uint32_t* tile_sum;     // [ceil(nbl / 4096)] scan tile totals
+  uint32_t* tile_off;     // [ceil(nbl / 4096)] scan tile offsets
   long long* count;       // total near particles (device)
   uint32_t* keys_c;       // compacted keys  (sort input)
   uint32_t* vals_c;       // compacted slots (sort input)
   int* near_list;         // compacted slots (slot order)
-  int* ncand;             // zeroed for particles that are not near
   const uint8_t* role;    // slab mode: inactive bodies' particles are never near
   int all_near;           // broadphase off: every active particle is near
-  int64_t p0;             // first slot of the range (slab mode: active range)
-  int64_t n;              // end of the range
-  int blocks;
   float inflate;
 };
 
