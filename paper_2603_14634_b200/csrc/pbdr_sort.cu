@@ -24,6 +24,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "pbdr_sort.cuh"
 
 namespace pbdr_dev {
@@ -90,14 +92,16 @@ pbdr_sort_onesweep(const uint32_t* __restrict__ keys_in, const uint32_t* __restr
   __shared__ uint32_t s_vals[kSortTile];
 
   const int64_t n = n_dev ? static_cast<int64_t>(*n_dev) : n_max;
+  // Persistent: the grid is at most one wave; each CTA keeps claiming tiles
+  // (in increasing order, so look-back only waits on running CTAs) until the
+  // device-side count is covered.
+  for (;;) {
   if (threadIdx.x == 0) s_tile = atomicAdd(tile_counter, 1u);
   for (int i = threadIdx.x; i < kSortWarps * kRadix; i += kSortThreads) (&s_warp_hist[0][0])[i] = 0u;
   __syncthreads();
 
   const uint32_t tile = s_tile;
-  // Tiles past a device-side count hold no keys; they never publish, and no
-  // earlier tile waits on them.
-  if (static_cast<int64_t>(tile) * kSortTile >= n) return;
+  if (static_cast<int64_t>(tile) * kSortTile >= n) return;  // block-uniform
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t lt_mask = (1u << lane) - 1u;
@@ -194,6 +198,25 @@ pbdr_sort_onesweep(const uint32_t* __restrict__ keys_in, const uint32_t* __restr
     keys_out[dst] = kk;
     vals_out[dst] = s_vals[j];
   }
+  __syncthreads();  // shared buffers are reused by the next tile
+  }
+}
+
+// Zeroes the histograms, tile counters and the status words of the tiles the
+// device-side count actually uses (instead of a memset sized for the maximum).
+__global__ void __launch_bounds__(256)
+pbdr_sort_zero(uint32_t* __restrict__ temp, int passes, int64_t tiles_max, int64_t n_max, const long long* n_dev) {
+  const int64_t n = n_dev ? static_cast<int64_t>(*n_dev) : n_max;
+  const int64_t need = (n + kSortTile - 1) / kSortTile + 1;
+  const int64_t tiles = need < tiles_max ? need : tiles_max;
+  const int64_t head = static_cast<int64_t>(passes) * kRadix + passes;  // hist + counters
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < head; i += stride) temp[i] = 0u;
+  uint32_t* status = temp + head;
+  const int64_t used = tiles * kRadix;
+  for (int p = 0; p < passes; ++p)
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < used; i += stride)
+      status[static_cast<int64_t>(p) * tiles_max * kRadix + i] = 0u;
 }
 
 size_t sort_temp_bytes(int64_t n, int passes) {
@@ -212,7 +235,11 @@ int sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t n, int key_bits, vo
   uint32_t* status = counters + passes;
   const size_t bytes = sort_temp_bytes(n, passes);
   if (hook) hook->before(kHookMemset);
-  cudaMemsetAsync(temp, 0, bytes, stream);
+  if (n_dev) {
+    pbdr_sort_zero<<<sm_count * 4, 256, 0, stream>>>(static_cast<uint32_t*>(temp), passes, tiles, n, n_dev);
+  } else {
+    cudaMemsetAsync(temp, 0, bytes, stream);
+  }
   if (hook) hook->after(kHookMemset);
   if (hook) hook->before(kHookHistogram);
   const int hist_blocks = sm_count * 4;
@@ -222,7 +249,8 @@ int sort_pairs(uint32_t* keys[2], uint32_t* vals[2], int64_t n, int key_bits, vo
   int cur = 0;
   for (int p = 0; p < passes; ++p) {
     if (hook) hook->before(kHookOnesweep);
-    pbdr_sort_onesweep<<<static_cast<unsigned>(tiles), kSortThreads, 0, stream>>>(
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(tiles, static_cast<int64_t>(sm_count) * 4));
+    pbdr_sort_onesweep<<<grid, kSortThreads, 0, stream>>>(
         keys[cur], vals[cur], keys[cur ^ 1], vals[cur ^ 1], n, n_dev, 8 * p, hist + p * kRadix,
         status + static_cast<size_t>(p) * tiles * kRadix, counters + p);
     if (hook) hook->after(kHookOnesweep);
