@@ -16,7 +16,7 @@ CSRC     := $(PKG)/csrc
 LIB      := $(PKG)/lib/libpbdr_gpu.so
 NVFLAGS  := $(ARCH) -std=c++17 -O3 -lineinfo --fmad=false -Xcompiler -fPIC,-ffp-contract=off \
             -Xptxas -v -Iinclude -I$(CSRC)
-CU_SRC   := $(CSRC)/pbdr_kernels.cu $(CSRC)/pbdr_sort.cu $(CSRC)/pbdr_engine.cu
+CU_SRC   := $(CSRC)/pbdr_kernels.cu $(CSRC)/pbdr_sort.cu $(CSRC)/pbdr_engine.cu $(CSRC)/pbdr_mesh.cu
 CXX_SRC  := $(CSRC)/pbdr_scene.cpp $(CSRC)/pbdr_errors.cpp $(CSRC)/pbdr_dropin.cpp
 HDRS     := include/pbdr_gpu.h $(wildcard include/pbdr/*.hpp) $(wildcard $(CSRC)/*.h) $(wildcard $(CSRC)/*.cuh)
 OBJDIR   := build/obj

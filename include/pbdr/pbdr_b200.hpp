@@ -27,6 +27,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <array>
 #include <vector>
 
 #include "pbdr_gpu.h"
@@ -178,6 +179,24 @@ struct Scene {
 int add_packed_body(Scene& scene, const std::vector<Vec3>& centers, double radius,
                     double total_mass, const Rotation& rotate, const Vec3& translate,
                     double jitter, uint64_t seed);
+
+// ---- Mesh packing (geometry.hpp:19-57) ------------------------------------------
+struct TriMesh {
+  std::vector<Vec3> vertices;
+  std::vector<std::array<int, 3>> triangles;
+};
+
+struct SpherePacking {
+  std::vector<Vec3> centers;
+  double radius = 0;
+  long ambiguous_count = 0;  // grid samples whose inside test stayed ambiguous
+  long candidate_count = 0;  // grid samples tested
+  size_t size() const { return centers.size(); }
+};
+
+// pack_mesh (geometry.cpp:151-195) on the GPU: grid points inside the closed
+// mesh by ray-crossing parity, bit-identical to the reference's fp64 test.
+SpherePacking pack_mesh(const TriMesh& mesh, double radius, int device = 0);
 
 // ---- step ---------------------------------------------------
 // Advances the scene by one substep dt = cfg.dt() on the GPU (device 0) and

@@ -243,6 +243,19 @@ enum {
 int pbdr_gpu_gather(pbdr_handle* h, int field, const int32_t* index, int64_t count, void* dst);
 int pbdr_gpu_scatter(pbdr_handle* h, int field, const int32_t* index, int64_t count, const void* src);
 
+/* ---- GPU pack_mesh (geometry.cpp:125-195) -----
+ * Replaces: pbdr::pack_mesh(const TriMesh&, double radius) (geometry.hpp:57).
+ * Grid candidates bb.min + radius + i * 2 radius (x slowest) inside the
+ * closed triangle mesh by ray-crossing parity -- the reference's fp64
+ * Moller-Trumbore test with its ambiguity band, re-cast along up to 8 fixed
+ * jittered directions (ambiguous after 8: outside), one GPU thread per
+ * candidate. centers (3 * capacity doubles, grid order) may be NULL to query
+ * the count. Errors as the reference: radius <= 0 or a bad index -> GENERIC
+ * (pbdr::Error), no candidate or none inside -> EMPTY_PACKING. */
+int pbdr_pack_mesh(const double* vertices, int32_t num_vertices, const int32_t* triangles, int32_t num_triangles,
+                   double radius, int device, double* centers, int64_t capacity, int64_t* count,
+                   int64_t* candidates, int64_t* ambiguous);
+
 /* ---- Host-side scene construction (no device work) ------------------------
  * The five BASELINE.json configs, generated deterministically from splitmix64
  * (rng.hpp:10-29) with pack_box lattices (geometry.cpp:32-55) and

@@ -1066,3 +1066,129 @@ unsigned oracle_inertia_solve(const double* I9, const double* dL, double* w, dou
 }
 
 }  // extern "C"
+
+// ---- pack_mesh restatement (geometry.cpp:73-195) ------------------------------
+// Test infrastructure: checks the GPU pack_mesh; pinned against the reference's
+// own pack_mesh (oracle/_ref) in tests/test_mesh.py.
+namespace {
+namespace mesh {
+struct V {
+  double x, y, z;
+};
+inline V sub(V a, V b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+inline double dot(V a, V b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+inline V cross(V a, V b) { return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x}; }
+inline double norm(V v) { return std::sqrt(dot(v, v)); }
+
+// splitmix64 as rng.hpp:10-29 (seed + golden gamma, next_unit = (u64 >> 11) * 2^-53).
+inline void unit3(uint64_t seed, double out[3]) {
+  uint64_t s = seed + 0x9E3779B97F4A7C15ull;
+  for (int k = 0; k < 3; ++k) {
+    uint64_t z = (s += 0x9E3779B97F4A7C15ull);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z = z ^ (z >> 31);
+    out[k] = static_cast<double>(z >> 11) * 0x1.0p-53;
+  }
+}
+
+// 0 miss, 1 hit, 2 ambiguous (edge/grazing band 1e-9, geometry.cpp:77-104)
+int ray_tri(V o, V d, V a, V b, V c) {
+  const V e1 = sub(b, a), e2 = sub(c, a);
+  const V pv = cross(d, e2);
+  const double det = dot(e1, pv);
+  const double scale = norm(e1) * norm(e2);
+  if (std::abs(det) <= 1e-9 * std::max(scale, 1e-12)) {
+    const V n = cross(e1, e2);
+    const double nn = norm(n);
+    if (nn <= 1e-12) return 0;
+    const V u = {n.x / nn, n.y / nn, n.z / nn};
+    return std::abs(dot(sub(o, a), u)) <= 1e-9 * std::max(1.0, norm(sub(o, a))) ? 2 : 0;
+  }
+  const double inv = 1.0 / det;
+  const V tv = sub(o, a);
+  const double u = dot(tv, pv) * inv;
+  const V qv = cross(tv, e1);
+  const double v = dot(d, qv) * inv;
+  const double t = dot(e2, qv) * inv;
+  if (u < -1e-9 || v < -1e-9 || u + v > 1.0 + 1e-9) return 0;
+  if (t < -1e-9) return 0;
+  if (u <= 1e-9 || v <= 1e-9 || u + v >= 1.0 - 1e-9 || t <= 1e-9) return 2;
+  return 1;
+}
+}  // namespace mesh
+}  // namespace
+
+extern "C" int oracle_pack_mesh(const double* verts, int nv, const int* tris, int nt, double radius, double* centers,
+                                long cap, long* count, long* candidates, long* ambiguous) {
+  using mesh::V;
+  if (!(radius > 0.0)) return 9;
+  for (long k = 0; k < 3L * nt; ++k)
+    if (tris[k] < 0 || tris[k] >= nv) return 9;
+  V mn = {verts[0], verts[1], verts[2]}, mx = mn;
+  for (int i = 0; i < nv; ++i) {
+    mn.x = std::min(mn.x, verts[3 * i]); mx.x = std::max(mx.x, verts[3 * i]);
+    mn.y = std::min(mn.y, verts[3 * i + 1]); mx.y = std::max(mx.y, verts[3 * i + 1]);
+    mn.z = std::min(mn.z, verts[3 * i + 2]); mx.z = std::max(mx.z, verts[3 * i + 2]);
+  }
+  const double pitch = 2.0 * radius;
+  const int nx = static_cast<int>(std::floor((mx.x - mn.x) / pitch + 1e-12));
+  const int ny = static_cast<int>(std::floor((mx.y - mn.y) / pitch + 1e-12));
+  const int nz = static_cast<int>(std::floor((mx.z - mn.z) / pitch + 1e-12));
+  if (nx < 1 || ny < 1 || nz < 1) return 3;
+  V dirs[8];
+  for (int a = 0; a < 8; ++a) {
+    V d = {0.577350269, 0.577350269, 0.577350269};
+    if (a > 0) {
+      double u[3];
+      mesh::unit3(0x5EEDull + static_cast<uint64_t>(a), u);
+      d.x += -0.3 + (0.3 - -0.3) * u[0];
+      d.y += -0.3 + (0.3 - -0.3) * u[1];
+      d.z += -0.3 + (0.3 - -0.3) * u[2];
+    }
+    const double n = mesh::norm(d);
+    dirs[a] = n > 0.0 ? V{d.x / n, d.y / n, d.z / n} : V{0, 0, 0};
+  }
+  const long total = static_cast<long>(nx) * ny * nz;
+  std::vector<uint8_t> inside(total, 0), amb(total, 0);
+#pragma omp parallel for schedule(dynamic, 64)
+  for (long i = 0; i < total; ++i) {
+    const int iz = static_cast<int>(i % nz), iy = static_cast<int>((i / nz) % ny), ix = static_cast<int>(i / (static_cast<long>(nz) * ny));
+    const V p = {mn.x + radius + ix * pitch, mn.y + radius + iy * pitch, mn.z + radius + iz * pitch};
+    bool resolved = false;
+    for (int a = 0; a < 8 && !resolved; ++a) {
+      long crossings = 0;
+      bool bad = false;
+      for (int t = 0; t < nt && !bad; ++t) {
+        const int* T = &tris[3 * t];
+        const V A = {verts[3 * T[0]], verts[3 * T[0] + 1], verts[3 * T[0] + 2]};
+        const V B = {verts[3 * T[1]], verts[3 * T[1] + 1], verts[3 * T[1] + 2]};
+        const V Cc = {verts[3 * T[2]], verts[3 * T[2] + 1], verts[3 * T[2] + 2]};
+        const int h = mesh::ray_tri(p, dirs[a], A, B, Cc);
+        if (h == 1) ++crossings;
+        if (h == 2) bad = true;
+      }
+      if (!bad) {
+        resolved = true;
+        inside[i] = (crossings % 2) == 1;
+      }
+    }
+    amb[i] = !resolved;
+  }
+  long c = 0, am = 0;
+  for (long i = 0; i < total; ++i) {
+    am += amb[i];
+    if (!inside[i]) continue;
+    if (centers && c < cap) {
+      const int iz = static_cast<int>(i % nz), iy = static_cast<int>((i / nz) % ny), ix = static_cast<int>(i / (static_cast<long>(nz) * ny));
+      centers[3 * c] = mn.x + radius + ix * pitch;
+      centers[3 * c + 1] = mn.y + radius + iy * pitch;
+      centers[3 * c + 2] = mn.z + radius + iz * pitch;
+    }
+    ++c;
+  }
+  *count = c;
+  *candidates = total;
+  *ambiguous = am;
+  return c == 0 ? 3 : 0;
+}

@@ -54,6 +54,7 @@ def olib():
         L.oracle_num_slots.restype = C.c_int64
         L.oracle_tile_kp.argtypes = [vp]
         L.oracle_tile_kp.restype = C.c_int
+        L.oracle_pack_mesh.argtypes = [vp, C.c_int, vp, C.c_int, C.c_double, vp, C.c_long, vp, vp, vp]
         L.oracle_set_roles.argtypes = [vp, vp]
         L.oracle_set_roles.restype = None
         for name in ("oracle_gather", "oracle_scatter"):
@@ -89,6 +90,7 @@ def rlib():
         L = C.CDLL(REF_PATH)
         vp = C.c_void_p
         L.ref_rng_u64.argtypes = [C.c_uint64, C.c_int, vp]
+        L.ref_pack_mesh.argtypes = [vp, C.c_int, vp, C.c_int, C.c_double, vp, C.c_long, vp, vp, vp]
         L.ref_rng_u64.restype = None
         L.ref_rng_unit.argtypes = [C.c_uint64, C.c_int, vp]
         L.ref_rng_unit.restype = None
@@ -318,3 +320,28 @@ def kat_momentum(m, xa, va, Pb, Lb, dt, linfix=True, angfix=True):
     err = olib().oracle_kat_momentum(n, _p(_f32(m)), _p(xa), _p(_f32(va)), _p(_f32(Pb)), _p(_f32(Lb)), dt,
                                      int(linfix), int(angfix), _p(xo), _p(vo), _p(axis))
     return int(err), xo, vo, axis
+
+
+def _pack_mesh_call(fn, vertices, triangles, radius):
+    v = np.ascontiguousarray(vertices, np.float64).reshape(-1, 3)
+    t = np.ascontiguousarray(triangles, np.int32).reshape(-1, 3)
+    cnt, cand, amb = C.c_long(), C.c_long(), C.c_long()
+    cap = 1
+    for _ in range(2):
+        out = np.empty((cap, 3), np.float64)
+        st = fn(_p(v), len(v), _p(t), len(t), radius, _p(out), cap, C.byref(cnt), C.byref(cand), C.byref(amb))
+        if st != 0 or cnt.value <= cap:
+            break
+        cap = cnt.value
+    return st, out[:cnt.value] if st == 0 else None, cand.value, amb.value
+
+
+def pack_mesh(vertices, triangles, radius):
+    """Oracle restatement of pack_mesh: (status, centers, candidates, ambiguous)."""
+    return _pack_mesh_call(olib().oracle_pack_mesh, vertices, triangles, radius)
+
+
+def ref_pack_mesh(vertices, triangles, radius):
+    """The reference's own pack_mesh (oracle/_ref); None when not built."""
+    L = rlib()
+    return None if L is None else _pack_mesh_call(L.ref_pack_mesh, vertices, triangles, radius)

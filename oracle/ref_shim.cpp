@@ -97,6 +97,31 @@ int ref_pack_box(double hx, double hy, double hz, int n, double* centers, double
   return static_cast<int>(p.centers.size());
 }
 
+// pack_mesh (geometry.cpp:151-195): returns the status (0 ok, 3 EmptyPackingError,
+// 9 other Error); centers in grid order.
+int ref_pack_mesh(const double* verts, int nv, const int* tris, int nt, double radius, double* centers,
+                  long cap, long* count, long* candidates, long* ambiguous) {
+  TriMesh m;
+  for (int i = 0; i < nv; ++i) m.vertices.push_back({verts[3 * i], verts[3 * i + 1], verts[3 * i + 2]});
+  for (int t = 0; t < nt; ++t) m.triangles.push_back({tris[3 * t], tris[3 * t + 1], tris[3 * t + 2]});
+  try {
+    SpherePacking p = pack_mesh(m, radius);
+    *count = static_cast<long>(p.centers.size());
+    *candidates = p.candidate_count;
+    *ambiguous = p.ambiguous_count;
+    for (size_t i = 0; i < p.centers.size() && static_cast<long>(i) < cap; ++i) {
+      centers[3 * i] = p.centers[i].x;
+      centers[3 * i + 1] = p.centers[i].y;
+      centers[3 * i + 2] = p.centers[i].z;
+    }
+  } catch (const EmptyPackingError&) {
+    return 3;
+  } catch (const Error&) {
+    return 9;
+  }
+  return 0;
+}
+
 int ref_polar(const double* a, double* r_out, double* s_out, double* q_out, double det_tol) {
   double* axis_out = nullptr;
   REF_GUARD({

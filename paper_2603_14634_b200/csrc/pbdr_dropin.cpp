@@ -198,6 +198,33 @@ Body make_body(const std::vector<Particle>& particles, const std::vector<int>& i
   return b;
 }
 
+SpherePacking pack_mesh(const TriMesh& mesh, double radius, int device) {
+  std::vector<double> v;
+  v.reserve(3 * mesh.vertices.size());
+  for (const Vec3& p : mesh.vertices) {
+    v.push_back(p.x);
+    v.push_back(p.y);
+    v.push_back(p.z);
+  }
+  std::vector<int32_t> t;
+  t.reserve(3 * mesh.triangles.size());
+  for (const auto& tri : mesh.triangles)
+    for (int k = 0; k < 3; ++k) t.push_back(tri[k]);
+  int64_t count = 0, cand = 0, amb = 0;
+  check(pbdr_pack_mesh(v.data(), static_cast<int32_t>(mesh.vertices.size()), t.data(),
+                       static_cast<int32_t>(mesh.triangles.size()), radius, device, nullptr, 0, &count, &cand, &amb));
+  std::vector<double> c(3 * static_cast<size_t>(count));
+  check(pbdr_pack_mesh(v.data(), static_cast<int32_t>(mesh.vertices.size()), t.data(),
+                       static_cast<int32_t>(mesh.triangles.size()), radius, device, c.data(), count, &count, &cand,
+                       &amb));
+  SpherePacking p;
+  p.radius = radius;
+  p.candidate_count = static_cast<long>(cand);
+  p.ambiguous_count = static_cast<long>(amb);
+  for (int64_t i = 0; i < count; ++i) p.centers.push_back({c[3 * i], c[3 * i + 1], c[3 * i + 2]});
+  return p;
+}
+
 int add_packed_body(Scene& scene, const std::vector<Vec3>& centers, double radius,
                     double total_mass, const Rotation& rotate, const Vec3& translate,
                     double jitter, uint64_t seed) {

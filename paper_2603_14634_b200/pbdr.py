@@ -171,6 +171,7 @@ def lib() -> C.CDLL:
         L.pbdr_scene_free.argtypes = [vp]
         L.pbdr_scene_free.restype = None
         L.pbdr_pack_box.argtypes = [C.c_double, C.c_double, C.c_double, C.c_int, vp, vp]
+        L.pbdr_pack_mesh.argtypes = [vp, C.c_int32, vp, C.c_int32, C.c_double, C.c_int, vp, i64, vp, vp, vp]
         L.pbdr_rng_u64.argtypes = [C.c_uint64, C.c_int, vp]
         L.pbdr_rng_u64.restype = None
         L.pbdr_rng_unit.argtypes = [C.c_uint64, C.c_int, vp]
@@ -568,6 +569,21 @@ def pack_box(half_extents, n):
     r = C.c_double()
     raise_status(lib().pbdr_pack_box(half_extents[0], half_extents[1], half_extents[2], n, _ptr(c), C.byref(r)))
     return c, r.value
+
+
+def pack_mesh(vertices, triangles, radius, device: int = 0):
+    """GPU pack_mesh (geometry.cpp:151-195): grid points inside the closed
+    triangle mesh, in grid order. Returns (centers[k, 3], candidates, ambiguous)."""
+    v = np.ascontiguousarray(vertices, np.float64).reshape(-1, 3)
+    t = np.ascontiguousarray(triangles, np.int32).reshape(-1, 3)
+    L = lib()
+    cnt, cand, amb = C.c_int64(), C.c_int64(), C.c_int64()
+    raise_status(L.pbdr_pack_mesh(_ptr(v), len(v), _ptr(t), len(t), radius, device, None, 0,
+                                  C.byref(cnt), C.byref(cand), C.byref(amb)))
+    out = np.empty((cnt.value, 3), np.float64)
+    raise_status(L.pbdr_pack_mesh(_ptr(v), len(v), _ptr(t), len(t), radius, device, _ptr(out), cnt.value,
+                                  C.byref(cnt), C.byref(cand), C.byref(amb)))
+    return out, cand.value, amb.value
 
 
 def rng_u64(seed, count):
