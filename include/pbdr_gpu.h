@@ -134,6 +134,13 @@ int pbdr_gpu_write_particles(pbdr_handle* h, const double* position, const doubl
  * pinned host memory. Either may be NULL. */
 int pbdr_gpu_read_f32(pbdr_handle* h, float* pos4, float* vel4);
 int pbdr_gpu_write_f32(pbdr_handle* h, const float* pos4, const float* vel4);
+/* Asynchronous versions on the handle's stream (host buffers must be pinned
+ * and stay valid until pbdr_gpu_sync, which also reports device errors). With
+ * one handle per batch slice, slices overlap their transfers with each
+ * other's compute. */
+int pbdr_gpu_write_f32_async(pbdr_handle* h, const float* pos4, const float* vel4);
+int pbdr_gpu_read_f32_async(pbdr_handle* h, float* pos4, float* vel4);
+int pbdr_gpu_step_frames_async(pbdr_handle* h, int64_t frames);
 
 /* Per-body com / orientation / momentum (compute_momentum body.cpp:72-83,
  * extract_pose body.cpp:103-124), computed on the device. */

@@ -908,6 +908,36 @@ int pbdr_gpu_write_f32(pbdr_handle* h, const float* pos4, const float* vel4) {
   return PBDR_OK;
 }
 
+// Asynchronous variants (pinned host memory; completion and device errors at
+// pbdr_gpu_sync): separate handles on separate streams overlap their host
+// transfers with each other's compute.
+int pbdr_gpu_write_f32_async(pbdr_handle* h, const float* pos4, const float* vel4) {
+  if (!h) return set_error(PBDR_ERR_GENERIC, "null handle");
+  PBDR_CUDA(cudaSetDevice(h->device));
+  if (pos4)
+    PBDR_CUDA(cudaMemcpyAsync(h->pos[h->cur], pos4, sizeof(float4) * h->n, cudaMemcpyHostToDevice, h->stream));
+  if (vel4)
+    PBDR_CUDA(cudaMemcpyAsync(h->vel, vel4, sizeof(float4) * h->n, cudaMemcpyHostToDevice, h->stream));
+  return PBDR_OK;
+}
+
+int pbdr_gpu_read_f32_async(pbdr_handle* h, float* pos4, float* vel4) {
+  if (!h) return set_error(PBDR_ERR_GENERIC, "null handle");
+  PBDR_CUDA(cudaSetDevice(h->device));
+  if (pos4)
+    PBDR_CUDA(cudaMemcpyAsync(pos4, h->pos[h->cur], sizeof(float4) * h->n, cudaMemcpyDeviceToHost, h->stream));
+  if (vel4)
+    PBDR_CUDA(cudaMemcpyAsync(vel4, h->vel, sizeof(float4) * h->n, cudaMemcpyDeviceToHost, h->stream));
+  return PBDR_OK;
+}
+
+int pbdr_gpu_step_frames_async(pbdr_handle* h, int64_t frames) {
+  if (!h) return set_error(PBDR_ERR_GENERIC, "null handle");
+  pbdr_host::clear_error();
+  PBDR_CUDA(cudaSetDevice(h->device));
+  return step_frames_async(h, frames);
+}
+
 int pbdr_gpu_read_particles(pbdr_handle* h, double* position, double* velocity) {
   if (!h) return set_error(PBDR_ERR_GENERIC, "null handle");
   std::vector<float4> p(h->n), v(h->n);

@@ -134,6 +134,9 @@ def lib() -> C.CDLL:
         L.pbdr_gpu_write_particles.argtypes = [vp, vp, vp]
         L.pbdr_gpu_read_f32.argtypes = [vp, vp, vp]
         L.pbdr_gpu_write_f32.argtypes = [vp, vp, vp]
+        L.pbdr_gpu_write_f32_async.argtypes = [vp, vp, vp]
+        L.pbdr_gpu_read_f32_async.argtypes = [vp, vp, vp]
+        L.pbdr_gpu_step_frames_async.argtypes = [vp, i64]
         L.pbdr_gpu_read_bodies.argtypes = [vp, vp]
         L.pbdr_last_error.restype = C.c_char_p
         L.pbdr_last_error_key.restype = C.c_char_p
@@ -488,6 +491,16 @@ class GpuSolver:
 
     def write_f32(self, pos4=None, vel4=None):
         raise_status(lib().pbdr_gpu_write_f32(self._h, _ptr(pos4), _ptr(vel4)))
+
+    # asynchronous (pinned buffers; completion and errors at sync())
+    def write_f32_async(self, pos4=None, vel4=None):
+        raise_status(lib().pbdr_gpu_write_f32_async(self._h, _ptr(pos4), _ptr(vel4)))
+
+    def read_f32_async(self, pos4=None, vel4=None):
+        raise_status(lib().pbdr_gpu_read_f32_async(self._h, _ptr(pos4), _ptr(vel4)))
+
+    def step_frames_async(self, frames: int = 1):
+        raise_status(lib().pbdr_gpu_step_frames_async(self._h, frames))
 
     def read_particles(self):
         p = np.empty((self.n, 3), np.float64)
