@@ -768,12 +768,18 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
   UP(h->cta_desc, cdesc.data(), cdesc.size());
   UP(h->anchor, anchor.data(), nb);
 #undef UP
-  cudaMemset(h->init, 0, sizeof(float4) * n);
-  cudaMemset(h->counter, 0, sizeof(long long));
-  cudaMemset(h->ncand, 0, sizeof(int) * n);
-  cudaMemset(h->cells, 0xFF, sizeof(uint4) * T);
-  cudaMemset(h->near_count, 0, sizeof(long long) * 2);
-  cudaMemset(h->rquat, 0, sizeof(float4) * nb);
+  {
+    cudaError_t m = cudaMemset(h->init, 0, sizeof(float4) * n);
+    if (m == cudaSuccess) m = cudaMemset(h->counter, 0, sizeof(long long));
+    if (m == cudaSuccess) m = cudaMemset(h->ncand, 0, sizeof(int) * n);
+    if (m == cudaSuccess) m = cudaMemset(h->cells, 0xFF, sizeof(uint4) * T);
+    if (m == cudaSuccess) m = cudaMemset(h->near_count, 0, sizeof(long long) * 2);
+    if (m == cudaSuccess) m = cudaMemset(h->rquat, 0, sizeof(float4) * nb);
+    if (m != cudaSuccess) {
+      release(h);
+      return cuda_fail(m, "initialise device buffers");
+    }
+  }
   h->pk_full = {h->cta_desc, h->warp_desc, h->body_desc, h->ctas};
   if (const char* e = std::getenv("PBDR_BROADPHASE")) h->broadphase = std::atoi(e) != 0;
   h->pk_iter = h->pk_active = h->pk_full;

@@ -27,14 +27,18 @@ MARGIN = 0.05
 class _Scene:
     """Config 5 at 8 x 8 x 4 cubes with x-velocities +-1.5 m/s by grid column
     (odd columns +x, even -x), so column pairs collide within a few frames --
-    also across the slab edges the tests place."""
+    also across the slab edges the tests place. `torque`: every body also
+    carries a torque program (ghosts then need exact anchors for the wrench)."""
 
-    def __init__(self, fast=False):
+    def __init__(self, fast=False, torque=False):
         g = P.GeneratedScene(5, seed=0, scale=GX)
         self.cfg = g.cfg
         nb = g.desc.num_bodies
         off = g.array("body_offsets", nb + 1, np.int64)
-        self.sc = P.scene_with_programs(g, [P.ForceProgram((0, 0, 0), (0, 0, 0), 0.0, float("inf"), 0, 0)] * nb)
+        rng = np.random.default_rng(5)
+        progs = [P.ForceProgram((0, 0, 0), tuple(rng.uniform(-0.02, 0.02, 3)) if torque else (0, 0, 0), 0.0,
+                                float("inf"), 0, 0) for _ in range(nb)]
+        self.sc = P.scene_with_programs(g, progs)
         com_x = self.sc.rest_com[:, 0]
         col = np.rint((com_x - com_x.min()) / 0.2).astype(int)
         body = np.repeat(np.arange(nb), np.diff(off))
@@ -46,8 +50,8 @@ class _Scene:
         self.rho, self.h = S.body_reach(self.sc.rest_offsets, off, self.sc.radius)
 
 
-def _scene(fast=False):
-    sc = _Scene(fast)
+def _scene(fast=False, torque=False):
+    sc = _Scene(fast, torque)
     return sc, sc.off, sc.rho, sc.h
 
 
@@ -156,6 +160,19 @@ def test_slab_threads_world3_matches_single_process(reference, pyoracle):
     geo = _crossing_geometry(3, coms, rho, h)
     assert _cross_pairs(pairs, coms[-1], geo) > 0, "contacts across the slab edges"
     engines = [OracleEngine(pyoracle.Oracle(g.desc, g.cfg, threads=2), g.cfg) for _ in range(3)]
+    states = S.run_threads(engines, off, FRAMES, geometry=geo)
+    _check_union(states, p_ref, v_ref, g.nb)
+
+
+def test_slab_threads_with_torque_programs(pyoracle):
+    # Ghosts integrate locally; with torque programs their wrench prepass uses
+    # anchored sums, so the anchors must travel with the halo (substep end).
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from slab_oracle_engine import OracleEngine
+    g, off, rho, h = _scene(torque=True)
+    p_ref, v_ref, coms, pairs = _reference(pyoracle, g)
+    geo = _crossing_geometry(2, coms, rho, h)
+    engines = [OracleEngine(pyoracle.Oracle(g.desc, g.cfg, threads=4), g.cfg) for _ in range(2)]
     states = S.run_threads(engines, off, FRAMES, geometry=geo)
     _check_union(states, p_ref, v_ref, g.nb)
 
