@@ -87,6 +87,7 @@ struct pbdr_handle {
   float* cand_rr = nullptr;
   DevError* err = nullptr;
   long long* counter = nullptr;
+  int* tile_ctr = nullptr;  // iteration kernel: dynamic tile claims (self-resetting)
   double* stats = nullptr;
   std::vector<void*> allocations;
   size_t device_bytes = 0;
@@ -393,6 +394,7 @@ void enqueue_iteration(pbdr_handle* h, int iter_index, pbdr_dev::LaunchHook* hoo
   it.linfix = h->linfix;
   it.angfix = h->angfix;
   it.timing = h->timing;
+  it.tile_ctr = h->tile_ctr;
   if (hook) hook->before(kHookIteration);
   if (h->pk_iter.ctas > 0) launch_iteration(it, h->pk_iter.ctas, h->kp, h->stream);
   if (hook) hook->after(kHookIteration);
@@ -734,6 +736,7 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
   rc |= dalloc(h, &h->cand_rr, static_cast<size_t>(n) * PBDR_NBR_CAP);
   rc |= dalloc(h, &h->err, 1);
   rc |= dalloc(h, &h->counter, 1);
+  rc |= dalloc(h, &h->tile_ctr, 2);
   rc |= dalloc(h, &h->stats, static_cast<size_t>(nb) * 13);
   if (rc != PBDR_OK) {
     const int code = pbdr_last_error_payload(nullptr, nullptr, nullptr);
@@ -771,6 +774,7 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
   {
     cudaError_t m = cudaMemset(h->init, 0, sizeof(float4) * n);
     if (m == cudaSuccess) m = cudaMemset(h->counter, 0, sizeof(long long));
+    if (m == cudaSuccess) m = cudaMemset(h->tile_ctr, 0, 2 * sizeof(int));
     if (m == cudaSuccess) m = cudaMemset(h->ncand, 0, sizeof(int) * n);
     if (m == cudaSuccess) m = cudaMemset(h->cells, 0xFF, sizeof(uint4) * T);
     if (m == cudaSuccess) m = cudaMemset(h->near_count, 0, sizeof(long long) * 2);

@@ -178,6 +178,17 @@ __device__ __forceinline__ void bulk_g2s_stream(void* dst, const void* src, uint
 #endif
 }
 
+// Asynchronous global -> shared copies (no register staging) for the next
+// tile's body table.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t done = 0;
   do {
@@ -787,32 +798,41 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  // Per-body table of the current tile (anchor, masses, first warp, warps),
-  // loaded by warp 0 while the bulk copies are in flight.
-  __shared__ float4 s_banc[kWarps];  // anchor xyz, M
-  __shared__ int2 s_bw[kWarps];      // first warp, warps
-  __shared__ float s_binv[kWarps];   // 1/M
-  __shared__ float4 s_brq[kWarps];   // warm-start rotation (w, x, y, z)
+  // Per-body table of a tile (anchor, masses, body descriptor, warm-start
+  // rotation), double-buffered: the next tile's table is copied in with
+  // cp.async while the current tile computes.
+  __shared__ float4 s_tanc[2][kWarps];
+  __shared__ float2 s_tmass[2][kWarps];
+  __shared__ int4 s_tdesc[2][kWarps];
+  __shared__ float4 s_trq[2][kWarps];
+  __shared__ int s_next;
   const bool fixes = A.linfix || A.angfix;
   const long long t_entry = A.timing ? clock64() : 0;  // phase clocks (debug launches only)
-  if (threadIdx.x == 0) mbar_init(&s_bar, 1);
-
-  // Tiles (packed CTAs of whole bodies) are walked with a grid stride; the
-  // next tile's descriptors are loaded one tile ahead, so a tile starts with
-  // the bulk copies and the body-table loads instead of a descriptor chain.
-  int tile = blockIdx.x;
-  int4 cd_n = ld_keep_nc(&A.cta_desc[tile]);
-  int4 wd_n = ld_keep_nc(&A.warp_desc[tile * kWarps + warp]);
-  for (uint32_t it_parity = 0; tile < A.ntiles; tile += gridDim.x, it_parity ^= 1u) {
-  const int4 cd = cd_n;  // first slot, slot count, first body, bodies
-  const int4 wd = wd_n;
-  {
-    const int tn = tile + static_cast<int>(gridDim.x);
-    if (tn < A.ntiles) {
-      cd_n = ld_keep_nc(&A.cta_desc[tn]);
-      wd_n = ld_keep_nc(&A.warp_desc[tn * kWarps + warp]);
+  // One CTA per tile (grid == ntiles): static; otherwise tiles are claimed
+  // dynamically, in increasing order.
+  const bool dynamic = static_cast<int>(gridDim.x) < A.ntiles;
+  if (threadIdx.x == 0) {
+    mbar_init(&s_bar, 1);
+    s_next = dynamic ? atomicAdd(A.tile_ctr, 1) : static_cast<int>(blockIdx.x);
+  }
+  __syncthreads();
+  int tile = s_next;
+  int tb = 0;  // table buffer of the current tile
+  int4 cd_n = make_int4(0, 0, 0, 0), wd_n = make_int4(-1, 0, 0, 1 << 16);
+  if (tile < A.ntiles) {
+    cd_n = ld_keep_nc(&A.cta_desc[tile]);
+    wd_n = ld_keep_nc(&A.warp_desc[tile * kWarps + warp]);
+    if (warp == 0 && lane < cd_n.w) {  // first tile's table: synchronous
+      const int bb = cd_n.z + lane;
+      s_tdesc[0][lane] = ld_keep_nc(&A.body_desc[bb]);
+      s_tanc[0][lane] = ld_keep(&A.anchor[bb]);
+      s_tmass[0][lane] = ld_keep_nc(&A.body_mass[bb]);
+      s_trq[0][lane] = ld_keep(&A.rquat[bb]);
     }
   }
+  for (uint32_t it_parity = 0; tile < A.ntiles; it_parity ^= 1u) {
+  const int4 cd = cd_n;  // first slot, slot count, first body, bodies
+  const int4 wd = wd_n;
   const int first = cd.x;
 
   if (threadIdx.x == 0) {
@@ -829,18 +849,9 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
 #ifdef PBDR_DIAG_TMAISSUE
     if (A.timing) A.timing[8 * static_cast<int64_t>(tile) + 7] = clock64();
 #endif
+    s_next = dynamic ? atomicAdd(A.tile_ctr, 1) : A.ntiles;  // the tile after this one
   }
-
-  if (warp == 0 && lane < cd.w) {
-    const int bb = cd.z + lane;
-    const int4 bdb = ld_keep_nc(&A.body_desc[bb]);
-    const float4 an = ld_keep(&A.anchor[bb]);
-    const float2 mass = ld_keep_nc(&A.body_mass[bb]);
-    s_banc[lane] = make_float4(an.x, an.y, an.z, mass.x);
-    s_binv[lane] = mass.y;
-    s_bw[lane] = make_int2(bdb.w, bdb.z);
-    s_brq[lane] = ld_keep(&A.rquat[bb]);
-  }
+  cp_async_wait_all();  // this tile's table (prefetched during the previous tile)
 
   const int b = wd.x;
   const int wi = wd.y;
@@ -857,10 +868,15 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
 
   long long* tm = A.timing ? A.timing + 8 * static_cast<int64_t>(tile) : nullptr;
   if (tm && threadIdx.x == 0) tm[0] = t_entry;  // CTA entry: stage = descriptors + table + bulk copies
-  __syncthreads();  // barrier initialised, per-body table filled
+  __syncthreads();  // barrier initialised, per-body table filled, next tile claimed
+  const int tile_next = s_next;
+  if (tile_next < A.ntiles) {  // next tile's descriptors, consumed at its start
+    cd_n = ld_keep_nc(&A.cta_desc[tile_next]);
+    wd_n = ld_keep_nc(&A.warp_desc[tile_next * kWarps + warp]);
+  }
   float a[3];
   {
-    const float4 an = s_banc[lb];
+    const float4 an = s_tanc[tb][lb];
     a[0] = an.x; a[1] = an.y; a[2] = an.z;
   }
   mbar_wait(&s_bar, it_parity);
@@ -1009,9 +1025,10 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
   // ---- per-body math A (warp 0, lane = body of the CTA) ---------------------
   if (PBDR_MATH_ACTIVE) {
     const int bb = cd.z + PBDR_MATH_BODY;
-    const float4 an = s_banc[PBDR_MATH_BODY];
-    const float invM = s_binv[PBDR_MATH_BODY];
-    const int2 bw = s_bw[PBDR_MATH_BODY];
+    const float4 an = make_float4(s_tanc[tb][PBDR_MATH_BODY].x, s_tanc[tb][PBDR_MATH_BODY].y,
+                                  s_tanc[tb][PBDR_MATH_BODY].z, s_tmass[tb][PBDR_MATH_BODY].x);
+    const float invM = s_tmass[tb][PBDR_MATH_BODY].y;
+    const int2 bw = make_int2(s_tdesc[tb][PBDR_MATH_BODY].w, s_tdesc[tb][PBDR_MATH_BODY].z);
     const int fw = bw.x;
     float S[21];
 #pragma unroll
@@ -1039,7 +1056,7 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
       R[kResLb + k] = S[18 + k] - tmp[k];
     }
     double qd[4];
-    const float4 rq4 = s_brq[PBDR_MATH_BODY];
+    const float4 rq4 = s_trq[tb][PBDR_MATH_BODY];
     const float rq[4] = {rq4.x, rq4.y, rq4.z, rq4.w};
 #ifdef PBDR_DIAG_NO_POLAR
     bool ok = true;  // diagnostic build only: identity rotation
@@ -1135,8 +1152,8 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
   // ---- per-body math B: momentum corrections -------------------------------
   if (PBDR_MATH_ACTIVE) {
     const int bb = cd.z + PBDR_MATH_BODY;
-    const float2 mass = make_float2(s_banc[PBDR_MATH_BODY].w, s_binv[PBDR_MATH_BODY]);
-    const int2 bw = s_bw[PBDR_MATH_BODY];
+    const float2 mass = s_tmass[tb][PBDR_MATH_BODY];
+    const int2 bw = make_int2(s_tdesc[tb][PBDR_MATH_BODY].w, s_tdesc[tb][PBDR_MATH_BODY].z);
     const int fw = bw.x;
     float S[15];
 #pragma unroll
@@ -1261,8 +1278,26 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
     tm[7] = smid;
 #endif
   }
+  if (tile_next < A.ntiles && warp == 0 && lane < cd_n.w) {
+    const int bb = cd_n.z + lane;
+    cp_async16(&s_tdesc[tb ^ 1][lane], &A.body_desc[bb]);
+    cp_async16(&s_tanc[tb ^ 1][lane], &A.anchor[bb]);
+    cp_async8(&s_tmass[tb ^ 1][lane], &A.body_mass[bb]);
+    cp_async16(&s_trq[tb ^ 1][lane], &A.rquat[bb]);
+  }
+  cp_async_commit();
   __syncthreads();  // the next tile's bulk copies overwrite the staging buffers
+  tile = tile_next;
+  tb ^= 1;
   }  // tiles
+  if (dynamic && threadIdx.x == 0) {
+    // The last CTA out resets the claim counter for the next launch.
+    __threadfence();
+    if (atomicAdd(A.tile_ctr + 1, 1) == static_cast<int>(gridDim.x) - 1) {
+      A.tile_ctr[0] = 0;
+      A.tile_ctr[1] = 0;
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1549,10 +1584,10 @@ cudaError_t prepare_iteration_kernel() {
   return e;
 }
 
-// Persistent grid (one wave of resident CTAs walking the tiles) measured no
-// faster than one CTA per tile on C4 (0.4406 vs 0.4399 ms); off by default.
+// Persistent grid: one wave of resident CTAs claims tiles dynamically and
+// prefetches each next tile's descriptors and body table.
 #ifndef PBDR_ITER_PERSISTENT
-#define PBDR_ITER_PERSISTENT 0
+#define PBDR_ITER_PERSISTENT 1
 #endif
 
 template <int KP>

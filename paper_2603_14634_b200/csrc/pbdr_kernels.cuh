@@ -182,6 +182,7 @@ struct IterArgs {
   float4* mom_acc;    // per body (P, L) accumulators for kPerSubstep
   long long* timing;  // optional per-CTA phase clocks (debug), else null
   int ntiles;         // packed CTAs (tiles) of this launch; set by launch_iteration
+  int* tile_ctr;      // [2] tile claim counter and finished-CTA counter (self-resetting, zero at create)
 };
 
 struct StatsArgs {
