@@ -728,39 +728,6 @@ __device__ __forceinline__ void pp_contact(const float x[3], float w, int64_t p,
   }
 }
 
-#ifndef PBDR_STAGE_INIT
-#define PBDR_STAGE_INIT 0
-#endif
-#ifndef PBDR_FLAT_CAND
-#define PBDR_FLAT_CAND 0
-#endif
-// Per-body math of the CTA's bodies: one lane per body on warp 0, or (per-warp
-// mode) lane 0 of warp b for body b, so the bodies' fp64 chains issue from
-// different warps / SM sub-partitions instead of sharing one warp.
-#ifndef PBDR_MATH_PER_WARP
-#define PBDR_MATH_PER_WARP 0
-#endif
-#if PBDR_MATH_PER_WARP
-#define PBDR_MATH_ACTIVE (lane == 0 && warp < cd.w)
-#define PBDR_MATH_BODY warp
-#else
-#define PBDR_MATH_ACTIVE (warp == 0 && lane < cd.w)
-#define PBDR_MATH_BODY lane
-#endif
-#ifndef PBDR_STAGE_REST
-#define PBDR_STAGE_REST 1
-#endif
-#if PBDR_STAGE_REST
-#define PBDR_REST_AT(gslot, sslot) s_rest[(sslot)]
-#else
-#define PBDR_REST_AT(gslot, sslot) __ldg(&A.rest[(gslot)])
-#endif
-#if PBDR_STAGE_INIT
-#define PBDR_INIT_AT(gslot, sslot) s_init[(sslot)]
-#else
-#define PBDR_INIT_AT(gslot, sslot) A.init[(gslot)]
-#endif
-
 constexpr int kResF = 32;
 enum ResSlot {
   kResC = 0,      // c (3), anchor-relative com of X_i
@@ -784,7 +751,7 @@ constexpr int iter_min_blocks() { return KP == 8 ? 2 : 3; }
 template <int KP>
 __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(IterArgs A) {
   constexpr int kSlots = kThreads * KP;  // particle slots staged per CTA
-  extern __shared__ float4 s_stage[];  // pos | vel | rest [| init], kSlots each
+  extern __shared__ float4 s_stage[];  // pos | vel | rest, kSlots each
   __shared__ float s_part[kWarps][21];
   __shared__ float s_res[kWarps][kResF];
   __shared__ __align__(8) uint64_t s_bar;
@@ -792,9 +759,6 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
   float4* s_pos = s_stage;
   float4* s_vel = s_stage + kSlots;
   float4* s_rest = s_stage + 2 * kSlots;
-#if PBDR_STAGE_INIT
-  float4* s_init = s_stage + 3 * kSlots;
-#endif
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -837,18 +801,10 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
 
   if (threadIdx.x == 0) {
     const uint32_t bytes = static_cast<uint32_t>(cd.y) * 16u;
-#if PBDR_STAGE_INIT
-    mbar_expect_tx(&s_bar, 4u * bytes);
-    bulk_g2s(s_init, A.init + first, bytes, &s_bar);
-#else
-    mbar_expect_tx(&s_bar, (PBDR_STAGE_REST ? 3u : 2u) * bytes);
-#endif
+    mbar_expect_tx(&s_bar, 3u * bytes);
     bulk_g2s_stream(s_pos, A.pos_in + first, bytes, &s_bar);
     bulk_g2s_stream(s_vel, A.vel + first, bytes, &s_bar);
-    if (PBDR_STAGE_REST) bulk_g2s_stream(s_rest, A.rest + first, bytes, &s_bar);
-#ifdef PBDR_DIAG_TMAISSUE
-    if (A.timing) A.timing[8 * static_cast<int64_t>(tile) + 7] = clock64();
-#endif
+    bulk_g2s_stream(s_rest, A.rest + first, bytes, &s_bar);
     s_next = dynamic ? atomicAdd(A.tile_ctr, 1) : A.ntiles;  // the tile after this one
   }
   cp_async_wait_all();  // this tile's table (prefetched during the previous tile)
@@ -890,42 +846,6 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
   for (int f = 0; f < 21; ++f) acc[f] = 0.0f;
 #pragma unroll
   for (int k = 0; k < KP; ++k) dX[k][0] = dX[k][1] = dX[k][2] = 0.0f;
-#if PBDR_FLAT_CAND
-  // Particle-particle deltas first, candidate rank c outermost: the loads of
-  // the lane's KP particles for one rank are independent and overlap. Per
-  // particle the sum still runs over c ascending from +0.
-  {
-    int cmax = 0;
-#pragma unroll
-    for (int k = 0; k < KP; ++k) cmax = max(cmax, ncs[k]);
-    for (int c = 0; c < cmax; ++c) {
-      int jj[KP];
-      float rr[KP];
-      float4 xj[KP];
-#pragma unroll
-      for (int k = 0; k < KP; ++k) {
-        const int64_t p = start + k * 32 * W + wi * 32 + lane;
-        jj[k] = 0;
-        rr[k] = 0.0f;
-        if (c < ncs[k]) {
-          jj[k] = A.cand_j[static_cast<int64_t>(c) * A.n + p];
-          rr[k] = A.cand_rr[static_cast<int64_t>(c) * A.n + p];
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < KP; ++k)
-        if (c < ncs[k]) xj[k] = A.pos_in[jj[k]];
-#pragma unroll
-      for (int k = 0; k < KP; ++k) {
-        if (!(c < ncs[k])) continue;
-        const int q = k * 32 * W + wi * 32 + lane;
-        const float4 x4 = s_pos[off + q];
-        const float x[3] = {x4.x, x4.y, x4.z};
-        pp_contact(x, x4.w, start + q, xj[k], jj[k], rr[k], A.relax, dX[k]);
-      }
-    }
-  }
-#endif
 #pragma unroll
   for (int k = 0; k < KP; ++k) {
     const int q = k * 32 * W + wi * 32 + lane;
@@ -933,7 +853,7 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
     const int64_t p = start + q;
     const float4 x4 = s_pos[off + q];
     const float4 v4 = s_vel[off + q];
-    const float4 r4 = PBDR_REST_AT(start + q, off + q);
+    const float4 r4 = s_rest[off + q];
     const float x[3] = {x4.x, x4.y, x4.z};
     const float m = v4.w;
 
@@ -950,7 +870,7 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
         dPG[2] = fmaf(push, Pn[2], dPG[2]);
         const float mu = A.planes.mu[pl];
         if (mu > 0.0f) {
-          const float4 xi = PBDR_INIT_AT(p, off + q);
+          const float4 xi = A.init[p];
           const float t[3] = {x[0] - xi.x, x[1] - xi.y, x[2] - xi.z};
           const float tn = dot3_fma(t, Pn);
           const float tt[3] = {fmaf(-tn, Pn[0], t[0]), fmaf(-tn, Pn[1], t[1]), fmaf(-tn, Pn[2], t[2])};
@@ -972,22 +892,14 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
         }
       }
     }
-#if PBDR_FLAT_CAND
-    float dPP[3] = {dX[k][0], dX[k][1], dX[k][2]};  // candidates summed before this loop
-#else
     float dPP[3] = {0.0f, 0.0f, 0.0f};
-#ifdef PBDR_DIAG_NO_PP
-    const int nc = 0;  // diagnostic build only
-#else
     const int nc = ncs[k];
-#endif
     for (int c = 0; c < nc; ++c) {
       const int j = A.cand_j[static_cast<int64_t>(c) * A.n + p];
       const float rr = A.cand_rr[static_cast<int64_t>(c) * A.n + p];
       const float4 xj = A.pos_in[j];
       pp_contact(x, x4.w, p, xj, j, rr, A.relax, dPP);
     }
-#endif
     const float v[3] = {v4.x, v4.y, v4.z};
     const float q0[3] = {r4.x, r4.y, r4.z};
     // Body sums: product fields accumulate with one fma per particle (the
@@ -1023,12 +935,12 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
   if (tm && threadIdx.x == 0) tm[2] = clock64();
 
   // ---- per-body math A (warp 0, lane = body of the CTA) ---------------------
-  if (PBDR_MATH_ACTIVE) {
-    const int bb = cd.z + PBDR_MATH_BODY;
-    const float4 an = make_float4(s_tanc[tb][PBDR_MATH_BODY].x, s_tanc[tb][PBDR_MATH_BODY].y,
-                                  s_tanc[tb][PBDR_MATH_BODY].z, s_tmass[tb][PBDR_MATH_BODY].x);
-    const float invM = s_tmass[tb][PBDR_MATH_BODY].y;
-    const int2 bw = make_int2(s_tdesc[tb][PBDR_MATH_BODY].w, s_tdesc[tb][PBDR_MATH_BODY].z);
+  if ((warp == 0 && lane < cd.w)) {
+    const int bb = cd.z + lane;
+    const float4 an = make_float4(s_tanc[tb][lane].x, s_tanc[tb][lane].y,
+                                  s_tanc[tb][lane].z, s_tmass[tb][lane].x);
+    const float invM = s_tmass[tb][lane].y;
+    const int2 bw = make_int2(s_tdesc[tb][lane].w, s_tdesc[tb][lane].z);
     const int fw = bw.x;
     float S[21];
 #pragma unroll
@@ -1048,7 +960,7 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
       Pb[k] = S[15 + k];
     }
     cross3(cb, Pb, tmp);
-    float* R = &s_res[PBDR_MATH_BODY][0];
+    float* R = &s_res[lane][0];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       R[kResC + k] = c[k];
@@ -1056,15 +968,9 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
       R[kResLb + k] = S[18 + k] - tmp[k];
     }
     double qd[4];
-    const float4 rq4 = s_trq[tb][PBDR_MATH_BODY];
+    const float4 rq4 = s_trq[tb][lane];
     const float rq[4] = {rq4.x, rq4.y, rq4.z, rq4.w};
-#ifdef PBDR_DIAG_NO_POLAR
-    bool ok = true;  // diagnostic build only: identity rotation
-    for (int f = 0; f < 9; ++f) R[kResR + f] = (f % 4 == 0) ? 1.0f : 0.0f;
-    qd[0] = 1.0; qd[1] = qd[2] = qd[3] = 0.0;
-#else
     const bool ok = polar_warm_f(&S[6], rq, &R[kResR], qd);
-#endif
     R[kResSmOk] = ok ? 1.0f : 0.0f;
     A.rquat[bb] = ok ? make_float4(static_cast<float>(qd[0]), static_cast<float>(qd[1]),
                                    static_cast<float>(qd[2]), static_cast<float>(qd[3]))
@@ -1093,13 +999,13 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
       if (!(q < n)) continue;
       const float4 x4 = s_pos[off + q];
       const float4 v4 = s_vel[off + q];
-      const float4 r4 = PBDR_REST_AT(start + q, off + q);
+      const float4 r4 = s_rest[off + q];
       const float x[3] = {x4.x, x4.y, x4.z};
       const float v[3] = {v4.x, v4.y, v4.z};
       const float q0[3] = {r4.x, r4.y, r4.z};
       float xi[3] = {0.0f, 0.0f, 0.0f};
       if (!A.incremental) {
-        const float4 i4 = PBDR_INIT_AT(start + q, off + q);
+        const float4 i4 = A.init[start + q];
         xi[0] = i4.x; xi[1] = i4.y; xi[2] = i4.z;
       }
       float xa[3], va[3], pa[3];
@@ -1150,10 +1056,10 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
   if (tm && threadIdx.x == 0) tm[4] = clock64();
 
   // ---- per-body math B: momentum corrections -------------------------------
-  if (PBDR_MATH_ACTIVE) {
-    const int bb = cd.z + PBDR_MATH_BODY;
-    const float2 mass = s_tmass[tb][PBDR_MATH_BODY];
-    const int2 bw = make_int2(s_tdesc[tb][PBDR_MATH_BODY].w, s_tdesc[tb][PBDR_MATH_BODY].z);
+  if ((warp == 0 && lane < cd.w)) {
+    const int bb = cd.z + lane;
+    const float2 mass = s_tmass[tb][lane];
+    const int2 bw = make_int2(s_tdesc[tb][lane].w, s_tdesc[tb][lane].z);
     const int fw = bw.x;
     float S[15];
 #pragma unroll
@@ -1165,7 +1071,7 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
 #pragma unroll
     for (int f = 0; f < 15; ++f) finite = finite && isfinite(S[f]);
     if (!finite) record_error(A.err, PBDR_DEVERR_NONFINITE, bb, A.substep_counter);
-    float* R = &s_res[PBDR_MATH_BODY][0];
+    float* R = &s_res[lane][0];
     const float M = mass.x, invM = mass.y;
     float ca[3], Pa[3], La[3], tmp[3], dv[3] = {0.0f, 0.0f, 0.0f}, om[3] = {0.0f, 0.0f, 0.0f};
 #pragma unroll
@@ -1211,12 +1117,7 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
       If[4] = S[13] + M * (ca[0] * ca[2]);
       If[5] = S[14] + M * (ca[1] * ca[2]);
       double nax[3];
-#ifdef PBDR_DIAG_NO_INERTIA
-      const unsigned e = 0;  // diagnostic build only
-      om[0] = dL[0] * If[0]; om[1] = dL[1] * If[1]; om[2] = dL[2] * If[2];
-#else
       const unsigned e = inertia_solve_f(If, dL, om, nax);
-#endif
       if (e) record_error(A.err, e, bb, A.substep_counter, nax);
     }
 #pragma unroll
@@ -1246,7 +1147,7 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
     const float4 v4 = s_vel[off + q];
     float xi[3] = {0.0f, 0.0f, 0.0f};
     if (!A.incremental) {
-      const float4 i4 = PBDR_INIT_AT(start + q, off + q);
+      const float4 i4 = A.init[start + q];
       xi[0] = i4.x; xi[1] = i4.y; xi[2] = i4.z;
     }
     const float x[3] = {x4.x, x4.y, x4.z};
@@ -1272,11 +1173,9 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
   }  // fixes
   if (tm && threadIdx.x == 0) {
     tm[6] = clock64();
-#ifndef PBDR_DIAG_TMAISSUE
     unsigned smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
     tm[7] = smid;
-#endif
   }
   if (tile_next < A.ntiles && warp == 0 && lane < cd_n.w) {
     const int bb = cd_n.z + lane;
@@ -1472,13 +1371,7 @@ __global__ void __launch_bounds__(kThreads) k_body_wrench(WrenchArgs A) {
 
 }  // namespace
 
-#ifndef PBDR_ITER_EXTRA_SMEM
-#define PBDR_ITER_EXTRA_SMEM 0
-#endif
-size_t iteration_smem_bytes(int kp) {
-  return sizeof(float4) * ((PBDR_STAGE_INIT ? 1 : 0) + (PBDR_STAGE_REST ? 1 : 0) + 2) * kThreads * kp +
-         PBDR_ITER_EXTRA_SMEM;
-}
+size_t iteration_smem_bytes(int kp) { return sizeof(float4) * 3 * kThreads * kp; }
 
 void launch_integrate(const IntegrateArgs& a, cudaStream_t s) {
   const unsigned blocks = static_cast<unsigned>((a.n - a.p0 + 255) / 256);
