@@ -328,3 +328,48 @@ def test_near_filter_covers_all_pairs(pbdr, pyoracle, cid, scale, frames):
     involved = set(np.nonzero(cnt)[0].tolist()) | set(lst[mask].tolist())
     assert involved and involved <= near
     assert len(near) < gpu.n  # the filter actually removes particles
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cid", [4, 5])
+def test_full_size_properties(pbdr, cid):
+    # BASELINE sizes (14.2M / 67.1M particles), where the oracle cannot follow:
+    # size-independent properties. (1) Determinism: two handles give
+    # bit-identical states. (2) In the first frames no body reaches the ground,
+    # so each scene is an isolated system under uniform gravity: its momentum
+    # follows P0 - M g t e_z and its angular momentum about its own com is
+    # conserved (body-body contacts are equal and opposite, the momentum
+    # constraint cancels shape matching's change), to fp32 resolution.
+    g = P.GeneratedScene(cid)
+    nb = g.desc.num_bodies
+    mass = g.array("total_mass", nb)
+    scene = g.array("body_scene", nb, np.int64) if cid == 4 else np.zeros(nb, np.int64)
+    a = P.GpuSolver(g.desc, g.cfg)
+    s0 = a.read_bodies()
+    frames = 2
+    a.step_frames(frames)
+    pa, va = a.read_f32()
+    s1 = a.read_bodies()
+    b = P.GpuSolver(g.desc, g.cfg)
+    b.step_frames(frames)
+    pb, vb = b.read_f32()
+    assert np.array_equal(pa, pb) and np.array_equal(va, vb)
+    assert pa[:, 2].min() > 0.05  # nobody near the ground yet
+
+    def per_scene(st):
+        ns = scene.max() + 1
+        M = np.bincount(scene, mass, ns)
+        C = np.stack([np.bincount(scene, mass * st[:, k], ns) for k in range(3)], 1) / M[:, None]
+        Pm = np.stack([np.bincount(scene, st[:, 7 + k], ns) for k in range(3)], 1)
+        r = st[:, 0:3] - C[scene]
+        Lb = st[:, 10:13] + np.cross(r, st[:, 7:10])
+        L = np.stack([np.bincount(scene, Lb[:, k], ns) for k in range(3)], 1)
+        return M, Pm, L
+
+    t = frames / g.cfg.frame_rate
+    M, P0, L0 = per_scene(s0)
+    _, P1, L1 = per_scene(s1)
+    expect = P0.copy()
+    expect[:, 2] -= M * g.cfg.gravity * t
+    assert np.abs(P1 - expect).max() <= 1e-5 * max(1.0, np.abs(expect).max())
+    assert np.abs(L1 - L0).max() <= 1e-4 * max(1e-3, np.abs(L0).max())
