@@ -50,6 +50,7 @@ struct pbdr_handle {
   float4* walpha = nullptr;
   bool has_torque = false;
   bool has_programs = false;  // any body with a ForceProgram
+  bool pairs_possible = true; // some scene holds two or more bodies
   bool broadphase = true;     // body-box filter before the hash grid (PBDR_BROADPHASE=0 disables)
   int kp = 4;                 // tile shape: particles per lane (pbdr_choose_kp)
   int per_substep = 0;
@@ -230,17 +231,20 @@ void enqueue_substep(pbdr_handle* h, pbdr_dev::LaunchHook* hook) {
   ia.inv_h = h->inv_h;
   ia.dt_d = h->dt_d;
   ia.mask = h->mask;
-  if (hook) hook->before(kHookMemset);
-  cudaMemsetAsync(h->box_min, 0xFF, sizeof(uint32_t) * 3 * h->nb, h->stream);
-  cudaMemsetAsync(h->box_max, 0x00, sizeof(uint32_t) * 3 * h->nb, h->stream);
-  cudaMemsetAsync(h->oversize, 0x00, sizeof(unsigned), h->stream);
-  cudaMemsetAsync(h->bcells, 0xFF, sizeof(uint2) * (size_t(1) << h->bhash_bits), h->stream);
-  if (hook) hook->after(kHookMemset, 4);
-  // Reset only the buckets the previous substep filled.
-  if (hook) hook->before(kHookRanges);
-  launch_cell_clear(h->cells, h->keys[h->sorted_buf], h->near_count + 1, h->n, h->stream);
-  launch_ncand_clear(h->ncand, h->near_list, h->near_count + 1, h->n, h->stream);
-  if (hook) hook->after(kHookRanges);
+  const bool pairs = h->pairs_possible || h->slab;
+  if (pairs) {
+    if (hook) hook->before(kHookMemset);
+    cudaMemsetAsync(h->box_min, 0xFF, sizeof(uint32_t) * 3 * h->nb, h->stream);
+    cudaMemsetAsync(h->box_max, 0x00, sizeof(uint32_t) * 3 * h->nb, h->stream);
+    cudaMemsetAsync(h->oversize, 0x00, sizeof(unsigned), h->stream);
+    cudaMemsetAsync(h->bcells, 0xFF, sizeof(uint2) * (size_t(1) << h->bhash_bits), h->stream);
+    if (hook) hook->after(kHookMemset, 4);
+    // Reset only the buckets the previous substep filled.
+    if (hook) hook->before(kHookRanges);
+    launch_cell_clear(h->cells, h->keys[h->sorted_buf], h->near_count + 1, h->n, h->stream);
+    launch_ncand_clear(h->ncand, h->near_list, h->near_count + 1, h->n, h->stream);
+    if (hook) hook->after(kHookRanges);
+  }
   if (h->has_torque) {
     WrenchArgs wa{};
     wa.pos = h->pos[h->cur];
@@ -262,6 +266,17 @@ void enqueue_substep(pbdr_handle* h, pbdr_dev::LaunchHook* hook) {
   if (hook) hook->before(kHookIntegrate);
   launch_integrate(ia, h->stream);
   if (hook) hook->after(kHookIntegrate);
+
+  if (!pairs) {
+    // Every scene holds a single body: no particle can have a contact
+    // candidate (candidates are other bodies of the same scene), so the hash
+    // grid is skipped; candidate counts stay 0 from creation. Only the substep
+    // counter advances, as k_cell_ranges would.
+    if (hook) hook->before(kHookRanges);
+    launch_tick(h->counter, h->stream);
+    if (hook) hook->after(kHookRanges);
+    return;
+  }
 
   // Body broadphase: partner bodies (box overlap within h) for the skip test.
   BroadArgs ba{};
@@ -785,6 +800,17 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
     }
   }
   h->pk_full = {h->cta_desc, h->warp_desc, h->body_desc, h->ctas};
+  {
+    // Contact candidates need two bodies of one scene (pinned P4).
+    std::vector<int> per_scene;
+    h->pairs_possible = false;
+    for (int32_t b = 0; b < nb && !h->pairs_possible; ++b) {
+      const int sc = scene[b];
+      if (sc < 0) continue;
+      if (static_cast<size_t>(sc) >= per_scene.size()) per_scene.resize(static_cast<size_t>(sc) + 1, 0);
+      h->pairs_possible = ++per_scene[sc] > 1;
+    }
+  }
   if (const char* e = std::getenv("PBDR_BROADPHASE")) h->broadphase = std::atoi(e) != 0;
   h->pk_iter = h->pk_active = h->pk_full;
   if (reset_errors(h) != PBDR_OK) {
@@ -799,6 +825,8 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
   h->launches_per_frame = static_cast<int64_t>(h->substeps) *
                           (4 + 2 + (h->has_torque ? 1 : 0) + 1 + 1 + (3 + h->bpasses) + 2 + 4 + (3 + h->passes) +
                            1 + 1 + h->iters);
+  if (!h->pairs_possible)  // single-body scenes: integrate + counter tick + iterations
+    h->launches_per_frame = static_cast<int64_t>(h->substeps) * ((h->has_torque ? 1 : 0) + 1 + 1 + h->iters);
   *out = h;
   return PBDR_OK;
 }

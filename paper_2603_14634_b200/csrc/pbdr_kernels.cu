@@ -1427,6 +1427,12 @@ void launch_scatter4(float4* dst, const float4* src, const int* idx, int64_t cou
   if (count > 0) k_scatter4<<<static_cast<unsigned>((count + 255) / 256), 256, 0, s>>>(dst, src, idx, count);
 }
 
+__global__ void k_tick(long long* substep_counter) {
+  atomicAdd(reinterpret_cast<unsigned long long*>(substep_counter), 1ull);
+}
+
+void launch_tick(long long* substep_counter, cudaStream_t s) { k_tick<<<1, 1, 0, s>>>(substep_counter); }
+
 static unsigned stride_grid(int64_t n_max) {
   const int64_t want = (n_max + 255) / 256;
   return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(want, 148 * 16)));

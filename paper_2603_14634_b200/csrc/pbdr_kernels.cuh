@@ -204,6 +204,7 @@ void launch_body_partners(const BroadArgs& a, cudaStream_t s);
 void launch_gather4(float4* dst, const float4* src, const int* idx, int64_t count, cudaStream_t s);
 void launch_scatter4(float4* dst, const float4* src, const int* idx, int64_t count, cudaStream_t s);
 void launch_near(const NearArgs& a, cudaStream_t s);
+void launch_tick(long long* substep_counter, cudaStream_t s);
 void launch_ncand_clear(int* ncand, const int* prev_near, const long long* prev_count, int64_t n_max,
                         cudaStream_t s);
 void launch_cell_clear(uint4* cells, const uint32_t* prev_keys, const long long* prev_count, int64_t n_max,
