@@ -399,7 +399,9 @@ def main():
     frame_ms = sum(v[0] for v in prof.values())
     it_ms, it_launches = prof["iteration"]
     it_avg_ms = it_ms / max(1, it_launches)
-    alg_bytes = n * BYTES_PER_ITERATION
+    # Scenes without candidate pairs run a substep's iterations in one launch.
+    iters_per_launch = max(1, (subs * iters) // max(1, it_launches))
+    alg_bytes = n * BYTES_PER_ITERATION * iters_per_launch
     achieved = alg_bytes / (it_avg_ms / 1e3) / 1e9
     peak, peak_src = measured_peak()
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,

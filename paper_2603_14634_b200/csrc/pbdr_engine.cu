@@ -377,7 +377,7 @@ void enqueue_substep(pbdr_handle* h, pbdr_dev::LaunchHook* hook) {
   if (hook) hook->after(kHookNeighbours);
 }
 
-void enqueue_iteration(pbdr_handle* h, int iter_index, pbdr_dev::LaunchHook* hook) {
+void enqueue_iteration(pbdr_handle* h, int iter_index, pbdr_dev::LaunchHook* hook, int n_iters = 1) {
   using namespace pbdr_dev;
   IterArgs it{};
   it.pos_in = h->pos[h->cur];
@@ -392,7 +392,8 @@ void enqueue_iteration(pbdr_handle* h, int iter_index, pbdr_dev::LaunchHook* hoo
   it.rquat = h->rquat;
   it.per_substep = h->per_substep;
   it.iter_index = iter_index;
-  it.last_iter = iter_index == h->iters - 1;
+  it.n_iters = n_iters;
+  it.last_iter = iter_index + n_iters - 1 == h->iters - 1;
   it.mom_acc = h->mom_acc;
   it.cta_desc = h->pk_iter.cta;
   it.warp_desc = h->pk_iter.warp;
@@ -417,9 +418,15 @@ void enqueue_iteration(pbdr_handle* h, int iter_index, pbdr_dev::LaunchHook* hoo
 }
 
 void enqueue_substeps(pbdr_handle* h, int64_t count, pbdr_dev::LaunchHook* hook) {
+  // Without candidate pairs a body's iterations only read its own particles:
+  // one launch runs all of them (state kept in shared memory).
+  const bool fused_iters = !h->pairs_possible && !h->slab;
   for (int64_t s = 0; s < count; ++s) {
     enqueue_substep(h, hook);
-    for (int i = 0; i < h->iters; ++i) enqueue_iteration(h, i, hook);
+    if (fused_iters)
+      enqueue_iteration(h, 0, hook, h->iters);
+    else
+      for (int i = 0; i < h->iters; ++i) enqueue_iteration(h, i, hook);
   }
 }
 
@@ -826,7 +833,7 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
                           (4 + 2 + (h->has_torque ? 1 : 0) + 1 + 1 + (3 + h->bpasses) + 2 + 4 + (3 + h->passes) +
                            1 + 1 + h->iters);
   if (!h->pairs_possible)  // single-body scenes: integrate + counter tick + iterations
-    h->launches_per_frame = static_cast<int64_t>(h->substeps) * ((h->has_torque ? 1 : 0) + 1 + 1 + h->iters);
+    h->launches_per_frame = static_cast<int64_t>(h->substeps) * ((h->has_torque ? 1 : 0) + 1 + 1 + 1);
   *out = h;
   return PBDR_OK;
 }

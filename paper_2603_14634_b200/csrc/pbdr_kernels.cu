@@ -748,7 +748,7 @@ enum ResSlot {
 template <int KP>
 constexpr int iter_min_blocks() { return KP == 8 ? 2 : 3; }
 
-template <int KP>
+template <int KP, bool MULTI>
 __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(IterArgs A) {
   constexpr int kSlots = kThreads * KP;  // particle slots staged per CTA
   extern __shared__ float4 s_stage[];  // pos | vel | rest, kSlots each
@@ -830,13 +830,22 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
     cd_n = ld_keep_nc(&A.cta_desc[tile_next]);
     wd_n = ld_keep_nc(&A.warp_desc[tile_next * kWarps + warp]);
   }
+  mbar_wait(&s_bar, it_parity);
+  if (tm && threadIdx.x == 0) tm[1] = clock64();
+
+  // Scenes without candidate pairs (one body per scene) run all iterations of
+  // the substep in one launch: a body's iteration reads only its own
+  // particles, so the state stays in shared memory between iterations.
+  const int n_iters = MULTI ? A.n_iters : 1;
+  for (int it = 0; it < n_iters; ++it) {
+  const int iter_index = A.iter_index + it;
+  const int last_iter = MULTI ? (A.last_iter && it == n_iters - 1) : A.last_iter;
+  if (it > 0) __syncthreads();  // previous iteration's state and table in smem
   float a[3];
   {
     const float4 an = s_tanc[tb][lb];
     a[0] = an.x; a[1] = an.y; a[2] = an.z;
   }
-  mbar_wait(&s_bar, it_parity);
-  if (tm && threadIdx.x == 0) tm[1] = clock64();
 
   float dX[KP][3];
 
@@ -972,11 +981,15 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
     const float rq[4] = {rq4.x, rq4.y, rq4.z, rq4.w};
     const bool ok = polar_warm_f(&S[6], rq, &R[kResR], qd);
     R[kResSmOk] = ok ? 1.0f : 0.0f;
-    A.rquat[bb] = ok ? make_float4(static_cast<float>(qd[0]), static_cast<float>(qd[1]),
-                                   static_cast<float>(qd[2]), static_cast<float>(qd[3]))
-                     : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    const float4 rq_new = ok ? make_float4(static_cast<float>(qd[0]), static_cast<float>(qd[1]),
+                                           static_cast<float>(qd[2]), static_cast<float>(qd[3]))
+                             : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    const float4 an_new = make_float4(an.x + c[0], an.y + c[1], an.z + c[2], 0.0f);
+    A.rquat[bb] = rq_new;
     if (!ok) record_error(A.err, PBDR_DEVERR_DEGENERATE, bb, A.substep_counter);
-    A.anchor[bb] = make_float4(an.x + c[0], an.y + c[1], an.z + c[2], 0.0f);
+    A.anchor[bb] = an_new;
+    s_trq[tb][lane] = rq_new;   // next iteration of a multi-iteration launch
+    s_tanc[tb][lane] = an_new;
   }
   __syncthreads();
   if (tm && threadIdx.x == 0) tm[3] = clock64();
@@ -1041,8 +1054,13 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
         accB[14] = fmaf(-mk, pa[1] * pa[2], accB[14]);
       } else {
         const int64_t p = start + q;
-        A.pos_out[p] = make_float4(xa[0], xa[1], xa[2], x4.w);
-        A.vel[p] = make_float4(va[0], va[1], va[2], v4.w);
+        if (MULTI) {
+          s_pos[off + q] = make_float4(xa[0], xa[1], xa[2], x4.w);
+          s_vel[off + q] = make_float4(va[0], va[1], va[2], v4.w);
+        } else {
+          A.pos_out[p] = make_float4(xa[0], xa[1], xa[2], x4.w);
+          A.vel[p] = make_float4(va[0], va[1], va[2], v4.w);
+        }
       }
     }
   }
@@ -1093,7 +1111,7 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
     if (A.per_substep) {
       // kPerSubstep: accumulate over the substep's iterations, correct once.
       float4 aP = make_float4(0.0f, 0.0f, 0.0f, 0.0f), aL = aP;
-      if (A.iter_index > 0) {
+      if (iter_index > 0) {
         aP = A.mom_acc[2 * bb];
         aL = A.mom_acc[2 * bb + 1];
       }
@@ -1103,7 +1121,7 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
       A.mom_acc[2 * bb + 1] = aL;
       dP[0] = aP.x; dP[1] = aP.y; dP[2] = aP.z;
       dL[0] = aL.x; dL[1] = aL.y; dL[2] = aL.z;
-      correct = A.last_iter != 0;
+      correct = last_iter != 0;
     }
     if (A.linfix && correct)
 #pragma unroll
@@ -1166,11 +1184,29 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
       xo[c] = fmaf(-wr[c], A.dt, fmaf(dv[c], A.dt, xa[c]));
     }
     const int64_t p = start + q;
-    A.pos_out[p] = make_float4(xo[0], xo[1], xo[2], x4.w);
-    A.vel[p] = make_float4(vo[0], vo[1], vo[2], v4.w);
+    if (MULTI) {
+      s_pos[off + q] = make_float4(xo[0], xo[1], xo[2], x4.w);
+      s_vel[off + q] = make_float4(vo[0], vo[1], vo[2], v4.w);
+    } else {
+      A.pos_out[p] = make_float4(xo[0], xo[1], xo[2], x4.w);
+      A.vel[p] = make_float4(vo[0], vo[1], vo[2], v4.w);
+    }
   }
   }  // live
   }  // fixes
+  }  // iterations of this launch
+  if (MULTI) {
+    __syncthreads();
+    if (live)
+#pragma unroll
+      for (int k = 0; k < KP; ++k) {
+        const int q = k * 32 * W + wi * 32 + lane;
+        if (q < n) {
+          A.pos_out[start + q] = s_pos[off + q];
+          A.vel[start + q] = s_vel[off + q];
+        }
+      }
+  }
   if (tm && threadIdx.x == 0) {
     tm[6] = clock64();
     unsigned smid;
@@ -1461,16 +1497,19 @@ static int g_iter_grid_cap[9] = {0};  // resident iteration CTAs on the device, 
 
 template <int KP>
 static cudaError_t prepare_one() {
-  cudaError_t e = cudaFuncSetAttribute(k_iteration<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(k_iteration<KP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(iteration_smem_bytes(KP)));
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k_iteration<KP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(iteration_smem_bytes(KP)));
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_iteration<KP>, kThreads, iteration_smem_bytes(KP));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_iteration<KP, false>, kThreads, iteration_smem_bytes(KP));
   g_iter_grid_cap[KP] = sms * per_sm;
 #ifdef PBDR_ITER_CARVEOUT
-  return cudaFuncSetAttribute(k_iteration<KP>, cudaFuncAttributePreferredSharedMemoryCarveout, PBDR_ITER_CARVEOUT);
+  return cudaFuncSetAttribute(k_iteration<KP, false>, cudaFuncAttributePreferredSharedMemoryCarveout, PBDR_ITER_CARVEOUT);
 #else
   return cudaSuccess;
 #endif
@@ -1495,7 +1534,10 @@ static void launch_iteration_kp(const IterArgs& a, int ctas, cudaStream_t s) {
   b.ntiles = ctas;
   int grid = ctas;
   if (PBDR_ITER_PERSISTENT && g_iter_grid_cap[KP] > 0 && !a.timing) grid = std::min(ctas, g_iter_grid_cap[KP]);
-  k_iteration<KP><<<grid, kThreads, iteration_smem_bytes(KP), s>>>(b);
+  if (a.n_iters > 1)
+    k_iteration<KP, true><<<grid, kThreads, iteration_smem_bytes(KP), s>>>(b);
+  else
+    k_iteration<KP, false><<<grid, kThreads, iteration_smem_bytes(KP), s>>>(b);
 }
 
 void launch_iteration(const IterArgs& a, int ctas, int kp, cudaStream_t s) {

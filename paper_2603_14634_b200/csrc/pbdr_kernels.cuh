@@ -178,6 +178,7 @@ struct IterArgs {
   int incremental, linfix, angfix;
   int per_substep;    // MomentumFrequency::kPerSubstep
   int iter_index;     // iteration within the substep
+  int n_iters;        // iterations run by this launch (> 1 only for scenes without candidate pairs)
   int last_iter;      // iteration_index == solver_iterations - 1
   float4* mom_acc;    // per body (P, L) accumulators for kPerSubstep
   long long* timing;  // optional per-CTA phase clocks (debug), else null
