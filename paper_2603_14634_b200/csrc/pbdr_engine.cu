@@ -530,6 +530,8 @@ int validate(const pbdr_scene_desc* d, const pbdr_solver_cfg* c) {
   if (d->num_particles >= (int64_t(1) << 31) - 1)
     return set_config_error("particles", "more than 2^31-2 particles per device");
   if (d->num_bodies <= 0) return set_config_error("bodies", "scene has no bodies");
+  if (d->num_bodies > 4 * 1024 * 1024)  // near-filter body scan: <= 1024 tiles of 4096
+    return set_config_error("bodies", "more than 4,194,304 bodies per device");
   if (!(d->contact_relaxation >= 0.0)) return set_config_error("contact_relaxation", "must be >= 0");
   const int planes = (d->has_ground ? 1 : 0) + std::max(0, d->num_walls);
   if (planes > PBDR_MAX_PLANES) return set_config_error("walls", "at most 8 planes (ground + walls)");
