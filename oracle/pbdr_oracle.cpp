@@ -707,9 +707,9 @@ void body_stats(State& s, pbdr_body_stats* out) {
 
 int finish_substep_errors(State& s) {
   if (!s.err_bits) return PBDR_OK;
+  if (s.err_bits & (PBDR_DEVERR_NONFINITE | PBDR_DEVERR_NBR_OVERFLOW)) return PBDR_ERR_SIMULATION;
   if (s.err_bits & PBDR_DEVERR_RANK_DEFICIENT) return PBDR_ERR_RANK_DEFICIENT;
-  if (s.err_bits & PBDR_DEVERR_DEGENERATE) return PBDR_ERR_DEGENERATE;
-  return PBDR_ERR_SIMULATION;
+  return PBDR_ERR_DEGENERATE;
 }
 
 }  // namespace

@@ -441,16 +441,20 @@ int check_errors(pbdr_handle* h) {
   // Errors are recorded after the substep counter advanced (cell_ranges).
   const int64_t substep = de.substep - 1;
   const int64_t frame = substep / std::max(1, h->substeps);
+  // Causes before consequences: a non-finite state also makes the polar
+  // degenerate, so it is reported as the SimulationError it is.
+  if (de.bits & PBDR_DEVERR_NONFINITE)
+    return pbdr_host::set_sim_error("non-finite body sums", frame, de.body, nullptr, PBDR_ERR_SIMULATION);
+  if (de.bits & PBDR_DEVERR_NBR_OVERFLOW)
+    return pbdr_host::set_sim_error("contact candidates exceed capacity " +
+                                        std::to_string(PBDR_NBR_CAP) + " per particle",
+                                    frame, de.body, nullptr, PBDR_ERR_SIMULATION);
   if (de.bits & PBDR_DEVERR_RANK_DEFICIENT)
     return pbdr_host::set_sim_error("angular momentum fix: dL along a singular inertia axis",
                                     frame, de.body, de.axis, PBDR_ERR_RANK_DEFICIENT);
   if (de.bits & PBDR_DEVERR_DEGENERATE)
     return pbdr_host::set_sim_error("shape matching: polar decomposition of a degenerate moment",
                                     frame, de.body, nullptr, PBDR_ERR_DEGENERATE);
-  if (de.bits & PBDR_DEVERR_NBR_OVERFLOW)
-    return pbdr_host::set_sim_error("contact candidates exceed capacity " +
-                                        std::to_string(PBDR_NBR_CAP) + " per particle",
-                                    frame, de.body, nullptr, PBDR_ERR_SIMULATION);
   return pbdr_host::set_sim_error("non-finite body sums", frame, de.body, nullptr,
                                   PBDR_ERR_SIMULATION);
 }
