@@ -184,7 +184,7 @@ def run_cpu(args, substeps_per_step):
     while True:
         assert o.step(substeps_per_step) == 0
         done += substeps_per_step
-        if time.perf_counter() - t0 > 8.0:
+        if time.perf_counter() - t0 > 12.0:  # about 10-30 s of CPU work
             break
     dt = time.perf_counter() - t0
     rate = g.num_particles * done / dt
