@@ -51,6 +51,7 @@ struct pbdr_handle {
   bool has_torque = false;
   bool has_programs = false;  // any body with a ForceProgram
   bool pairs_possible = true; // some scene holds two or more bodies
+  bool coop_iters = true;     // one-wave scenes with pairs: cooperative multi-iteration launch
   bool broadphase = true;     // body-box filter before the hash grid (PBDR_BROADPHASE=0 disables)
   int kp = 4;                 // tile shape: particles per lane (pbdr_choose_kp)
   int per_substep = 0;
@@ -393,6 +394,9 @@ void enqueue_iteration(pbdr_handle* h, int iter_index, pbdr_dev::LaunchHook* hoo
   it.per_substep = h->per_substep;
   it.iter_index = iter_index;
   it.n_iters = n_iters;
+  it.multi_pairs = (n_iters > 1 && h->pairs_possible) ? 1 : 0;
+  it.pos_b[0] = h->pos[h->cur];
+  it.pos_b[1] = h->pos[h->cur ^ 1];
   it.last_iter = iter_index + n_iters - 1 == h->iters - 1;
   it.mom_acc = h->mom_acc;
   it.cta_desc = h->pk_iter.cta;
@@ -419,8 +423,12 @@ void enqueue_iteration(pbdr_handle* h, int iter_index, pbdr_dev::LaunchHook* hoo
 
 void enqueue_substeps(pbdr_handle* h, int64_t count, pbdr_dev::LaunchHook* hook) {
   // Without candidate pairs a body's iterations only read its own particles:
-  // one launch runs all of them (state kept in shared memory).
-  const bool fused_iters = !h->pairs_possible && !h->slab;
+  // one launch runs all of them (state kept in shared memory). With pairs, a
+  // scene whose tiles fit in one wave does the same in a cooperative launch
+  // with a grid barrier between iterations (small latency-bound scenes).
+  const bool fused_iters =
+      !h->slab && (!h->pairs_possible || (h->pk_iter.ctas <= pbdr_dev::iteration_coop_capacity(h->kp) &&
+                                          h->coop_iters));
   for (int64_t s = 0; s < count; ++s) {
     enqueue_substep(h, hook);
     if (fused_iters)
@@ -825,6 +833,7 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
     }
   }
   if (const char* e = std::getenv("PBDR_BROADPHASE")) h->broadphase = std::atoi(e) != 0;
+  if (const char* e = std::getenv("PBDR_COOP_ITERS")) h->coop_iters = std::atoi(e) != 0;
   h->pk_iter = h->pk_active = h->pk_full;
   if (reset_errors(h) != PBDR_OK) {
     const int code = pbdr_last_error_payload(nullptr, nullptr, nullptr);

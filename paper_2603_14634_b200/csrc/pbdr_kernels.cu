@@ -16,6 +16,7 @@
 // The op order of every fp32 expression is pinned and
 // mirrored by oracle/pbdr_oracle.cpp; the library is compiled with
 // --fmad=false so the CUDA path and the oracle agree bit for bit.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -906,7 +907,9 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
     for (int c = 0; c < nc; ++c) {
       const int j = A.cand_j[static_cast<int64_t>(c) * A.n + p];
       const float rr = A.cand_rr[static_cast<int64_t>(c) * A.n + p];
-      const float4 xj = A.pos_in[j];
+      // Multi-iteration launch with pairs: neighbours' X_i come from the
+      // buffer the previous iteration wrote (after a grid barrier; L2 only).
+      const float4 xj = (MULTI && A.multi_pairs) ? __ldcg(&A.pos_b[it & 1][j]) : A.pos_in[j];
       pp_contact(x, x4.w, p, xj, j, rr, A.relax, dPP);
     }
     const float v[3] = {v4.x, v4.y, v4.z};
@@ -1057,6 +1060,7 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
         if (MULTI) {
           s_pos[off + q] = make_float4(xa[0], xa[1], xa[2], x4.w);
           s_vel[off + q] = make_float4(va[0], va[1], va[2], v4.w);
+          if (A.multi_pairs && it + 1 < n_iters) __stcg(&A.pos_b[(it + 1) & 1][p], s_pos[off + q]);
         } else {
           A.pos_out[p] = make_float4(xa[0], xa[1], xa[2], x4.w);
           A.vel[p] = make_float4(va[0], va[1], va[2], v4.w);
@@ -1187,6 +1191,7 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
     if (MULTI) {
       s_pos[off + q] = make_float4(xo[0], xo[1], xo[2], x4.w);
       s_vel[off + q] = make_float4(vo[0], vo[1], vo[2], v4.w);
+      if (A.multi_pairs && it + 1 < n_iters) __stcg(&A.pos_b[(it + 1) & 1][p], s_pos[off + q]);
     } else {
       A.pos_out[p] = make_float4(xo[0], xo[1], xo[2], x4.w);
       A.vel[p] = make_float4(vo[0], vo[1], vo[2], v4.w);
@@ -1194,6 +1199,7 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
   }
   }  // live
   }  // fixes
+  if (MULTI && A.multi_pairs && it + 1 < n_iters) cooperative_groups::this_grid().sync();
   }  // iterations of this launch
   if (MULTI) {
     __syncthreads();
@@ -1494,6 +1500,7 @@ void launch_neighbours(const NeighbourArgs& a, cudaStream_t s) {
 }
 
 static int g_iter_grid_cap[9] = {0};  // resident iteration CTAs on the device, per KP (persistent grid)
+static int g_iter_coop_cap[9] = {0};  // resident multi-iteration CTAs (cooperative launch), per KP
 
 template <int KP>
 static cudaError_t prepare_one() {
@@ -1508,6 +1515,9 @@ static cudaError_t prepare_one() {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_iteration<KP, false>, kThreads, iteration_smem_bytes(KP));
   g_iter_grid_cap[KP] = sms * per_sm;
+  int per_sm_multi = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_multi, k_iteration<KP, true>, kThreads, iteration_smem_bytes(KP));
+  g_iter_coop_cap[KP] = sms * per_sm_multi;
 #ifdef PBDR_ITER_CARVEOUT
   return cudaFuncSetAttribute(k_iteration<KP, false>, cudaFuncAttributePreferredSharedMemoryCarveout, PBDR_ITER_CARVEOUT);
 #else
@@ -1534,11 +1544,27 @@ static void launch_iteration_kp(const IterArgs& a, int ctas, cudaStream_t s) {
   b.ntiles = ctas;
   int grid = ctas;
   if (PBDR_ITER_PERSISTENT && g_iter_grid_cap[KP] > 0 && !a.timing) grid = std::min(ctas, g_iter_grid_cap[KP]);
-  if (a.n_iters > 1)
+  if (a.n_iters > 1 && a.multi_pairs) {
+    // One wave of tiles iterating together: grid barriers need a cooperative
+    // launch (every CTA resident; the engine checks iteration_coop_capacity).
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(ctas));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = iteration_smem_bytes(KP);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_iteration<KP, true>, b);
+  } else if (a.n_iters > 1) {
     k_iteration<KP, true><<<grid, kThreads, iteration_smem_bytes(KP), s>>>(b);
-  else
+  } else
     k_iteration<KP, false><<<grid, kThreads, iteration_smem_bytes(KP), s>>>(b);
 }
+
+int iteration_coop_capacity(int kp) { return g_iter_coop_cap[kp == 2 ? 2 : (kp == 4 ? 4 : 8)]; }
 
 void launch_iteration(const IterArgs& a, int ctas, int kp, cudaStream_t s) {
   switch (kp) {

@@ -373,3 +373,21 @@ def test_full_size_properties(pbdr, cid):
     expect[:, 2] -= M * g.cfg.gravity * t
     assert np.abs(P1 - expect).max() <= 1e-5 * max(1.0, np.abs(expect).max())
     assert np.abs(L1 - L0).max() <= 1e-4 * max(1e-3, np.abs(L0).max())
+
+
+@pytest.mark.parametrize("coop", ["1", "0"])
+def test_one_wave_multi_iteration_path(pbdr, pyoracle, monkeypatch, coop):
+    # Scenes whose tiles fit in one wave run a substep's iterations in one
+    # cooperative launch (grid barrier per iteration); PBDR_COOP_ITERS=0 forces
+    # one launch per iteration. Both equal the oracle bit for bit.
+    monkeypatch.setenv("PBDR_COOP_ITERS", coop)
+    g = P.GeneratedScene(2)
+    gpu = P.GpuSolver(g.desc, g.cfg)
+    orc = pyoracle.Oracle(g.desc, g.cfg)
+    gpu.step_frames(3)
+    assert orc.step(3 * g.cfg.substeps) == 0
+    gp, gv = gpu.read_f32()
+    op, ov = orc.read_f32()
+    assert_same(gp, op, f"coop={coop} positions")
+    assert_same(gv, ov, f"coop={coop} velocities")
+    assert gpu.info.launches_per_frame > 0
