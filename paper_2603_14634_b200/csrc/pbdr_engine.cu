@@ -90,6 +90,7 @@ struct pbdr_handle {
   DevError* err = nullptr;
   long long* counter = nullptr;
   int* tile_ctr = nullptr;  // iteration kernel: dynamic tile claims (self-resetting)
+  int* big_list = nullptr;  // bodies larger than one CTA (ascending ids)
   double* stats = nullptr;
   std::vector<void*> allocations;
   size_t device_bytes = 0;
@@ -114,10 +115,14 @@ struct pbdr_handle {
     int4* warp = nullptr;
     int4* body = nullptr;
     int ctas = 0;
+    int* big = nullptr;  // bodies larger than one CTA (one cluster each)
+    int nbig = 0;
   };
   Packing pk_full, pk_iter, pk_active;
   std::vector<int64_t> h_bstart;  // host copy: first slot of each body
   std::vector<int> h_bcount;      // host copy: particles of each body
+  int big_cluster = 0;            // CTAs per cluster of the big-body kernel (0: no big body)
+  int big_warps = 0;              // warps per CTA of the big-body kernel
 
   // Slab mode (x-slab decomposition of one scene, pbdr_gpu_set_roles).
   bool slab = false;
@@ -261,8 +266,10 @@ void enqueue_substep(pbdr_handle* h, pbdr_dev::LaunchHook* hook) {
     wa.err = h->err;
     wa.substep_counter = h->counter;
     if (hook) hook->before(kHookIntegrate);
+    wa.big_list = h->pk_active.big;
     if (h->pk_active.ctas > 0) launch_wrench(wa, h->pk_active.ctas, h->kp, h->stream);
-    if (hook) hook->after(kHookIntegrate);
+    if (h->pk_active.nbig > 0) launch_wrench_big(wa, h->pk_active.nbig, h->stream);
+    if (hook) hook->after(kHookIntegrate, (h->pk_active.ctas > 0 ? 1 : 0) + (h->pk_active.nbig > 0 ? 1 : 0));
   }
   if (hook) hook->before(kHookIntegrate);
   launch_integrate(ia, h->stream);
@@ -415,9 +422,13 @@ void enqueue_iteration(pbdr_handle* h, int iter_index, pbdr_dev::LaunchHook* hoo
   it.angfix = h->angfix;
   it.timing = h->timing;
   it.tile_ctr = h->tile_ctr;
+  it.big_list = h->pk_iter.big;
   if (hook) hook->before(kHookIteration);
   if (h->pk_iter.ctas > 0) launch_iteration(it, h->pk_iter.ctas, h->kp, h->stream);
-  if (hook) hook->after(kHookIteration);
+  // Bodies larger than one CTA: one cluster each, same iteration semantics
+  // (they read pos_in and write pos_out / vel of their own slots only).
+  if (h->pk_iter.nbig > 0) launch_iteration_big(it, h->pk_iter.nbig, h->big_cluster, h->big_warps, h->stream);
+  if (hook) hook->after(kHookIteration, (h->pk_iter.ctas > 0 ? 1 : 0) + (h->pk_iter.nbig > 0 ? 1 : 0));
   h->cur ^= 1;
 }
 
@@ -425,10 +436,11 @@ void enqueue_substeps(pbdr_handle* h, int64_t count, pbdr_dev::LaunchHook* hook)
   // Without candidate pairs a body's iterations only read its own particles:
   // one launch runs all of them (state kept in shared memory). With pairs, a
   // scene whose tiles fit in one wave does the same in a cooperative launch
-  // with a grid barrier between iterations (small latency-bound scenes).
+  // with a grid barrier between iterations (small latency-bound scenes) --
+  // unless it has bodies larger than one CTA, whose cluster launch is separate.
   const bool fused_iters =
       !h->slab && (!h->pairs_possible || (h->pk_iter.ctas <= pbdr_dev::iteration_coop_capacity(h->kp) &&
-                                          h->coop_iters));
+                                          h->coop_iters && h->pk_iter.nbig == 0));
   for (int64_t s = 0; s < count; ++s) {
     enqueue_substep(h, hook);
     if (fused_iters)
@@ -494,13 +506,16 @@ int build_graph(pbdr_handle* h, int parity) {
 }
 
 // Packs bodies (ascending ids) into 8-warp CTAs: a body of n particles takes
-// W = ceil(n/128) warps; consecutive ids (slot-contiguous in the body-major
-// layout) share a CTA while its warps last. bdesc[b] = (first slot, n, W,
-// first warp in the CTA) is written for the listed bodies only.
+// W = ceil(n/(32 kp)) warps; consecutive ids (slot-contiguous in the body-major
+// layout) share a CTA while its warps last. Bodies of more than 8 warps go to
+// `big` (one CTA cluster each). bdesc[b] = (first slot, n, W, first warp in the
+// CTA; 0 for big bodies) is written for the listed bodies only.
 void pack_bodies(const std::vector<int>& list, const std::vector<int64_t>& bstart, const std::vector<int>& bcount,
-                 int kp, std::vector<int4>& cdesc, std::vector<int4>& wdesc, std::vector<int4>& bdesc) {
+                 int kp, std::vector<int4>& cdesc, std::vector<int4>& wdesc, std::vector<int4>& bdesc,
+                 std::vector<int>& big) {
   cdesc.clear();
   wdesc.clear();
+  big.clear();
   int used = 0, prev = -2;
   auto close = [&] {
     for (; used < PBDR_CTA_WARPS && used > 0; ++used) wdesc.push_back(make_int4(-1, 0, 0, 1 << 16));
@@ -510,6 +525,11 @@ void pack_bodies(const std::vector<int>& list, const std::vector<int64_t>& bstar
     const int cnt = bcount[b];
     const int first_slot = static_cast<int>(bstart[b]);
     const int W = pbdr_body_warps(cnt, kp);
+    if (W > PBDR_CTA_WARPS) {
+      bdesc[b] = make_int4(first_slot, cnt, W, 0);
+      big.push_back(b);
+      continue;
+    }
     if (used + W > PBDR_CTA_WARPS || (used > 0 && b != prev + 1)) close();
     if (used == 0) cdesc.push_back(make_int4(first_slot, 0, b, 0));
     cdesc.back().y += cnt;
@@ -591,6 +611,7 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
   std::vector<int4> bdesc(nb);
   std::vector<int4> wdesc;
   std::vector<int4> cdesc;
+  std::vector<int> big;
   std::vector<char> seen(n, 0);
   h->slot_to_particle.resize(n);
   h->h_bstart.assign(nb, 0);
@@ -604,12 +625,13 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
       release(h);
       return set_config_error("bodies.particle_indices", "empty body " + std::to_string(b));
     }
-    if (cnt > PBDR_MAX_BODY_PARTICLES) {
+    if (cnt > PBDR_MAX_BODY_PARTICLES_BIG) {
       release(h);
       return set_config_error("bodies.particle_indices",
                               "body " + std::to_string(b) + " has " + std::to_string(cnt) +
-                                  " particles; the fused iteration kernel holds at most " +
-                                  std::to_string(PBDR_MAX_BODY_PARTICLES));
+                                  " particles; a body is processed by at most one " +
+                                  std::to_string(PBDR_MAX_CLUSTER_CTAS) + "-CTA cluster (" +
+                                  std::to_string(PBDR_MAX_BODY_PARTICLES_BIG) + " particles)");
     }
     const int64_t first_slot = slot;
     for (int64_t k = k0; k < k1; ++k, ++slot) {
@@ -669,7 +691,12 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
     int max_body = 0;
     for (int32_t b = 0; b < nb; ++b) max_body = std::max(max_body, h->h_bcount[b]);
     h->kp = pbdr_choose_kp(n, nb, max_body, d->tile_kp);
-    pack_bodies(all, h->h_bstart, h->h_bcount, h->kp, cdesc, wdesc, bdesc);
+    pack_bodies(all, h->h_bstart, h->h_bcount, h->kp, cdesc, wdesc, bdesc, big);
+    if (!big.empty()) {
+      const int wmax = pbdr_body_warps(max_body, h->kp);
+      h->big_cluster = pbdr_dev::big_cluster_size(wmax);
+      h->big_warps = pbdr_dev::big_cta_warps(wmax, h->big_cluster);
+    }
   }
   h->ctas = static_cast<int>(wdesc.size() / PBDR_CTA_WARPS);
   h->p_lo = 0;
@@ -774,6 +801,7 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
   rc |= dalloc(h, &h->counter, 1);
   rc |= dalloc(h, &h->tile_ctr, 2);
   rc |= dalloc(h, &h->stats, static_cast<size_t>(nb) * 13);
+  if (!big.empty()) rc |= dalloc(h, &h->big_list, big.size());
   if (rc != PBDR_OK) {
     const int code = pbdr_last_error_payload(nullptr, nullptr, nullptr);
     release(h);
@@ -783,6 +811,16 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
   if (e != cudaSuccess) {
     release(h);
     return cuda_fail(e, "cudaFuncSetAttribute(k_iteration)");
+  }
+  if (h->big_cluster > 0) {
+    e = pbdr_dev::big_cluster_check(h->big_cluster, h->big_warps);
+    if (e != cudaSuccess) {
+      release(h);
+      return set_config_error("bodies.particle_indices",
+                              "clusters of " + std::to_string(h->big_cluster) +
+                                  " iteration CTAs cannot be resident on this device (" +
+                                  cudaGetErrorString(e) + ")");
+    }
   }
   e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
   if (e != cudaSuccess) {
@@ -806,6 +844,7 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
   UP(h->warp_desc, wdesc.data(), wdesc.size());
   UP(h->cta_desc, cdesc.data(), cdesc.size());
   UP(h->anchor, anchor.data(), nb);
+  if (!big.empty()) UP(h->big_list, big.data(), big.size());
 #undef UP
   {
     cudaError_t m = cudaMemset(h->init, 0, sizeof(float4) * n);
@@ -820,7 +859,7 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
       return cuda_fail(m, "initialise device buffers");
     }
   }
-  h->pk_full = {h->cta_desc, h->warp_desc, h->body_desc, h->ctas};
+  h->pk_full = {h->cta_desc, h->warp_desc, h->body_desc, h->ctas, h->big_list, static_cast<int>(big.size())};
   {
     // Contact candidates need two bodies of one scene (pinned P4).
     std::vector<int> per_scene;
@@ -844,11 +883,15 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
   // body sort (memset, histogram, scan, passes) + body ranges + partners +
   // near flag / scan / compact + particle sort (memset, histogram, scan,
   // passes) + cell ranges + neighbours + iterations.
+  // Bodies larger than one CTA add their own launches (cluster iteration,
+  // looping torque prepass); a scene of only such bodies has no tile launch.
+  const int tile_l = h->ctas > 0 ? 1 : 0, big_l = big.empty() ? 0 : 1;
+  const int torque_l = h->has_torque ? tile_l + big_l : 0;
   h->launches_per_frame = static_cast<int64_t>(h->substeps) *
-                          (4 + 2 + (h->has_torque ? 1 : 0) + 1 + 1 + (3 + h->bpasses) + 2 + 4 + (3 + h->passes) +
-                           1 + 1 + h->iters);
-  if (!h->pairs_possible)  // single-body scenes: integrate + counter tick + iterations
-    h->launches_per_frame = static_cast<int64_t>(h->substeps) * ((h->has_torque ? 1 : 0) + 1 + 1 + 1);
+                          (4 + 2 + torque_l + 1 + 1 + (3 + h->bpasses) + 2 + 4 + (3 + h->passes) + 1 + 1 +
+                           static_cast<int64_t>(h->iters) * (tile_l + big_l));
+  if (!h->pairs_possible)  // single-body scenes: integrate + counter tick + all iterations in one launch
+    h->launches_per_frame = static_cast<int64_t>(h->substeps) * (torque_l + 1 + 1 + tile_l + big_l);
   *out = h;
   return PBDR_OK;
 }
@@ -876,7 +919,9 @@ static void enqueue_stats(pbdr_handle* h, double* out) {
   sa.body_desc = h->pk_iter.body;
   sa.body_mass = h->body_mass;
   sa.out = out;
+  sa.big_list = h->pk_iter.big;
   if (h->pk_iter.ctas > 0) pbdr_dev::launch_stats(sa, h->pk_iter.ctas, h->kp, h->stream);
+  if (h->pk_iter.nbig > 0) pbdr_dev::launch_stats_big(sa, h->pk_iter.nbig, h->stream);
 }
 
 static int step_frames_async(pbdr_handle* h, int64_t frames) {
@@ -1301,6 +1346,10 @@ int pbdr_gpu_set_roles(pbdr_handle* h, const int8_t* roles) {
     rc |= dalloc(h, &h->slab_active.cta, nb);
     rc |= dalloc(h, &h->slab_active.warp, static_cast<size_t>(nb) * PBDR_CTA_WARPS);
     rc |= dalloc(h, &h->slab_active.body, nb);
+    if (h->big_cluster > 0) {
+      rc |= dalloc(h, &h->slab_iter.big, nb);
+      rc |= dalloc(h, &h->slab_active.big, nb);
+    }
     if (rc != PBDR_OK) return PBDR_ERR_CUDA;
   }
   std::vector<uint8_t> r(nb);
@@ -1316,17 +1365,22 @@ int pbdr_gpu_set_roles(pbdr_handle* h, const int8_t* roles) {
     hi = std::max(hi, h->h_bstart[b] + h->h_bcount[b]);
   }
   std::vector<int4> cd, wd, bd(nb, make_int4(0, 0, 0, 0));
+  std::vector<int> big;
   PBDR_CUDA(cudaMemcpy(h->role, r.data(), nb, cudaMemcpyHostToDevice));
   if (!active.empty())
     PBDR_CUDA(cudaMemcpy(h->active_list, active.data(), sizeof(int) * active.size(), cudaMemcpyHostToDevice));
   auto upload = [&](const std::vector<int>& list, pbdr_handle::Packing& dev) -> int {
-    pack_bodies(list, h->h_bstart, h->h_bcount, h->kp, cd, wd, bd);
+    pack_bodies(list, h->h_bstart, h->h_bcount, h->kp, cd, wd, bd, big);
     dev.ctas = static_cast<int>(cd.size());
+    dev.nbig = static_cast<int>(big.size());
+    if (!big.empty())
+      PBDR_CUDA(cudaMemcpy(dev.big, big.data(), sizeof(int) * big.size(), cudaMemcpyHostToDevice));
     if (!cd.empty()) {
       PBDR_CUDA(cudaMemcpy(dev.cta, cd.data(), sizeof(int4) * cd.size(), cudaMemcpyHostToDevice));
       PBDR_CUDA(cudaMemcpy(dev.warp, wd.data(), sizeof(int4) * wd.size(), cudaMemcpyHostToDevice));
-      PBDR_CUDA(cudaMemcpy(dev.body, bd.data(), sizeof(int4) * bd.size(), cudaMemcpyHostToDevice));
     }
+    if (!cd.empty() || !big.empty())
+      PBDR_CUDA(cudaMemcpy(dev.body, bd.data(), sizeof(int4) * bd.size(), cudaMemcpyHostToDevice));
     return PBDR_OK;
   };
   int rc = upload(owned, h->slab_iter);

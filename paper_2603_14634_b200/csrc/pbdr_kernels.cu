@@ -729,6 +729,88 @@ __device__ __forceinline__ void pp_contact(const float x[3], float w, int64_t p,
   }
 }
 
+// Phase A of one particle (slot p; X_i = x4, V = v4, rest = r4, nc candidates):
+// ground/wall contacts with friction, Jacobi particle contacts, and the
+// particle's terms of the 21 bsm body sums (com, dX, Apq, P_bsm, L_bsm).
+template <bool MULTI>
+__device__ __forceinline__ void phase_a_particle(const IterArgs& A, int it, int64_t p, float4 x4, float4 v4,
+                                                 float4 r4, int nc, const float a[3], float (&dXk)[3],
+                                                 float (&acc)[21]) {
+  const float x[3] = {x4.x, x4.y, x4.z};
+  const float m = v4.w;
+
+  float dPG[3] = {0.0f, 0.0f, 0.0f};
+  for (int pl = 0; pl < A.planes.count; ++pl) {
+    const float* Pp = A.planes.p[pl];
+    const float* Pn = A.planes.n[pl];
+    const float xp[3] = {x[0] - Pp[0], x[1] - Pp[1], x[2] - Pp[2]};
+    const float d = dot3_fma(xp, Pn) - r4.w;
+    if (d < 0.0f) {
+      const float push = -(A.relax * d);
+      dPG[0] = fmaf(push, Pn[0], dPG[0]);
+      dPG[1] = fmaf(push, Pn[1], dPG[1]);
+      dPG[2] = fmaf(push, Pn[2], dPG[2]);
+      const float mu = A.planes.mu[pl];
+      if (mu > 0.0f) {
+        const float4 xi = A.init[p];
+        const float t[3] = {x[0] - xi.x, x[1] - xi.y, x[2] - xi.z};
+        const float tn = dot3_fma(t, Pn);
+        const float tt[3] = {fmaf(-tn, Pn[0], t[0]), fmaf(-tn, Pn[1], t[1]), fmaf(-tn, Pn[2], t[2])};
+        const float len2 = dot3_fma(tt, tt);
+        if (len2 > 0.0f) {
+          const float len = sqrtf(len2);
+          const float lim = mu * (-d);
+          if (len <= lim) {
+            dPG[0] = dPG[0] - tt[0];
+            dPG[1] = dPG[1] - tt[1];
+            dPG[2] = dPG[2] - tt[2];
+          } else {
+            const float fr = lim / len;
+            dPG[0] = fmaf(-tt[0], fr, dPG[0]);
+            dPG[1] = fmaf(-tt[1], fr, dPG[1]);
+            dPG[2] = fmaf(-tt[2], fr, dPG[2]);
+          }
+        }
+      }
+    }
+  }
+  float dPP[3] = {0.0f, 0.0f, 0.0f};
+  for (int c = 0; c < nc; ++c) {
+    const int j = A.cand_j[static_cast<int64_t>(c) * A.n + p];
+    const float rr = A.cand_rr[static_cast<int64_t>(c) * A.n + p];
+    // Multi-iteration launch with pairs: neighbours' X_i come from the
+    // buffer the previous iteration wrote (after a grid barrier; L2 only).
+    const float4 xj = (MULTI && A.multi_pairs) ? __ldcg(&A.pos_b[it & 1][j]) : A.pos_in[j];
+    pp_contact(x, x4.w, p, xj, j, rr, A.relax, dPP);
+  }
+  const float v[3] = {v4.x, v4.y, v4.z};
+  const float q0[3] = {r4.x, r4.y, r4.z};
+  // Body sums: product fields accumulate with one fma per particle (the
+  // first stage of the pinned reduction tree), cross products are summed.
+  float pp[3], pb[3], mp[3], vb[3], mvb[3], kb[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    dXk[c] = dPG[c] + dPP[c];
+    pp[c] = x[c] - a[c];
+    pb[c] = pp[c] + dXk[c];
+    vb[c] = fmaf(dXk[c], A.inv_dt, v[c]);
+    mp[c] = m * pp[c];
+    mvb[c] = m * vb[c];
+  }
+  cross3_fma(pb, mvb, kb);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    acc[c] = fmaf(m, pp[c], acc[c]);
+    acc[3 + c] = fmaf(m, dXk[c], acc[3 + c]);
+    acc[15 + c] = fmaf(m, vb[c], acc[15 + c]);
+    acc[18 + c] = acc[18 + c] + kb[c];
+  }
+#pragma unroll
+  for (int rI = 0; rI < 3; ++rI)
+#pragma unroll
+    for (int cI = 0; cI < 3; ++cI) acc[6 + 3 * rI + cI] = fmaf(mp[rI], q0[cI], acc[6 + 3 * rI + cI]);
+}
+
 constexpr int kResF = 32;
 enum ResSlot {
   kResC = 0,      // c (3), anchor-relative com of X_i
@@ -741,6 +823,187 @@ enum ResSlot {
   kResW = 25,     // omega (3)
   kResA = 28,     // anchor a (3)
 };
+
+// Per-body math A from the 21 bsm sums S of body bb (anchor an, 1/M):
+// com c, P_bsm, L_bsm about the predicted com, warm-started polar of Apq;
+// results into R (kRes* slots), new anchor and rotation to global memory.
+__device__ __forceinline__ void body_math_a(const IterArgs& A, int bb, const float (&S)[21], float4 an,
+                                            float invM, float4 rq4, float* R, float4& rq_new,
+                                            float4& an_new) {
+  bool finite = true;
+#pragma unroll
+  for (int f = 0; f < 21; ++f) finite = finite && isfinite(S[f]);
+  if (!finite) record_error(A.err, PBDR_DEVERR_NONFINITE, bb, A.substep_counter);
+  float c[3], cb[3], Pb[3], tmp[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    c[k] = S[k] * invM;
+    cb[k] = c[k] + S[3 + k] * invM;
+    Pb[k] = S[15 + k];
+  }
+  cross3(cb, Pb, tmp);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    R[kResC + k] = c[k];
+    R[kResPb + k] = Pb[k];
+    R[kResLb + k] = S[18 + k] - tmp[k];
+  }
+  double qd[4];
+  const float rq[4] = {rq4.x, rq4.y, rq4.z, rq4.w};
+  const bool ok = polar_warm_f(&S[6], rq, &R[kResR], qd);
+  R[kResSmOk] = ok ? 1.0f : 0.0f;
+  rq_new = ok ? make_float4(static_cast<float>(qd[0]), static_cast<float>(qd[1]), static_cast<float>(qd[2]),
+                            static_cast<float>(qd[3]))
+              : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+  an_new = make_float4(an.x + c[0], an.y + c[1], an.z + c[2], 0.0f);
+  A.rquat[bb] = rq_new;
+  if (!ok) record_error(A.err, PBDR_DEVERR_DEGENERATE, bb, A.substep_counter);
+  A.anchor[bb] = an_new;
+}
+
+// Phase B of one particle: shape-matching delta (R q0 + c - p, when the polar
+// is valid), X_a = X_i + dX and V_a (incremental or legacy velocity update).
+__device__ __forceinline__ void phase_b_particle(const IterArgs& A, int64_t p, float4 x4, float4 v4, float4 r4,
+                                                 const float a[3], bool sm_ok, const float (&Rf)[9],
+                                                 const float (&c)[3], float (&dXk)[3], float (&xa)[3],
+                                                 float (&va)[3], float (&pa)[3]) {
+  const float x[3] = {x4.x, x4.y, x4.z};
+  const float v[3] = {v4.x, v4.y, v4.z};
+  const float q0[3] = {r4.x, r4.y, r4.z};
+  float xi[3] = {0.0f, 0.0f, 0.0f};
+  if (!A.incremental) {
+    const float4 i4 = A.init[p];
+    xi[0] = i4.x; xi[1] = i4.y; xi[2] = i4.z;
+  }
+#pragma unroll
+  for (int cI = 0; cI < 3; ++cI) {
+    const float pk = x[cI] - a[cI];
+    float dsm = 0.0f;
+    if (sm_ok) {
+      const float Rrow[3] = {Rf[3 * cI], Rf[3 * cI + 1], Rf[3 * cI + 2]};
+      const float g = dot3_fma(Rrow, q0);
+      dsm = g - (pk - c[cI]);
+    }
+    dXk[cI] = dXk[cI] + dsm;
+    xa[cI] = x[cI] + dXk[cI];
+    va[cI] = A.incremental ? fmaf(dXk[cI], A.inv_dt, v[cI]) : (xa[cI] - xi[cI]) * A.inv_dt;
+    pa[cI] = pk + dXk[cI];
+  }
+}
+
+// The particle's terms of the 15 asm sums: dX, P_asm, L_asm and the inertia
+// (anchor-relative; parallel axis applied in body_math_b).
+__device__ __forceinline__ void accum_b(float mk, const float (&dXk)[3], const float (&va)[3],
+                                        const float (&pa)[3], float (&accB)[15]) {
+  const float mva[3] = {mk * va[0], mk * va[1], mk * va[2]};
+  float ka[3];
+  cross3_fma(pa, mva, ka);
+  const float s2 = dot3_fma(pa, pa);
+#pragma unroll
+  for (int cI = 0; cI < 3; ++cI) {
+    accB[cI] = fmaf(mk, dXk[cI], accB[cI]);
+    accB[3 + cI] = fmaf(mk, va[cI], accB[3 + cI]);
+    accB[6 + cI] = accB[6 + cI] + ka[cI];
+    accB[9 + cI] = fmaf(mk, fmaf(-pa[cI], pa[cI], s2), accB[9 + cI]);
+  }
+  accB[12] = fmaf(-mk, pa[0] * pa[1], accB[12]);
+  accB[13] = fmaf(-mk, pa[0] * pa[2], accB[13]);
+  accB[14] = fmaf(-mk, pa[1] * pa[2], accB[14]);
+}
+
+// Per-body math B from the 15 asm sums S of body bb: com c_asm, P_asm,
+// L_asm; the SM-induced momentum change (accumulated over the substep for
+// kPerSubstep); linear fix dv = dP/M and angular fix omega = pinv(I) dL.
+// Reads kResC/kResPb/kResLb and writes kResCa/kResDv/kResW of R.
+__device__ __forceinline__ void body_math_b(const IterArgs& A, int bb, const float (&S)[15], float2 mass,
+                                            float* R, int iter_index, int last_iter) {
+  bool finite = true;
+#pragma unroll
+  for (int f = 0; f < 15; ++f) finite = finite && isfinite(S[f]);
+  if (!finite) record_error(A.err, PBDR_DEVERR_NONFINITE, bb, A.substep_counter);
+  const float M = mass.x, invM = mass.y;
+  float ca[3], Pa[3], La[3], tmp[3], dv[3] = {0.0f, 0.0f, 0.0f}, om[3] = {0.0f, 0.0f, 0.0f};
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    ca[k] = R[kResC + k] + S[k] * invM;
+    Pa[k] = S[3 + k];
+  }
+  cross3(ca, Pa, tmp);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) La[k] = S[6 + k] - tmp[k];
+  // SM-induced momentum change of this iteration (P_bsm - P_asm, L_asm - L_bsm).
+  float dP[3], dL[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    dP[k] = R[kResPb + k] - Pa[k];
+    dL[k] = La[k] - R[kResLb + k];
+  }
+  bool correct = true;
+  if (A.per_substep) {
+    // kPerSubstep: accumulate over the substep's iterations, correct once.
+    float4 aP = make_float4(0.0f, 0.0f, 0.0f, 0.0f), aL = aP;
+    if (iter_index > 0) {
+      aP = A.mom_acc[2 * bb];
+      aL = A.mom_acc[2 * bb + 1];
+    }
+    aP.x = aP.x + dP[0]; aP.y = aP.y + dP[1]; aP.z = aP.z + dP[2];
+    aL.x = aL.x + dL[0]; aL.y = aL.y + dL[1]; aL.z = aL.z + dL[2];
+    A.mom_acc[2 * bb] = aP;
+    A.mom_acc[2 * bb + 1] = aL;
+    dP[0] = aP.x; dP[1] = aP.y; dP[2] = aP.z;
+    dL[0] = aL.x; dL[1] = aL.y; dL[2] = aL.z;
+    correct = last_iter != 0;
+  }
+  if (A.linfix && correct)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) dv[k] = dP[k] * invM;
+  if (A.angfix && correct) {
+    float If[6];
+    If[0] = S[9] - M * (ca[1] * ca[1] + ca[2] * ca[2]);
+    If[1] = S[10] - M * (ca[0] * ca[0] + ca[2] * ca[2]);
+    If[2] = S[11] - M * (ca[0] * ca[0] + ca[1] * ca[1]);
+    If[3] = S[12] + M * (ca[0] * ca[1]);
+    If[4] = S[13] + M * (ca[0] * ca[2]);
+    If[5] = S[14] + M * (ca[1] * ca[2]);
+    double nax[3];
+    const unsigned e = inertia_solve_f(If, dL, om, nax);
+    if (e) record_error(A.err, e, bb, A.substep_counter, nax);
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    R[kResCa + k] = ca[k];
+    R[kResDv + k] = dv[k];
+    R[kResW + k] = om[k];
+  }
+}
+
+// Phase C of one particle: momentum corrections (Eq. 1 then Eq. 2) on top of
+// X_a, V_a: v = V_a + dv - omega x r, x = X_a + dt dv - dt omega x r.
+__device__ __forceinline__ void phase_c_particle(const IterArgs& A, int64_t p, float4 x4, float4 v4,
+                                                 const float a[3], const float (&dXk)[3], const float (&ca)[3],
+                                                 const float (&dv)[3], const float (&om)[3], float (&xo)[3],
+                                                 float (&vo)[3]) {
+  float xi[3] = {0.0f, 0.0f, 0.0f};
+  if (!A.incremental) {
+    const float4 i4 = A.init[p];
+    xi[0] = i4.x; xi[1] = i4.y; xi[2] = i4.z;
+  }
+  const float x[3] = {x4.x, x4.y, x4.z};
+  const float v[3] = {v4.x, v4.y, v4.z};
+  float xa[3], va[3], r[3], wr[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    xa[c] = x[c] + dXk[c];
+    va[c] = A.incremental ? fmaf(dXk[c], A.inv_dt, v[c]) : (xa[c] - xi[c]) * A.inv_dt;
+    r[c] = ((x[c] - a[c]) + dXk[c]) - ca[c];
+  }
+  cross3_fma(om, r, wr);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    vo[c] = (va[c] + dv[c]) - wr[c];
+    xo[c] = fmaf(-wr[c], A.dt, fmaf(dv[c], A.dt, xa[c]));
+  }
+}
 
 // KP = 8 particles per lane, 8-warp CTAs: 96 KB of staged state per CTA, so
 // two CTAs per SM with up to 128 registers (no spills). Measured on C4:
@@ -861,83 +1124,7 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
     const int q = k * 32 * W + wi * 32 + lane;
     if (!(live && q < n)) continue;
     const int64_t p = start + q;
-    const float4 x4 = s_pos[off + q];
-    const float4 v4 = s_vel[off + q];
-    const float4 r4 = s_rest[off + q];
-    const float x[3] = {x4.x, x4.y, x4.z};
-    const float m = v4.w;
-
-    float dPG[3] = {0.0f, 0.0f, 0.0f};
-    for (int pl = 0; pl < A.planes.count; ++pl) {
-      const float* Pp = A.planes.p[pl];
-      const float* Pn = A.planes.n[pl];
-      const float xp[3] = {x[0] - Pp[0], x[1] - Pp[1], x[2] - Pp[2]};
-      const float d = dot3_fma(xp, Pn) - r4.w;
-      if (d < 0.0f) {
-        const float push = -(A.relax * d);
-        dPG[0] = fmaf(push, Pn[0], dPG[0]);
-        dPG[1] = fmaf(push, Pn[1], dPG[1]);
-        dPG[2] = fmaf(push, Pn[2], dPG[2]);
-        const float mu = A.planes.mu[pl];
-        if (mu > 0.0f) {
-          const float4 xi = A.init[p];
-          const float t[3] = {x[0] - xi.x, x[1] - xi.y, x[2] - xi.z};
-          const float tn = dot3_fma(t, Pn);
-          const float tt[3] = {fmaf(-tn, Pn[0], t[0]), fmaf(-tn, Pn[1], t[1]), fmaf(-tn, Pn[2], t[2])};
-          const float len2 = dot3_fma(tt, tt);
-          if (len2 > 0.0f) {
-            const float len = sqrtf(len2);
-            const float lim = mu * (-d);
-            if (len <= lim) {
-              dPG[0] = dPG[0] - tt[0];
-              dPG[1] = dPG[1] - tt[1];
-              dPG[2] = dPG[2] - tt[2];
-            } else {
-              const float fr = lim / len;
-              dPG[0] = fmaf(-tt[0], fr, dPG[0]);
-              dPG[1] = fmaf(-tt[1], fr, dPG[1]);
-              dPG[2] = fmaf(-tt[2], fr, dPG[2]);
-            }
-          }
-        }
-      }
-    }
-    float dPP[3] = {0.0f, 0.0f, 0.0f};
-    const int nc = ncs[k];
-    for (int c = 0; c < nc; ++c) {
-      const int j = A.cand_j[static_cast<int64_t>(c) * A.n + p];
-      const float rr = A.cand_rr[static_cast<int64_t>(c) * A.n + p];
-      // Multi-iteration launch with pairs: neighbours' X_i come from the
-      // buffer the previous iteration wrote (after a grid barrier; L2 only).
-      const float4 xj = (MULTI && A.multi_pairs) ? __ldcg(&A.pos_b[it & 1][j]) : A.pos_in[j];
-      pp_contact(x, x4.w, p, xj, j, rr, A.relax, dPP);
-    }
-    const float v[3] = {v4.x, v4.y, v4.z};
-    const float q0[3] = {r4.x, r4.y, r4.z};
-    // Body sums: product fields accumulate with one fma per particle (the
-    // first stage of the pinned reduction tree), cross products are summed.
-    float pp[3], pb[3], mp[3], vb[3], mvb[3], kb[3];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      dX[k][c] = dPG[c] + dPP[c];
-      pp[c] = x[c] - a[c];
-      pb[c] = pp[c] + dX[k][c];
-      vb[c] = fmaf(dX[k][c], A.inv_dt, v[c]);
-      mp[c] = m * pp[c];
-      mvb[c] = m * vb[c];
-    }
-    cross3_fma(pb, mvb, kb);
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      acc[c] = fmaf(m, pp[c], acc[c]);
-      acc[3 + c] = fmaf(m, dX[k][c], acc[3 + c]);
-      acc[15 + c] = fmaf(m, vb[c], acc[15 + c]);
-      acc[18 + c] = acc[18 + c] + kb[c];
-    }
-#pragma unroll
-    for (int rI = 0; rI < 3; ++rI)
-#pragma unroll
-      for (int cI = 0; cI < 3; ++cI) acc[6 + 3 * rI + cI] = fmaf(mp[rI], q0[cI], acc[6 + 3 * rI + cI]);
+    phase_a_particle<MULTI>(A, it, p, s_pos[off + q], s_vel[off + q], s_rest[off + q], ncs[k], a, dX[k], acc);
   }
   if (live) {
     const float tot = warp_reduce_scatter<21>(acc);  // lane f: total of field f
@@ -960,37 +1147,8 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
     for (int u = 1; u < bw.y; ++u)
 #pragma unroll
       for (int f = 0; f < 21; ++f) S[f] = S[f] + s_part[fw + u][f];
-    bool finite = true;
-#pragma unroll
-    for (int f = 0; f < 21; ++f) finite = finite && isfinite(S[f]);
-    if (!finite) record_error(A.err, PBDR_DEVERR_NONFINITE, bb, A.substep_counter);
-    float c[3], cb[3], Pb[3], tmp[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      c[k] = S[k] * invM;
-      cb[k] = c[k] + S[3 + k] * invM;
-      Pb[k] = S[15 + k];
-    }
-    cross3(cb, Pb, tmp);
-    float* R = &s_res[lane][0];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      R[kResC + k] = c[k];
-      R[kResPb + k] = Pb[k];
-      R[kResLb + k] = S[18 + k] - tmp[k];
-    }
-    double qd[4];
-    const float4 rq4 = s_trq[tb][lane];
-    const float rq[4] = {rq4.x, rq4.y, rq4.z, rq4.w};
-    const bool ok = polar_warm_f(&S[6], rq, &R[kResR], qd);
-    R[kResSmOk] = ok ? 1.0f : 0.0f;
-    const float4 rq_new = ok ? make_float4(static_cast<float>(qd[0]), static_cast<float>(qd[1]),
-                                           static_cast<float>(qd[2]), static_cast<float>(qd[3]))
-                             : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-    const float4 an_new = make_float4(an.x + c[0], an.y + c[1], an.z + c[2], 0.0f);
-    A.rquat[bb] = rq_new;
-    if (!ok) record_error(A.err, PBDR_DEVERR_DEGENERATE, bb, A.substep_counter);
-    A.anchor[bb] = an_new;
+    float4 rq_new, an_new;
+    body_math_a(A, bb, S, an, invM, s_trq[tb][lane], &s_res[lane][0], rq_new, an_new);
     s_trq[tb][lane] = rq_new;   // next iteration of a multi-iteration launch
     s_tanc[tb][lane] = an_new;
   }
@@ -1015,46 +1173,10 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
       if (!(q < n)) continue;
       const float4 x4 = s_pos[off + q];
       const float4 v4 = s_vel[off + q];
-      const float4 r4 = s_rest[off + q];
-      const float x[3] = {x4.x, x4.y, x4.z};
-      const float v[3] = {v4.x, v4.y, v4.z};
-      const float q0[3] = {r4.x, r4.y, r4.z};
-      float xi[3] = {0.0f, 0.0f, 0.0f};
-      if (!A.incremental) {
-        const float4 i4 = A.init[start + q];
-        xi[0] = i4.x; xi[1] = i4.y; xi[2] = i4.z;
-      }
       float xa[3], va[3], pa[3];
-#pragma unroll
-      for (int cI = 0; cI < 3; ++cI) {
-        const float pk = x[cI] - a[cI];
-        float dsm = 0.0f;
-        if (sm_ok) {
-          const float Rrow[3] = {Rf[3 * cI], Rf[3 * cI + 1], Rf[3 * cI + 2]};
-          const float g = dot3_fma(Rrow, q0);
-          dsm = g - (pk - c[cI]);
-        }
-        dX[k][cI] = dX[k][cI] + dsm;
-        xa[cI] = x[cI] + dX[k][cI];
-        va[cI] = A.incremental ? fmaf(dX[k][cI], A.inv_dt, v[cI]) : (xa[cI] - xi[cI]) * A.inv_dt;
-        pa[cI] = pk + dX[k][cI];
-      }
+      phase_b_particle(A, start + q, x4, v4, s_rest[off + q], a, sm_ok, Rf, c, dX[k], xa, va, pa);
       if (fixes) {
-        const float mk = v4.w;
-        const float mva[3] = {mk * va[0], mk * va[1], mk * va[2]};
-        float ka[3];
-        cross3_fma(pa, mva, ka);
-        const float s2 = dot3_fma(pa, pa);
-#pragma unroll
-        for (int cI = 0; cI < 3; ++cI) {
-          accB[cI] = fmaf(mk, dX[k][cI], accB[cI]);
-          accB[3 + cI] = fmaf(mk, va[cI], accB[3 + cI]);
-          accB[6 + cI] = accB[6 + cI] + ka[cI];
-          accB[9 + cI] = fmaf(mk, fmaf(-pa[cI], pa[cI], s2), accB[9 + cI]);
-        }
-        accB[12] = fmaf(-mk, pa[0] * pa[1], accB[12]);
-        accB[13] = fmaf(-mk, pa[0] * pa[2], accB[13]);
-        accB[14] = fmaf(-mk, pa[1] * pa[2], accB[14]);
+        accum_b(v4.w, dX[k], va, pa, accB);
       } else {
         const int64_t p = start + q;
         if (MULTI) {
@@ -1089,65 +1211,7 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
     for (int u = 1; u < bw.y; ++u)
 #pragma unroll
       for (int f = 0; f < 15; ++f) S[f] = S[f] + s_part[fw + u][f];
-    bool finite = true;
-#pragma unroll
-    for (int f = 0; f < 15; ++f) finite = finite && isfinite(S[f]);
-    if (!finite) record_error(A.err, PBDR_DEVERR_NONFINITE, bb, A.substep_counter);
-    float* R = &s_res[lane][0];
-    const float M = mass.x, invM = mass.y;
-    float ca[3], Pa[3], La[3], tmp[3], dv[3] = {0.0f, 0.0f, 0.0f}, om[3] = {0.0f, 0.0f, 0.0f};
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      ca[k] = R[kResC + k] + S[k] * invM;
-      Pa[k] = S[3 + k];
-    }
-    cross3(ca, Pa, tmp);
-#pragma unroll
-    for (int k = 0; k < 3; ++k) La[k] = S[6 + k] - tmp[k];
-    // SM-induced momentum change of this iteration (P_bsm - P_asm, L_asm - L_bsm).
-    float dP[3], dL[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      dP[k] = R[kResPb + k] - Pa[k];
-      dL[k] = La[k] - R[kResLb + k];
-    }
-    bool correct = true;
-    if (A.per_substep) {
-      // kPerSubstep: accumulate over the substep's iterations, correct once.
-      float4 aP = make_float4(0.0f, 0.0f, 0.0f, 0.0f), aL = aP;
-      if (iter_index > 0) {
-        aP = A.mom_acc[2 * bb];
-        aL = A.mom_acc[2 * bb + 1];
-      }
-      aP.x = aP.x + dP[0]; aP.y = aP.y + dP[1]; aP.z = aP.z + dP[2];
-      aL.x = aL.x + dL[0]; aL.y = aL.y + dL[1]; aL.z = aL.z + dL[2];
-      A.mom_acc[2 * bb] = aP;
-      A.mom_acc[2 * bb + 1] = aL;
-      dP[0] = aP.x; dP[1] = aP.y; dP[2] = aP.z;
-      dL[0] = aL.x; dL[1] = aL.y; dL[2] = aL.z;
-      correct = last_iter != 0;
-    }
-    if (A.linfix && correct)
-#pragma unroll
-      for (int k = 0; k < 3; ++k) dv[k] = dP[k] * invM;
-    if (A.angfix && correct) {
-      float If[6];
-      If[0] = S[9] - M * (ca[1] * ca[1] + ca[2] * ca[2]);
-      If[1] = S[10] - M * (ca[0] * ca[0] + ca[2] * ca[2]);
-      If[2] = S[11] - M * (ca[0] * ca[0] + ca[1] * ca[1]);
-      If[3] = S[12] + M * (ca[0] * ca[1]);
-      If[4] = S[13] + M * (ca[0] * ca[2]);
-      If[5] = S[14] + M * (ca[1] * ca[2]);
-      double nax[3];
-      const unsigned e = inertia_solve_f(If, dL, om, nax);
-      if (e) record_error(A.err, e, bb, A.substep_counter, nax);
-    }
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      R[kResCa + k] = ca[k];
-      R[kResDv + k] = dv[k];
-      R[kResW + k] = om[k];
-    }
+    body_math_b(A, bb, S, mass, &s_res[lane][0], iter_index, last_iter);
   }
   __syncthreads();
   if (tm && threadIdx.x == 0) tm[5] = clock64();
@@ -1167,27 +1231,9 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
     if (!(q < n)) continue;
     const float4 x4 = s_pos[off + q];
     const float4 v4 = s_vel[off + q];
-    float xi[3] = {0.0f, 0.0f, 0.0f};
-    if (!A.incremental) {
-      const float4 i4 = A.init[start + q];
-      xi[0] = i4.x; xi[1] = i4.y; xi[2] = i4.z;
-    }
-    const float x[3] = {x4.x, x4.y, x4.z};
-    const float v[3] = {v4.x, v4.y, v4.z};
-    float xa[3], va[3], r[3], wr[3], xo[3], vo[3];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      xa[c] = x[c] + dX[k][c];
-      va[c] = A.incremental ? fmaf(dX[k][c], A.inv_dt, v[c]) : (xa[c] - xi[c]) * A.inv_dt;
-      r[c] = ((x[c] - a[c]) + dX[k][c]) - ca[c];
-    }
-    cross3_fma(om, r, wr);
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      vo[c] = (va[c] + dv[c]) - wr[c];
-      xo[c] = fmaf(-wr[c], A.dt, fmaf(dv[c], A.dt, xa[c]));
-    }
     const int64_t p = start + q;
+    float xo[3], vo[3];
+    phase_c_particle(A, p, x4, v4, a, dX[k], ca, dv, om, xo, vo);
     if (MULTI) {
       s_pos[off + q] = make_float4(xo[0], xo[1], xo[2], x4.w);
       s_vel[off + q] = make_float4(vo[0], vo[1], vo[2], v4.w);
@@ -1242,71 +1288,265 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
 }
 
 // ---------------------------------------------------------------------------
-// Per-body trajectory sample: com, orientation (extract_pose), P, L.
+// Bodies larger than one CTA (W = pbdr_body_warps(n, 8) > 8 warps): one
+// thread-block cluster per body. CTA r of the cluster (w = blockDim/32 warps,
+// w = ceil(W / cluster) <= 8 so that the warps spread evenly) stages and
+// computes the body's warps r*w .. r*w+w-1 with the same slot -> (warp, lane, k) map, the
+// same per-particle code and the same reduction tree as k_iteration: lane
+// sums over k, xor butterfly, then the per-warp partials -- written into the
+// leader CTA's shared memory over DSMEM -- summed serially in warp order by
+// the leader, which runs the per-body math; the other CTAs read the results
+// back over DSMEM. Cluster barriers order the phases (release/acquire, so the
+// remote stores are visible after them). KP = 8: a scene with such a body
+// always reduces with the KP = 8 tree (pbdr_choose_kp).
 // ---------------------------------------------------------------------------
-template <int KP>
-__global__ void __launch_bounds__(kThreads) k_body_stats(StatsArgs A) {
-  __shared__ float s_part[kWarps][18];
+constexpr int kBigMaxWarps = PBDR_MAX_CLUSTER_CTAS * kWarps;  // 128 warps = 32768 particles
+
+__global__ void __launch_bounds__(kThreads, 2) k_iteration_big(IterArgs A) {
+  constexpr int KP = PBDR_KP_MAX;
+  const int nt = blockDim.x;           // 32 * warps per CTA (launch_iteration_big)
+  const int kSlots = nt * KP;
+  extern __shared__ float4 s_stage[];  // pos | vel | rest of this CTA's warps, [k][warp][lane]
+  __shared__ float s_part[kBigMaxWarps][21];  // leader: per-warp partials of the body
+  __shared__ float s_res[kResF];              // leader: per-body results; others: their copy
+  __shared__ float s_sum[21];                 // leader: body sums
+  __shared__ float4 s_rq;                     // leader: warm-start rotation across iterations
+  __shared__ __align__(8) uint64_t s_bar;
+  float4* s_pos = s_stage;
+  float4* s_vel = s_stage + kSlots;
+  float4* s_rest = s_stage + 2 * kSlots;
+
+  cooperative_groups::cluster_group cluster = cooperative_groups::this_cluster();
+  const int r = static_cast<int>(cluster.block_rank());
+  const int ncl = static_cast<int>(cluster.num_blocks());
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int4 cd = A.cta_desc[blockIdx.x];
-  const int4 wd = A.warp_desc[blockIdx.x * kWarps + warp];
-  const int b = wd.x;
-  const int wi = wd.y;
-  const bool live = b >= 0;
-  float acc[18];
+  const int b = A.big_list[blockIdx.x / ncl];
+  const int4 bd = A.body_desc[b];
+  const int start = bd.x, n = bd.y, W = bd.z;
+  const int wi = r * (nt >> 5) + warp;
+  const bool live = wi < W;
+  const int K = pbdr_body_slots(n, W);
+  const bool fixes = A.linfix || A.angfix;
+  const int n_iters = A.multi_pairs ? 1 : A.n_iters;  // several only without pairs (state stays in smem)
+  float* lead_part = cluster.map_shared_rank(&s_part[0][0], 0);
+  const float* lead_res = cluster.map_shared_rank(&s_res[0], 0);
+
+  if (threadIdx.x == 0) {
+    mbar_init(&s_bar, 1);
+    // Row k of the body holds slots k*32*W .. (k+1)*32*W; this CTA's part of
+    // it is the nt slots from k*32*W + r*nt (clipped to the row and to n).
+    uint32_t total = 0;
+    for (int k = 0; k < K; ++k) {
+      const int q0 = k * 32 * W + r * nt;
+      const int q1 = min(min(q0 + nt, (k + 1) * 32 * W), n);
+      if (q1 > q0) total += 3u * 16u * static_cast<uint32_t>(q1 - q0);
+    }
+    mbar_expect_tx(&s_bar, total);
+    for (int k = 0; k < K; ++k) {
+      const int q0 = k * 32 * W + r * nt;
+      const int q1 = min(min(q0 + nt, (k + 1) * 32 * W), n);
+      if (q1 <= q0) continue;
+      const uint32_t bytes = 16u * static_cast<uint32_t>(q1 - q0);
+      bulk_g2s_stream(s_pos + k * nt, A.pos_in + start + q0, bytes, &s_bar);
+      bulk_g2s_stream(s_vel + k * nt, A.vel + start + q0, bytes, &s_bar);
+      bulk_g2s_stream(s_rest + k * nt, A.rest + start + q0, bytes, &s_bar);
+    }
+    if (r == 0) s_rq = A.rquat[b];
+  }
+  if (threadIdx.x < 3) s_res[kResA + threadIdx.x] = (&A.anchor[b].x)[threadIdx.x];
+  int ncs[KP];
 #pragma unroll
-  for (int f = 0; f < 18; ++f) acc[f] = 0.0f;
-  if (live) {
-    const int4 bd = make_int4(wd.z, wd.w & 0xFFFF, wd.w >> 16, 0);
-    const float4 an = A.anchor[b];
-    const float a[3] = {an.x, an.y, an.z};
+  for (int k = 0; k < KP; ++k) {
+    const int q = k * 32 * W + wi * 32 + lane;
+    ncs[k] = (live && q < n) ? A.ncand[start + q] : 0;
+  }
+  cluster.sync();  // every CTA of the cluster running (DSMEM targets exist), barrier initialised
+  mbar_wait(&s_bar, 0);
+
+  for (int it = 0; it < n_iters; ++it) {
+    const int iter_index = A.iter_index + it;
+    const int last_iter = A.last_iter && it == n_iters - 1;
+    const float a[3] = {s_res[kResA], s_res[kResA + 1], s_res[kResA + 2]};
+    float dX[KP][3];
+
+    // ---- Phase A ----------------------------------------------------------
+    float acc[21];
+#pragma unroll
+    for (int f = 0; f < 21; ++f) acc[f] = 0.0f;
+#pragma unroll
+    for (int k = 0; k < KP; ++k) dX[k][0] = dX[k][1] = dX[k][2] = 0.0f;
 #pragma unroll
     for (int k = 0; k < KP; ++k) {
-      const int q = k * 32 * bd.z + wi * 32 + lane;
-      if (q >= bd.y) continue;
-      const int64_t p = bd.x + q;
-      const float4 x4 = A.pos[p];
-      const float4 v4 = A.vel[p];
-      const float4 r4 = A.rest[p];
-      const float mk = v4.w;
-      const float pp[3] = {x4.x - a[0], x4.y - a[1], x4.z - a[2]};
-      const float mp[3] = {mk * pp[0], mk * pp[1], mk * pp[2]};
-      const float mv[3] = {mk * v4.x, mk * v4.y, mk * v4.z};
-      const float q0[3] = {r4.x, r4.y, r4.z};
-      float kk[3];
-      cross3(pp, mv, kk);
-      acc[0] = acc[0] + mp[0];
-      acc[1] = acc[1] + mp[1];
-      acc[2] = acc[2] + mp[2];
-#pragma unroll
-      for (int rI = 0; rI < 3; ++rI)
-#pragma unroll
-        for (int cI = 0; cI < 3; ++cI) acc[3 + 3 * rI + cI] = acc[3 + 3 * rI + cI] + mp[rI] * q0[cI];
-      acc[12] = acc[12] + mv[0];
-      acc[13] = acc[13] + mv[1];
-      acc[14] = acc[14] + mv[2];
-      acc[15] = acc[15] + kk[0];
-      acc[16] = acc[16] + kk[1];
-      acc[17] = acc[17] + kk[2];
+      const int q = k * 32 * W + wi * 32 + lane;
+      if (!(live && q < n)) continue;
+      const int li = k * nt + threadIdx.x;
+      phase_a_particle<false>(A, it, start + q, s_pos[li], s_vel[li], s_rest[li], ncs[k], a, dX[k], acc);
     }
-    warp_butterfly<18>(acc);
-    if (lane == 0)
+    if (live) {
+      const float tot = warp_reduce_scatter<21>(acc);
+      if (lane < 21) lead_part[wi * 21 + lane] = tot;
+    }
+    cluster.sync();
+    if (r == 0) {
+      // Stage 3 of the tree: per field, serially over the warps (one thread
+      // per field), then the body math on one thread.
+      if (threadIdx.x < 21) {
+        float t = s_part[0][threadIdx.x];
+        for (int u = 1; u < W; ++u) t = t + s_part[u][threadIdx.x];
+        s_sum[threadIdx.x] = t;
+      }
+      __syncthreads();
+    }
+    if (r == 0 && threadIdx.x == 0) {
+      float S[21];
 #pragma unroll
-      for (int f = 0; f < 18; ++f) s_part[warp][f] = acc[f];
+      for (int f = 0; f < 21; ++f) S[f] = s_sum[f];
+      const float4 an = make_float4(a[0], a[1], a[2], 0.0f);
+      float4 rq_new, an_new;
+      body_math_a(A, b, S, an, A.body_mass[b].y, s_rq, s_res, rq_new, an_new);
+      s_rq = rq_new;
+      s_res[kResA] = an_new.x;
+      s_res[kResA + 1] = an_new.y;
+      s_res[kResA + 2] = an_new.z;
+    }
+    cluster.sync();
+    if (r != 0 && threadIdx.x < kResF) s_res[threadIdx.x] = lead_res[threadIdx.x];
+    __syncthreads();
+
+    // ---- Phase B ----------------------------------------------------------
+    float accB[15];
+#pragma unroll
+    for (int f = 0; f < 15; ++f) accB[f] = 0.0f;
+    if (live) {
+      const bool sm_ok = s_res[kResSmOk] != 0.0f;
+      float Rf[9], c[3];
+#pragma unroll
+      for (int f = 0; f < 9; ++f) Rf[f] = s_res[kResR + f];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) c[k] = s_res[kResC + k];
+#pragma unroll
+      for (int k = 0; k < KP; ++k) {
+        const int q = k * 32 * W + wi * 32 + lane;
+        if (!(q < n)) continue;
+        const int li = k * nt + threadIdx.x;
+        const float4 x4 = s_pos[li];
+        const float4 v4 = s_vel[li];
+        float xa[3], va[3], pa[3];
+        phase_b_particle(A, start + q, x4, v4, s_rest[li], a, sm_ok, Rf, c, dX[k], xa, va, pa);
+        if (fixes) {
+          accum_b(v4.w, dX[k], va, pa, accB);
+        } else if (n_iters > 1) {
+          s_pos[li] = make_float4(xa[0], xa[1], xa[2], x4.w);
+          s_vel[li] = make_float4(va[0], va[1], va[2], v4.w);
+        } else {
+          A.pos_out[start + q] = make_float4(xa[0], xa[1], xa[2], x4.w);
+          A.vel[start + q] = make_float4(va[0], va[1], va[2], v4.w);
+        }
+      }
+    }
+    if (fixes) {
+      if (live) {
+        const float tot = warp_reduce_scatter<15>(accB);  // lanes 2f, 2f+1: field f
+        if ((lane & 1) == 0 && (lane >> 1) < 15) lead_part[wi * 21 + (lane >> 1)] = tot;
+      }
+      cluster.sync();
+      if (r == 0) {
+        if (threadIdx.x < 15) {
+          float t = s_part[0][threadIdx.x];
+          for (int u = 1; u < W; ++u) t = t + s_part[u][threadIdx.x];
+          s_sum[threadIdx.x] = t;
+        }
+        __syncthreads();
+      }
+      if (r == 0 && threadIdx.x == 0) {
+        float S[15];
+#pragma unroll
+        for (int f = 0; f < 15; ++f) S[f] = s_sum[f];
+        body_math_b(A, b, S, A.body_mass[b], s_res, iter_index, last_iter);
+      }
+      cluster.sync();
+      if (r != 0 && threadIdx.x < kResF) s_res[threadIdx.x] = lead_res[threadIdx.x];
+      __syncthreads();
+
+      // ---- Phase C --------------------------------------------------------
+      if (live) {
+        float ca[3], dv[3], om[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          ca[k] = s_res[kResCa + k];
+          dv[k] = s_res[kResDv + k];
+          om[k] = s_res[kResW + k];
+        }
+#pragma unroll
+        for (int k = 0; k < KP; ++k) {
+          const int q = k * 32 * W + wi * 32 + lane;
+          if (!(q < n)) continue;
+          const int li = k * nt + threadIdx.x;
+          const float4 x4 = s_pos[li];
+          const float4 v4 = s_vel[li];
+          float xo[3], vo[3];
+          phase_c_particle(A, start + q, x4, v4, a, dX[k], ca, dv, om, xo, vo);
+          if (n_iters > 1) {
+            s_pos[li] = make_float4(xo[0], xo[1], xo[2], x4.w);
+            s_vel[li] = make_float4(vo[0], vo[1], vo[2], v4.w);
+          } else {
+            A.pos_out[start + q] = make_float4(xo[0], xo[1], xo[2], x4.w);
+            A.vel[start + q] = make_float4(vo[0], vo[1], vo[2], v4.w);
+          }
+        }
+      }
+    }
+    __syncthreads();  // s_res (anchor) and the staged state of the next iteration
   }
-  __syncthreads();
-  if (!(warp == 0 && lane < cd.w)) return;
-  const int bb = cd.z + lane;
-  const int4 bd = A.body_desc[bb];
+  if (n_iters > 1 && live)
+#pragma unroll
+    for (int k = 0; k < KP; ++k) {
+      const int q = k * 32 * W + wi * 32 + lane;
+      if (q < n) {
+        const int li = k * nt + threadIdx.x;
+        A.pos_out[start + q] = s_pos[li];
+        A.vel[start + q] = s_vel[li];
+      }
+    }
+  cluster.sync();  // the leader's shared memory outlives every remote read
+}
+
+// ---------------------------------------------------------------------------
+// Per-body trajectory sample: com, orientation (extract_pose), P, L.
+// ---------------------------------------------------------------------------
+// Terms of particle p in the 18 trajectory sums (anchor-relative m x, Apq, P,
+// L about the anchor).
+__device__ __forceinline__ void stats_accum(const StatsArgs& A, int64_t p, const float a[3], float (&acc)[18]) {
+  const float4 x4 = A.pos[p];
+  const float4 v4 = A.vel[p];
+  const float4 r4 = A.rest[p];
+  const float mk = v4.w;
+  const float pp[3] = {x4.x - a[0], x4.y - a[1], x4.z - a[2]};
+  const float mp[3] = {mk * pp[0], mk * pp[1], mk * pp[2]};
+  const float mv[3] = {mk * v4.x, mk * v4.y, mk * v4.z};
+  const float q0[3] = {r4.x, r4.y, r4.z};
+  float kk[3];
+  cross3(pp, mv, kk);
+  acc[0] = acc[0] + mp[0];
+  acc[1] = acc[1] + mp[1];
+  acc[2] = acc[2] + mp[2];
+#pragma unroll
+  for (int rI = 0; rI < 3; ++rI)
+#pragma unroll
+    for (int cI = 0; cI < 3; ++cI) acc[3 + 3 * rI + cI] = acc[3 + 3 * rI + cI] + mp[rI] * q0[cI];
+  acc[12] = acc[12] + mv[0];
+  acc[13] = acc[13] + mv[1];
+  acc[14] = acc[14] + mv[2];
+  acc[15] = acc[15] + kk[0];
+  acc[16] = acc[16] + kk[1];
+  acc[17] = acc[17] + kk[2];
+}
+
+// Trajectory sample of body bb from its 18 sums: com, orientation, P, L.
+__device__ __forceinline__ void stats_body_out(const StatsArgs& A, int bb, const float (&S)[18]) {
   const float4 an = A.anchor[bb];
   const float a[3] = {an.x, an.y, an.z};
-  float S[18];
-#pragma unroll
-  for (int f = 0; f < 18; ++f) S[f] = s_part[bd.w][f];
-  for (int u = 1; u < bd.z; ++u)
-#pragma unroll
-    for (int f = 0; f < 18; ++f) S[f] = S[f] + s_part[bd.w + u][f];
   const float invM = A.body_mass[bb].y;
   float c[3], P[3], tmp[3];
 #pragma unroll
@@ -1331,11 +1571,130 @@ __global__ void __launch_bounds__(kThreads) k_body_stats(StatsArgs A) {
   for (int k = 0; k < 4; ++k) o[3 + k] = qd[k];
 }
 
+template <int KP>
+__global__ void __launch_bounds__(kThreads) k_body_stats(StatsArgs A) {
+  __shared__ float s_part[kWarps][18];
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int4 cd = A.cta_desc[blockIdx.x];
+  const int4 wd = A.warp_desc[blockIdx.x * kWarps + warp];
+  const int b = wd.x;
+  const int wi = wd.y;
+  const bool live = b >= 0;
+  float acc[18];
+#pragma unroll
+  for (int f = 0; f < 18; ++f) acc[f] = 0.0f;
+  if (live) {
+    const int4 bd = make_int4(wd.z, wd.w & 0xFFFF, wd.w >> 16, 0);
+    const float4 an = A.anchor[b];
+    const float a[3] = {an.x, an.y, an.z};
+#pragma unroll
+    for (int k = 0; k < KP; ++k) {
+      const int q = k * 32 * bd.z + wi * 32 + lane;
+      if (q >= bd.y) continue;
+      stats_accum(A, bd.x + q, a, acc);
+    }
+    warp_butterfly<18>(acc);
+    if (lane == 0)
+#pragma unroll
+      for (int f = 0; f < 18; ++f) s_part[warp][f] = acc[f];
+  }
+  __syncthreads();
+  if (!(warp == 0 && lane < cd.w)) return;
+  const int bb = cd.z + lane;
+  const int4 bd = A.body_desc[bb];
+  float S[18];
+#pragma unroll
+  for (int f = 0; f < 18; ++f) S[f] = s_part[bd.w][f];
+  for (int u = 1; u < bd.z; ++u)
+#pragma unroll
+    for (int f = 0; f < 18; ++f) S[f] = S[f] + s_part[bd.w + u][f];
+  stats_body_out(A, bb, S);
+}
+
+
+// Trajectory sample of a body larger than one CTA: one CTA per body, each warp
+// loops over the body's warps wi = warp, warp + 8, ... (same tree).
+__global__ void __launch_bounds__(kThreads) k_body_stats_big(StatsArgs A) {
+  __shared__ float s_part[kBigMaxWarps][18];
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int b = A.big_list[blockIdx.x];
+  const int4 bd = A.body_desc[b];
+  const float4 an = A.anchor[b];
+  const float a[3] = {an.x, an.y, an.z};
+  for (int wi = warp; wi < bd.z; wi += kWarps) {
+    float acc[18];
+#pragma unroll
+    for (int f = 0; f < 18; ++f) acc[f] = 0.0f;
+#pragma unroll
+    for (int k = 0; k < PBDR_KP_MAX; ++k) {
+      const int q = k * 32 * bd.z + wi * 32 + lane;
+      if (q < bd.y) stats_accum(A, bd.x + q, a, acc);
+    }
+    warp_butterfly<18>(acc);
+    if (lane == 0)
+#pragma unroll
+      for (int f = 0; f < 18; ++f) s_part[wi][f] = acc[f];
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  float S[18];
+#pragma unroll
+  for (int f = 0; f < 18; ++f) S[f] = s_part[0][f];
+  for (int u = 1; u < bd.z; ++u)
+#pragma unroll
+    for (int f = 0; f < 18; ++f) S[f] = S[f] + s_part[u][f];
+  stats_body_out(A, b, S);
+}
+
 // ---------------------------------------------------------------------------
 // Torque programs: per-body com, inertia and alpha = pinv(I) tau of X at the
 // substep start (distribute_wrench, body.cpp:126-150). Same reduction tree as
 // every body sum (pbdr_pinned.h); the oracle mirrors it (integrate()).
 // ---------------------------------------------------------------------------
+// Terms of particle p in the 9 wrench sums (anchor-relative m x and inertia).
+__device__ __forceinline__ void wrench_accum(const WrenchArgs& A, int64_t p, const float a[3], float (&acc)[9]) {
+  const float4 x4 = A.pos[p];
+  const float mk = A.vel[p].w;
+  const float pp[3] = {x4.x - a[0], x4.y - a[1], x4.z - a[2]};
+  const float s2 = (pp[0] * pp[0] + pp[1] * pp[1]) + pp[2] * pp[2];
+  acc[0] = acc[0] + mk * pp[0];
+  acc[1] = acc[1] + mk * pp[1];
+  acc[2] = acc[2] + mk * pp[2];
+  acc[3] = acc[3] + mk * (s2 - pp[0] * pp[0]);
+  acc[4] = acc[4] + mk * (s2 - pp[1] * pp[1]);
+  acc[5] = acc[5] + mk * (s2 - pp[2] * pp[2]);
+  acc[6] = acc[6] + -(mk * (pp[0] * pp[1]));
+  acc[7] = acc[7] + -(mk * (pp[0] * pp[2]));
+  acc[8] = acc[8] + -(mk * (pp[1] * pp[2]));
+}
+
+// com, inertia and alpha = pinv(I) tau of body bb from its 9 sums.
+__device__ __forceinline__ void wrench_body_out(const WrenchArgs& A, int bb, const float (&S)[9],
+                                                const BodyProgram& pr) {
+  const float2 mass = A.body_mass[bb];
+  const float M = mass.x, invM = mass.y;
+  const float4 an = A.anchor[bb];
+  float c[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) c[k] = S[k] * invM;
+  float If[6];
+  If[0] = S[3] - M * (c[1] * c[1] + c[2] * c[2]);
+  If[1] = S[4] - M * (c[0] * c[0] + c[2] * c[2]);
+  If[2] = S[5] - M * (c[0] * c[0] + c[1] * c[1]);
+  If[3] = S[6] + M * (c[0] * c[1]);
+  If[4] = S[7] + M * (c[0] * c[2]);
+  If[5] = S[8] + M * (c[1] * c[2]);
+  const float tau[3] = {pr.tx, pr.ty, pr.tz};
+  float al[3];
+  double nax[3];
+  const unsigned e = inertia_solve_f(If, tau, al, nax);
+  if (e) record_error(A.err, e, bb, A.substep_counter, nax);
+  A.wcom[bb] = make_float4(an.x + c[0], an.y + c[1], an.z + c[2], 0.0f);
+  A.walpha[bb] = make_float4(al[0], al[1], al[2], 0.0f);
+}
+
 template <int KP>
 __global__ void __launch_bounds__(kThreads) k_body_wrench(WrenchArgs A) {
   __shared__ float s_part[kWarps][9];
@@ -1357,20 +1716,7 @@ __global__ void __launch_bounds__(kThreads) k_body_wrench(WrenchArgs A) {
     for (int k = 0; k < KP; ++k) {
       const int q = k * 32 * W + wi * 32 + lane;
       if (q >= n) continue;
-      const int64_t p = start + q;
-      const float4 x4 = A.pos[p];
-      const float mk = A.vel[p].w;
-      const float pp[3] = {x4.x - a[0], x4.y - a[1], x4.z - a[2]};
-      const float s2 = (pp[0] * pp[0] + pp[1] * pp[1]) + pp[2] * pp[2];
-      acc[0] = acc[0] + mk * pp[0];
-      acc[1] = acc[1] + mk * pp[1];
-      acc[2] = acc[2] + mk * pp[2];
-      acc[3] = acc[3] + mk * (s2 - pp[0] * pp[0]);
-      acc[4] = acc[4] + mk * (s2 - pp[1] * pp[1]);
-      acc[5] = acc[5] + mk * (s2 - pp[2] * pp[2]);
-      acc[6] = acc[6] + -(mk * (pp[0] * pp[1]));
-      acc[7] = acc[7] + -(mk * (pp[0] * pp[2]));
-      acc[8] = acc[8] + -(mk * (pp[1] * pp[2]));
+      wrench_accum(A, start + q, a, acc);
     }
     warp_butterfly<9>(acc);
     if (lane == 0)
@@ -1389,26 +1735,44 @@ __global__ void __launch_bounds__(kThreads) k_body_wrench(WrenchArgs A) {
   for (int u = 1; u < bd.z; ++u)
 #pragma unroll
     for (int f = 0; f < 9; ++f) S[f] = S[f] + s_part[bd.w + u][f];
-  const float2 mass = A.body_mass[bb];
-  const float M = mass.x, invM = mass.y;
-  const float4 an = A.anchor[bb];
-  float c[3];
+  wrench_body_out(A, bb, S, pr);
+}
+
+
+// Torque prepass of a body larger than one CTA (one CTA per body, looping warps).
+__global__ void __launch_bounds__(kThreads) k_body_wrench_big(WrenchArgs A) {
+  __shared__ float s_part[kBigMaxWarps][9];
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int b = A.big_list[blockIdx.x];
+  const BodyProgram pr = A.programs[b];
+  if (!(pr.flags & 4)) return;  // CTA-uniform
+  const int4 bd = A.body_desc[b];
+  const float4 an = A.anchor[b];
+  const float a[3] = {an.x, an.y, an.z};
+  for (int wi = warp; wi < bd.z; wi += kWarps) {
+    float acc[9];
 #pragma unroll
-  for (int k = 0; k < 3; ++k) c[k] = S[k] * invM;
-  float If[6];
-  If[0] = S[3] - M * (c[1] * c[1] + c[2] * c[2]);
-  If[1] = S[4] - M * (c[0] * c[0] + c[2] * c[2]);
-  If[2] = S[5] - M * (c[0] * c[0] + c[1] * c[1]);
-  If[3] = S[6] + M * (c[0] * c[1]);
-  If[4] = S[7] + M * (c[0] * c[2]);
-  If[5] = S[8] + M * (c[1] * c[2]);
-  const float tau[3] = {pr.tx, pr.ty, pr.tz};
-  float al[3];
-  double nax[3];
-  const unsigned e = inertia_solve_f(If, tau, al, nax);
-  if (e) record_error(A.err, e, bb, A.substep_counter, nax);
-  A.wcom[bb] = make_float4(an.x + c[0], an.y + c[1], an.z + c[2], 0.0f);
-  A.walpha[bb] = make_float4(al[0], al[1], al[2], 0.0f);
+    for (int f = 0; f < 9; ++f) acc[f] = 0.0f;
+#pragma unroll
+    for (int k = 0; k < PBDR_KP_MAX; ++k) {
+      const int q = k * 32 * bd.z + wi * 32 + lane;
+      if (q < bd.y) wrench_accum(A, bd.x + q, a, acc);
+    }
+    warp_butterfly<9>(acc);
+    if (lane == 0)
+#pragma unroll
+      for (int f = 0; f < 9; ++f) s_part[wi][f] = acc[f];
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  float S[9];
+#pragma unroll
+  for (int f = 0; f < 9; ++f) S[f] = s_part[0][f];
+  for (int u = 1; u < bd.z; ++u)
+#pragma unroll
+    for (int f = 0; f < 9; ++f) S[f] = S[f] + s_part[u][f];
+  wrench_body_out(A, b, S, pr);
 }
 
 }  // namespace
@@ -1588,6 +1952,63 @@ void launch_stats(const StatsArgs& a, int ctas, int kp, cudaStream_t s) {
     case 4: k_body_stats<4><<<ctas, kThreads, 0, s>>>(a); break;
     default: k_body_stats<8><<<ctas, kThreads, 0, s>>>(a); break;
   }
+}
+
+// ---- bodies larger than one CTA ---------------------------------------------
+int big_cluster_size(int max_warps) { return (max_warps + kWarps - 1) / kWarps; }
+
+static bool g_big_prepared = false;
+static cudaError_t prepare_big() {
+  if (g_big_prepared) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(k_iteration_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(iteration_smem_bytes(PBDR_KP_MAX)));
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_iteration_big, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  g_big_prepared = e == cudaSuccess;
+  return e;
+}
+
+static cudaLaunchConfig_t big_config(unsigned grid, int cluster, int warps, cudaStream_t s,
+                                     cudaLaunchAttribute* attr) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(32 * warps);
+  cfg.dynamicSmemBytes = sizeof(float4) * 3 * 32 * warps * PBDR_KP_MAX;
+  cfg.stream = s;
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = static_cast<unsigned>(cluster);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cfg;
+}
+
+int big_cta_warps(int max_warps, int cluster) { return (max_warps + cluster - 1) / cluster; }
+
+cudaError_t big_cluster_check(int cluster, int warps) {
+  if (cluster < 1 || cluster > PBDR_MAX_CLUSTER_CTAS || warps < 1 || warps > kWarps) return cudaErrorInvalidValue;
+  cudaError_t e = prepare_big();
+  if (e != cudaSuccess) return e;
+  cudaLaunchAttribute attr[1];
+  cudaLaunchConfig_t cfg = big_config(static_cast<unsigned>(cluster), cluster, warps, nullptr, attr);
+  int active = 0;
+  e = cudaOccupancyMaxActiveClusters(&active, k_iteration_big, &cfg);
+  if (e != cudaSuccess) return e;
+  return active > 0 ? cudaSuccess : cudaErrorInvalidClusterSize;
+}
+
+void launch_iteration_big(const IterArgs& a, int nbig, int cluster, int warps, cudaStream_t s) {
+  cudaLaunchAttribute attr[1];
+  cudaLaunchConfig_t cfg = big_config(static_cast<unsigned>(nbig * cluster), cluster, warps, s, attr);
+  cudaLaunchKernelEx(&cfg, k_iteration_big, a);
+}
+
+void launch_stats_big(const StatsArgs& a, int nbig, cudaStream_t s) {
+  k_body_stats_big<<<nbig, kThreads, 0, s>>>(a);
+}
+
+void launch_wrench_big(const WrenchArgs& a, int nbig, cudaStream_t s) {
+  k_body_wrench_big<<<nbig, kThreads, 0, s>>>(a);
 }
 
 }  // namespace pbdr_dev

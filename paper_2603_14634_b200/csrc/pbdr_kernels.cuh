@@ -49,6 +49,7 @@ struct WrenchArgs {
   float4* walpha;  // per body: alpha (xyz)
   DevError* err;
   const long long* substep_counter;
+  const int* big_list;  // k_body_wrench_big: one CTA per listed body
 };
 
 struct IntegrateArgs {
@@ -186,6 +187,7 @@ struct IterArgs {
   long long* timing;  // optional per-CTA phase clocks (debug), else null
   int ntiles;         // packed CTAs (tiles) of this launch; set by launch_iteration
   int* tile_ctr;      // [2] tile claim counter and finished-CTA counter (self-resetting, zero at create)
+  const int* big_list;  // bodies of more than one CTA (k_iteration_big, one cluster each)
 };
 
 struct StatsArgs {
@@ -198,6 +200,7 @@ struct StatsArgs {
   const int4* body_desc;
   const float2* body_mass;
   double* out;  // 13 doubles per body: com[3], quat[4], P[3], L[3]
+  const int* big_list;  // k_body_stats_big: one CTA per listed body
 };
 
 void launch_integrate(const IntegrateArgs& a, cudaStream_t s);
@@ -220,5 +223,16 @@ void launch_iteration(const IterArgs& a, int ctas, int kp, cudaStream_t s);
 int iteration_coop_capacity(int kp);  // CTAs a cooperative multi-iteration launch may use
 void launch_stats(const StatsArgs& a, int ctas, int kp, cudaStream_t s);
 void launch_wrench(const WrenchArgs& a, int ctas, int kp, cudaStream_t s);
+
+// Bodies larger than one iteration CTA (pbdr_body_warps(n, 8) > 8 warps, up to
+// PBDR_MAX_BODY_PARTICLES_BIG particles): one thread-block cluster of
+// `cluster` CTAs per body (k_iteration_big), and one looping CTA per body for
+// the per-frame statistics and the torque prepass.
+int big_cluster_size(int max_warps);              // CTAs per cluster for bodies of up to max_warps warps
+int big_cta_warps(int max_warps, int cluster);    // warps per CTA (spread evenly over the cluster)
+cudaError_t big_cluster_check(int cluster, int warps);  // cudaSuccess if such clusters can be resident
+void launch_iteration_big(const IterArgs& a, int nbig, int cluster, int warps, cudaStream_t s);
+void launch_stats_big(const StatsArgs& a, int nbig, cudaStream_t s);
+void launch_wrench_big(const WrenchArgs& a, int nbig, cudaStream_t s);
 
 }  // namespace pbdr_dev

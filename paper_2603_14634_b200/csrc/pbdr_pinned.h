@@ -38,7 +38,11 @@
 #ifndef PBDR_CTA_WARPS
 #define PBDR_CTA_WARPS 8          /* warps per iteration CTA                */
 #endif
-#define PBDR_MAX_BODY_PARTICLES (PBDR_KP_MAX * 32 * PBDR_CTA_WARPS) /* 2048 */
+#define PBDR_MAX_BODY_PARTICLES (PBDR_KP_MAX * 32 * PBDR_CTA_WARPS) /* 2048: one CTA */
+/* Larger bodies take a thread-block cluster of up to 16 CTAs (same slot ->
+ * warp map and reduction tree, W up to 128 warps). */
+#define PBDR_MAX_CLUSTER_CTAS 16
+#define PBDR_MAX_BODY_PARTICLES_BIG (PBDR_MAX_BODY_PARTICLES * PBDR_MAX_CLUSTER_CTAS) /* 32768 */
 
 PBDR_HD int pbdr_body_warps(int n, int kp) { return (n + 32 * kp - 1) / (32 * kp); }
 PBDR_HD int pbdr_body_slots(int n, int w) { return (n + 32 * w - 1) / (32 * w); }
@@ -48,7 +52,8 @@ PBDR_HD int pbdr_body_slots(int n, int w) { return (n + 32 * w - 1) / (32 * w); 
  * and want the most parallel layout (KP = 2); scenes of small bodies (mean
  * <= 384 particles) run best with KP = 8 (one warp per body up to 256
  * particles, two CTAs per SM); larger bodies with KP = 4. KP is raised until
- * the largest body fits one CTA. `forced` (scene_desc.tile_kp) overrides. The
+ * the largest body fits one CTA, or to PBDR_KP_MAX when it does not (such a
+ * body runs on a CTA cluster). `forced` (scene_desc.tile_kp) overrides. The
  * oracle applies the same rule, so both sides reduce with the same tree. */
 PBDR_HD int pbdr_choose_kp(long long n_particles, int n_bodies, int max_body, int forced) {
   int kp;

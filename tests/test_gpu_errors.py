@@ -58,7 +58,9 @@ def test_non_finite_state_is_reported(pbdr):
 
 
 def test_oversized_body_is_a_config_error(pbdr):
-    x = _lattice(13, 13, 13)  # 2197 > 2048 particles
+    # Bodies above one CTA run on a cluster of up to 16 CTAs (32768
+    # particles, tests/test_gpu_big_bodies.py); beyond that: ConfigError.
+    x = _lattice(33, 33, 31)  # 33759 > 32768 particles
     sc = P.ArrayScene(**P.rigid_body_arrays([x], 0.01, [1.0]), has_ground=False)
     with pytest.raises(P.ConfigError):
         P.GpuSolver(sc.desc, P.solver_cfg())
