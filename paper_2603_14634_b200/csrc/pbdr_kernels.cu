@@ -1010,7 +1010,7 @@ __device__ __forceinline__ void phase_c_particle(const IterArgs& A, int64_t p, f
 // 0.382 ms per iteration vs 0.436 for KP = 4 at three CTAs per SM (80
 // registers, spills) -- more particles in flight per SM, fewer warps per body.
 template <int KP>
-constexpr int iter_min_blocks() { return KP == 8 ? 2 : 3; }
+constexpr int iter_min_blocks() { return (KP == 8 ? 16 : 24) / kWarps; }  // 16 or 24 resident warps per SM
 
 template <int KP, bool MULTI>
 __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(IterArgs A) {
