@@ -827,6 +827,7 @@ enum ResSlot {
 // Per-body math A from the 21 bsm sums S of body bb (anchor an, 1/M):
 // com c, P_bsm, L_bsm about the predicted com, warm-started polar of Apq;
 // results into R (kRes* slots), new anchor and rotation to global memory.
+template <bool kStore = true>  // false: the caller stores rquat / anchor (after a cluster barrier)
 __device__ __forceinline__ void body_math_a(const IterArgs& A, int bb, const float (&S)[21], float4 an,
                                             float invM, float4 rq4, float* R, float4& rq_new,
                                             float4& an_new) {
@@ -856,9 +857,9 @@ __device__ __forceinline__ void body_math_a(const IterArgs& A, int bb, const flo
                             static_cast<float>(qd[3]))
               : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
   an_new = make_float4(an.x + c[0], an.y + c[1], an.z + c[2], 0.0f);
-  A.rquat[bb] = rq_new;
+  if (kStore) A.rquat[bb] = rq_new;
   if (!ok) record_error(A.err, PBDR_DEVERR_DEGENERATE, bb, A.substep_counter);
-  A.anchor[bb] = an_new;
+  if (kStore) A.anchor[bb] = an_new;
 }
 
 // Phase B of one particle: shape-matching delta (R q0 + c - p, when the polar
@@ -1302,6 +1303,16 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
 // ---------------------------------------------------------------------------
 constexpr int kBigMaxWarps = PBDR_MAX_CLUSTER_CTAS * kWarps;  // 128 warps = 32768 particles
 
+// Cluster barrier without release/acquire semantics: for the barriers that
+// only order execution (every CTA started; no CTA exits while another still
+// reads its shared memory -- those reads have completed, their values were
+// stored to local shared memory before a __syncthreads). The default
+// cluster.sync() releases, which waits for this CTA's outstanding global
+// stores (the phase-C writeback) -- measured as membar stalls.
+__device__ __forceinline__ void cluster_sync_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+}
+
 __global__ void __launch_bounds__(kThreads, 2) k_iteration_big(IterArgs A) {
   constexpr int KP = PBDR_KP_MAX;
   const int nt = blockDim.x;           // 32 * warps per CTA (launch_iteration_big)
@@ -1361,7 +1372,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_iteration_big(IterArgs A) {
     const int q = k * 32 * W + wi * 32 + lane;
     ncs[k] = (live && q < n) ? A.ncand[start + q] : 0;
   }
-  cluster.sync();  // every CTA of the cluster running (DSMEM targets exist), barrier initialised
+  __syncthreads();         // s_res anchor, barrier init (CTA-local ordering)
+  cluster_sync_relaxed();  // every CTA of the cluster running (DSMEM targets exist)
   mbar_wait(&s_bar, 0);
 
   for (int it = 0; it < n_iters; ++it) {
@@ -1404,7 +1416,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_iteration_big(IterArgs A) {
       for (int f = 0; f < 21; ++f) S[f] = s_sum[f];
       const float4 an = make_float4(a[0], a[1], a[2], 0.0f);
       float4 rq_new, an_new;
-      body_math_a(A, b, S, an, A.body_mass[b].y, s_rq, s_res, rq_new, an_new);
+      body_math_a<false>(A, b, S, an, A.body_mass[b].y, s_rq, s_res, rq_new, an_new);
       s_rq = rq_new;
       s_res[kResA] = an_new.x;
       s_res[kResA + 1] = an_new.y;
@@ -1412,6 +1424,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_iteration_big(IterArgs A) {
     }
     cluster.sync();
     if (r != 0 && threadIdx.x < kResF) s_res[threadIdx.x] = lead_res[threadIdx.x];
+    if (r == 0 && threadIdx.x == 0) {  // after the barrier: its release need not wait for them
+      A.rquat[b] = s_rq;
+      A.anchor[b] = make_float4(s_res[kResA], s_res[kResA + 1], s_res[kResA + 2], 0.0f);
+    }
     __syncthreads();
 
     // ---- Phase B ----------------------------------------------------------
@@ -1509,7 +1525,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_iteration_big(IterArgs A) {
         A.vel[start + q] = s_vel[li];
       }
     }
-  cluster.sync();  // the leader's shared memory outlives every remote read
+  cluster_sync_relaxed();  // the leader's shared memory outlives every remote read
 }
 
 // ---------------------------------------------------------------------------

@@ -46,9 +46,10 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--sizes", default="12,13,16,21,26,32")
 ap.add_argument("--target", type=int, default=8_000_000, help="particles per case")
 ap.add_argument("--frames", type=int, default=3)
+ap.add_argument("--case", choices=["single", "pile", "both"], default="both")
 a = ap.parse_args()
 cfg = P.solver_cfg(frame_rate=240.0)
-for pile in (False, True):
+for pile in {"single": (False,), "pile": (True,), "both": (False, True)}[a.case]:
     for n_axis in [int(x) for x in a.sizes.split(",")]:
         sc = scene(n_axis, a.target, pile)
         s = P.GpuSolver(sc.desc, cfg)

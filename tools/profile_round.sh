@@ -17,4 +17,8 @@ ncu --set full --import-source on --clock-control none -k regex:k_iteration -s 4
 ncu --set full --import-source on --clock-control none -k regex:"k_integrate|k_neighbours|k_onesweep|k_body_partners" -s 8 -c 4 -f \
     -o gpurun_out/${TAG}_prologue python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e \
     > gpurun_out/${TAG}_ncu_prologue.log 2>&1
+# The cluster kernel for bodies above one CTA (16^3 boxes touching in rows).
+ncu --set full --import-source on --clock-control none -k regex:k_iteration_big -s 20 -c 1 -f \
+    -o gpurun_out/${TAG}_iteration_big python tools/big_body_bench.py --sizes 16 --case pile --frames 1 \
+    > gpurun_out/${TAG}_ncu_big.log 2>&1 || true
 echo done
