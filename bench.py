@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--scale", type=int, default=0, help="config size knob (0 = BASELINE size)")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--tile-kp", type=int, default=0, help="force the iteration tile shape (2, 4, 8; 0 = automatic)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-slices", type=int, default=4,
@@ -363,6 +364,8 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     g, name, extra = workload(args, rank, world)
+    if args.tile_kp:
+        g.desc.tile_kp = args.tile_kp
     solver = P.GpuSolver(g.desc, g.cfg, device=local)
     n = solver.n
     subs = g.cfg.substeps

@@ -168,6 +168,8 @@ typedef struct pbdr_info {
   float cell_size;            /* h = 2 r_max, fp32 */
   float dt;                   /* fp32 substep */
   int32_t tile_kp;            /* particles per lane of the iteration tiles */
+  int32_t scene_cluster;      /* batched scenes: CTAs per scene cluster running a substep's
+                                 iterations in one launch (0: per-iteration launches) */
 } pbdr_info;
 int pbdr_gpu_info(pbdr_handle* h, pbdr_info* out);
 

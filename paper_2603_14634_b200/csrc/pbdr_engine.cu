@@ -52,6 +52,9 @@ struct pbdr_handle {
   bool has_programs = false;  // any body with a ForceProgram
   bool pairs_possible = true; // some scene holds two or more bodies
   bool coop_iters = true;     // one-wave scenes with pairs: cooperative multi-iteration launch
+  int scene_cluster = 0;      // batched scenes of equal tile count C <= 8: one C-CTA cluster per scene
+                              // runs all iterations of a substep in one launch (0: not applicable)
+  bool cluster_iters = true;  // use scene_cluster when available (PBDR_CLUSTER_ITERS=0 disables)
   bool broadphase = true;     // body-box filter before the hash grid (PBDR_BROADPHASE=0 disables)
   int kp = 4;                 // tile shape: particles per lane (pbdr_choose_kp)
   int per_substep = 0;
@@ -121,6 +124,7 @@ struct pbdr_handle {
   Packing pk_full, pk_iter, pk_active;
   std::vector<int64_t> h_bstart;  // host copy: first slot of each body
   std::vector<int> h_bcount;      // host copy: particles of each body
+  std::vector<int> h_bscene;      // host copy: scene of each body
   int big_cluster = 0;            // CTAs per cluster of the big-body kernel (0: no big body)
   int big_warps = 0;              // warps per CTA of the big-body kernel
 
@@ -385,6 +389,11 @@ void enqueue_substep(pbdr_handle* h, pbdr_dev::LaunchHook* hook) {
   if (hook) hook->after(kHookNeighbours);
 }
 
+// Batched scenes iterate in one launch per substep, one cluster per scene.
+bool use_scene_clusters(const pbdr_handle* h) {
+  return h->scene_cluster > 0 && h->cluster_iters && !h->slab && !h->timing;
+}
+
 void enqueue_iteration(pbdr_handle* h, int iter_index, pbdr_dev::LaunchHook* hook, int n_iters = 1) {
   using namespace pbdr_dev;
   IterArgs it{};
@@ -401,7 +410,8 @@ void enqueue_iteration(pbdr_handle* h, int iter_index, pbdr_dev::LaunchHook* hoo
   it.per_substep = h->per_substep;
   it.iter_index = iter_index;
   it.n_iters = n_iters;
-  it.multi_pairs = (n_iters > 1 && h->pairs_possible) ? 1 : 0;
+  it.multi_pairs = (n_iters > 1 && h->pairs_possible) ? (use_scene_clusters(h) ? 2 : 1) : 0;
+  it.cluster = it.multi_pairs == 2 ? h->scene_cluster : 1;
   it.pos_b[0] = h->pos[h->cur];
   it.pos_b[1] = h->pos[h->cur ^ 1];
   it.last_iter = iter_index + n_iters - 1 == h->iters - 1;
@@ -432,15 +442,19 @@ void enqueue_iteration(pbdr_handle* h, int iter_index, pbdr_dev::LaunchHook* hoo
   h->cur ^= 1;
 }
 
+bool fused_iterations(const pbdr_handle* h) {
+  return !h->slab && (!h->pairs_possible || use_scene_clusters(h) ||
+                      (h->pk_iter.ctas <= pbdr_dev::iteration_coop_capacity(h->kp) && h->coop_iters &&
+                       h->pk_iter.nbig == 0));
+}
+
 void enqueue_substeps(pbdr_handle* h, int64_t count, pbdr_dev::LaunchHook* hook) {
   // Without candidate pairs a body's iterations only read its own particles:
   // one launch runs all of them (state kept in shared memory). With pairs, a
   // scene whose tiles fit in one wave does the same in a cooperative launch
   // with a grid barrier between iterations (small latency-bound scenes) --
   // unless it has bodies larger than one CTA, whose cluster launch is separate.
-  const bool fused_iters =
-      !h->slab && (!h->pairs_possible || (h->pk_iter.ctas <= pbdr_dev::iteration_coop_capacity(h->kp) &&
-                                          h->coop_iters && h->pk_iter.nbig == 0));
+  const bool fused_iters = fused_iterations(h);
   for (int64_t s = 0; s < count; ++s) {
     enqueue_substep(h, hook);
     if (fused_iters)
@@ -507,12 +521,13 @@ int build_graph(pbdr_handle* h, int parity) {
 
 // Packs bodies (ascending ids) into 8-warp CTAs: a body of n particles takes
 // W = ceil(n/(32 kp)) warps; consecutive ids (slot-contiguous in the body-major
-// layout) share a CTA while its warps last. Bodies of more than 8 warps go to
+// layout) of one scene share a CTA while its warps last (a tile never spans
+// two batched scenes, so a scene is a run of whole tiles). Bodies of more than 8 warps go to
 // `big` (one CTA cluster each). bdesc[b] = (first slot, n, W, first warp in the
 // CTA; 0 for big bodies) is written for the listed bodies only.
 void pack_bodies(const std::vector<int>& list, const std::vector<int64_t>& bstart, const std::vector<int>& bcount,
-                 int kp, std::vector<int4>& cdesc, std::vector<int4>& wdesc, std::vector<int4>& bdesc,
-                 std::vector<int>& big) {
+                 const std::vector<int>& bscene, int kp, std::vector<int4>& cdesc, std::vector<int4>& wdesc,
+                 std::vector<int4>& bdesc, std::vector<int>& big) {
   cdesc.clear();
   wdesc.clear();
   big.clear();
@@ -530,7 +545,7 @@ void pack_bodies(const std::vector<int>& list, const std::vector<int64_t>& bstar
       big.push_back(b);
       continue;
     }
-    if (used + W > PBDR_CTA_WARPS || (used > 0 && b != prev + 1)) close();
+    if (used + W > PBDR_CTA_WARPS || (used > 0 && (b != prev + 1 || bscene[b] != bscene[prev]))) close();
     if (used == 0) cdesc.push_back(make_int4(first_slot, 0, b, 0));
     cdesc.back().y += cnt;
     cdesc.back().w += 1;
@@ -616,6 +631,7 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
   h->slot_to_particle.resize(n);
   h->h_bstart.assign(nb, 0);
   h->h_bcount.assign(nb, 0);
+  h->h_bscene.assign(nb, 0);
   double rmax = 0.0;
   int64_t slot = 0;
   for (int32_t b = 0; b < nb; ++b) {
@@ -663,6 +679,7 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
     mass[b] = make_float2(static_cast<float>(d->total_mass[b]), static_cast<float>(1.0 / d->total_mass[b]));
     anchor[b] = make_float4(pos[first_slot].x, pos[first_slot].y, pos[first_slot].z, 0.0f);
     scene[b] = d->body_scene ? d->body_scene[b] : 0;
+    h->h_bscene[b] = scene[b];
     BodyProgram bp{};
     if (d->programs) {
       const pbdr_force_program& p = d->programs[b];
@@ -691,7 +708,7 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
     int max_body = 0;
     for (int32_t b = 0; b < nb; ++b) max_body = std::max(max_body, h->h_bcount[b]);
     h->kp = pbdr_choose_kp(n, nb, max_body, d->tile_kp);
-    pack_bodies(all, h->h_bstart, h->h_bcount, h->kp, cdesc, wdesc, bdesc, big);
+    pack_bodies(all, h->h_bstart, h->h_bcount, h->h_bscene, h->kp, cdesc, wdesc, bdesc, big);
     if (!big.empty()) {
       const int wmax = pbdr_body_warps(max_body, h->kp);
       h->big_cluster = pbdr_dev::big_cluster_size(wmax);
@@ -873,6 +890,33 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
   }
   if (const char* e = std::getenv("PBDR_BROADPHASE")) h->broadphase = std::atoi(e) != 0;
   if (const char* e = std::getenv("PBDR_COOP_ITERS")) h->coop_iters = std::atoi(e) != 0;
+  if (const char* e = std::getenv("PBDR_CLUSTER_ITERS")) h->cluster_iters = std::atoi(e) != 0;
+  if (h->pairs_possible && big.empty() && h->ctas > 0) {
+    // Batched scenes as runs of whole tiles, every scene the same number C of
+    // tiles (C <= 8, a portable cluster) and no scene in two runs: candidates
+    // pair bodies of one scene only (P4), so a C-CTA cluster holds every
+    // particle a scene's iterations read.
+    std::vector<int> run_of_scene;
+    int C = 0, run = 0;
+    bool ok = true;
+    for (int t = 0; t < h->ctas && ok; ++t) {
+      const int b0 = cdesc[t].z, b1 = cdesc[t].z + cdesc[t].w - 1;
+      const int sc = scene[b0];
+      ok = sc >= 0 && scene[b1] == sc;
+      if (!ok) break;
+      if (t > 0 && scene[cdesc[t - 1].z] == sc) {
+        ++run;
+      } else {
+        if (t > 0) ok = C == 0 ? (C = run, true) : run == C;
+        run = 1;
+        if (static_cast<size_t>(sc) >= run_of_scene.size()) run_of_scene.resize(static_cast<size_t>(sc) + 1, 0);
+        ok = ok && run_of_scene[sc]++ == 0;
+      }
+    }
+    if (ok) ok = C == 0 ? (C = run, true) : run == C;
+    if (ok && C >= 1 && C <= 8 && h->ctas % C == 0 && pbdr_dev::iteration_scene_clusters(h->kp, C) > 0)
+      h->scene_cluster = C;
+  }
   h->pk_iter = h->pk_active = h->pk_full;
   if (reset_errors(h) != PBDR_OK) {
     const int code = pbdr_last_error_payload(nullptr, nullptr, nullptr);
@@ -889,7 +933,7 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
   const int torque_l = h->has_torque ? tile_l + big_l : 0;
   h->launches_per_frame = static_cast<int64_t>(h->substeps) *
                           (4 + 2 + torque_l + 1 + 1 + (3 + h->bpasses) + 2 + 4 + (3 + h->passes) + 1 + 1 +
-                           static_cast<int64_t>(h->iters) * (tile_l + big_l));
+                           static_cast<int64_t>(fused_iterations(h) ? 1 : h->iters) * (tile_l + big_l));
   if (!h->pairs_possible)  // single-body scenes: integrate + counter tick + all iterations in one launch
     h->launches_per_frame = static_cast<int64_t>(h->substeps) * (torque_l + 1 + 1 + tile_l + big_l);
   *out = h;
@@ -1109,6 +1153,7 @@ int pbdr_gpu_info(pbdr_handle* h, pbdr_info* o) {
   o->cell_size = h->h;
   o->dt = h->dt;
   o->tile_kp = h->kp;
+  o->scene_cluster = use_scene_clusters(h) ? h->scene_cluster : 0;
   return PBDR_OK;
 }
 
@@ -1370,7 +1415,7 @@ int pbdr_gpu_set_roles(pbdr_handle* h, const int8_t* roles) {
   if (!active.empty())
     PBDR_CUDA(cudaMemcpy(h->active_list, active.data(), sizeof(int) * active.size(), cudaMemcpyHostToDevice));
   auto upload = [&](const std::vector<int>& list, pbdr_handle::Packing& dev) -> int {
-    pack_bodies(list, h->h_bstart, h->h_bcount, h->kp, cd, wd, bd, big);
+    pack_bodies(list, h->h_bstart, h->h_bcount, h->h_bscene, h->kp, cd, wd, bd, big);
     dev.ctas = static_cast<int>(cd.size());
     dev.nbig = static_cast<int>(big.size());
     if (!big.empty())

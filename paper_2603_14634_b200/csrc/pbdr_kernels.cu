@@ -729,6 +729,18 @@ __device__ __forceinline__ void pp_contact(const float x[3], float w, int64_t p,
   }
 }
 
+// Barrier between the iterations of a multi-iteration launch with pairs: the
+// whole grid (cooperative launch, one-wave scenes) or the CTA cluster that
+// holds one batched scene (multi_pairs == 2; candidates never leave a scene,
+// pinned P4). Both release this CTA's X_{i+1} stores (L2) and acquire the
+// others' before the next iteration's gathers.
+__device__ __forceinline__ void multi_barrier(const IterArgs& A) {
+  if (A.multi_pairs == 2)
+    cooperative_groups::this_cluster().sync();
+  else
+    cooperative_groups::this_grid().sync();
+}
+
 // Phase A of one particle (slot p; X_i = x4, V = v4, rest = r4, nc candidates):
 // ground/wall contacts with friction, Jacobi particle contacts, and the
 // particle's terms of the 21 bsm body sums (com, dX, Apq, P_bsm, L_bsm).
@@ -1246,9 +1258,13 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
   }
   }  // live
   }  // fixes
-  if (MULTI && A.multi_pairs && it + 1 < n_iters) cooperative_groups::this_grid().sync();
+  if (MULTI && A.multi_pairs && it + 1 < n_iters) multi_barrier(A);
   }  // iterations of this launch
   if (MULTI) {
+    // With pairs and an even count the last iteration gathered neighbours
+    // from pos_b[1] == pos_out: every CTA of the barrier group must be past
+    // that phase A before the final state overwrites it.
+    if (A.multi_pairs && !(n_iters & 1)) multi_barrier(A);
     __syncthreads();
     if (live)
 #pragma unroll
@@ -1924,7 +1940,28 @@ static void launch_iteration_kp(const IterArgs& a, int ctas, cudaStream_t s) {
   b.ntiles = ctas;
   int grid = ctas;
   if (PBDR_ITER_PERSISTENT && g_iter_grid_cap[KP] > 0 && !a.timing) grid = std::min(ctas, g_iter_grid_cap[KP]);
-  if (a.n_iters > 1 && a.multi_pairs) {
+  if (a.n_iters > 1 && a.multi_pairs == 2) {
+    // Batched scenes: one cluster of a.cluster CTAs per scene (its tiles),
+    // one tile per CTA, iterating together with cluster barriers.
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(ctas));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = iteration_smem_bytes(KP);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = static_cast<unsigned>(a.cluster);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+#ifndef PBDR_CLUSTER_POLICY
+#define PBDR_CLUSTER_POLICY cudaClusterSchedulingPolicySpread
+#endif
+    attr[1].id = cudaLaunchAttributeClusterSchedulingPolicyPreference;
+    attr[1].val.clusterSchedulingPolicyPreference = PBDR_CLUSTER_POLICY;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    cudaLaunchKernelEx(&cfg, k_iteration<KP, true>, b);
+  } else if (a.n_iters > 1 && a.multi_pairs) {
     // One wave of tiles iterating together: grid barriers need a cooperative
     // launch (every CTA resident; the engine checks iteration_coop_capacity).
     cudaLaunchConfig_t cfg{};
@@ -1945,6 +1982,35 @@ static void launch_iteration_kp(const IterArgs& a, int ctas, cudaStream_t s) {
 }
 
 int iteration_coop_capacity(int kp) { return g_iter_coop_cap[kp == 2 ? 2 : (kp == 4 ? 4 : 8)]; }
+
+template <int KP>
+static int scene_clusters_kp(int cluster) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(cluster));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = iteration_smem_bytes(KP);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = static_cast<unsigned>(cluster);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, k_iteration<KP, true>, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int iteration_scene_clusters(int kp, int cluster) {
+  switch (kp) {
+    case 2: return scene_clusters_kp<2>(cluster);
+    case 4: return scene_clusters_kp<4>(cluster);
+    default: return scene_clusters_kp<8>(cluster);
+  }
+}
 
 void launch_iteration(const IterArgs& a, int ctas, int kp, cudaStream_t s) {
   switch (kp) {

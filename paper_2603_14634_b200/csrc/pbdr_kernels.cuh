@@ -180,7 +180,9 @@ struct IterArgs {
   int per_substep;    // MomentumFrequency::kPerSubstep
   int iter_index;     // iteration within the substep
   int n_iters;        // iterations run by this launch (> 1: scenes without pairs, or one-wave cooperative)
-  int multi_pairs;    // n_iters > 1 with contact pairs: cooperative launch, grid barrier per iteration
+  int multi_pairs;    // n_iters > 1 with contact pairs: 1 = cooperative launch, grid barrier per
+                      // iteration; 2 = one cluster per batched scene, cluster barrier per iteration
+  int cluster;        // multi_pairs == 2: CTAs (tiles) per scene cluster
   float4* pos_b[2];   // multi_pairs: the two position buffers (pos_in, pos_out) alternated per iteration
   int last_iter;      // iteration_index == solver_iterations - 1
   float4* mom_acc;    // per body (P, L) accumulators for kPerSubstep
@@ -221,6 +223,7 @@ size_t iteration_smem_bytes(int kp);
 cudaError_t prepare_iteration_kernel();
 void launch_iteration(const IterArgs& a, int ctas, int kp, cudaStream_t s);
 int iteration_coop_capacity(int kp);  // CTAs a cooperative multi-iteration launch may use
+int iteration_scene_clusters(int kp, int cluster);  // resident scene clusters of `cluster` CTAs (0: none)
 void launch_stats(const StatsArgs& a, int ctas, int kp, cudaStream_t s);
 void launch_wrench(const WrenchArgs& a, int ctas, int kp, cudaStream_t s);
 

@@ -107,7 +107,7 @@ class Info(C.Structure):
                 ("hash_bits", C.c_int32), ("sort_passes", C.c_int32),
                 ("launches_per_frame", C.c_int64), ("device_bytes", C.c_int64),
                 ("device", C.c_int32), ("sm_count", C.c_int32), ("cell_size", C.c_float),
-                ("dt", C.c_float), ("tile_kp", C.c_int32)]
+                ("dt", C.c_float), ("tile_kp", C.c_int32), ("scene_cluster", C.c_int32)]
 
 
 _lib = None

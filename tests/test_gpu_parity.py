@@ -391,3 +391,31 @@ def test_one_wave_multi_iteration_path(pbdr, pyoracle, monkeypatch, coop):
     assert_same(gp, op, f"coop={coop} positions")
     assert_same(gv, ov, f"coop={coop} velocities")
     assert gpu.info.launches_per_frame > 0
+
+
+@pytest.mark.parametrize("cluster,kp", [("1", 0), ("1", 8), ("0", 8)])
+def test_scene_cluster_path(pbdr, pyoracle, monkeypatch, cluster, kp):
+    # Batched scenes (config 4) run a substep's iterations in one launch, one
+    # thread-block cluster per scene (its tiles), with a cluster barrier per
+    # iteration; PBDR_CLUSTER_ITERS=0 forces one launch per iteration. Both
+    # equal the oracle bit for bit through body-body and ground contact.
+    monkeypatch.setenv("PBDR_CLUSTER_ITERS", cluster)
+    g = P.GeneratedScene(4, scale=6)
+    g.desc.tile_kp = kp
+    gpu = P.GpuSolver(g.desc, g.cfg)
+    if cluster == "1":
+        # KP = 2 (the small-scene default): 4 warps per cube, 8 tiles per
+        # scene; KP = 8: one warp per cube, 2 tiles per scene.
+        assert gpu.info.scene_cluster == (2 if kp == 8 else 8)
+    else:
+        assert gpu.info.scene_cluster == 0
+    orc = pyoracle.Oracle(g.desc, g.cfg)
+    frames = 100
+    gpu.step_frames(frames)
+    assert orc.step(frames * g.cfg.substeps) == 0
+    gp, gv = gpu.read_f32()
+    op, ov = orc.read_f32()
+    assert_same(gp, op, f"cluster={cluster} kp={kp} positions")
+    assert_same(gv, ov, f"cluster={cluster} kp={kp} velocities")
+    gpu.debug_prologue()
+    assert gpu.debug_candidates()[0].sum() > 0, "expected contacts by now"
