@@ -1195,7 +1195,9 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
         if (MULTI) {
           s_pos[off + q] = make_float4(xa[0], xa[1], xa[2], x4.w);
           s_vel[off + q] = make_float4(va[0], va[1], va[2], v4.w);
-          if (A.multi_pairs && it + 1 < n_iters) __stcg(&A.pos_b[(it + 1) & 1][p], s_pos[off + q]);
+          // Only particles with candidates are gathered by others (the
+          // candidate relation is symmetric, P4), so only they are published.
+          if (A.multi_pairs && it + 1 < n_iters && ncs[k] > 0) __stcg(&A.pos_b[(it + 1) & 1][p], s_pos[off + q]);
         } else {
           A.pos_out[p] = make_float4(xa[0], xa[1], xa[2], x4.w);
           A.vel[p] = make_float4(va[0], va[1], va[2], v4.w);
@@ -1250,7 +1252,7 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
     if (MULTI) {
       s_pos[off + q] = make_float4(xo[0], xo[1], xo[2], x4.w);
       s_vel[off + q] = make_float4(vo[0], vo[1], vo[2], v4.w);
-      if (A.multi_pairs && it + 1 < n_iters) __stcg(&A.pos_b[(it + 1) & 1][p], s_pos[off + q]);
+      if (A.multi_pairs && it + 1 < n_iters && ncs[k] > 0) __stcg(&A.pos_b[(it + 1) & 1][p], s_pos[off + q]);
     } else {
       A.pos_out[p] = make_float4(xo[0], xo[1], xo[2], x4.w);
       A.vel[p] = make_float4(vo[0], vo[1], vo[2], v4.w);
