@@ -51,7 +51,7 @@ def parse():
     ap.add_argument("--tile-kp", type=int, default=0, help="force the iteration tile shape (2, 4, 8; 0 = automatic)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-slices", type=int, default=4,
+    ap.add_argument("--e2e-slices", type=int, default=16,
                     help="batched config: drive the e2e leg as this many handles/streams (1 = one handle)")
     return ap.parse_args()
 

@@ -52,6 +52,8 @@ struct pbdr_handle {
   bool has_programs = false;  // any body with a ForceProgram
   bool pairs_possible = true; // some scene holds two or more bodies
   bool coop_iters = true;     // one-wave scenes with pairs: cooperative multi-iteration launch
+  int2* scene_range = nullptr;  // per body (first body, bodies) of its scene when scenes are contiguous
+                                // runs of <= PBDR_PARTNER_CAP bodies (k_scene_partners), else null
   int scene_cluster = 0;      // batched scenes of equal tile count C <= 8: one C-CTA cluster per scene
                               // runs all iterations of a substep in one launch (0: not applicable)
   bool cluster_iters = true;  // use scene_cluster when available (PBDR_CLUSTER_ITERS=0 disables)
@@ -216,6 +218,9 @@ struct EventHook final : pbdr_dev::LaunchHook {
 };
 
 // Enqueues one substep (integrate .. iterations) on h->stream.
+// Batched scenes of few bodies find partners per scene (no body sort).
+bool scene_partners(const pbdr_handle* h) { return h->scene_range != nullptr && !h->slab; }
+
 void enqueue_substep(pbdr_handle* h, pbdr_dev::LaunchHook* hook) {
   using namespace pbdr_dev;
   IntegrateArgs ia{};
@@ -247,8 +252,9 @@ void enqueue_substep(pbdr_handle* h, pbdr_dev::LaunchHook* hook) {
     cudaMemsetAsync(h->box_min, 0xFF, sizeof(uint32_t) * 3 * h->nb, h->stream);
     cudaMemsetAsync(h->box_max, 0x00, sizeof(uint32_t) * 3 * h->nb, h->stream);
     cudaMemsetAsync(h->oversize, 0x00, sizeof(unsigned), h->stream);
-    cudaMemsetAsync(h->bcells, 0xFF, sizeof(uint2) * (size_t(1) << h->bhash_bits), h->stream);
-    if (hook) hook->after(kHookMemset, 4);
+    if (!scene_partners(h))
+      cudaMemsetAsync(h->bcells, 0xFF, sizeof(uint2) * (size_t(1) << h->bhash_bits), h->stream);
+    if (hook) hook->after(kHookMemset, scene_partners(h) ? 3 : 4);
     // Reset only the buckets the previous substep filled.
     if (hook) hook->before(kHookRanges);
     launch_cell_clear(h->cells, h->keys[h->sorted_buf], h->near_count + 1, h->n, h->stream);
@@ -307,7 +313,12 @@ void enqueue_substep(pbdr_handle* h, pbdr_dev::LaunchHook* hook) {
   ba.max_extent = h->max_extent;
   ba.inflate = h->inflate;
   ba.mask = h->bmask;
-  if (h->broadphase) {
+  ba.scene_range = h->scene_range;
+  if (h->broadphase && scene_partners(h)) {
+    if (hook) hook->before(kHookBroadphase);
+    launch_scene_partners(ba, h->stream);
+    if (hook) hook->after(kHookBroadphase);
+  } else if (h->broadphase) {
     if (hook) hook->before(kHookBroadphase);
     launch_body_keys(ba, h->stream);
     if (hook) hook->after(kHookBroadphase);
@@ -891,6 +902,37 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
   if (const char* e = std::getenv("PBDR_BROADPHASE")) h->broadphase = std::atoi(e) != 0;
   if (const char* e = std::getenv("PBDR_COOP_ITERS")) h->coop_iters = std::atoi(e) != 0;
   if (const char* e = std::getenv("PBDR_CLUSTER_ITERS")) h->cluster_iters = std::atoi(e) != 0;
+  if (h->pairs_possible && d->body_scene) {
+    // Scenes as contiguous body runs of <= PBDR_PARTNER_CAP bodies: partners
+    // are found per scene (k_scene_partners) instead of on the coarse grid.
+    std::vector<int2> rng(nb);
+    std::vector<char> seen;
+    bool ok = true;
+    for (int32_t b = 0; b < nb && ok;) {
+      const int sc = scene[b];
+      int32_t e = b;
+      while (e < nb && scene[e] == sc) ++e;
+      ok = sc >= 0 && e - b <= PBDR_PARTNER_CAP;
+      if (ok) {
+        if (static_cast<size_t>(sc) >= seen.size()) seen.resize(static_cast<size_t>(sc) + 1, 0);
+        ok = !seen[sc];
+        seen[sc] = 1;
+      }
+      for (int32_t i = b; i < e; ++i) rng[i] = make_int2(b, e - b);
+      b = e;
+    }
+    if (ok) {
+      void* p = nullptr;
+      if (cudaMalloc(&p, sizeof(int2) * nb) == cudaSuccess) {
+        h->allocations.push_back(p);
+        h->scene_range = static_cast<int2*>(p);
+        cudaMemcpy(h->scene_range, rng.data(), sizeof(int2) * nb, cudaMemcpyHostToDevice);
+        h->device_bytes += sizeof(int2) * nb;
+      }
+    }
+  }
+  if (const char* e = std::getenv("PBDR_SCENE_PARTNERS"))
+    if (std::atoi(e) == 0) h->scene_range = nullptr;
   if (h->pairs_possible && big.empty() && h->ctas > 0) {
     // Batched scenes as runs of whole tiles, every scene the same number C of
     // tiles (C <= 8, a portable cluster) and no scene in two runs: candidates
@@ -932,7 +974,8 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
   const int tile_l = h->ctas > 0 ? 1 : 0, big_l = big.empty() ? 0 : 1;
   const int torque_l = h->has_torque ? tile_l + big_l : 0;
   h->launches_per_frame = static_cast<int64_t>(h->substeps) *
-                          (4 + 2 + torque_l + 1 + 1 + (3 + h->bpasses) + 2 + 4 + (3 + h->passes) + 1 + 1 +
+                          ((scene_partners(h) ? 3 + 1 : 4 + 1 + (3 + h->bpasses) + 2) + 2 + torque_l + 1 + 4 +
+                           (3 + h->passes) + 1 + 1 +
                            static_cast<int64_t>(fused_iterations(h) ? 1 : h->iters) * (tile_l + big_l));
   if (!h->pairs_possible)  // single-body scenes: integrate + counter tick + all iterations in one launch
     h->launches_per_frame = static_cast<int64_t>(h->substeps) * (torque_l + 1 + 1 + tile_l + big_l);

@@ -216,11 +216,14 @@ __device__ __forceinline__ float ord2f(uint32_t u) {
 __global__ void __launch_bounds__(256) k_integrate_key(IntegrateArgs A) {
   const int64_t p = A.p0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   int b = p < A.n ? A.body_of[p] : -1;
+  // State loads issued with the body id (not after it): the kernel is
+  // latency-bound on these three streams.
+  const float4 x = p < A.n ? A.pos[p] : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+  const float4 v = p < A.n ? A.vel[p] : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
   if (A.role && b >= 0 && A.role[b] == 0) b = -1;  // slab mode: not simulated here
   const bool valid = b >= 0;
   float4 xn = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
   if (valid) {
-    const float4 x = A.pos[p];
     BodyProgram pr{};
     if (A.has_programs) pr = A.programs[b];  // scenes without programs skip the 48-B record
     float a[3] = {0.0f, 0.0f, (pr.flags & 2) ? 0.0f : -A.gravity};
@@ -242,7 +245,6 @@ __global__ void __launch_bounds__(256) k_integrate_key(IntegrateArgs A) {
         a[2] = a[2] + ar[2];
       }
     }
-    const float4 v = A.vel[p];
     A.init[p] = make_float4(x.x, x.y, x.z, 0.0f);
     float4 vn;
     vn.x = v.x + A.dt * a[0];
@@ -260,26 +262,49 @@ __global__ void __launch_bounds__(256) k_integrate_key(IntegrateArgs A) {
     const int32_t cz = pbdr_cell_coord(xn.z, A.inv_h);
     A.key_all[p] = pbdr_cell_hash(cx, cy, cz, static_cast<uint32_t>(A.body_scene[b]), A.mask);
   }
-  // Body boxes of X~: warp-reduce when the whole warp is one body (the common
-  // case in body-major order), else one atomic per lane. min/max are exact and
-  // order-free, so the boxes are deterministic.
+  // Body boxes of X~: warp-reduce when the warp holds at most two bodies, the
+  // first lane's and the last lane's (the common case in body-major order:
+  // a body of >= 32 particles), else one atomic per lane. min/max are exact
+  // and order-free, so the boxes are deterministic.
+  const int lane = threadIdx.x & 31;
   const int b0 = __shfl_sync(kFull, b, 0);
-  const bool uniform = __all_sync(kFull, b == b0) && b0 >= 0;
+  const int b1 = __shfl_sync(kFull, b, 31);
+  const bool two = __all_sync(kFull, b == b0 || b == b1) && b0 >= 0 && b1 >= 0;
   float lo[3] = {xn.x, xn.y, xn.z}, hi[3] = {xn.x, xn.y, xn.z};
-  if (uniform) {
+  if (two) {
+    // Group 0 = lanes of b0, group 1 = lanes of b1 (the same group when
+    // b0 == b1); each lane folds only its own group's values.
+    const bool g1 = b != b0;
+    float lo0[3], hi0[3], lo1[3], hi1[3];
 #pragma unroll
-    for (int off = 16; off >= 1; off >>= 1)
+    for (int c = 0; c < 3; ++c) {
+      lo0[c] = g1 ? INFINITY : lo[c];
+      hi0[c] = g1 ? -INFINITY : hi[c];
+      lo1[c] = g1 ? lo[c] : INFINITY;
+      hi1[c] = g1 ? hi[c] : -INFINITY;
+    }
+    const uint32_t o_lo0[3] = {__reduce_min_sync(kFull, f2ord(lo0[0])), __reduce_min_sync(kFull, f2ord(lo0[1])),
+                               __reduce_min_sync(kFull, f2ord(lo0[2]))};
+    const uint32_t o_hi0[3] = {__reduce_max_sync(kFull, f2ord(hi0[0])), __reduce_max_sync(kFull, f2ord(hi0[1])),
+                               __reduce_max_sync(kFull, f2ord(hi0[2]))};
+    if (lane == 0)
 #pragma unroll
       for (int c = 0; c < 3; ++c) {
-        lo[c] = fminf(lo[c], __shfl_xor_sync(kFull, lo[c], off));
-        hi[c] = fmaxf(hi[c], __shfl_xor_sync(kFull, hi[c], off));
+        atomicMin(&A.box_min[3 * b0 + c], o_lo0[c]);
+        atomicMax(&A.box_max[3 * b0 + c], o_hi0[c]);
       }
-    if ((threadIdx.x & 31) == 0)
+    if (b1 != b0) {
+      const uint32_t o_lo1[3] = {__reduce_min_sync(kFull, f2ord(lo1[0])), __reduce_min_sync(kFull, f2ord(lo1[1])),
+                                 __reduce_min_sync(kFull, f2ord(lo1[2]))};
+      const uint32_t o_hi1[3] = {__reduce_max_sync(kFull, f2ord(hi1[0])), __reduce_max_sync(kFull, f2ord(hi1[1])),
+                                 __reduce_max_sync(kFull, f2ord(hi1[2]))};
+      if (lane == 31)
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        atomicMin(&A.box_min[3 * b0 + c], f2ord(lo[c]));
-        atomicMax(&A.box_max[3 * b0 + c], f2ord(hi[c]));
-      }
+        for (int c = 0; c < 3; ++c) {
+          atomicMin(&A.box_min[3 * b1 + c], o_lo1[c]);
+          atomicMax(&A.box_max[3 * b1 + c], o_hi1[c]);
+        }
+    }
   } else if (valid) {
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
@@ -386,6 +411,36 @@ __global__ void __launch_bounds__(256) k_body_partners(BroadArgs A) {
     count += __popc(m);
   }
   if (lane == 0) A.npartners[b] = count > PBDR_PARTNER_CAP ? -1 : count;
+}
+
+// Batched scenes of at most PBDR_PARTNER_CAP bodies, each scene a contiguous
+// body range: partners by testing every body of the scene (lane l tests body
+// first + l) with the same inflated-box overlap as k_body_partners. One launch
+// replaces the coarse-grid keys, body sort, ranges and partner search; the
+// partner set (all that the near filter uses) is the same.
+__global__ void __launch_bounds__(256) k_scene_partners(BroadArgs A) {
+  const int b = static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (b >= A.nb) return;  // warp-uniform
+  const int2 rng = A.scene_range[b];  // (first body, bodies) of b's scene
+  float lo[3], hi[3];
+  load_box(A.box_min, A.box_max, b, lo, hi);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    lo[k] = lo[k] - (A.inflate + fabsf(lo[k]) * 1e-6f);
+    hi[k] = hi[k] + (A.inflate + fabsf(hi[k]) * 1e-6f);
+  }
+  const int o = rng.x + lane;
+  bool hit = false;
+  if (lane < rng.y && o != b) {
+    float olo[3], ohi[3];
+    load_box(A.box_min, A.box_max, o, olo, ohi);
+    hit = !(olo[0] > hi[0] || ohi[0] < lo[0] || olo[1] > hi[1] || ohi[1] < lo[1] || olo[2] > hi[2] ||
+            ohi[2] < lo[2]);
+  }
+  const unsigned m = __ballot_sync(kFull, hit);
+  if (hit) A.partners[static_cast<int64_t>(b) * PBDR_PARTNER_CAP + __popc(m & ((1u << lane) - 1u))] = o;
+  if (lane == 0) A.npartners[b] = __popc(m);
 }
 
 // ---------------------------------------------------------------------------
@@ -1827,6 +1882,11 @@ void launch_body_keys(const BroadArgs& a, cudaStream_t s) {
 void launch_body_ranges(const BroadArgs& a, cudaStream_t s) {
   if (a.nb == 0) return;
   k_body_ranges<<<(a.nb + 255) / 256, 256, 0, s>>>(a);
+}
+
+void launch_scene_partners(const BroadArgs& a, cudaStream_t s) {
+  if (a.nb <= 0) return;
+  k_scene_partners<<<static_cast<unsigned>((static_cast<int64_t>(a.nb) * 32 + 255) / 256), 256, 0, s>>>(a);
 }
 
 void launch_body_partners(const BroadArgs& a, cudaStream_t s) {

@@ -91,6 +91,7 @@ struct BroadArgs {
   int* partners;       // [nb * PBDR_PARTNER_CAP]
   unsigned* oversize;  // set when a body box exceeds max_extent (disables the skip)
   const int* list;     // slab mode: the active bodies (ascending), else null (all bodies)
+  const int2* scene_range;  // per body: (first body, bodies) of its scene (k_scene_partners)
   int nb;              // bodies in the list (all bodies when list is null)
   float inv_cell;      // 1 / coarse cell
   float max_extent;    // coarse cell - inflation: the largest box the grid guarantees
@@ -209,6 +210,7 @@ void launch_integrate(const IntegrateArgs& a, cudaStream_t s);
 void launch_body_keys(const BroadArgs& a, cudaStream_t s);
 void launch_body_ranges(const BroadArgs& a, cudaStream_t s);
 void launch_body_partners(const BroadArgs& a, cudaStream_t s);
+void launch_scene_partners(const BroadArgs& a, cudaStream_t s);  // batched scenes (scene_range)
 void launch_gather4(float4* dst, const float4* src, const int* idx, int64_t count, cudaStream_t s);
 void launch_scatter4(float4* dst, const float4* src, const int* idx, int64_t count, cudaStream_t s);
 void launch_near(const NearArgs& a, cudaStream_t s);

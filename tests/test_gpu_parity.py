@@ -419,3 +419,22 @@ def test_scene_cluster_path(pbdr, pyoracle, monkeypatch, cluster, kp):
     assert_same(gv, ov, f"cluster={cluster} kp={kp} velocities")
     gpu.debug_prologue()
     assert gpu.debug_candidates()[0].sum() > 0, "expected contacts by now"
+
+
+def test_scene_partners_equal_coarse_grid(pbdr, monkeypatch):
+    # Batched scenes find body partners per scene (k_scene_partners) instead of
+    # on the coarse body grid; the near set and the candidate lists built from
+    # them are identical once bodies touch (config 4, after landing).
+    out = []
+    for flag in ("1", "0"):
+        monkeypatch.setenv("PBDR_SCENE_PARTNERS", flag)
+        g = P.GeneratedScene(4, scale=6)
+        gpu = P.GpuSolver(g.desc, g.cfg)
+        gpu.step_frames(90)
+        gpu.debug_prologue()
+        k, v = gpu.debug_sorted()
+        cnt, lst = gpu.debug_candidates()
+        out.append((np.sort(v), cnt, np.where(np.arange(P.NBR_CAP)[None, :] < cnt[:, None], lst, -1)))
+    assert out[0][1].sum() > 0
+    for a, b, what in zip(out[0], out[1], ("near set", "candidate counts", "candidate lists")):
+        assert_same(a, b, what)
