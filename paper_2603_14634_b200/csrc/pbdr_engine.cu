@@ -57,6 +57,7 @@ struct pbdr_handle {
   int scene_cluster = 0;      // batched scenes of equal tile count C <= 8: one C-CTA cluster per scene
                               // runs all iterations of a substep in one launch (0: not applicable)
   bool cluster_iters = true;  // use scene_cluster when available (PBDR_CLUSTER_ITERS=0 disables)
+  bool fuse_integrate = true; // scene clusters integrate the next substep (PBDR_FUSE_INTEGRATE=0 disables)
   bool broadphase = true;     // body-box filter before the hash grid (PBDR_BROADPHASE=0 disables)
   int kp = 4;                 // tile shape: particles per lane (pbdr_choose_kp)
   int per_substep = 0;
@@ -221,7 +222,12 @@ struct EventHook final : pbdr_dev::LaunchHook {
 // Batched scenes of few bodies find partners per scene (no body sort).
 bool scene_partners(const pbdr_handle* h) { return h->scene_range != nullptr && !h->slab; }
 
-void enqueue_substep(pbdr_handle* h, pbdr_dev::LaunchHook* hook) {
+void reset_boxes(pbdr_handle* h) {
+  cudaMemsetAsync(h->box_min, 0xFF, sizeof(uint32_t) * 3 * h->nb, h->stream);
+  cudaMemsetAsync(h->box_max, 0x00, sizeof(uint32_t) * 3 * h->nb, h->stream);
+}
+
+pbdr_dev::IntegrateArgs integrate_args(const pbdr_handle* h) {
   using namespace pbdr_dev;
   IntegrateArgs ia{};
   ia.pos = h->pos[h->cur];
@@ -246,15 +252,22 @@ void enqueue_substep(pbdr_handle* h, pbdr_dev::LaunchHook* hook) {
   ia.inv_h = h->inv_h;
   ia.dt_d = h->dt_d;
   ia.mask = h->mask;
+  return ia;
+}
+
+// `integrated`: the previous substep's scene-cluster launch already ran this
+// substep's integrate (and reset and filled the body boxes).
+void enqueue_substep(pbdr_handle* h, pbdr_dev::LaunchHook* hook, bool integrated = false) {
+  using namespace pbdr_dev;
+  const IntegrateArgs ia = integrate_args(h);
   const bool pairs = h->pairs_possible || h->slab;
   if (pairs) {
     if (hook) hook->before(kHookMemset);
-    cudaMemsetAsync(h->box_min, 0xFF, sizeof(uint32_t) * 3 * h->nb, h->stream);
-    cudaMemsetAsync(h->box_max, 0x00, sizeof(uint32_t) * 3 * h->nb, h->stream);
+    if (!integrated) reset_boxes(h);
     cudaMemsetAsync(h->oversize, 0x00, sizeof(unsigned), h->stream);
     if (!scene_partners(h))
       cudaMemsetAsync(h->bcells, 0xFF, sizeof(uint2) * (size_t(1) << h->bhash_bits), h->stream);
-    if (hook) hook->after(kHookMemset, scene_partners(h) ? 3 : 4);
+    if (hook) hook->after(kHookMemset, (integrated ? 1 : 3) + (scene_partners(h) ? 0 : 1));
     // Reset only the buckets the previous substep filled.
     if (hook) hook->before(kHookRanges);
     launch_cell_clear(h->cells, h->keys[h->sorted_buf], h->near_count + 1, h->n, h->stream);
@@ -281,9 +294,11 @@ void enqueue_substep(pbdr_handle* h, pbdr_dev::LaunchHook* hook) {
     if (h->pk_active.nbig > 0) launch_wrench_big(wa, h->pk_active.nbig, h->stream);
     if (hook) hook->after(kHookIntegrate, (h->pk_active.ctas > 0 ? 1 : 0) + (h->pk_active.nbig > 0 ? 1 : 0));
   }
-  if (hook) hook->before(kHookIntegrate);
-  launch_integrate(ia, h->stream);
-  if (hook) hook->after(kHookIntegrate);
+  if (!integrated) {
+    if (hook) hook->before(kHookIntegrate);
+    launch_integrate(ia, h->stream);
+    if (hook) hook->after(kHookIntegrate);
+  }
 
   if (!pairs) {
     // Every scene holds a single body: no particle can have a contact
@@ -405,7 +420,8 @@ bool use_scene_clusters(const pbdr_handle* h) {
   return h->scene_cluster > 0 && h->cluster_iters && !h->slab && !h->timing;
 }
 
-void enqueue_iteration(pbdr_handle* h, int iter_index, pbdr_dev::LaunchHook* hook, int n_iters = 1) {
+void enqueue_iteration(pbdr_handle* h, int iter_index, pbdr_dev::LaunchHook* hook, int n_iters = 1,
+                       bool fuse_integrate = false) {
   using namespace pbdr_dev;
   IterArgs it{};
   it.pos_in = h->pos[h->cur];
@@ -423,6 +439,8 @@ void enqueue_iteration(pbdr_handle* h, int iter_index, pbdr_dev::LaunchHook* hoo
   it.n_iters = n_iters;
   it.multi_pairs = (n_iters > 1 && h->pairs_possible) ? (use_scene_clusters(h) ? 2 : 1) : 0;
   it.cluster = it.multi_pairs == 2 ? h->scene_cluster : 1;
+  it.fuse_integrate = fuse_integrate ? 1 : 0;
+  if (fuse_integrate) it.ia = integrate_args(h);
   it.pos_b[0] = h->pos[h->cur];
   it.pos_b[1] = h->pos[h->cur ^ 1];
   it.last_iter = iter_index + n_iters - 1 == h->iters - 1;
@@ -453,6 +471,11 @@ void enqueue_iteration(pbdr_handle* h, int iter_index, pbdr_dev::LaunchHook* hoo
   h->cur ^= 1;
 }
 
+// Torque programs need the k_body_wrench prepass between the substeps.
+bool fuse_next_integrate(const pbdr_handle* h) {
+  return use_scene_clusters(h) && !h->has_torque && h->fuse_integrate;
+}
+
 bool fused_iterations(const pbdr_handle* h) {
   return !h->slab && (!h->pairs_possible || use_scene_clusters(h) ||
                       (h->pk_iter.ctas <= pbdr_dev::iteration_coop_capacity(h->kp) && h->coop_iters &&
@@ -466,12 +489,22 @@ void enqueue_substeps(pbdr_handle* h, int64_t count, pbdr_dev::LaunchHook* hook)
   // with a grid barrier between iterations (small latency-bound scenes) --
   // unless it has bodies larger than one CTA, whose cluster launch is separate.
   const bool fused_iters = fused_iterations(h);
+  bool integrated = false;
   for (int64_t s = 0; s < count; ++s) {
-    enqueue_substep(h, hook);
+    enqueue_substep(h, hook, integrated);
+    // Scene clusters integrate the next substep of this call in their final
+    // writeback (never across calls: the state a call leaves is X, not X~).
+    const bool fuse = fused_iters && fuse_next_integrate(h) && s + 1 < count;
+    if (fuse) {
+      if (hook) hook->before(pbdr_dev::kHookMemset);
+      reset_boxes(h);  // after this substep's broadphase consumed them
+      if (hook) hook->after(pbdr_dev::kHookMemset, 2);
+    }
     if (fused_iters)
-      enqueue_iteration(h, 0, hook, h->iters);
+      enqueue_iteration(h, 0, hook, h->iters, fuse);
     else
       for (int i = 0; i < h->iters; ++i) enqueue_iteration(h, i, hook);
+    integrated = fuse;
   }
 }
 
@@ -902,6 +935,7 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
   if (const char* e = std::getenv("PBDR_BROADPHASE")) h->broadphase = std::atoi(e) != 0;
   if (const char* e = std::getenv("PBDR_COOP_ITERS")) h->coop_iters = std::atoi(e) != 0;
   if (const char* e = std::getenv("PBDR_CLUSTER_ITERS")) h->cluster_iters = std::atoi(e) != 0;
+  if (const char* e = std::getenv("PBDR_FUSE_INTEGRATE")) h->fuse_integrate = std::atoi(e) != 0;
   if (h->pairs_possible && d->body_scene) {
     // Scenes as contiguous body runs of <= PBDR_PARTNER_CAP bodies: partners
     // are found per scene (k_scene_partners) instead of on the coarse grid.
@@ -977,6 +1011,7 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
                           ((scene_partners(h) ? 3 + 1 : 4 + 1 + (3 + h->bpasses) + 2) + 2 + torque_l + 1 + 4 +
                            (3 + h->passes) + 1 + 1 +
                            static_cast<int64_t>(fused_iterations(h) ? 1 : h->iters) * (tile_l + big_l));
+  if (fuse_next_integrate(h)) h->launches_per_frame -= h->substeps - 1;  // integrate inside the cluster launch
   if (!h->pairs_possible)  // single-body scenes: integrate + counter tick + all iterations in one launch
     h->launches_per_frame = static_cast<int64_t>(h->substeps) * (torque_l + 1 + 1 + tile_l + big_l);
   *out = h;

@@ -213,6 +213,51 @@ __device__ __forceinline__ float ord2f(uint32_t u) {
   return __uint_as_float((u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u);
 }
 
+// integrate of one particle of body b:
+// x_init <- x; v~ = v + dt a; x~ = x + dt v~, with a = gravity (unless
+// exempt) + the body's active force program (F/M, alpha x (x - c)). Shared by
+// k_integrate_key and the scene-cluster iteration kernel, which integrates the
+// next substep in its final writeback.
+__device__ __forceinline__ void integrate_one(const IntegrateArgs& A, int b, float4 x, float4 v, float4& xn,
+                                              float4& vn) {
+  BodyProgram pr{};
+  if (A.has_programs) pr = A.programs[b];  // scenes without programs skip the 48-B record
+  float a[3] = {0.0f, 0.0f, (pr.flags & 2) ? 0.0f : -A.gravity};
+  const double t = static_cast<double>(*A.substep_counter) * A.dt_d;
+  if ((pr.flags & 1) && t >= pr.t_start && t < pr.t_stop) {
+    const float invM = A.body_mass[b].y;
+    a[0] = a[0] + pr.fx * invM;
+    a[1] = a[1] + pr.fy * invM;
+    a[2] = a[2] + pr.fz * invM;
+    if (pr.flags & 4) {
+      const float4 c = A.wcom[b];
+      const float4 al = A.walpha[b];
+      const float r[3] = {x.x - c.x, x.y - c.y, x.z - c.z};
+      const float alv[3] = {al.x, al.y, al.z};
+      float ar[3];
+      cross3(alv, r, ar);
+      a[0] = a[0] + ar[0];
+      a[1] = a[1] + ar[1];
+      a[2] = a[2] + ar[2];
+    }
+  }
+  vn.x = v.x + A.dt * a[0];
+  vn.y = v.y + A.dt * a[1];
+  vn.z = v.z + A.dt * a[2];
+  vn.w = v.w;
+  xn.x = x.x + A.dt * vn.x;
+  xn.y = x.y + A.dt * vn.y;
+  xn.z = x.z + A.dt * vn.z;
+  xn.w = x.w;
+}
+
+__device__ __forceinline__ uint32_t integrate_key(const IntegrateArgs& A, int b, float4 xn) {
+  const int32_t cx = pbdr_cell_coord(xn.x, A.inv_h);
+  const int32_t cy = pbdr_cell_coord(xn.y, A.inv_h);
+  const int32_t cz = pbdr_cell_coord(xn.z, A.inv_h);
+  return pbdr_cell_hash(cx, cy, cz, static_cast<uint32_t>(A.body_scene[b]), A.mask);
+}
+
 __global__ void __launch_bounds__(256) k_integrate_key(IntegrateArgs A) {
   const int64_t p = A.p0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   int b = p < A.n ? A.body_of[p] : -1;
@@ -224,43 +269,12 @@ __global__ void __launch_bounds__(256) k_integrate_key(IntegrateArgs A) {
   const bool valid = b >= 0;
   float4 xn = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
   if (valid) {
-    BodyProgram pr{};
-    if (A.has_programs) pr = A.programs[b];  // scenes without programs skip the 48-B record
-    float a[3] = {0.0f, 0.0f, (pr.flags & 2) ? 0.0f : -A.gravity};
-    const double t = static_cast<double>(*A.substep_counter) * A.dt_d;
-    if ((pr.flags & 1) && t >= pr.t_start && t < pr.t_stop) {
-      const float invM = A.body_mass[b].y;
-      a[0] = a[0] + pr.fx * invM;
-      a[1] = a[1] + pr.fy * invM;
-      a[2] = a[2] + pr.fz * invM;
-      if (pr.flags & 4) {
-        const float4 c = A.wcom[b];
-        const float4 al = A.walpha[b];
-        const float r[3] = {x.x - c.x, x.y - c.y, x.z - c.z};
-        const float alv[3] = {al.x, al.y, al.z};
-        float ar[3];
-        cross3(alv, r, ar);
-        a[0] = a[0] + ar[0];
-        a[1] = a[1] + ar[1];
-        a[2] = a[2] + ar[2];
-      }
-    }
-    A.init[p] = make_float4(x.x, x.y, x.z, 0.0f);
     float4 vn;
-    vn.x = v.x + A.dt * a[0];
-    vn.y = v.y + A.dt * a[1];
-    vn.z = v.z + A.dt * a[2];
-    vn.w = v.w;
-    xn.x = x.x + A.dt * vn.x;
-    xn.y = x.y + A.dt * vn.y;
-    xn.z = x.z + A.dt * vn.z;
-    xn.w = x.w;
+    integrate_one(A, b, x, v, xn, vn);
+    A.init[p] = make_float4(x.x, x.y, x.z, 0.0f);
     A.vel[p] = vn;
     A.pos[p] = xn;
-    const int32_t cx = pbdr_cell_coord(xn.x, A.inv_h);
-    const int32_t cy = pbdr_cell_coord(xn.y, A.inv_h);
-    const int32_t cz = pbdr_cell_coord(xn.z, A.inv_h);
-    A.key_all[p] = pbdr_cell_hash(cx, cy, cz, static_cast<uint32_t>(A.body_scene[b]), A.mask);
+    A.key_all[p] = integrate_key(A, b, xn);
   }
   // Body boxes of X~: warp-reduce when the warp holds at most two bodies, the
   // first lane's and the last lane's (the common case in body-major order:
@@ -1323,7 +1337,43 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
     // that phase A before the final state overwrites it.
     if (A.multi_pairs && !(n_iters & 1)) multi_barrier(A);
     __syncthreads();
-    if (live)
+    if (live && A.fuse_integrate) {
+      // Next substep's integrate on the final state (the same arithmetic as
+      // k_integrate_key): X~ and V~ go out instead of X and V, X_init = X,
+      // the cell keys, and the body box from one warp reduction per warp.
+      uint32_t lo[3] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu}, hi[3] = {0u, 0u, 0u};
+#pragma unroll
+      for (int k = 0; k < KP; ++k) {
+        const int q = k * 32 * W + wi * 32 + lane;
+        if (q < n) {
+          const int64_t p = start + q;
+          const float4 x4 = s_pos[off + q];
+          float4 xn, vn;
+          integrate_one(A.ia, b, x4, s_vel[off + q], xn, vn);
+          A.ia.init[p] = make_float4(x4.x, x4.y, x4.z, 0.0f);
+          A.pos_out[p] = xn;
+          A.vel[p] = vn;
+          A.ia.key_all[p] = integrate_key(A.ia, b, xn);
+          const uint32_t o[3] = {f2ord(xn.x), f2ord(xn.y), f2ord(xn.z)};
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            lo[c] = min(lo[c], o[c]);
+            hi[c] = max(hi[c], o[c]);
+          }
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        lo[c] = __reduce_min_sync(kFull, lo[c]);
+        hi[c] = __reduce_max_sync(kFull, hi[c]);
+      }
+      if (lane == 0)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          atomicMin(&A.ia.box_min[3 * b + c], lo[c]);
+          atomicMax(&A.ia.box_max[3 * b + c], hi[c]);
+        }
+    } else if (live) {
 #pragma unroll
       for (int k = 0; k < KP; ++k) {
         const int q = k * 32 * W + wi * 32 + lane;
@@ -1332,6 +1382,7 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
           A.vel[start + q] = s_vel[off + q];
         }
       }
+    }
   }
   if (tm && threadIdx.x == 0) {
     tm[6] = clock64();

@@ -184,6 +184,9 @@ struct IterArgs {
   int multi_pairs;    // n_iters > 1 with contact pairs: 1 = cooperative launch, grid barrier per
                       // iteration; 2 = one cluster per batched scene, cluster barrier per iteration
   int cluster;        // multi_pairs == 2: CTAs (tiles) per scene cluster
+  int fuse_integrate; // multi-iteration launch: the final writeback also integrates the next
+                      // substep (writes X~, V~, X_init, cell keys, body boxes) with `ia`
+  IntegrateArgs ia;
   float4* pos_b[2];   // multi_pairs: the two position buffers (pos_in, pos_out) alternated per iteration
   int last_iter;      // iteration_index == solver_iterations - 1
   float4* mom_acc;    // per body (P, L) accumulators for kPerSubstep

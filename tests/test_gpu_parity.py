@@ -393,13 +393,16 @@ def test_one_wave_multi_iteration_path(pbdr, pyoracle, monkeypatch, coop):
     assert gpu.info.launches_per_frame > 0
 
 
-@pytest.mark.parametrize("cluster,kp", [("1", 0), ("1", 8), ("0", 8)])
-def test_scene_cluster_path(pbdr, pyoracle, monkeypatch, cluster, kp):
+@pytest.mark.parametrize("cluster,kp,fuse", [("1", 0, "1"), ("1", 8, "1"), ("1", 8, "0"), ("0", 8, "1")])
+def test_scene_cluster_path(pbdr, pyoracle, monkeypatch, cluster, kp, fuse):
     # Batched scenes (config 4) run a substep's iterations in one launch, one
     # thread-block cluster per scene (its tiles), with a cluster barrier per
-    # iteration; PBDR_CLUSTER_ITERS=0 forces one launch per iteration. Both
-    # equal the oracle bit for bit through body-body and ground contact.
+    # iteration, and integrate the next substep of the frame in the final
+    # writeback; PBDR_CLUSTER_ITERS=0 forces one launch per iteration,
+    # PBDR_FUSE_INTEGRATE=0 the separate integrate kernel. All equal the
+    # oracle bit for bit through body-body and ground contact.
     monkeypatch.setenv("PBDR_CLUSTER_ITERS", cluster)
+    monkeypatch.setenv("PBDR_FUSE_INTEGRATE", fuse)
     g = P.GeneratedScene(4, scale=6)
     g.desc.tile_kp = kp
     gpu = P.GpuSolver(g.desc, g.cfg)
@@ -415,8 +418,8 @@ def test_scene_cluster_path(pbdr, pyoracle, monkeypatch, cluster, kp):
     assert orc.step(frames * g.cfg.substeps) == 0
     gp, gv = gpu.read_f32()
     op, ov = orc.read_f32()
-    assert_same(gp, op, f"cluster={cluster} kp={kp} positions")
-    assert_same(gv, ov, f"cluster={cluster} kp={kp} velocities")
+    assert_same(gp, op, f"cluster={cluster} kp={kp} fuse={fuse} positions")
+    assert_same(gv, ov, f"cluster={cluster} kp={kp} fuse={fuse} velocities")
     gpu.debug_prologue()
     assert gpu.debug_candidates()[0].sum() > 0, "expected contacts by now"
 
@@ -438,3 +441,28 @@ def test_scene_partners_equal_coarse_grid(pbdr, monkeypatch):
     assert out[0][1].sum() > 0
     for a, b, what in zip(out[0], out[1], ("near set", "candidate counts", "candidate lists")):
         assert_same(a, b, what)
+
+
+def test_scene_cluster_force_programs(pbdr, pyoracle):
+    # Force programs (no torque) on batched scenes keep the fused path: the
+    # next substep's integrate inside the cluster launch applies F/M, gravity
+    # exemption and the [t_start, t_stop) window (it opens and closes inside
+    # the first frame) exactly as the integrate kernel does.
+    g = P.GeneratedScene(4, scale=4)
+    rng = np.random.default_rng(5)
+    progs = []
+    for b in range(g.desc.num_bodies):
+        kind = b % 4
+        F = tuple(rng.uniform(-3, 3, 3)) if kind in (1, 3) else (0.0, 0.0, 0.0)
+        t0, t1 = (0.0015, 0.0032) if kind == 3 else (0.0, float("inf"))
+        progs.append(P.ForceProgram(F, (0.0, 0.0, 0.0), t0, t1, int(kind == 2), 0))
+    sc = P.scene_with_programs(g, progs)
+    gpu = P.GpuSolver(sc.desc, g.cfg)
+    assert gpu.info.scene_cluster > 0
+    orc = pyoracle.Oracle(sc.desc, g.cfg)
+    gpu.step_frames(3)
+    assert orc.step(3 * g.cfg.substeps) == 0
+    gp, gv = gpu.read_f32()
+    op, ov = orc.read_f32()
+    assert_same(gp, op, "positions")
+    assert_same(gv, ov, "velocities")
