@@ -1186,7 +1186,9 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
   for (int it = 0; it < n_iters; ++it) {
   const int iter_index = A.iter_index + it;
   const int last_iter = MULTI ? (A.last_iter && it == n_iters - 1) : A.last_iter;
-  if (it > 0) __syncthreads();  // previous iteration's state and table in smem
+  // Previous iteration's state and table in smem (the grid / cluster barrier
+  // that ended it already synchronised this CTA).
+  if (it > 0 && !A.multi_pairs) __syncthreads();
   float a[3];
   {
     const float4 an = s_tanc[tb][lb];
