@@ -58,6 +58,10 @@ struct pbdr_handle {
                               // runs all iterations of a substep in one launch (0: not applicable)
   bool cluster_iters = true;  // use scene_cluster when available (PBDR_CLUSTER_ITERS=0 disables)
   bool fuse_integrate = true; // scene clusters integrate the next substep (PBDR_FUSE_INTEGRATE=0 disables)
+  bool split_iso = true;      // isolated tiles iterate in one launch (PBDR_SPLIT_ISOLATED=0 disables)
+  int* iso_list = nullptr;    // [ctas] isolated tiles of the current substep
+  int* contact_list = nullptr;  // [ctas] the other tiles
+  int* tile_counts = nullptr;   // [2] sizes of the two lists (device)
   bool broadphase = true;     // body-box filter before the hash grid (PBDR_BROADPHASE=0 disables)
   int kp = 4;                 // tile shape: particles per lane (pbdr_choose_kp)
   int per_substep = 0;
@@ -420,10 +424,14 @@ bool use_scene_clusters(const pbdr_handle* h) {
   return h->scene_cluster > 0 && h->cluster_iters && !h->slab && !h->timing;
 }
 
+// `list`/`count`: iterate only the tiles of a device-side list (the contact
+// tiles of this substep) instead of every tile.
 void enqueue_iteration(pbdr_handle* h, int iter_index, pbdr_dev::LaunchHook* hook, int n_iters = 1,
-                       bool fuse_integrate = false) {
+                       bool fuse_integrate = false, const int* list = nullptr, const int* count = nullptr) {
   using namespace pbdr_dev;
   IterArgs it{};
+  it.tile_list = list;
+  it.tile_count = count;
   it.pos_in = h->pos[h->cur];
   it.pos_out = h->pos[h->cur ^ 1];
   it.vel = h->vel;
@@ -437,7 +445,9 @@ void enqueue_iteration(pbdr_handle* h, int iter_index, pbdr_dev::LaunchHook* hoo
   it.per_substep = h->per_substep;
   it.iter_index = iter_index;
   it.n_iters = n_iters;
-  it.multi_pairs = (n_iters > 1 && h->pairs_possible) ? (use_scene_clusters(h) ? 2 : 1) : 0;
+  const bool isolated = n_iters > 1 && list != nullptr;  // enqueue_isolated
+  it.multi_pairs = (n_iters > 1 && h->pairs_possible && !isolated) ? (use_scene_clusters(h) ? 2 : 1) : 0;
+  if (isolated) it.pos_out = h->pos[h->cur ^ (n_iters & 1)];
   it.cluster = it.multi_pairs == 2 ? h->scene_cluster : 1;
   it.fuse_integrate = fuse_integrate ? 1 : 0;
   if (fuse_integrate) it.ia = integrate_args(h);
@@ -466,9 +476,41 @@ void enqueue_iteration(pbdr_handle* h, int iter_index, pbdr_dev::LaunchHook* hoo
   if (h->pk_iter.ctas > 0) launch_iteration(it, h->pk_iter.ctas, h->kp, h->stream);
   // Bodies larger than one CTA: one cluster each, same iteration semantics
   // (they read pos_in and write pos_out / vel of their own slots only).
-  if (h->pk_iter.nbig > 0) launch_iteration_big(it, h->pk_iter.nbig, h->big_cluster, h->big_warps, h->stream);
-  if (hook) hook->after(kHookIteration, (h->pk_iter.ctas > 0 ? 1 : 0) + (h->pk_iter.nbig > 0 ? 1 : 0));
+  const bool big = h->pk_iter.nbig > 0 && !isolated;
+  if (big) launch_iteration_big(it, h->pk_iter.nbig, h->big_cluster, h->big_warps, h->stream);
+  if (hook) hook->after(kHookIteration, (h->pk_iter.ctas > 0 ? 1 : 0) + (big ? 1 : 0));
   h->cur ^= 1;
+}
+
+// Isolated tiles (no body with a partner this substep) iterate all of the
+// substep's iterations in one launch, state in shared memory; the contact
+// tiles then iterate launch by launch. Both write only their own slots and no
+// contact tile gathers a particle of an isolated one (pairs are symmetric),
+// so the split changes no result. The isolated launch leaves its final state
+// in the buffer the contact launches end in (they flip it per iteration).
+void enqueue_isolated(pbdr_handle* h, pbdr_dev::LaunchHook* hook) {
+  using namespace pbdr_dev;
+  if (hook) hook->before(kHookMemset);
+  cudaMemsetAsync(h->tile_counts, 0, 2 * sizeof(int), h->stream);
+  if (hook) hook->after(kHookMemset);
+  ClassifyArgs ca{};
+  ca.cta_desc = h->pk_iter.cta;
+  ca.npartners = h->npartners;
+  ca.iso_list = h->iso_list;
+  ca.contact_list = h->contact_list;
+  ca.counts = h->tile_counts;
+  ca.ntiles = h->pk_iter.ctas;
+  if (hook) hook->before(kHookBroadphase);
+  launch_classify_tiles(ca, h->stream);
+  if (hook) hook->after(kHookBroadphase);
+  const int cur = h->cur;
+  enqueue_iteration(h, 0, hook, h->iters, false, h->iso_list, h->tile_counts);
+  h->cur = cur;
+}
+
+bool split_isolated(const pbdr_handle* h) {
+  return h->split_iso && !h->slab && h->pairs_possible && h->broadphase && h->pk_iter.ctas > 0 &&
+         h->iso_list != nullptr;
 }
 
 // Torque programs need the k_body_wrench prepass between the substeps.
@@ -500,10 +542,15 @@ void enqueue_substeps(pbdr_handle* h, int64_t count, pbdr_dev::LaunchHook* hook)
       reset_boxes(h);  // after this substep's broadphase consumed them
       if (hook) hook->after(pbdr_dev::kHookMemset, 2);
     }
-    if (fused_iters)
+    if (fused_iters) {
       enqueue_iteration(h, 0, hook, h->iters, fuse);
-    else
+    } else if (split_isolated(h)) {
+      enqueue_isolated(h, hook);
+      for (int i = 0; i < h->iters; ++i)
+        enqueue_iteration(h, i, hook, 1, false, h->contact_list, h->tile_counts + 1);
+    } else {
       for (int i = 0; i < h->iters; ++i) enqueue_iteration(h, i, hook);
+    }
     integrated = fuse;
   }
 }
@@ -936,6 +983,17 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
   if (const char* e = std::getenv("PBDR_COOP_ITERS")) h->coop_iters = std::atoi(e) != 0;
   if (const char* e = std::getenv("PBDR_CLUSTER_ITERS")) h->cluster_iters = std::atoi(e) != 0;
   if (const char* e = std::getenv("PBDR_FUSE_INTEGRATE")) h->fuse_integrate = std::atoi(e) != 0;
+  if (const char* e = std::getenv("PBDR_SPLIT_ISOLATED")) h->split_iso = std::atoi(e) != 0;
+  if (h->ctas > 0) {
+    int rc2 = dalloc(h, &h->iso_list, static_cast<size_t>(h->ctas));
+    rc2 |= dalloc(h, &h->contact_list, static_cast<size_t>(h->ctas));
+    rc2 |= dalloc(h, &h->tile_counts, 2);
+    if (rc2 != PBDR_OK) {
+      const int code = pbdr_last_error_payload(nullptr, nullptr, nullptr);
+      release(h);
+      return code ? code : PBDR_ERR_CUDA;
+    }
+  }
   if (h->pairs_possible && d->body_scene) {
     // Scenes as contiguous body runs of <= PBDR_PARTNER_CAP bodies: partners
     // are found per scene (k_scene_partners) instead of on the coarse grid.
@@ -1012,6 +1070,8 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
                            (3 + h->passes) + 1 + 1 +
                            static_cast<int64_t>(fused_iterations(h) ? 1 : h->iters) * (tile_l + big_l));
   if (fuse_next_integrate(h)) h->launches_per_frame -= h->substeps - 1;  // integrate inside the cluster launch
+  if (h->pairs_possible && !fused_iterations(h) && split_isolated(h))
+    h->launches_per_frame += static_cast<int64_t>(h->substeps) * 3;  // counts memset, classify, isolated launch
   if (!h->pairs_possible)  // single-body scenes: integrate + counter tick + all iterations in one launch
     h->launches_per_frame = static_cast<int64_t>(h->substeps) * (torque_l + 1 + 1 + tile_l + big_l);
   *out = h;

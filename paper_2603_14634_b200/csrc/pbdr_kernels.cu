@@ -457,6 +457,24 @@ __global__ void __launch_bounds__(256) k_scene_partners(BroadArgs A) {
   if (lane == 0) A.npartners[b] = __popc(m);
 }
 
+// Isolated tiles: every body of the tile has no partner this substep (so no
+// particle of it has a candidate, and none is anyone's candidate: pairs are
+// symmetric). They run all iterations of the substep in one launch with the
+// state in shared memory; the other (contact) tiles iterate launch by
+// launch. Lists are built with atomics: tiles are independent, so their
+// order changes nothing.
+__global__ void __launch_bounds__(256) k_classify_tiles(ClassifyArgs A) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= A.ntiles) return;
+  const int4 cd = A.cta_desc[t];
+  bool iso = true;
+  for (int i = 0; i < cd.w && iso; ++i) iso = A.npartners[cd.z + i] == 0;
+  if (iso)
+    A.iso_list[atomicAdd(&A.counts[0], 1)] = t;
+  else
+    A.contact_list[atomicAdd(&A.counts[1], 1)] = t;
+}
+
 // ---------------------------------------------------------------------------
 // cell ranges: per-bucket (start, end) of the sorted array and the body of
 // every sorted entry (slots ascend within a bucket, so bodies do too).
@@ -1119,8 +1137,11 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
   const bool fixes = A.linfix || A.angfix;
   const long long t_entry = A.timing ? clock64() : 0;  // phase clocks (debug launches only)
   // One CTA per tile (grid == ntiles): static; otherwise tiles are claimed
-  // dynamically, in increasing order.
-  const bool dynamic = static_cast<int>(gridDim.x) < A.ntiles;
+  // dynamically, in increasing order. With a device-side tile list (isolated /
+  // contact tiles of this substep) claim c is tile tile_list[c] of tile_count.
+  const int ntiles = A.tile_count ? *A.tile_count : A.ntiles;
+  const bool dynamic = A.tile_count != nullptr || static_cast<int>(gridDim.x) < ntiles;
+  auto tid = [&](int c) { return A.tile_list ? A.tile_list[c] : c; };
   if (threadIdx.x == 0) {
     mbar_init(&s_bar, 1);
     s_next = dynamic ? atomicAdd(A.tile_ctr, 1) : static_cast<int>(blockIdx.x);
@@ -1129,9 +1150,10 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
   int tile = s_next;
   int tb = 0;  // table buffer of the current tile
   int4 cd_n = make_int4(0, 0, 0, 0), wd_n = make_int4(-1, 0, 0, 1 << 16);
-  if (tile < A.ntiles) {
-    cd_n = ld_keep_nc(&A.cta_desc[tile]);
-    wd_n = ld_keep_nc(&A.warp_desc[tile * kWarps + warp]);
+  if (tile < ntiles) {
+    const int t0 = tid(tile);
+    cd_n = ld_keep_nc(&A.cta_desc[t0]);
+    wd_n = ld_keep_nc(&A.warp_desc[t0 * kWarps + warp]);
     if (warp == 0 && lane < cd_n.w) {  // first tile's table: synchronous
       const int bb = cd_n.z + lane;
       s_tdesc[0][lane] = ld_keep_nc(&A.body_desc[bb]);
@@ -1140,7 +1162,7 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
       s_trq[0][lane] = ld_keep(&A.rquat[bb]);
     }
   }
-  for (uint32_t it_parity = 0; tile < A.ntiles; it_parity ^= 1u) {
+  for (uint32_t it_parity = 0; tile < ntiles; it_parity ^= 1u) {
   const int4 cd = cd_n;  // first slot, slot count, first body, bodies
   const int4 wd = wd_n;
   const int first = cd.x;
@@ -1151,7 +1173,7 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
     bulk_g2s_stream(s_pos, A.pos_in + first, bytes, &s_bar);
     bulk_g2s_stream(s_vel, A.vel + first, bytes, &s_bar);
     bulk_g2s_stream(s_rest, A.rest + first, bytes, &s_bar);
-    s_next = dynamic ? atomicAdd(A.tile_ctr, 1) : A.ntiles;  // the tile after this one
+    s_next = dynamic ? atomicAdd(A.tile_ctr, 1) : ntiles;  // the tile after this one
   }
   cp_async_wait_all();  // this tile's table (prefetched during the previous tile)
 
@@ -1172,9 +1194,10 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
   if (tm && threadIdx.x == 0) tm[0] = t_entry;  // CTA entry: stage = descriptors + table + bulk copies
   __syncthreads();  // barrier initialised, per-body table filled, next tile claimed
   const int tile_next = s_next;
-  if (tile_next < A.ntiles) {  // next tile's descriptors, consumed at its start
-    cd_n = ld_keep_nc(&A.cta_desc[tile_next]);
-    wd_n = ld_keep_nc(&A.warp_desc[tile_next * kWarps + warp]);
+  if (tile_next < ntiles) {  // next tile's descriptors, consumed at its start
+    const int t1 = tid(tile_next);
+    cd_n = ld_keep_nc(&A.cta_desc[t1]);
+    wd_n = ld_keep_nc(&A.warp_desc[t1 * kWarps + warp]);
   }
   mbar_wait(&s_bar, it_parity);
   if (tm && threadIdx.x == 0) tm[1] = clock64();
@@ -1392,7 +1415,7 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
     tm[7] = smid;
   }
-  if (tile_next < A.ntiles && warp == 0 && lane < cd_n.w) {
+  if (tile_next < ntiles && warp == 0 && lane < cd_n.w) {
     const int bb = cd_n.z + lane;
     cp_async16(&s_tdesc[tb ^ 1][lane], &A.body_desc[bb]);
     cp_async16(&s_tanc[tb ^ 1][lane], &A.anchor[bb]);
@@ -1937,6 +1960,11 @@ void launch_body_ranges(const BroadArgs& a, cudaStream_t s) {
   k_body_ranges<<<(a.nb + 255) / 256, 256, 0, s>>>(a);
 }
 
+void launch_classify_tiles(const ClassifyArgs& a, cudaStream_t s) {
+  if (a.ntiles <= 0) return;
+  k_classify_tiles<<<(a.ntiles + 255) / 256, 256, 0, s>>>(a);
+}
+
 void launch_scene_partners(const BroadArgs& a, cudaStream_t s) {
   if (a.nb <= 0) return;
   k_scene_partners<<<static_cast<unsigned>((static_cast<int64_t>(a.nb) * 32 + 255) / 256), 256, 0, s>>>(a);
@@ -2055,6 +2083,7 @@ static void launch_iteration_kp(const IterArgs& a, int ctas, cudaStream_t s) {
   b.ntiles = ctas;
   int grid = ctas;
   if (PBDR_ITER_PERSISTENT && g_iter_grid_cap[KP] > 0 && !a.timing) grid = std::min(ctas, g_iter_grid_cap[KP]);
+  if (a.tile_count && g_iter_grid_cap[KP] > 0) grid = std::min(ctas, g_iter_grid_cap[KP]);  // count on the device
   if (a.n_iters > 1 && a.multi_pairs == 2) {
     // Batched scenes: one cluster of a.cluster CTAs per scene (its tiles),
     // one tile per CTA, iterating together with cluster barriers.

@@ -184,6 +184,8 @@ struct IterArgs {
   int multi_pairs;    // n_iters > 1 with contact pairs: 1 = cooperative launch, grid barrier per
                       // iteration; 2 = one cluster per batched scene, cluster barrier per iteration
   int cluster;        // multi_pairs == 2: CTAs (tiles) per scene cluster
+  const int* tile_list;   // optional: claim c processes tile tile_list[c] ...
+  const int* tile_count;  // ... of a device-side count (isolated / contact tiles), else null
   int fuse_integrate; // multi-iteration launch: the final writeback also integrates the next
                       // substep (writes X~, V~, X_init, cell keys, body boxes) with `ia`
   IntegrateArgs ia;
@@ -194,6 +196,15 @@ struct IterArgs {
   int ntiles;         // packed CTAs (tiles) of this launch; set by launch_iteration
   int* tile_ctr;      // [2] tile claim counter and finished-CTA counter (self-resetting, zero at create)
   const int* big_list;  // bodies of more than one CTA (k_iteration_big, one cluster each)
+};
+
+struct ClassifyArgs {
+  const int4* cta_desc;   // tiles of the iteration packing
+  const int* npartners;   // per body (-1: overflow, searched in full)
+  int* iso_list;          // tiles whose bodies all have no partner
+  int* contact_list;      // the other tiles
+  int* counts;            // [2] sizes of the two lists (zeroed before the launch)
+  int ntiles;
 };
 
 struct StatsArgs {
@@ -213,7 +224,8 @@ void launch_integrate(const IntegrateArgs& a, cudaStream_t s);
 void launch_body_keys(const BroadArgs& a, cudaStream_t s);
 void launch_body_ranges(const BroadArgs& a, cudaStream_t s);
 void launch_body_partners(const BroadArgs& a, cudaStream_t s);
-void launch_scene_partners(const BroadArgs& a, cudaStream_t s);  // batched scenes (scene_range)
+void launch_scene_partners(const BroadArgs& a, cudaStream_t s);
+void launch_classify_tiles(const ClassifyArgs& a, cudaStream_t s);  // batched scenes (scene_range)
 void launch_gather4(float4* dst, const float4* src, const int* idx, int64_t count, cudaStream_t s);
 void launch_scatter4(float4* dst, const float4* src, const int* idx, int64_t count, cudaStream_t s);
 void launch_near(const NearArgs& a, cudaStream_t s);

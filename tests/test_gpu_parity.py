@@ -466,3 +466,34 @@ def test_scene_cluster_force_programs(pbdr, pyoracle):
     op, ov = orc.read_f32()
     assert_same(gp, op, "positions")
     assert_same(gv, ov, "velocities")
+
+
+@pytest.mark.parametrize("cid,scale,frames", [(3, 250, 200), (5, 6, 40)])
+def test_isolated_tile_split(pbdr, pyoracle, monkeypatch, cid, scale, frames):
+    # Tiles whose bodies have no broadphase partner this substep iterate all of
+    # the substep's iterations in one launch (state in shared memory); the
+    # others iterate launch by launch. With the one-wave cooperative path off,
+    # the split path equals the unsplit one bit for bit through landing and
+    # body-body contact, and the oracle over the first frames.
+    monkeypatch.setenv("PBDR_COOP_ITERS", "0")
+    runs = []
+    for split in ("1", "0"):
+        monkeypatch.setenv("PBDR_SPLIT_ISOLATED", split)
+        g = P.GeneratedScene(cid, scale=scale)
+        gpu = P.GpuSolver(g.desc, g.cfg)
+        if split == "1":
+            orc = pyoracle.Oracle(g.desc, g.cfg)
+            gpu.step_frames(2)
+            assert orc.step(2 * g.cfg.substeps) == 0
+            gp, gv = gpu.read_f32()
+            op, ov = orc.read_f32()
+            assert_same(gp, op, "split positions vs oracle")
+            assert_same(gv, ov, "split velocities vs oracle")
+            gpu.step_frames(frames - 2)
+        else:
+            gpu.step_frames(frames)
+        gpu.debug_prologue()
+        runs.append((gpu.read_f32(), gpu.debug_candidates()[0].sum()))
+    assert runs[0][1] > 0, "expected contacts by the end"
+    assert_same(runs[0][0][0], runs[1][0][0], "positions split vs unsplit")
+    assert_same(runs[0][0][1], runs[1][0][1], "velocities split vs unsplit")
