@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--scale", type=int, default=0, help="config size knob (0 = BASELINE size)")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--preroll", type=int, default=0,
+                    help="untimed frames simulated before the warm-up (measure a later, contact-rich window)")
     ap.add_argument("--tile-kp", type=int, default=0, help="force the iteration tile shape (2, 4, 8; 0 = automatic)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -371,6 +373,8 @@ def main():
     subs = g.cfg.substeps
     iters = g.cfg.solver_iterations
 
+    if args.preroll > 0:
+        solver.step_frames(args.preroll)
     # Warm-up (also instantiates the per-frame CUDA graphs).
     solver.step_frames(max(3, args.warmup))
 
@@ -431,6 +435,7 @@ def main():
                        "substeps_per_step": subs, "iterations": iters, "frame_rate_hz": g.cfg.frame_rate,
                        "l2": f"inputs larger than L2 ({n * 64 / 1e6:.0f} MB particle state per GPU)"
                        if n * 64 > 126e6 else "state fits in L2 (latency-bound config)",
+                       "timed_frames": f"{args.preroll + max(3, args.warmup) + 1}..{args.preroll + max(3, args.warmup) + args.steps}",
                        **extra},
             "roofline": roofline,
             "cpu_baseline": cpu,

@@ -52,6 +52,8 @@ struct pbdr_handle {
   bool has_programs = false;  // any body with a ForceProgram
   bool pairs_possible = true; // some scene holds two or more bodies
   bool coop_iters = true;     // one-wave scenes with pairs: cooperative multi-iteration launch
+  float4* sorted_pos = nullptr;  // X~ in sorted (cell-key) order, for the neighbour search
+  bool single_scene = false;     // every body in scene 0
   int2* scene_range = nullptr;  // per body (first body, bodies) of its scene when scenes are contiguous
                                 // runs of <= PBDR_PARTNER_CAP bodies (k_scene_partners), else null
   int scene_cluster = 0;      // batched scenes of equal tile count C <= 8: one C-CTA cluster per scene
@@ -389,6 +391,8 @@ void enqueue_substep(pbdr_handle* h, pbdr_dev::LaunchHook* hook, bool integrated
   ra.body_of = h->body_of;
   ra.cells = h->cells;
   ra.sorted_body = h->sorted_body;
+  ra.pos = h->pos[h->cur];
+  ra.sorted_pos = h->sorted_pos;
   ra.substep_counter = h->counter;
   ra.n = h->n;
   if (hook) hook->before(kHookRanges);
@@ -405,6 +409,8 @@ void enqueue_substep(pbdr_handle* h, pbdr_dev::LaunchHook* hook, bool integrated
   na.cells = h->cells;
   na.sorted_body = h->sorted_body;
   na.sorted_vals = h->vals[sb];
+  na.sorted_pos = h->sorted_pos;
+  na.single_scene = h->single_scene ? 1 : 0;
   na.ncand = h->ncand;
   na.cand_j = h->cand_j;
   na.cand_rr = h->cand_rr;
@@ -902,6 +908,7 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
   rc |= dalloc(h, &h->partners, static_cast<size_t>(nb) * PBDR_PARTNER_CAP);
   rc |= dalloc(h, &h->oversize, 1);
   rc |= dalloc(h, &h->sorted_body, n);
+  rc |= dalloc(h, &h->sorted_pos, n);
   rc |= dalloc(h, &h->ncand, n);
   rc |= dalloc(h, &h->cand_j, static_cast<size_t>(n) * PBDR_NBR_CAP);
   rc |= dalloc(h, &h->cand_rr, static_cast<size_t>(n) * PBDR_NBR_CAP);
@@ -971,6 +978,8 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
   {
     // Contact candidates need two bodies of one scene (pinned P4).
     std::vector<int> per_scene;
+    h->single_scene = true;
+    for (int32_t b = 0; b < nb; ++b) h->single_scene = h->single_scene && scene[b] == 0;
     h->pairs_possible = false;
     for (int32_t b = 0; b < nb && !h->pairs_possible; ++b) {
       const int sc = scene[b];

@@ -488,8 +488,10 @@ __global__ void __launch_bounds__(256) k_cell_ranges(RangesArgs A) {
   }
   for (int64_t s = g; s < m; s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const uint32_t k = A.keys[s];
-    const int body = A.body_of[A.vals[s]];
+    const uint32_t v = A.vals[s];
+    const int body = A.body_of[v];
     A.sorted_body[s] = body;
+    A.sorted_pos[s] = A.pos[v];
     // Entries of a bucket ascend by slot, hence by body: the first entry holds
     // the bucket's smallest body, the last its largest.
     if (s == 0 || A.keys[s - 1] != k) {
@@ -705,11 +707,13 @@ struct CandList {
 __device__ __forceinline__ void scan_range(const NeighbourArgs& A, uint32_t lo, uint32_t hi, int bi, int si,
                                            float4 xi, int32_t cx, int32_t cy, int32_t cz, CandList& L) {
   for (uint32_t s = lo; s < hi; ++s) {
+    // Body, slot and position of the entry come from sorted-order copies
+    // (k_cell_ranges), read side by side: no dependent gathers per entry.
     const int bj = A.sorted_body[s];
     if (bj == bi) continue;
-    if (A.body_scene[bj] != si) continue;
+    if (!A.single_scene && A.body_scene[bj] != si) continue;
+    const float4 xj = A.sorted_pos[s];
     const int j = static_cast<int>(A.sorted_vals[s]);
-    const float4 xj = A.pos[j];
     const int32_t jx = pbdr_cell_coord(xj.x, A.inv_h);
     const int32_t jy = pbdr_cell_coord(xj.y, A.inv_h);
     const int32_t jz = pbdr_cell_coord(xj.z, A.inv_h);
@@ -731,7 +735,9 @@ __device__ __forceinline__ void scan_bucket(const NeighbourArgs& A, uint32_t key
 }
 
 __device__ __forceinline__ void neighbours_one(const NeighbourArgs& A, int64_t t) {
-  const int64_t i = A.near_list[t];
+  // Near particles in sorted (cell-key) order: neighbouring threads search
+  // overlapping cells, so bucket entries are shared through L1/L2.
+  const int64_t i = A.sorted_vals[t];
   const float4 xi = A.pos[i];
   const int bi = A.body_of[i];
   const int si = A.body_scene[bi];

@@ -133,6 +133,8 @@ struct RangesArgs {
   const int* body_of;
   uint4* cells;  // per bucket (start, end, first body, last body); start = ~0 when empty
   int* sorted_body;
+  const float4* pos;     // X~
+  float4* sorted_pos;    // X~ of every sorted entry
   long long* substep_counter;
   int64_t n;
 };
@@ -147,6 +149,8 @@ struct NeighbourArgs {
   const uint4* cells;
   const int* sorted_body;
   const uint32_t* sorted_vals;
+  const float4* sorted_pos;  // X~ of the sorted entries (k_cell_ranges)
+  int single_scene;          // every body in scene 0: no scene test per entry
   int* ncand;
   int* cand_j;     // slot-major: [k * n + i]
   float* cand_rr;  // slot-major
