@@ -53,6 +53,11 @@ struct pbdr_handle {
   bool pairs_possible = true; // some scene holds two or more bodies
   bool coop_iters = true;     // one-wave scenes with pairs: cooperative multi-iteration launch
   float4* sorted_pos = nullptr;  // X~ in sorted (cell-key) order, for the neighbour search
+  uint8_t* near_flag = nullptr;  // near-filter test per particle (count pass -> write pass)
+  float4* obb_q = nullptr;       // oriented near-filter boxes per body (null: PBDR_OBB=0)
+  float4* obb_c = nullptr;
+  float4* obb_lo = nullptr;
+  float4* obb_hi = nullptr;
   bool single_scene = false;     // every body in scene 0
   int2* scene_range = nullptr;  // per body (first body, bodies) of its scene when scenes are contiguous
                                 // runs of <= PBDR_PARTNER_CAP bodies (k_scene_partners), else null
@@ -375,9 +380,21 @@ void enqueue_substep(pbdr_handle* h, pbdr_dev::LaunchHook* hook, bool integrated
   nr.role = h->slab ? h->role : nullptr;
   nr.all_near = h->broadphase ? 0 : 1;
   nr.inflate = h->inflate;
+  nr.near_flag = h->near_flag;
+  // Oriented boxes pay off in large piles; batched small scenes keep the
+  // axis-aligned test (their per-scene partners are few and contacts sparse).
+  const bool obb = h->obb_q && !scene_partners(h);
+  if (obb) {
+    nr.rquat = h->rquat;
+    nr.anchor = h->anchor;
+    nr.obb_q = h->obb_q;
+    nr.obb_c = h->obb_c;
+    nr.obb_lo = h->obb_lo;
+    nr.obb_hi = h->obb_hi;
+  }
   if (hook) hook->before(kHookBroadphase);
   launch_near(nr, h->stream);
-  if (hook) hook->after(kHookBroadphase, 4);
+  if (hook) hook->after(kHookBroadphase, (obb && h->broadphase) ? 5 : 4);
 
   const int sb = sort_pairs(h->keys, h->vals, h->n, h->hash_bits, h->sort_temp, h->sm_count,
                             h->stream, hook, h->near_count);
@@ -909,6 +926,16 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
   rc |= dalloc(h, &h->oversize, 1);
   rc |= dalloc(h, &h->sorted_body, n);
   rc |= dalloc(h, &h->sorted_pos, n);
+  rc |= dalloc(h, &h->near_flag, n);
+  {
+    const char* e = std::getenv("PBDR_OBB");
+    if (!e || std::atoi(e) != 0) {
+      rc |= dalloc(h, &h->obb_q, nb);
+      rc |= dalloc(h, &h->obb_c, nb);
+      rc |= dalloc(h, &h->obb_lo, nb);
+      rc |= dalloc(h, &h->obb_hi, nb);
+    }
+  }
   rc |= dalloc(h, &h->ncand, n);
   rc |= dalloc(h, &h->cand_j, static_cast<size_t>(n) * PBDR_NBR_CAP);
   rc |= dalloc(h, &h->cand_rr, static_cast<size_t>(n) * PBDR_NBR_CAP);
@@ -1075,7 +1102,8 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
   const int tile_l = h->ctas > 0 ? 1 : 0, big_l = big.empty() ? 0 : 1;
   const int torque_l = h->has_torque ? tile_l + big_l : 0;
   h->launches_per_frame = static_cast<int64_t>(h->substeps) *
-                          ((scene_partners(h) ? 3 + 1 : 4 + 1 + (3 + h->bpasses) + 2) + 2 + torque_l + 1 + 4 +
+                          ((scene_partners(h) ? 3 + 1 : 4 + 1 + (3 + h->bpasses) + 2) + 2 + torque_l + 1 +
+                           (h->obb_q && h->broadphase && !scene_partners(h) ? 5 : 4) +
                            (3 + h->passes) + 1 + 1 +
                            static_cast<int64_t>(fused_iterations(h) ? 1 : h->iters) * (tile_l + big_l));
   if (fuse_next_integrate(h)) h->launches_per_frame -= h->substeps - 1;  // integrate inside the cluster launch

@@ -543,8 +543,103 @@ __device__ __forceinline__ int near_body_setup(const NearArgs& A, int t, int lan
   return np;
 }
 
-// Near test of particle slot p against the np partner boxes held by lanes.
-__device__ __forceinline__ bool near_test(const NearArgs& A, bool valid, int64_t p, int np, const NearBoxes& bx) {
+// Rotation of an oriented-box frame (columns = the frame axes) from a unit
+// quaternion (w, x, y, z). The same function builds the bounds (k_body_obb)
+// and tests against them, so both use the same bits.
+__device__ __forceinline__ void obb_axes(float4 q, float R[9]) {
+  const float w = q.x, x = q.y, y = q.z, z = q.w;
+  R[0] = 1.0f - 2.0f * (y * y + z * z);
+  R[1] = 2.0f * (x * y - w * z);
+  R[2] = 2.0f * (x * z + w * y);
+  R[3] = 2.0f * (x * y + w * z);
+  R[4] = 1.0f - 2.0f * (x * x + z * z);
+  R[5] = 2.0f * (y * z - w * x);
+  R[6] = 2.0f * (x * z - w * y);
+  R[7] = 2.0f * (y * z + w * x);
+  R[8] = 1.0f - 2.0f * (x * x + y * y);
+}
+
+// Frame coordinates R^T (x - c).
+__device__ __forceinline__ void obb_local(const float R[9], float4 c, float4 x, float r[3]) {
+  const float d[3] = {x.x - c.x, x.y - c.y, x.z - c.z};
+#pragma unroll
+  for (int k = 0; k < 3; ++k) r[k] = (R[k] * d[0] + R[3 + k] * d[1]) + R[6 + k] * d[2];
+}
+
+// Oriented box of body b (one warp): frame from its warm-start rotation
+// (normalised; identity before the first iteration), centre = anchor, and the
+// exact bounds of its particles' X~ in that frame. Any frame bounds the body;
+// a frame that follows its rotation bounds it tightly.
+__device__ __forceinline__ void body_obb(const NearArgs& A, int t, int lane) {
+  const int b = A.list ? A.list[t] : t;
+  if (A.npartners[b] == 0 || (A.role && A.role[b] == 0)) return;
+  float4 q = A.rquat[b];
+  const float n2 = (q.x * q.x + q.y * q.y) + (q.z * q.z + q.w * q.w);
+  if (!(n2 > 0.0f) || !isfinite(n2)) {
+    q = make_float4(1.0f, 0.0f, 0.0f, 0.0f);
+  } else {
+    const float inv = rsqrtf(n2);
+    q = make_float4(q.x * inv, q.y * inv, q.z * inv, q.w * inv);
+  }
+  const float4 c = A.anchor[b];
+  float R[9];
+  obb_axes(q, R);
+  const int4 bd = A.body_desc[b];
+  float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int qd = lane; qd < bd.y; qd += 32) {
+    float r[3];
+    obb_local(R, c, A.pos[bd.x + qd], r);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      lo[k] = fminf(lo[k], r[k]);
+      hi[k] = fmaxf(hi[k], r[k]);
+    }
+  }
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      lo[k] = fminf(lo[k], __shfl_xor_sync(kFull, lo[k], off));
+      hi[k] = fmaxf(hi[k], __shfl_xor_sync(kFull, hi[k], off));
+    }
+  if (lane == 0) {
+    A.obb_q[b] = q;
+    A.obb_c[b] = c;
+    A.obb_lo[b] = make_float4(lo[0], lo[1], lo[2], 0.0f);
+    A.obb_hi[b] = make_float4(hi[0], hi[1], hi[2], 0.0f);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_body_obb(NearArgs A) {
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < A.nbl; t += nw)  // warp-uniform
+    body_obb(A, t, lane);
+}
+
+// Inside partner o's oriented box inflated by h: a candidate j of o lies in
+// o's box and within h of x (|R^T e|_inf <= |e|_2 for a rotation), with the
+// inflation enlarged far beyond fp32 rounding of the frame coordinates.
+__device__ __forceinline__ bool in_obb(const NearArgs& A, int o, float4 x) {
+  const float4 lo = A.obb_lo[o], hi = A.obb_hi[o];
+  float R[9];
+  obb_axes(A.obb_q[o], R);
+  float r[3];
+  obb_local(R, A.obb_c[o], x, r);
+  const float lv[3] = {lo.x, lo.y, lo.z}, hv[3] = {hi.x, hi.y, hi.z};
+  bool in = true;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const float m = A.inflate * 1.0001f + 1e-5f * (fabsf(lv[k]) + fabsf(hv[k])) + 1e-6f;
+    in = in && r[k] >= lv[k] - m && r[k] <= hv[k] + m;
+  }
+  return in;
+}
+
+// Near test of particle slot p against the np partner boxes held by lanes
+// (axis-aligned; then oriented when available).
+__device__ __forceinline__ bool near_test(const NearArgs& A, bool valid, int64_t p, int np, const NearBoxes& bx,
+                                          const int* partners) {
   float4 xi = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
   if (valid) xi = A.pos[p];
   bool in_any = false;
@@ -555,8 +650,9 @@ __device__ __forceinline__ bool near_test(const NearArgs& A, bool valid, int64_t
       lo[c] = __shfl_sync(kFull, bx.lo[c], k);
       hi[c] = __shfl_sync(kFull, bx.hi[c], k);
     }
-    in_any = in_any || (xi.x >= lo[0] && xi.x <= hi[0] && xi.y >= lo[1] && xi.y <= hi[1] && xi.z >= lo[2] &&
-                        xi.z <= hi[2]);
+    bool in = xi.x >= lo[0] && xi.x <= hi[0] && xi.y >= lo[1] && xi.y <= hi[1] && xi.z >= lo[2] && xi.z <= hi[2];
+    if (in && A.obb_q) in = in_obb(A, partners[k], xi);
+    in_any = in_any || in;
   }
   return valid && in_any;
 }
@@ -574,7 +670,10 @@ __global__ void __launch_bounds__(256) k_near_count(NearArgs A) {
   } else if (np > 0) {
     for (int base = 0; base < n; base += 32) {
       const int q = base + lane;
-      cnt += __popc(__ballot_sync(kFull, near_test(A, q < n, start + static_cast<int64_t>(q), np, bx)));
+      const int64_t p = start + static_cast<int64_t>(q);
+      const bool near = near_test(A, q < n, p, np, bx, A.partners + static_cast<int64_t>(b) * PBDR_PARTNER_CAP);
+      if (q < n) A.near_flag[p] = near ? 1 : 0;  // k_near_write reuses the test
+      cnt += __popc(__ballot_sync(kFull, near));
     }
   }
   if (lane == 0) A.body_near[t] = cnt;
@@ -585,14 +684,15 @@ __global__ void __launch_bounds__(256) k_near_write(NearArgs A) {
   const int lane = threadIdx.x & 31;
   if (t >= A.nbl) return;
   if (A.body_near[t] == 0u) return;  // warp-uniform
-  int b, start, n;
-  NearBoxes bx{};
-  const int np = near_body_setup(A, t, lane, b, start, n, bx);
+  const int b = A.list ? A.list[t] : t;
+  const int4 bd = A.body_desc[b];
+  const int start = bd.x, n = bd.y;
+  const bool all = A.all_near || A.npartners[b] < 0;  // the count kernel took the same branch
   uint32_t off = A.body_off[t] + A.tile_off[t / kScanTile];
   for (int base = 0; base < n; base += 32) {
     const int q = base + lane;
     const int64_t p = start + static_cast<int64_t>(q);
-    const bool near = np < 0 ? q < n : near_test(A, q < n, p, np, bx);
+    const bool near = q < n && (all || A.near_flag[p] != 0);
     const unsigned bal = __ballot_sync(kFull, near);
     if (near) {
       const uint32_t o = off + __popc(bal & ((1u << lane) - 1u));
@@ -1984,6 +2084,8 @@ void launch_body_partners(const BroadArgs& a, cudaStream_t s) {
 void launch_near(const NearArgs& a, cudaStream_t s) {
   if (a.nbl > 0) {
     const unsigned wblocks = static_cast<unsigned>((static_cast<int64_t>(a.nbl) * 32 + 255) / 256);
+    if (a.obb_q && !a.all_near)
+      k_body_obb<<<std::min<unsigned>(wblocks, 148u * 16u), 256, 0, s>>>(a);
     k_near_count<<<wblocks, 256, 0, s>>>(a);
     k_near_scan_tiles<<<(a.nbl + kScanTile - 1) / kScanTile, 1024, 0, s>>>(a);
     k_near_scan_top<<<1, 1024, 0, s>>>(a);

@@ -123,6 +123,18 @@ struct NearArgs {
   const uint8_t* role;    // slab mode: inactive bodies' particles are never near
   int all_near;           // broadphase off: every active particle is near
   float inflate;
+  // Oriented boxes (optional, null = axis-aligned test only): per body the
+  // frame (unit quaternion from the warm-start rotation, centre = anchor) and
+  // the bounds of its X~ in that frame, built by k_body_obb for every body
+  // with partners; a particle is near only if it is also inside a partner's
+  // h-inflated oriented box.
+  const float4* rquat;    // warm-start rotation per body (0 = none: identity frame)
+  const float4* anchor;
+  float4* obb_q;          // [nb] unit quaternion of the frame
+  float4* obb_c;          // [nb] centre
+  float4* obb_lo;         // [nb] bounds in the frame
+  float4* obb_hi;
+  uint8_t* near_flag;     // [n] per particle of bodies with partners: the count kernel's test result
 };
 
 struct RangesArgs {
