@@ -204,6 +204,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // ---------------------------------------------------------------------------
 // integrate + cell key
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 // Order-preserving float <-> uint encoding for atomicMin/atomicMax boxes.
 __device__ __forceinline__ uint32_t f2ord(float f) {
   const uint32_t u = __float_as_uint(f);
@@ -1293,6 +1297,21 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
   for (int k = 0; k < KP; ++k) {
     const int q = k * 32 * W + wi * 32 + lane;
     ncs[k] = (live && q < n) ? A.ncand[start + q] : 0;  // prefetched: off the phase-A chain
+  }
+  // First candidate of each particle: its slot now, and its position and
+  // contact radius pulled into L2, while the tile's staging copies are in
+  // flight -- in contact-rich states phase A otherwise waits on two dependent
+  // HBM round trips per particle (-5% iteration time in a settled C5 pile).
+  if (!MULTI || !A.multi_pairs) {
+#pragma unroll
+    for (int k = 0; k < KP; ++k) {
+      if (ncs[k] > 0) {
+        const int64_t p = start + k * 32 * W + wi * 32 + lane;
+        const int j = __ldg(&A.cand_j[p]);
+        prefetch_l2(&A.pos_in[j]);
+        prefetch_l2(&A.cand_rr[p]);
+      }
+    }
   }
   const int off = start - first;
 
