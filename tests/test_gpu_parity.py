@@ -426,11 +426,14 @@ def test_scene_cluster_path(pbdr, pyoracle, monkeypatch, cluster, kp, fuse):
 
 def test_scene_partners_equal_coarse_grid(pbdr, monkeypatch):
     # Batched scenes find body partners per scene (k_scene_partners) instead of
-    # on the coarse body grid; the near set and the candidate lists built from
-    # them are identical once bodies touch (config 4, after landing).
+    # on the coarse body grid, and keep the axis-aligned near test; the coarse
+    # path adds the oriented-box test, which may only shrink the near set. The
+    # candidate lists are identical in all three set-ups once bodies touch
+    # (config 4, after landing).
     out = []
-    for flag in ("1", "0"):
-        monkeypatch.setenv("PBDR_SCENE_PARTNERS", flag)
+    for scene, obb in (("1", "1"), ("0", "0"), ("0", "1")):
+        monkeypatch.setenv("PBDR_SCENE_PARTNERS", scene)
+        monkeypatch.setenv("PBDR_OBB", obb)
         g = P.GeneratedScene(4, scale=6)
         gpu = P.GpuSolver(g.desc, g.cfg)
         gpu.step_frames(90)
@@ -439,8 +442,11 @@ def test_scene_partners_equal_coarse_grid(pbdr, monkeypatch):
         cnt, lst = gpu.debug_candidates()
         out.append((np.sort(v), cnt, np.where(np.arange(P.NBR_CAP)[None, :] < cnt[:, None], lst, -1)))
     assert out[0][1].sum() > 0
-    for a, b, what in zip(out[0], out[1], ("near set", "candidate counts", "candidate lists")):
-        assert_same(a, b, what)
+    assert_same(out[0][0], out[1][0], "near set (axis-aligned test, both partner searches)")
+    assert set(out[2][0].tolist()) <= set(out[1][0].tolist())
+    for o in out[1:]:
+        assert_same(out[0][1], o[1], "candidate counts")
+        assert_same(out[0][2], o[2], "candidate lists")
 
 
 def test_scene_cluster_force_programs(pbdr, pyoracle):
