@@ -49,9 +49,9 @@ PBDR_HD int pbdr_body_slots(int n, int w) { return (n + 32 * w - 1) / (32 * w); 
 
 /* Tile shape KP (particles per lane), one per scene, chosen from the scene's
  * size (measured on B200): small scenes are latency-bound
- * and want the most parallel layout (KP = 2); scenes of small bodies (mean
- * <= 384 particles) run best with KP = 8 (one warp per body up to 256
- * particles, two CTAs per SM); larger bodies with KP = 4. KP is raised until
+ * and want the most parallel layout (KP = 2); scenes whose mean body fits one
+ * warp at KP = 8 (<= 256 particles) run best with KP = 8 (two CTAs per SM);
+ * larger or mixed bodies with KP = 4 (three CTAs per SM). KP is raised until
  * the largest body fits one CTA, or to PBDR_KP_MAX when it does not (such a
  * body runs on a CTA cluster). `forced` (scene_desc.tile_kp) overrides. The
  * oracle applies the same rule, so both sides reduce with the same tree. */
@@ -61,7 +61,7 @@ PBDR_HD int pbdr_choose_kp(long long n_particles, int n_bodies, int max_body, in
     kp = forced;
   else if (n_particles < 131072)
     kp = 2;
-  else if (n_particles <= 384LL * n_bodies)
+  else if (n_particles <= 256LL * n_bodies)
     kp = 8;
   else
     kp = 4;
