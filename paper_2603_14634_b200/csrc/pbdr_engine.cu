@@ -511,7 +511,7 @@ void enqueue_iteration(pbdr_handle* h, int iter_index, pbdr_dev::LaunchHook* hoo
 // contact tile gathers a particle of an isolated one (pairs are symmetric),
 // so the split changes no result. The isolated launch leaves its final state
 // in the buffer the contact launches end in (they flip it per iteration).
-void enqueue_isolated(pbdr_handle* h, pbdr_dev::LaunchHook* hook) {
+void enqueue_isolated(pbdr_handle* h, pbdr_dev::LaunchHook* hook, bool fuse_integrate) {
   using namespace pbdr_dev;
   if (hook) hook->before(kHookMemset);
   cudaMemsetAsync(h->tile_counts, 0, 2 * sizeof(int), h->stream);
@@ -527,7 +527,7 @@ void enqueue_isolated(pbdr_handle* h, pbdr_dev::LaunchHook* hook) {
   launch_classify_tiles(ca, h->stream);
   if (hook) hook->after(kHookBroadphase);
   const int cur = h->cur;
-  enqueue_iteration(h, 0, hook, h->iters, false, h->iso_list, h->tile_counts);
+  enqueue_iteration(h, 0, hook, h->iters, fuse_integrate, h->iso_list, h->tile_counts);
   h->cur = cur;
 }
 
@@ -536,9 +536,13 @@ bool split_isolated(const pbdr_handle* h) {
          h->iso_list != nullptr;
 }
 
-// Torque programs need the k_body_wrench prepass between the substeps.
+// The launch that ends a substep also integrates the next substep of the same
+// call (its final writeback has X and V in hand). Torque programs need the
+// k_body_wrench prepass between the substeps; cluster bodies have their own
+// launch; slab ranks integrate ghosts too.
 bool fuse_next_integrate(const pbdr_handle* h) {
-  return use_scene_clusters(h) && !h->has_torque && h->fuse_integrate;
+  return h->fuse_integrate && !h->has_torque && !h->slab && h->pairs_possible && h->pk_iter.nbig == 0 &&
+         h->pk_iter.ctas > 0;
 }
 
 bool fused_iterations(const pbdr_handle* h) {
@@ -557,9 +561,9 @@ void enqueue_substeps(pbdr_handle* h, int64_t count, pbdr_dev::LaunchHook* hook)
   bool integrated = false;
   for (int64_t s = 0; s < count; ++s) {
     enqueue_substep(h, hook, integrated);
-    // Scene clusters integrate the next substep of this call in their final
-    // writeback (never across calls: the state a call leaves is X, not X~).
-    const bool fuse = fused_iters && fuse_next_integrate(h) && s + 1 < count;
+    // The substep's last launch integrates the next substep of this call in
+    // its final writeback (never across calls: a call leaves X, not X~).
+    const bool fuse = fuse_next_integrate(h) && s + 1 < count;
     if (fuse) {
       if (hook) hook->before(pbdr_dev::kHookMemset);
       reset_boxes(h);  // after this substep's broadphase consumed them
@@ -568,11 +572,11 @@ void enqueue_substeps(pbdr_handle* h, int64_t count, pbdr_dev::LaunchHook* hook)
     if (fused_iters) {
       enqueue_iteration(h, 0, hook, h->iters, fuse);
     } else if (split_isolated(h)) {
-      enqueue_isolated(h, hook);
+      enqueue_isolated(h, hook, fuse);
       for (int i = 0; i < h->iters; ++i)
-        enqueue_iteration(h, i, hook, 1, false, h->contact_list, h->tile_counts + 1);
+        enqueue_iteration(h, i, hook, 1, fuse && i + 1 == h->iters, h->contact_list, h->tile_counts + 1);
     } else {
-      for (int i = 0; i < h->iters; ++i) enqueue_iteration(h, i, hook);
+      for (int i = 0; i < h->iters; ++i) enqueue_iteration(h, i, hook, 1, fuse && i + 1 == h->iters);
     }
     integrated = fuse;
   }

@@ -1020,6 +1020,48 @@ __device__ __forceinline__ void phase_a_particle(const IterArgs& A, int it, int6
     for (int cI = 0; cI < 3; ++cI) acc[6 + 3 * rI + cI] = fmaf(mp[rI], q0[cI], acc[6 + 3 * rI + cI]);
 }
 
+// Final state of one particle in a launch that ends the substep: X and V
+// out, or -- with fuse -- the next substep's integrate on them (the integrate
+// kernel's arithmetic): X~ and V~ out, X_init and the cell key, the body box
+// folded into lo/hi (ordered uints) for warp_box_commit.
+__device__ __forceinline__ void store_final(const IterArgs& A, int64_t p, int b, float4 xo, float4 vo, bool fuse,
+                                            uint32_t (&lo)[3], uint32_t (&hi)[3]) {
+  if (!fuse) {
+    A.pos_out[p] = xo;
+    A.vel[p] = vo;
+    return;
+  }
+  float4 xn, vn;
+  integrate_one(A.ia, b, xo, vo, xn, vn);
+  A.ia.init[p] = make_float4(xo.x, xo.y, xo.z, 0.0f);
+  A.pos_out[p] = xn;
+  A.vel[p] = vn;
+  A.ia.key_all[p] = integrate_key(A.ia, b, xn);
+  const uint32_t o[3] = {f2ord(xn.x), f2ord(xn.y), f2ord(xn.z)};
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    lo[c] = min(lo[c], o[c]);
+    hi[c] = max(hi[c], o[c]);
+  }
+}
+
+// The warp's particles (one body) fold into the body box. All lanes.
+__device__ __forceinline__ void warp_box_commit(const IterArgs& A, int b, const uint32_t (&lo)[3],
+                                                const uint32_t (&hi)[3], int lane) {
+  uint32_t l[3], h[3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    l[c] = __reduce_min_sync(kFull, lo[c]);
+    h[c] = __reduce_max_sync(kFull, hi[c]);
+  }
+  if (lane == 0)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      atomicMin(&A.ia.box_min[3 * b + c], l[c]);
+      atomicMax(&A.ia.box_max[3 * b + c], h[c]);
+    }
+}
+
 constexpr int kResF = 32;
 enum ResSlot {
   kResC = 0,      // c (3), anchor-relative com of X_i
@@ -1222,7 +1264,10 @@ __device__ __forceinline__ void phase_c_particle(const IterArgs& A, int64_t p, f
 template <int KP>
 constexpr int iter_min_blocks() { return (KP == 8 ? 16 : 24) / kWarps; }  // 16 or 24 resident warps per SM
 
-template <int KP, bool MULTI>
+// FUSE (single-iteration launches only): the launch ends the substep and
+// integrates the next one in its writeback (a separate instantiation, so the
+// other iterations keep their register allocation).
+template <int KP, bool MULTI, bool FUSE = false>
 __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(IterArgs A) {
   constexpr int kSlots = kThreads * KP;  // particle slots staged per CTA
   extern __shared__ float4 s_stage[];  // pos | vel | rest, kSlots each
@@ -1392,6 +1437,10 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
   float accB[15];
 #pragma unroll
   for (int f = 0; f < 15; ++f) accB[f] = 0.0f;
+  // Launch that ends the substep and integrates the next one (not MULTI:
+  // the multi-iteration tail below does its own).
+  const bool fuse_out = FUSE && !MULTI && last_iter;
+  uint32_t flo[3] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu}, fhi[3] = {0u, 0u, 0u};
   if (live) {
     const bool sm_ok = res[kResSmOk] != 0.0f;
     float Rf[9], c[3];
@@ -1418,11 +1467,12 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
           // candidate relation is symmetric, P4), so only they are published.
           if (A.multi_pairs && it + 1 < n_iters && ncs[k] > 0) __stcg(&A.pos_b[(it + 1) & 1][p], s_pos[off + q]);
         } else {
-          A.pos_out[p] = make_float4(xa[0], xa[1], xa[2], x4.w);
-          A.vel[p] = make_float4(va[0], va[1], va[2], v4.w);
+          store_final(A, p, b, make_float4(xa[0], xa[1], xa[2], x4.w), make_float4(va[0], va[1], va[2], v4.w),
+                      fuse_out, flo, fhi);
         }
       }
     }
+    if (fuse_out && !fixes) warp_box_commit(A, b, flo, fhi, lane);
   }
   if (fixes) {
 
@@ -1473,10 +1523,11 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
       s_vel[off + q] = make_float4(vo[0], vo[1], vo[2], v4.w);
       if (A.multi_pairs && it + 1 < n_iters && ncs[k] > 0) __stcg(&A.pos_b[(it + 1) & 1][p], s_pos[off + q]);
     } else {
-      A.pos_out[p] = make_float4(xo[0], xo[1], xo[2], x4.w);
-      A.vel[p] = make_float4(vo[0], vo[1], vo[2], v4.w);
+      store_final(A, p, b, make_float4(xo[0], xo[1], xo[2], x4.w), make_float4(vo[0], vo[1], vo[2], v4.w),
+                  fuse_out, flo, fhi);
     }
   }
+  if (fuse_out) warp_box_commit(A, b, flo, fhi, lane);
   }  // live
   }  // fixes
   if (MULTI && A.multi_pairs && it + 1 < n_iters) multi_barrier(A);
@@ -2173,6 +2224,9 @@ static cudaError_t prepare_one() {
   cudaError_t e = cudaFuncSetAttribute(k_iteration<KP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(iteration_smem_bytes(KP)));
   if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k_iteration<KP, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(iteration_smem_bytes(KP)));
+  if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(k_iteration<KP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(iteration_smem_bytes(KP)));
   if (e != cudaSuccess) return e;
@@ -2249,7 +2303,10 @@ static void launch_iteration_kp(const IterArgs& a, int ctas, cudaStream_t s) {
   } else if (a.n_iters > 1) {
     k_iteration<KP, true><<<grid, kThreads, iteration_smem_bytes(KP), s>>>(b);
   } else
-    k_iteration<KP, false><<<grid, kThreads, iteration_smem_bytes(KP), s>>>(b);
+    if (a.fuse_integrate)
+      k_iteration<KP, false, true><<<grid, kThreads, iteration_smem_bytes(KP), s>>>(b);
+    else
+      k_iteration<KP, false><<<grid, kThreads, iteration_smem_bytes(KP), s>>>(b);
 }
 
 int iteration_coop_capacity(int kp) { return g_iter_coop_cap[kp == 2 ? 2 : (kp == 4 ? 4 : 8)]; }
