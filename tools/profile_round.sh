@@ -9,6 +9,7 @@ mkdir -p gpurun_out
 python bench.py --steps 5 --warmup 3 > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err
 bash tools/all_configs.sh > gpurun_out/${TAG}_all_configs.txt 2>&1 || true
 bash tools/contact_windows.sh > gpurun_out/${TAG}_contact_windows.txt 2>&1 || true
+bash tools/whole_runs.sh > gpurun_out/${TAG}_whole_runs.txt 2>&1 || true
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 700 --csv \
     --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
     > gpurun_out/${TAG}_ncu_launches.log 2>&1
