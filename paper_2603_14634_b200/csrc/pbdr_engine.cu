@@ -71,6 +71,8 @@ struct pbdr_handle {
   int* tile_counts = nullptr;   // [2] sizes of the two lists (device)
   bool broadphase = true;     // body-box filter before the hash grid (PBDR_BROADPHASE=0 disables)
   int kp = 4;                 // tile shape: particles per lane (pbdr_choose_kp)
+  int launch_kp = 4;          // instantiation the tiles run on (kp, or 7 for one-warp bodies at kp 8)
+  bool kp7 = true;            // PBDR_KP7=0 keeps the KP = 8 instantiation
   int per_substep = 0;
   int debug_iter = 0;  // iteration index for the replay hook
   uint32_t* keys[2] = {nullptr, nullptr};
@@ -301,7 +303,7 @@ void enqueue_substep(pbdr_handle* h, pbdr_dev::LaunchHook* hook, bool integrated
     wa.substep_counter = h->counter;
     if (hook) hook->before(kHookIntegrate);
     wa.big_list = h->pk_active.big;
-    if (h->pk_active.ctas > 0) launch_wrench(wa, h->pk_active.ctas, h->kp, h->stream);
+    if (h->pk_active.ctas > 0) launch_wrench(wa, h->pk_active.ctas, h->launch_kp, h->stream);
     if (h->pk_active.nbig > 0) launch_wrench_big(wa, h->pk_active.nbig, h->stream);
     if (hook) hook->after(kHookIntegrate, (h->pk_active.ctas > 0 ? 1 : 0) + (h->pk_active.nbig > 0 ? 1 : 0));
   }
@@ -496,7 +498,7 @@ void enqueue_iteration(pbdr_handle* h, int iter_index, pbdr_dev::LaunchHook* hoo
   it.tile_ctr = h->tile_ctr;
   it.big_list = h->pk_iter.big;
   if (hook) hook->before(kHookIteration);
-  if (h->pk_iter.ctas > 0) launch_iteration(it, h->pk_iter.ctas, h->kp, h->stream);
+  if (h->pk_iter.ctas > 0) launch_iteration(it, h->pk_iter.ctas, h->launch_kp, h->stream);
   // Bodies larger than one CTA: one cluster each, same iteration semantics
   // (they read pos_in and write pos_out / vel of their own slots only).
   const bool big = h->pk_iter.nbig > 0 && !isolated;
@@ -547,7 +549,7 @@ bool fuse_next_integrate(const pbdr_handle* h) {
 
 bool fused_iterations(const pbdr_handle* h) {
   return !h->slab && (!h->pairs_possible || use_scene_clusters(h) ||
-                      (h->pk_iter.ctas <= pbdr_dev::iteration_coop_capacity(h->kp) && h->coop_iters &&
+                      (h->pk_iter.ctas <= pbdr_dev::iteration_coop_capacity(h->launch_kp) && h->coop_iters &&
                        h->pk_iter.nbig == 0));
 }
 
@@ -826,6 +828,13 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
     int max_body = 0;
     for (int32_t b = 0; b < nb; ++b) max_body = std::max(max_body, h->h_bcount[b]);
     h->kp = pbdr_choose_kp(n, nb, max_body, d->tile_kp);
+    if (const char* e = std::getenv("PBDR_KP7")) h->kp7 = std::atoi(e) != 0;
+    // Bodies of at most 7 * 32 particles at KP = 8 each take one warp whose
+    // lanes hold at most 7 particles: the KP = 7 instantiation runs the same
+    // tiles with the same trees (W = 1 either way) without the empty eighth
+    // row (fewer registers and instructions). The tile shape reported and
+    // used by the oracle stays 8.
+    h->launch_kp = (h->kp == 8 && max_body <= 7 * 32 && h->kp7) ? 7 : h->kp;
     pack_bodies(all, h->h_bstart, h->h_bcount, h->h_bscene, h->kp, cdesc, wdesc, bdesc, big);
     if (!big.empty()) {
       const int wmax = pbdr_body_warps(max_body, h->kp);
@@ -1088,7 +1097,7 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
       }
     }
     if (ok) ok = C == 0 ? (C = run, true) : run == C;
-    if (ok && C >= 1 && C <= 8 && h->ctas % C == 0 && pbdr_dev::iteration_scene_clusters(h->kp, C) > 0)
+    if (ok && C >= 1 && C <= 8 && h->ctas % C == 0 && pbdr_dev::iteration_scene_clusters(h->launch_kp, C) > 0)
       h->scene_cluster = C;
   }
   h->pk_iter = h->pk_active = h->pk_full;
@@ -1143,7 +1152,7 @@ static void enqueue_stats(pbdr_handle* h, double* out) {
   sa.body_mass = h->body_mass;
   sa.out = out;
   sa.big_list = h->pk_iter.big;
-  if (h->pk_iter.ctas > 0) pbdr_dev::launch_stats(sa, h->pk_iter.ctas, h->kp, h->stream);
+  if (h->pk_iter.ctas > 0) pbdr_dev::launch_stats(sa, h->pk_iter.ctas, h->launch_kp, h->stream);
   if (h->pk_iter.nbig > 0) pbdr_dev::launch_stats_big(sa, h->pk_iter.nbig, h->stream);
 }
 

@@ -1262,7 +1262,7 @@ __device__ __forceinline__ void phase_c_particle(const IterArgs& A, int64_t p, f
 // 0.382 ms per iteration vs 0.436 for KP = 4 at three CTAs per SM (80
 // registers, spills) -- more particles in flight per SM, fewer warps per body.
 template <int KP>
-constexpr int iter_min_blocks() { return (KP == 8 ? 16 : 24) / kWarps; }  // 16 or 24 resident warps per SM
+constexpr int iter_min_blocks() { return (KP >= 7 ? 16 : 24) / kWarps; }  // 16 or 24 resident warps per SM
 
 // FUSE (single-iteration launches only): the launch ends the substep and
 // integrates the next one in its writeback (a separate instantiation, so the
@@ -2248,6 +2248,7 @@ static cudaError_t prepare_one() {
 cudaError_t prepare_iteration_kernel() {
   cudaError_t e = prepare_one<2>();
   if (e == cudaSuccess) e = prepare_one<4>();
+  if (e == cudaSuccess) e = prepare_one<7>();
   if (e == cudaSuccess) e = prepare_one<8>();
   return e;
 }
@@ -2309,7 +2310,7 @@ static void launch_iteration_kp(const IterArgs& a, int ctas, cudaStream_t s) {
       k_iteration<KP, false><<<grid, kThreads, iteration_smem_bytes(KP), s>>>(b);
 }
 
-int iteration_coop_capacity(int kp) { return g_iter_coop_cap[kp == 2 ? 2 : (kp == 4 ? 4 : 8)]; }
+int iteration_coop_capacity(int kp) { return g_iter_coop_cap[kp == 2 ? 2 : (kp == 4 ? 4 : (kp == 7 ? 7 : 8))]; }
 
 template <int KP>
 static int scene_clusters_kp(int cluster) {
@@ -2336,6 +2337,7 @@ int iteration_scene_clusters(int kp, int cluster) {
   switch (kp) {
     case 2: return scene_clusters_kp<2>(cluster);
     case 4: return scene_clusters_kp<4>(cluster);
+    case 7: return scene_clusters_kp<7>(cluster);
     default: return scene_clusters_kp<8>(cluster);
   }
 }
@@ -2344,6 +2346,7 @@ void launch_iteration(const IterArgs& a, int ctas, int kp, cudaStream_t s) {
   switch (kp) {
     case 2: launch_iteration_kp<2>(a, ctas, s); break;
     case 4: launch_iteration_kp<4>(a, ctas, s); break;
+    case 7: launch_iteration_kp<7>(a, ctas, s); break;
     default: launch_iteration_kp<8>(a, ctas, s); break;
   }
 }
@@ -2352,6 +2355,7 @@ void launch_wrench(const WrenchArgs& a, int ctas, int kp, cudaStream_t s) {
   switch (kp) {
     case 2: k_body_wrench<2><<<ctas, kThreads, 0, s>>>(a); break;
     case 4: k_body_wrench<4><<<ctas, kThreads, 0, s>>>(a); break;
+    case 7: k_body_wrench<7><<<ctas, kThreads, 0, s>>>(a); break;
     default: k_body_wrench<8><<<ctas, kThreads, 0, s>>>(a); break;
   }
 }
@@ -2360,6 +2364,7 @@ void launch_stats(const StatsArgs& a, int ctas, int kp, cudaStream_t s) {
   switch (kp) {
     case 2: k_body_stats<2><<<ctas, kThreads, 0, s>>>(a); break;
     case 4: k_body_stats<4><<<ctas, kThreads, 0, s>>>(a); break;
+    case 7: k_body_stats<7><<<ctas, kThreads, 0, s>>>(a); break;
     default: k_body_stats<8><<<ctas, kThreads, 0, s>>>(a); break;
   }
 }
