@@ -887,9 +887,12 @@ __global__ void __launch_bounds__(128) k_neighbours(NeighbourArgs A) {
 // One solver iteration, fused (pinned P1-P8). A CTA (8 warps) holds whole,
 // consecutive bodies; its contiguous slot range of pos/vel/rest is staged in
 // shared memory by three cp.async.bulk copies. A body of n particles owns
-// W = ceil(n/128) warps; lane l of body-warp wi owns q = k*32*W + wi*32 + l,
-// k < 4. Warp 0 runs the per-body fp64 math for all bodies of the CTA, one
-// lane per body.
+// W = ceil(n/(32 KP)) warps (KP = the scene's tile shape); lane l of body-warp
+// wi owns q = k*32*W + wi*32 + l, k < KP. Warp 0 runs the per-body fp64 math
+// for all bodies of the CTA, one lane per body. The same kernel runs one
+// iteration per launch, all iterations of a substep on chip (MULTI: isolated
+// tiles, one-wave cooperative grids, or one cluster per batched scene), and
+// -- FUSE -- the substep's last iteration followed by the next integrate.
 // ---------------------------------------------------------------------------
 // Pinned fused multiply-adds (P8): only these explicit fmaf() are
 // contracted (the library builds with --fmad=false); the oracle uses std::fmaf
