@@ -1410,8 +1410,17 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
     phase_a_particle<MULTI>(A, it, p, s_pos[off + q], s_vel[off + q], s_rest[off + q], ncs[k], a, dX[k], acc);
   }
   if (live) {
-    const float tot = warp_reduce_scatter<21>(acc);  // lane f: total of field f
-    if (lane < 21) s_part[warp][lane] = tot;
+    // 21 fields as 16 + 5 (each its own power-of-two reduce-scatter: fewer
+    // shuffles than padding to 32; every field's tree is the same butterfly).
+    float a16[16], a5[5];
+#pragma unroll
+    for (int f = 0; f < 16; ++f) a16[f] = acc[f];
+#pragma unroll
+    for (int f = 0; f < 5; ++f) a5[f] = acc[16 + f];
+    const float t16 = warp_reduce_scatter<16>(a16);  // lanes 2f, 2f+1: field f
+    const float t5 = warp_reduce_scatter<5>(a5);     // lanes 4f..4f+3: field 16 + f
+    if ((lane & 1) == 0) s_part[warp][lane >> 1] = t16;
+    if ((lane & 3) == 0 && (lane >> 2) < 5) s_part[warp][16 + (lane >> 2)] = t5;
   }
   __syncthreads();
   if (tm && threadIdx.x == 0) tm[2] = clock64();
