@@ -1736,8 +1736,15 @@ __global__ void __launch_bounds__(kThreads, 2) k_iteration_big(IterArgs A) {
       phase_a_particle<false>(A, it, start + q, s_pos[li], s_vel[li], s_rest[li], ncs[k], a, dX[k], acc);
     }
     if (live) {
-      const float tot = warp_reduce_scatter<21>(acc);
-      if (lane < 21) lead_part[wi * 21 + lane] = tot;
+      float a16[16], a5[5];  // 16 + 5 fields, as in k_iteration
+#pragma unroll
+      for (int f = 0; f < 16; ++f) a16[f] = acc[f];
+#pragma unroll
+      for (int f = 0; f < 5; ++f) a5[f] = acc[16 + f];
+      const float t16 = warp_reduce_scatter<16>(a16);
+      const float t5 = warp_reduce_scatter<5>(a5);
+      if ((lane & 1) == 0) lead_part[wi * 21 + (lane >> 1)] = t16;
+      if ((lane & 3) == 0 && (lane >> 2) < 5) lead_part[wi * 21 + 16 + (lane >> 2)] = t5;
     }
     cluster.sync();
     if (r == 0) {
