@@ -1436,6 +1436,8 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
     float S[21];
 #pragma unroll
     for (int f = 0; f < 21; ++f) S[f] = s_part[fw][f];
+    // Kept rolled (with the plane loop: smaller code, C3 +5%, C5 +3%).
+#pragma unroll 1
     for (int u = 1; u < bw.y; ++u)
 #pragma unroll
       for (int f = 0; f < 21; ++f) S[f] = S[f] + s_part[fw + u][f];
@@ -1507,6 +1509,7 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
     float S[15];
 #pragma unroll
     for (int f = 0; f < 15; ++f) S[f] = s_part[fw][f];
+#pragma unroll 1
     for (int u = 1; u < bw.y; ++u)
 #pragma unroll
       for (int f = 0; f < 15; ++f) S[f] = S[f] + s_part[fw + u][f];
