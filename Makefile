@@ -14,19 +14,25 @@ ARCH     := -gencode arch=compute_100a,code=sm_100a
 PKG      := paper_2603_14634_b200
 CSRC     := $(PKG)/csrc
 LIB      := $(PKG)/lib/libpbdr_gpu.so
+# Host-only half (scene generation, RNG, pack_box, the thread-local error
+# state): no CUDA, so the CPU reference arm of bench.py can build its inputs
+# without mapping the GPU library. libpbdr_gpu.so links against it.
+HOST_LIB := $(PKG)/lib/libpbdr_host.so
 NVFLAGS  := $(ARCH) -std=c++17 -O3 -lineinfo --fmad=false -Xcompiler -fPIC,-ffp-contract=off \
             -Xptxas -v -Iinclude -I$(CSRC)
 CU_SRC   := $(CSRC)/pbdr_kernels.cu $(CSRC)/pbdr_sort.cu $(CSRC)/pbdr_engine.cu $(CSRC)/pbdr_mesh.cu
-CXX_SRC  := $(CSRC)/pbdr_scene.cpp $(CSRC)/pbdr_errors.cpp $(CSRC)/pbdr_dropin.cpp
+CXX_SRC  := $(CSRC)/pbdr_dropin.cpp
+HOST_SRC := $(CSRC)/pbdr_scene.cpp $(CSRC)/pbdr_errors.cpp
 HDRS     := include/pbdr_gpu.h $(wildcard include/pbdr/*.hpp) $(wildcard $(CSRC)/*.h) $(wildcard $(CSRC)/*.cuh)
 OBJDIR   := build/obj
 CU_OBJ   := $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(CU_SRC))
 CXX_OBJ  := $(patsubst $(CSRC)/%.cpp,$(OBJDIR)/%.o,$(CXX_SRC))
+HOST_OBJ := $(patsubst $(CSRC)/%.cpp,$(OBJDIR)/%.o,$(HOST_SRC))
 
 .PHONY: all lib oracle ref clean
 all: lib oracle build/test_dropin
 
-lib: $(LIB)
+lib: $(HOST_LIB) $(LIB)
 
 $(OBJDIR)/%.o: $(CSRC)/%.cu $(HDRS)
 	@mkdir -p $(OBJDIR)
@@ -37,9 +43,14 @@ $(OBJDIR)/%.o: $(CSRC)/%.cpp $(HDRS)
 	$(CXX) -std=c++17 -O3 -fPIC -ffp-contract=off -Wall -Wextra -Iinclude -I$(CSRC) \
 	    -I/usr/local/cuda/include -c $< -o $@
 
-$(LIB): $(CU_OBJ) $(CXX_OBJ)
+$(HOST_LIB): $(HOST_OBJ)
 	@mkdir -p $(PKG)/lib
-	$(NVCC) $(ARCH) -shared -o $@ $^ -lcudart
+	$(CXX) -shared -o $@ $^
+
+$(LIB): $(CU_OBJ) $(CXX_OBJ) $(HOST_LIB)
+	@mkdir -p $(PKG)/lib
+	$(NVCC) $(ARCH) -shared -o $@ $(CU_OBJ) $(CXX_OBJ) -L$(PKG)/lib -lpbdr_host -lcudart \
+	    -Xlinker -rpath,'$$ORIGIN'
 
 oracle:
 	$(MAKE) -C oracle
@@ -50,7 +61,7 @@ ref:
 build/test_dropin: tests/cpp/test_dropin.cpp $(LIB) $(HDRS)
 	@mkdir -p build
 	$(CXX) -std=c++17 -O2 -Iinclude tests/cpp/test_dropin.cpp -o $@ \
-	    -L$(PKG)/lib -lpbdr_gpu -Wl,-rpath,'$$ORIGIN/../$(PKG)/lib'
+	    -L$(PKG)/lib -lpbdr_gpu -lpbdr_host -Wl,-rpath,'$$ORIGIN/../$(PKG)/lib'
 
 clean:
 	rm -rf build $(PKG)/lib oracle/build

@@ -126,9 +126,18 @@ int pbdr_gpu_step(pbdr_handle* h, int64_t substeps);
  * (SPEC.md:425). */
 int pbdr_gpu_step_frames(pbdr_handle* h, int64_t frames);
 
-/* State transfer, in the caller's particle order (Scene::particles). */
+/* State transfer, in the caller's particle order (Scene::particles, fp64,
+ * 3 doubles per particle; either pointer may be NULL). Staged through HBM and
+ * converted / permuted on the device. Writing positions drops the warm-start
+ * rotations and re-anchors the body sums, so the next step is the step of a
+ * handle created from the written state. */
 int pbdr_gpu_read_particles(pbdr_handle* h, double* position, double* velocity);
 int pbdr_gpu_write_particles(pbdr_handle* h, const double* position, const double* velocity);
+/* Simulation time, as the substep index t/dt: ForceProgram::active(t)
+ * windows (scene.hpp:53-61) and SimulationError frame indices
+ * (errors.hpp:39-44) follow it. A new handle starts at 0; each substep adds 1. */
+int pbdr_gpu_set_time(pbdr_handle* h, int64_t substep);
+int pbdr_gpu_get_time(pbdr_handle* h, int64_t* substep);
 /* Fast fp32 transfer in the device's body-major order, 4 floats per particle:
  * pos4 = (x, y, z, inv_mass), vel4 = (vx, vy, vz, mass). Pointers may be
  * pinned host memory. Either may be NULL. */

@@ -111,6 +111,8 @@ struct pbdr_handle {
   int* tile_ctr = nullptr;  // iteration kernel: dynamic tile claims (self-resetting)
   int* big_list = nullptr;  // bodies larger than one CTA (ascending ids)
   double* stats = nullptr;
+  double* xfer = nullptr;        // fp64 staging of pbdr_gpu_read/write_particles (6 n, lazy)
+  int* slot_particle = nullptr;  // device copy of slot_to_particle (lazy)
   std::vector<void*> allocations;
   size_t device_bytes = 0;
 
@@ -1275,45 +1277,82 @@ int pbdr_gpu_step_frames_async(pbdr_handle* h, int64_t frames) {
   return step_frames_async(h, frames);
 }
 
+// The reference-shaped transfer (fp64, the caller's particle order): the
+// host arrays are staged in HBM and converted and permuted by a kernel
+// (k_particles_in / _out), so no host loop and no device round trip.
+static int ensure_xfer(pbdr_handle* h) {
+  if (h->xfer) return PBDR_OK;
+  int rc = dalloc(h, &h->xfer, 6 * static_cast<size_t>(h->n));
+  if (rc == PBDR_OK) rc = dalloc(h, &h->slot_particle, static_cast<size_t>(h->n));
+  if (rc != PBDR_OK) return rc;
+  std::vector<int> sp(h->n);
+  for (int64_t s = 0; s < h->n; ++s) sp[s] = static_cast<int>(h->slot_to_particle[s]);
+  PBDR_CUDA(cudaMemcpy(h->slot_particle, sp.data(), sizeof(int) * h->n, cudaMemcpyHostToDevice));
+  return PBDR_OK;
+}
+
 int pbdr_gpu_read_particles(pbdr_handle* h, double* position, double* velocity) {
   if (!h) return set_error(PBDR_ERR_GENERIC, "null handle");
-  std::vector<float4> p(h->n), v(h->n);
-  const int rc = pbdr_gpu_read_f32(h, reinterpret_cast<float*>(p.data()), reinterpret_cast<float*>(v.data()));
+  PBDR_CUDA(cudaSetDevice(h->device));
+  const int rc = ensure_xfer(h);
   if (rc != PBDR_OK) return rc;
-  for (int64_t s = 0; s < h->n; ++s) {
-    const int64_t i = h->slot_to_particle[s];
-    if (position) {
-      position[3 * i] = p[s].x; position[3 * i + 1] = p[s].y; position[3 * i + 2] = p[s].z;
-    }
-    if (velocity) {
-      velocity[3 * i] = v[s].x; velocity[3 * i + 1] = v[s].y; velocity[3 * i + 2] = v[s].z;
-    }
-  }
+  const size_t bytes = sizeof(double) * 3 * h->n;
+  double* xd = position ? h->xfer : nullptr;
+  double* vd = velocity ? h->xfer + 3 * h->n : nullptr;
+  pbdr_dev::launch_particles_out(h->pos[h->cur], h->vel, xd, vd, h->slot_particle, h->n, h->stream);
+  PBDR_CUDA(cudaGetLastError());
+  if (position) PBDR_CUDA(cudaMemcpyAsync(position, xd, bytes, cudaMemcpyDeviceToHost, h->stream));
+  if (velocity) PBDR_CUDA(cudaMemcpyAsync(velocity, vd, bytes, cudaMemcpyDeviceToHost, h->stream));
+  PBDR_CUDA(cudaStreamSynchronize(h->stream));
   return PBDR_OK;
 }
 
 int pbdr_gpu_write_particles(pbdr_handle* h, const double* position, const double* velocity) {
   if (!h) return set_error(PBDR_ERR_GENERIC, "null handle");
-  // New positions: drop the warm-start rotations (the next polar starts cold).
   PBDR_CUDA(cudaSetDevice(h->device));
-  PBDR_CUDA(cudaMemset(h->rquat, 0, sizeof(float4) * h->nb));
-  std::vector<float4> p(h->n), v(h->n);
-  int rc = pbdr_gpu_read_f32(h, reinterpret_cast<float*>(p.data()), reinterpret_cast<float*>(v.data()));
+  const int rc = ensure_xfer(h);
   if (rc != PBDR_OK) return rc;
-  for (int64_t s = 0; s < h->n; ++s) {
-    const int64_t i = h->slot_to_particle[s];
-    if (position) {
-      p[s].x = static_cast<float>(position[3 * i]);
-      p[s].y = static_cast<float>(position[3 * i + 1]);
-      p[s].z = static_cast<float>(position[3 * i + 2]);
-    }
-    if (velocity) {
-      v[s].x = static_cast<float>(velocity[3 * i]);
-      v[s].y = static_cast<float>(velocity[3 * i + 1]);
-      v[s].z = static_cast<float>(velocity[3 * i + 2]);
-    }
+  const size_t bytes = sizeof(double) * 3 * h->n;
+  double* xd = position ? h->xfer : nullptr;
+  double* vd = velocity ? h->xfer + 3 * h->n : nullptr;
+  // Everything on the handle's stream, after the work already queued there.
+  if (position) PBDR_CUDA(cudaMemcpyAsync(xd, position, bytes, cudaMemcpyHostToDevice, h->stream));
+  if (velocity) PBDR_CUDA(cudaMemcpyAsync(vd, velocity, bytes, cudaMemcpyHostToDevice, h->stream));
+  pbdr_dev::launch_particles_in(h->pos[h->cur], h->vel, xd, vd, h->slot_particle, h->n, h->stream);
+  PBDR_CUDA(cudaGetLastError());
+  if (position) {
+    // New positions: the warm-start rotations are dropped (the next polar
+    // starts cold) and each body's anchor moves to its first slot, exactly as
+    // a handle created from this state would have them.
+    PBDR_CUDA(cudaMemsetAsync(h->rquat, 0, sizeof(float4) * h->nb, h->stream));
+    pbdr_dev::launch_anchor_reset(h->anchor, h->pk_full.body, h->pos[h->cur], h->nb, h->stream);
+    PBDR_CUDA(cudaGetLastError());
   }
-  return pbdr_gpu_write_f32(h, reinterpret_cast<const float*>(p.data()), reinterpret_cast<const float*>(v.data()));
+  PBDR_CUDA(cudaStreamSynchronize(h->stream));
+  return PBDR_OK;
+}
+
+// Simulation time as a substep index t / dt (ForceProgram windows,
+// scene.hpp:60, and the frame index of SimulationError, errors.hpp:39-44).
+int pbdr_gpu_set_time(pbdr_handle* h, int64_t substep) {
+  if (!h) return set_error(PBDR_ERR_GENERIC, "null handle");
+  if (substep < 0) return set_config_error("time", "must be >= 0");
+  PBDR_CUDA(cudaSetDevice(h->device));
+  const long long c = substep;
+  PBDR_CUDA(cudaMemcpyAsync(h->counter, &c, sizeof c, cudaMemcpyHostToDevice, h->stream));
+  PBDR_CUDA(cudaStreamSynchronize(h->stream));
+  h->substeps_done = substep;
+  return PBDR_OK;
+}
+
+int pbdr_gpu_get_time(pbdr_handle* h, int64_t* substep) {
+  if (!h || !substep) return set_error(PBDR_ERR_GENERIC, "null argument");
+  PBDR_CUDA(cudaSetDevice(h->device));
+  long long c = 0;
+  PBDR_CUDA(cudaStreamSynchronize(h->stream));
+  PBDR_CUDA(cudaMemcpy(&c, h->counter, sizeof c, cudaMemcpyDeviceToHost));
+  *substep = c;
+  return PBDR_OK;
 }
 
 int pbdr_gpu_read_bodies(pbdr_handle* h, pbdr_body_stats* out) {

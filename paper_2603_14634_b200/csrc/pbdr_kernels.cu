@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <stdint.h>
 
 #include "pbdr_kernels.cuh"
@@ -2211,16 +2212,91 @@ void launch_scatter4(float4* dst, const float4* src, const int* idx, int64_t cou
   if (count > 0) k_scatter4<<<static_cast<unsigned>((count + 255) / 256), 256, 0, s>>>(dst, src, idx, count);
 }
 
+static unsigned stride_grid(int64_t n_max) {
+  const int64_t want = (n_max + 255) / 256;
+  return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(want, 148 * 16)));
+}
+
+// pbdr_gpu_write_particles / read_particles on the device: the caller's fp64
+// Scene::particles arrays (position[3i..], velocity[3i..], body.hpp:11-17) are
+// staged in HBM and converted (round to nearest) and permuted into the
+// body-major float4 slots, or the reverse. Slot s holds caller particle
+// slot_particle[s]; .w (inverse mass / mass) is kept.
+__global__ void __launch_bounds__(256) k_particles_in(float4* __restrict__ pos, float4* __restrict__ vel,
+                                                      const double* __restrict__ x, const double* __restrict__ v,
+                                                      const int* __restrict__ slot_particle, int64_t n) {
+  for (int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; s < n;
+       s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = slot_particle[s];
+    if (x) {
+      float4 p = pos[s];
+      p.x = static_cast<float>(x[3 * i]);
+      p.y = static_cast<float>(x[3 * i + 1]);
+      p.z = static_cast<float>(x[3 * i + 2]);
+      pos[s] = p;
+    }
+    if (v) {
+      float4 q = vel[s];
+      q.x = static_cast<float>(v[3 * i]);
+      q.y = static_cast<float>(v[3 * i + 1]);
+      q.z = static_cast<float>(v[3 * i + 2]);
+      vel[s] = q;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_particles_out(const float4* __restrict__ pos,
+                                                       const float4* __restrict__ vel, double* __restrict__ x,
+                                                       double* __restrict__ v,
+                                                       const int* __restrict__ slot_particle, int64_t n) {
+  for (int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; s < n;
+       s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = slot_particle[s];
+    if (x) {
+      const float4 p = pos[s];
+      x[3 * i] = p.x;
+      x[3 * i + 1] = p.y;
+      x[3 * i + 2] = p.z;
+    }
+    if (v) {
+      const float4 q = vel[s];
+      v[3 * i] = q.x;
+      v[3 * i + 1] = q.y;
+      v[3 * i + 2] = q.z;
+    }
+  }
+}
+
+// After new positions: each body's anchor (origin of its fp32 body sums) is
+// its first slot's position, as at create.
+__global__ void __launch_bounds__(256) k_anchor_reset(float4* __restrict__ anchor, const int4* __restrict__ body_desc,
+                                                      const float4* __restrict__ pos, int nb) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < nb) {
+    const float4 p = pos[body_desc[b].x];
+    anchor[b] = make_float4(p.x, p.y, p.z, 0.0f);
+  }
+}
+
+void launch_particles_in(float4* pos, float4* vel, const double* x, const double* v, const int* slot_particle,
+                         int64_t n, cudaStream_t s) {
+  if (n > 0) k_particles_in<<<stride_grid(n), 256, 0, s>>>(pos, vel, x, v, slot_particle, n);
+}
+
+void launch_particles_out(const float4* pos, const float4* vel, double* x, double* v, const int* slot_particle,
+                          int64_t n, cudaStream_t s) {
+  if (n > 0) k_particles_out<<<stride_grid(n), 256, 0, s>>>(pos, vel, x, v, slot_particle, n);
+}
+
+void launch_anchor_reset(float4* anchor, const int4* body_desc, const float4* pos, int nb, cudaStream_t s) {
+  if (nb > 0) k_anchor_reset<<<(nb + 255) / 256, 256, 0, s>>>(anchor, body_desc, pos, nb);
+}
+
 __global__ void k_tick(long long* substep_counter) {
   atomicAdd(reinterpret_cast<unsigned long long*>(substep_counter), 1ull);
 }
 
 void launch_tick(long long* substep_counter, cudaStream_t s) { k_tick<<<1, 1, 0, s>>>(substep_counter); }
-
-static unsigned stride_grid(int64_t n_max) {
-  const int64_t want = (n_max + 255) / 256;
-  return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(want, 148 * 16)));
-}
 
 void launch_ncand_clear(int* ncand, const int* prev_near, const long long* prev_count, int64_t n_max,
                         cudaStream_t s) {
@@ -2260,6 +2336,13 @@ static cudaError_t prepare_one() {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_iteration<KP, false>, kThreads, iteration_smem_bytes(KP));
   g_iter_grid_cap[KP] = sms * per_sm;
+  // Debug/test cap on the persistent grid (PBDR_ITER_GRID_CAP=k): small scenes
+  // then take the multi-tile path (dynamic claims, next-tile table prefetch)
+  // that otherwise only BASELINE-size scenes reach. Re-read at every create.
+  if (const char* cap = std::getenv("PBDR_ITER_GRID_CAP")) {
+    const int c = std::atoi(cap);
+    if (c > 0) g_iter_grid_cap[KP] = std::min(g_iter_grid_cap[KP], c);
+  }
   int per_sm_multi = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_multi, k_iteration<KP, true>, kThreads, iteration_smem_bytes(KP));
   g_iter_coop_cap[KP] = sms * per_sm_multi;

@@ -246,6 +246,11 @@ void launch_gather4(float4* dst, const float4* src, const int* idx, int64_t coun
 void launch_scatter4(float4* dst, const float4* src, const int* idx, int64_t count, cudaStream_t s);
 void launch_near(const NearArgs& a, cudaStream_t s);
 void launch_tick(long long* substep_counter, cudaStream_t s);
+void launch_particles_in(float4* pos, float4* vel, const double* x, const double* v, const int* slot_particle,
+                         int64_t n, cudaStream_t s);
+void launch_particles_out(const float4* pos, const float4* vel, double* x, double* v, const int* slot_particle,
+                          int64_t n, cudaStream_t s);
+void launch_anchor_reset(float4* anchor, const int4* body_desc, const float4* pos, int nb, cudaStream_t s);
 void launch_ncand_clear(int* ncand, const int* prev_near, const long long* prev_count, int64_t n_max,
                         cudaStream_t s);
 void launch_cell_clear(uint4* cells, const uint32_t* prev_keys, const long long* prev_count, int64_t n_max,

@@ -17,6 +17,10 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PBDR_LIB_PATH") or os.path.join(_HERE, "lib", "libpbdr_gpu.so")
+# Host-only half of the ABI (scene generation, RNG, pack_box, last-error
+# state): no CUDA. libpbdr_gpu.so links against it, so both handles see one
+# error state; the CPU reference arm loads only this one.
+HOST_LIB_PATH = os.path.join(os.path.dirname(LIB_PATH), "libpbdr_host.so")
 
 NBR_CAP = 32
 KCLASS_NAMES = ("integrate_key", "sort_histogram", "sort_onesweep", "cell_ranges",
@@ -138,9 +142,8 @@ def lib() -> C.CDLL:
         L.pbdr_gpu_read_f32_async.argtypes = [vp, vp, vp]
         L.pbdr_gpu_step_frames_async.argtypes = [vp, i64]
         L.pbdr_gpu_read_bodies.argtypes = [vp, vp]
-        L.pbdr_last_error.restype = C.c_char_p
-        L.pbdr_last_error_key.restype = C.c_char_p
-        L.pbdr_last_error_payload.argtypes = [dp, C.POINTER(i64), C.POINTER(i32)]
+        L.pbdr_gpu_set_time.argtypes = [vp, i64]
+        L.pbdr_gpu_get_time.argtypes = [vp, C.POINTER(i64)]
         L.pbdr_gpu_info.argtypes = [vp, C.POINTER(Info)]
         L.pbdr_gpu_time_frames.argtypes = [vp, i64, C.POINTER(C.c_float)]
         L.pbdr_gpu_profile_frames.argtypes = [vp, i64, vp, vp]
@@ -164,6 +167,26 @@ def lib() -> C.CDLL:
         L.pbdr_gpu_set_roles.argtypes = [vp, vp]
         for name in ("pbdr_gpu_gather", "pbdr_gpu_scatter"):
             getattr(L, name).argtypes = [vp, C.c_int, vp, i64, vp]
+        L.pbdr_pack_mesh.argtypes = [vp, C.c_int32, vp, C.c_int32, C.c_double, C.c_int, vp, i64, vp, vp, vp]
+        _lib = L
+    return _lib
+
+
+_host = None
+
+
+def host_lib() -> C.CDLL:
+    """Loads the host-only half of the ABI (no CUDA): scene generators,
+    splitmix64, pack_box and the last-error state."""
+    global _host
+    if _host is None:
+        if not os.path.exists(HOST_LIB_PATH):
+            raise ImportError(f"{HOST_LIB_PATH} is missing: run __graft_entry__.build()")
+        L = C.CDLL(HOST_LIB_PATH)
+        vp, i32, i64, dp = C.c_void_p, C.c_int32, C.c_int64, C.POINTER(C.c_double)
+        L.pbdr_last_error.restype = C.c_char_p
+        L.pbdr_last_error_key.restype = C.c_char_p
+        L.pbdr_last_error_payload.argtypes = [dp, C.POINTER(i64), C.POINTER(i32)]
         L.pbdr_scene_generate.argtypes = [C.c_int, C.c_uint64, i64, C.POINTER(vp)]
         L.pbdr_scene_generate_c4_shard.argtypes = [C.c_uint64, i64, i64, C.POINTER(vp)]
         L.pbdr_scene_view.argtypes = [vp, C.POINTER(SceneDesc), C.POINTER(SolverCfg)]
@@ -174,20 +197,19 @@ def lib() -> C.CDLL:
         L.pbdr_scene_free.argtypes = [vp]
         L.pbdr_scene_free.restype = None
         L.pbdr_pack_box.argtypes = [C.c_double, C.c_double, C.c_double, C.c_int, vp, vp]
-        L.pbdr_pack_mesh.argtypes = [vp, C.c_int32, vp, C.c_int32, C.c_double, C.c_int, vp, i64, vp, vp, vp]
         L.pbdr_rng_u64.argtypes = [C.c_uint64, C.c_int, vp]
         L.pbdr_rng_u64.restype = None
         L.pbdr_rng_unit.argtypes = [C.c_uint64, C.c_int, vp]
         L.pbdr_rng_unit.restype = None
-        _lib = L
-    return _lib
+        _host = L
+    return _host
 
 
 def raise_status(status: int):
     """Maps a C-ABI status to the matching pbdr exception (errors.hpp:8-44)."""
     if status == OK:
         return
-    L = lib()
+    L = host_lib()
     msg = L.pbdr_last_error().decode(errors="replace")
     axis = (C.c_double * 3)()
     frame = C.c_int64()
@@ -344,10 +366,11 @@ def scene_with_programs(src, programs) -> "ArrayScene":
 
 
 class GeneratedScene:
-    """One of the five BASELINE.json configs, built by the library's host generator."""
+    """One of the five BASELINE.json configs, built by the host generator
+    (libpbdr_host.so: no CUDA, so the CPU arms can use it too)."""
 
     def __init__(self, config_id: int, seed: int = 0, scale: int = 0, c4_first_scene: int | None = None):
-        L = lib()
+        L = host_lib()
         h = C.c_void_p()
         if c4_first_scene is None:
             st = L.pbdr_scene_generate(config_id, seed, scale, C.byref(h))
@@ -385,7 +408,7 @@ class GeneratedScene:
 
     def close(self):
         if getattr(self, "_h", None):
-            lib().pbdr_scene_free(self._h)
+            host_lib().pbdr_scene_free(self._h)
             self._h = None
 
     def __del__(self):
@@ -513,6 +536,15 @@ class GpuSolver:
         vel = None if vel is None else np.ascontiguousarray(vel, np.float64)
         raise_status(lib().pbdr_gpu_write_particles(self._h, _ptr(pos), _ptr(vel)))
 
+    def set_time(self, substep: int):
+        """Simulation time as a substep index (ForceProgram windows, error frames)."""
+        raise_status(lib().pbdr_gpu_set_time(self._h, substep))
+
+    def get_time(self) -> int:
+        t = C.c_int64()
+        raise_status(lib().pbdr_gpu_get_time(self._h, C.byref(t)))
+        return t.value
+
     def read_bodies(self):
         out = np.zeros((self.nb, 13), np.float64)
         raise_status(lib().pbdr_gpu_read_bodies(self._h, _ptr(out)))
@@ -580,7 +612,7 @@ def pack_box(half_extents, n):
     """geometry.cpp:32-55 pack_box through the library's host helper."""
     c = np.empty((n ** 3, 3), np.float64)
     r = C.c_double()
-    raise_status(lib().pbdr_pack_box(half_extents[0], half_extents[1], half_extents[2], n, _ptr(c), C.byref(r)))
+    raise_status(host_lib().pbdr_pack_box(half_extents[0], half_extents[1], half_extents[2], n, _ptr(c), C.byref(r)))
     return c, r.value
 
 
@@ -601,13 +633,13 @@ def pack_mesh(vertices, triangles, radius, device: int = 0):
 
 def rng_u64(seed, count):
     out = np.empty(count, np.uint64)
-    lib().pbdr_rng_u64(seed, count, _ptr(out))
+    host_lib().pbdr_rng_u64(seed, count, _ptr(out))
     return out
 
 
 def rng_unit(seed, count):
     out = np.empty(count, np.float64)
-    lib().pbdr_rng_unit(seed, count, _ptr(out))
+    host_lib().pbdr_rng_unit(seed, count, _ptr(out))
     return out
 
 

@@ -24,14 +24,24 @@ def declared_functions():
 def test_library_exports_every_declared_symbol(pbdr):
     names = declared_functions()
     assert len(names) >= 30
-    out = subprocess.run(["nm", "-D", "--defined-only", P.LIB_PATH], capture_output=True, text=True).stdout
-    exported = set(line.split()[-1] for line in out.splitlines() if line.strip())
+    exported = set()
+    for path in (P.LIB_PATH, P.HOST_LIB_PATH):  # the CUDA library and its host-only half
+        out = subprocess.run(["nm", "-D", "--defined-only", path], capture_output=True, text=True).stdout
+        exported |= set(line.split()[-1] for line in out.splitlines() if line.strip())
     missing = [n for n in names if n not in exported]
     assert not missing, missing
     L = pbdr.lib()
     for n in names:
         getattr(L, n)
     assert L.pbdr_abi_version() == 1
+
+
+def test_host_library_has_no_cuda(pbdr):
+    # The CPU reference arm builds its inputs through libpbdr_host.so alone.
+    out = subprocess.run(["ldd", P.HOST_LIB_PATH], capture_output=True, text=True).stdout
+    assert "cuda" not in out and "pbdr_gpu" not in out
+    deps = subprocess.run(["ldd", P.LIB_PATH], capture_output=True, text=True).stdout
+    assert "libpbdr_host.so" in deps
 
 
 def test_library_is_sm100a_only(pbdr):

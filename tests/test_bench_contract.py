@@ -27,3 +27,16 @@ def test_reference_arm_other_ranks_are_silent():
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
                           "--warmup", "1"], capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
     assert out.returncode == 0 and out.stdout.strip() == ""
+
+
+def test_reference_arm_maps_no_cuda_library():
+    # The reference arm builds its sample with the host-only generator and runs
+    # the oracle: libpbdr_gpu.so (the product) must never be mapped.
+    code = ("import sys, runpy; sys.argv = ['bench.py', '--impl', 'reference', '--steps', '1', '--warmup', '1', "
+            "'--config', '1']\n"
+            "runpy.run_path('bench.py', run_name='__main__')\n"
+            "maps = open('/proc/self/maps').read()\n"
+            "assert 'libpbdr_gpu' not in maps, 'CUDA library mapped'\n"
+            "assert 'liboracle' in maps and 'libpbdr_host' in maps\n")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]

@@ -1,0 +1,129 @@
+"""Oracle parity at the BASELINE sizes (north_star bars on the real inputs).
+
+Configs 3, 4 and 5 at their full size -- 8192 bodies (2.98M particles), 4096
+scenes (14.2M) and 131,072 cubes (67.1M) -- step one substep through the
+library's default execution path (pbdr_gpu_step: the persistent multi-tile
+iteration grid with next-tile table prefetch, isolated-tile split, scene
+clusters, whatever the handle picks) and are compared with the CPU oracle on
+the same seeded inputs:
+
+* hash-cell assignment of every particle and the contact-candidate set of
+  every particle: bit-exact (north_star);
+* positions and velocities after the substep: max |dx| <= 1e-5 m (north_star),
+  and in fact bit-exact (P1-P8).
+
+Each config is checked twice: from the generated scene (frame 0) and after a
+GPU pre-roll into the landed, contact-rich pile (the GPU state, anchors and
+warm-start rotations are uploaded into the oracle first). Configs 3 and 4 are
+also compared after one whole frame (10 substeps, the CUDA-graph frame path
+with the next substep's integrate fused into the last iteration launch).
+
+The small-scene suite reaches the persistent-grid path only through
+PBDR_ITER_GRID_CAP (test_persistent_grid_path below): at full size it is the
+default. Host memory: the C5 cases hold ~40 GB (oracle state plus the
+candidate lists of both sides).
+"""
+import gc
+import os
+
+import numpy as np
+import pytest
+
+from paper_2603_14634_b200 import pbdr as P
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+# config -> frames of GPU pre-roll for the landed case (inside each config's run)
+LANDED = {3: 300, 4: 150, 5: 80}
+
+
+def assert_same(a, b, what):
+    if not np.array_equal(a, b):
+        diff = np.abs(a.astype(np.float64) - b.astype(np.float64))
+        idx = np.unravel_index(np.argmax(diff), diff.shape)
+        raise AssertionError(f"{what}: {np.count_nonzero(diff)} differ, max {diff.max():.3g} at {idx}")
+
+
+def compare_candidates(gpu, orc):
+    gcnt, glst = gpu.debug_candidates()
+    ocnt, olst = orc.read_candidates()
+    assert_same(gcnt, ocnt, "candidate counts")
+    invalid = np.arange(P.NBR_CAP)[None, :] >= gcnt[:, None]
+    np.putmask(glst, invalid, -1)
+    np.putmask(olst, invalid, -1)
+    assert_same(glst, olst, "candidate lists")
+    pairs = int(gcnt.sum())
+    del glst, olst, invalid
+    gc.collect()
+    return pairs
+
+
+def compare_state(gpu, orc, what):
+    gp, gv = gpu.read_f32()
+    op, ov = orc.read_f32()
+    assert np.abs(gp[:, :3].astype(np.float64) - op[:, :3]).max() <= 1e-5, what  # north_star bar
+    assert_same(gp, op, f"{what}: positions")
+    assert_same(gv, ov, f"{what}: velocities")
+
+
+@pytest.mark.parametrize("when", ["start", "landed"])
+@pytest.mark.parametrize("cid", [3, 4, 5])
+def test_fullsize_one_substep(pbdr, pyoracle, cid, when):
+    g = P.GeneratedScene(cid)
+    gpu = P.GpuSolver(g.desc, g.cfg)
+    orc = pyoracle.Oracle(g.desc, g.cfg)
+    if when == "landed":
+        gpu.step_frames(LANDED[cid])
+        p4, v4 = gpu.read_f32()
+        orc.write_f32(p4, v4)
+        orc.write_anchor(gpu.debug_anchor())
+        orc.write_rquat(gpu.debug_rquat())
+        del p4, v4
+    # The library's own substep path (not the per-iteration replay hook).
+    gpu.step(1)
+    orc.integrate()
+    orc.candidates()
+    assert_same(gpu.debug_keys()[0], orc.keys()[0], "cell hash")
+    pairs = compare_candidates(gpu, orc)
+    if when == "landed":
+        assert pairs > 0, "expected contacts in the landed pile"
+    for _ in range(g.cfg.solver_iterations):
+        orc.iteration()
+    orc.end_substep()
+    compare_state(gpu, orc, f"C{cid} {when}, one substep")
+    assert_same(gpu.debug_anchor(), orc.read_anchor(), "anchors")
+    assert_same(gpu.debug_rquat(), orc.read_rquat(), "warm-start rotations")
+
+
+@pytest.mark.parametrize("cid", [3, 4])
+def test_fullsize_one_frame(pbdr, pyoracle, cid):
+    g = P.GeneratedScene(cid)
+    gpu = P.GpuSolver(g.desc, g.cfg)
+    orc = pyoracle.Oracle(g.desc, g.cfg)
+    gpu.step_frames(1)  # graph replay; fused next-substep integrate
+    assert orc.step(g.cfg.substeps) == 0
+    compare_state(gpu, orc, f"C{cid}, one frame")
+    assert_same(gpu.read_bodies(), orc.body_stats(), "body stats")
+
+
+@pytest.mark.parametrize("cid,scale,frames", [(3, 250, 200), (5, 6, 40), (2, 0, 60)])
+def test_persistent_grid_path(pbdr, pyoracle, monkeypatch, cid, scale, frames):
+    # The persistent iteration grid (a CTA loops over tiles claimed from a
+    # counter and prefetches the next tile's descriptors and body table) only
+    # engages when tiles outnumber resident CTAs. Capping the grid at 4 CTAs
+    # makes these small scenes take it, through landing and body-body contact,
+    # with the cooperative one-wave path off.
+    monkeypatch.setenv("PBDR_ITER_GRID_CAP", "4")
+    monkeypatch.setenv("PBDR_COOP_ITERS", "0")
+    g = P.GeneratedScene(cid, scale=scale)
+    gpu = P.GpuSolver(g.desc, g.cfg)
+    assert gpu.info.num_ctas > 4
+    orc = pyoracle.Oracle(g.desc, g.cfg)
+    gpu.step_frames(frames)
+    assert orc.step(frames * g.cfg.substeps) == 0
+    compare_state(gpu, orc, f"C{cid} capped grid, {frames} frames")
+    gpu.debug_prologue()
+    assert gpu.debug_candidates()[0].sum() > 0, "expected contacts by now"
+    monkeypatch.delenv("PBDR_ITER_GRID_CAP")
+    g1 = P.GeneratedScene(1)
+    P.GpuSolver(g1.desc, g1.cfg).close()  # restores the uncapped grid for later handles
