@@ -22,7 +22,7 @@ NVFLAGS  := $(ARCH) -std=c++17 -O3 -lineinfo --fmad=false -Xcompiler -fPIC,-ffp-
             -Xptxas -v -Iinclude -I$(CSRC)
 CU_SRC   := $(CSRC)/pbdr_kernels.cu $(CSRC)/pbdr_sort.cu $(CSRC)/pbdr_engine.cu $(CSRC)/pbdr_mesh.cu
 CXX_SRC  := $(CSRC)/pbdr_dropin.cpp
-HOST_SRC := $(CSRC)/pbdr_scene.cpp $(CSRC)/pbdr_errors.cpp
+HOST_SRC := $(CSRC)/pbdr_scene.cpp $(CSRC)/pbdr_errors.cpp $(CSRC)/pbdr_hostmath.cpp $(CSRC)/pbdr_body.cpp
 HDRS     := include/pbdr_gpu.h $(wildcard include/pbdr/*.hpp) $(wildcard $(CSRC)/*.h) $(wildcard $(CSRC)/*.cuh)
 OBJDIR   := build/obj
 CU_OBJ   := $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(CU_SRC))
@@ -30,7 +30,7 @@ CXX_OBJ  := $(patsubst $(CSRC)/%.cpp,$(OBJDIR)/%.o,$(CXX_SRC))
 HOST_OBJ := $(patsubst $(CSRC)/%.cpp,$(OBJDIR)/%.o,$(HOST_SRC))
 
 .PHONY: all lib oracle ref clean
-all: lib oracle build/test_dropin
+all: lib oracle build/test_dropin build/libdropin_shim.so
 
 lib: $(HOST_LIB) $(LIB)
 
@@ -61,6 +61,16 @@ ref:
 build/test_dropin: tests/cpp/test_dropin.cpp $(LIB) $(HDRS)
 	@mkdir -p build
 	$(CXX) -std=c++17 -O2 -Iinclude tests/cpp/test_dropin.cpp -o $@ \
+	    -L$(PKG)/lib -lpbdr_gpu -lpbdr_host -Wl,-rpath,'$$ORIGIN/../$(PKG)/lib'
+
+# Test infrastructure: the oracle's extern "C" shim over the reference's public
+# math/body/geometry API (oracle/ref_shim.cpp), compiled UNCHANGED against this
+# repository's drop-in headers (include/pbdr/*.hpp) and libraries instead of the
+# reference's. tests/test_dropin_headers.py compares it with the same shim
+# built on the reference's own code (oracle/_ref/libpbdr_ref.so).
+build/libdropin_shim.so: oracle/ref_shim.cpp $(HOST_LIB) $(LIB) $(HDRS)
+	@mkdir -p build
+	$(CXX) -std=c++20 -O2 -fPIC -shared -Wall -Wextra -Iinclude oracle/ref_shim.cpp -o $@ \
 	    -L$(PKG)/lib -lpbdr_gpu -lpbdr_host -Wl,-rpath,'$$ORIGIN/../$(PKG)/lib'
 
 clean:

@@ -81,38 +81,48 @@ def olib():
     return _olib
 
 
+def _bind_ref_api(L):
+    vp = C.c_void_p
+    L.ref_rng_u64.argtypes = [C.c_uint64, C.c_int, vp]
+    L.ref_pack_mesh.argtypes = [vp, C.c_int, vp, C.c_int, C.c_double, vp, C.c_long, vp, vp, vp]
+    L.ref_rng_u64.restype = None
+    L.ref_rng_unit.argtypes = [C.c_uint64, C.c_int, vp]
+    L.ref_rng_unit.restype = None
+    L.ref_pack_box.argtypes = [C.c_double, C.c_double, C.c_double, C.c_int, vp, vp]
+    L.ref_polar.argtypes = [vp, vp, vp, vp, C.c_double]
+    L.ref_sym_eigen.argtypes = [vp, vp, vp]
+    L.ref_invert_spd.argtypes = [vp, vp, vp]
+    L.ref_pseudo_invert_spd.argtypes = [vp, vp, vp, vp]
+    L.ref_inverse.argtypes = [vp, vp]
+    L.ref_body_props.argtypes = [C.c_int, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+    L.ref_extract_pose.argtypes = [C.c_int, vp, vp, vp, vp, vp]
+    L.ref_distribute_wrench.argtypes = [C.c_int, vp, vp, vp, vp, vp, vp]
+    L.ref_geodesic_deg.argtypes = [vp, vp]
+    L.ref_geodesic_deg.restype = C.c_double
+    L.ref_unwrapped_deg.argtypes = [vp, vp]
+    L.ref_unwrapped_deg.restype = C.c_double
+    L.ref_quat_to_matrix.argtypes = [vp, vp]
+    L.ref_quat_to_matrix.restype = None
+    L.ref_matrix_to_quat.argtypes = [vp, vp]
+    L.ref_matrix_to_quat.restype = None
+    return L
+
+
 def rlib():
     """The reference's own math/body/geometry (oracle/_ref); None when not built."""
     global _rlib
     if _rlib is None:
         if not os.path.exists(REF_PATH):
             return None
-        L = C.CDLL(REF_PATH)
-        vp = C.c_void_p
-        L.ref_rng_u64.argtypes = [C.c_uint64, C.c_int, vp]
-        L.ref_pack_mesh.argtypes = [vp, C.c_int, vp, C.c_int, C.c_double, vp, C.c_long, vp, vp, vp]
-        L.ref_rng_u64.restype = None
-        L.ref_rng_unit.argtypes = [C.c_uint64, C.c_int, vp]
-        L.ref_rng_unit.restype = None
-        L.ref_pack_box.argtypes = [C.c_double, C.c_double, C.c_double, C.c_int, vp, vp]
-        L.ref_polar.argtypes = [vp, vp, vp, vp, C.c_double]
-        L.ref_sym_eigen.argtypes = [vp, vp, vp]
-        L.ref_invert_spd.argtypes = [vp, vp, vp]
-        L.ref_pseudo_invert_spd.argtypes = [vp, vp, vp, vp]
-        L.ref_inverse.argtypes = [vp, vp]
-        L.ref_body_props.argtypes = [C.c_int, vp, vp, vp, vp, vp, vp, vp, vp, vp]
-        L.ref_extract_pose.argtypes = [C.c_int, vp, vp, vp, vp, vp]
-        L.ref_distribute_wrench.argtypes = [C.c_int, vp, vp, vp, vp, vp, vp]
-        L.ref_geodesic_deg.argtypes = [vp, vp]
-        L.ref_geodesic_deg.restype = C.c_double
-        L.ref_unwrapped_deg.argtypes = [vp, vp]
-        L.ref_unwrapped_deg.restype = C.c_double
-        L.ref_quat_to_matrix.argtypes = [vp, vp]
-        L.ref_quat_to_matrix.restype = None
-        L.ref_matrix_to_quat.argtypes = [vp, vp]
-        L.ref_matrix_to_quat.restype = None
-        _rlib = L
+        _rlib = _bind_ref_api(C.CDLL(REF_PATH))
     return _rlib
+
+
+def ref_api(path):
+    """ref_shim.cpp's extern "C" functions from any build of it: the
+    reference's own code (oracle/_ref) or the product's drop-in headers and
+    libraries (build/libdropin_shim.so)."""
+    return _bind_ref_api(C.CDLL(path))
 
 
 class Oracle:

@@ -1,8 +1,13 @@
-// Implementation of the C++ drop-in layer (include/pbdr/pbdr_b200.hpp) on top
-// of the C-ABI. Conversions only: all simulation work runs in the CUDA kernels.
+// Implementation of the C++ drop-in's solver layer (include/pbdr/solver.hpp,
+// pack_mesh of geometry.hpp) on top of the C-ABI. Conversions only: all
+// simulation work runs in the CUDA kernels. The host helpers (math, body,
+// scene set-up) live in libpbdr_host.so (csrc/pbdr_hostmath.cpp, pbdr_body.cpp).
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstring>
+#include <memory>
+#include <string>
 #include <vector>
 
 #include "pbdr/pbdr_b200.hpp"
@@ -10,7 +15,10 @@
 namespace pbdr {
 
 void throw_last_error(int status) {
-  const std::string msg = pbdr_last_error();
+  // The C-ABI message is already formatted like the reference's what()
+  // strings; the exception constructors add the key prefix / frame suffix
+  // again, so they get the bare message.
+  std::string msg = pbdr_last_error();
   double axis[3] = {0, 0, 0};
   int64_t frame = -1;
   int32_t body = -1;
@@ -20,8 +28,18 @@ void throw_last_error(int status) {
     case PBDR_ERR_RANK_DEFICIENT: throw RankDeficientError(msg, axis[0], axis[1], axis[2]);
     case PBDR_ERR_EMPTY_PACKING: throw EmptyPackingError(msg);
     case PBDR_ERR_INVALID_MOMENT: throw InvalidMomentError(msg);
-    case PBDR_ERR_CONFIG: throw ConfigError(pbdr_last_error_key(), msg);
-    case PBDR_ERR_SIMULATION: throw SimulationError(msg, static_cast<long>(frame));
+    case PBDR_ERR_CONFIG: {
+      const std::string key = pbdr_last_error_key();
+      const std::string prefix = "config key '" + key + "': ";
+      if (msg.compare(0, prefix.size(), prefix) == 0) msg.erase(0, prefix.size());
+      throw ConfigError(key, msg);
+    }
+    case PBDR_ERR_SIMULATION: {
+      const std::string suffix = " (frame " + std::to_string(frame) + ")";
+      if (msg.size() >= suffix.size() && msg.compare(msg.size() - suffix.size(), suffix.size(), suffix) == 0)
+        msg.erase(msg.size() - suffix.size());
+      throw SimulationError(msg, static_cast<long>(frame));
+    }
     default: throw Error(msg);
   }
 }
@@ -31,53 +49,6 @@ static void check(int status) {
 }
 
 namespace {
-
-// Largest/middle eigenvalue test for a chain-like rest shape (body.cpp:39-46
-// semantics): collinear when the middle principal second moment is negligible.
-void collinearity(const std::vector<Vec3>& q, const std::vector<double>& m, Body& b) {
-  double S[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
-  for (size_t k = 0; k < q.size(); ++k) {
-    const double v[3] = {q[k].x, q[k].y, q[k].z};
-    for (int i = 0; i < 3; ++i)
-      for (int j = 0; j < 3; ++j) S[i][j] += m[k] * v[i] * v[j];
-  }
-  double V[3][3] = {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}};
-  for (int sweep = 0; sweep < 32; ++sweep) {
-    const double off = std::fabs(S[0][1]) + std::fabs(S[0][2]) + std::fabs(S[1][2]);
-    if (off <= 1e-15 * (std::fabs(S[0][0]) + std::fabs(S[1][1]) + std::fabs(S[2][2]) + 1e-300)) break;
-    for (int p = 0; p < 2; ++p)
-      for (int r = p + 1; r < 3; ++r) {
-        if (S[p][r] == 0.0) continue;
-        const double th = (S[r][r] - S[p][p]) / (2 * S[p][r]);
-        const double t = (th >= 0 ? 1.0 : -1.0) / (std::fabs(th) + std::sqrt(th * th + 1));
-        const double c = 1 / std::sqrt(t * t + 1), s = t * c;
-        for (int k = 0; k < 3; ++k) {
-          const double a = S[k][p], bb = S[k][r];
-          S[k][p] = c * a - s * bb;
-          S[k][r] = s * a + c * bb;
-        }
-        for (int k = 0; k < 3; ++k) {
-          const double a = S[p][k], bb = S[r][k];
-          S[p][k] = c * a - s * bb;
-          S[r][k] = s * a + c * bb;
-        }
-        for (int k = 0; k < 3; ++k) {
-          const double a = V[k][p], bb = V[k][r];
-          V[k][p] = c * a - s * bb;
-          V[k][r] = s * a + c * bb;
-        }
-      }
-  }
-  int idx[3] = {0, 1, 2};
-  std::sort(idx, idx + 3, [&](int a, int c) { return S[a][a] < S[c][c]; });
-  const double mid = S[idx[1]][idx[1]], top = S[idx[2]][idx[2]];
-  if (mid <= 1e-8 * std::max(top, 1e-300)) {
-    b.collinear = true;
-    const int k = idx[2];
-    const double n = std::sqrt(V[0][k] * V[0][k] + V[1][k] * V[1][k] + V[2][k] * V[2][k]);
-    b.rest_axis = {V[0][k] / n, V[1][k] / n, V[2][k] / n};
-  }
-}
 
 struct Flat {
   std::vector<double> pos, vel, inv_mass, radius, rest, mass, com;
@@ -175,29 +146,6 @@ pbdr_solver_cfg to_c(const SolverConfig& c) {
 
 }  // namespace
 
-Body make_body(const std::vector<Particle>& particles, const std::vector<int>& indices) {
-  if (indices.empty()) throw Error("make_body: empty particle set");
-  Body b;
-  b.particle_indices = indices;
-  double mass = 0;
-  Vec3 wsum{0, 0, 0};
-  std::vector<double> m;
-  m.reserve(indices.size());
-  for (int i : indices) {
-    const Particle& p = particles.at(static_cast<size_t>(i));
-    if (!(p.inv_mass > 0)) throw Error("pinned particles are not supported in rigid bodies");
-    const double mi = 1.0 / p.inv_mass;
-    m.push_back(mi);
-    mass += mi;
-    wsum += p.position * mi;
-  }
-  b.total_mass = mass;
-  b.rest_com = wsum / mass;
-  for (int i : indices) b.rest_offsets.push_back(particles[static_cast<size_t>(i)].position - b.rest_com);
-  collinearity(b.rest_offsets, m, b);
-  return b;
-}
-
 SpherePacking pack_mesh(const TriMesh& mesh, double radius, int device) {
   std::vector<double> v;
   v.reserve(3 * mesh.vertices.size());
@@ -225,60 +173,7 @@ SpherePacking pack_mesh(const TriMesh& mesh, double radius, int device) {
   return p;
 }
 
-int add_packed_body(Scene& scene, const std::vector<Vec3>& centers, double radius,
-                    double total_mass, const Rotation& rotate, const Vec3& translate,
-                    double jitter, uint64_t seed) {
-  if (centers.empty()) throw EmptyPackingError("add_packed_body: empty packing");
-  if (!(total_mass > 0)) throw ConfigError("total_mass", "must be > 0");
-  const int id = static_cast<int>(scene.bodies.size());
-  const double inv_mass = static_cast<double>(centers.size()) / total_mass;
-  uint64_t state = seed + 0x9E3779B97F4A7C15ull;  // splitmix64 (rng.hpp:10-29)
-  auto unit = [&]() {
-    state += 0x9E3779B97F4A7C15ull;
-    uint64_t z = state;
-    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-    z = z ^ (z >> 31);
-    return static_cast<double>(z >> 11) * (1.0 / 9007199254740992.0);
-  };
-  std::vector<int> idx;
-  for (const Vec3& c : centers) {
-    Particle p;
-    p.position = rotate.rotate(c) + translate;
-    if (jitter > 0) {
-      const double jx = -jitter + 2 * jitter * unit();
-      const double jy = -jitter + 2 * jitter * unit();
-      const double jz = -jitter + 2 * jitter * unit();
-      p.position += Vec3{jx, jy, jz};
-    }
-    p.inv_mass = inv_mass;
-    p.radius = radius;
-    p.body_id = id;
-    idx.push_back(static_cast<int>(scene.particles.size()));
-    scene.particles.push_back(p);
-  }
-  scene.bodies.push_back(make_body(scene.particles, idx));
-  if (!scene.programs.empty()) scene.programs.emplace_back();
-  if (!scene.body_scene.empty()) scene.body_scene.push_back(0);
-  return id;
-}
-
-void SolverConfig::validate() const {
-  if (!(frame_rate > 0)) throw ConfigError("frame_rate", "must be > 0");
-  if (substeps < 1) throw ConfigError("substeps", "must be >= 1");
-  if (solver_iterations < 1) throw ConfigError("solver_iterations", "must be >= 1");
-}
-
-void Scene::validate() const {
-  const double nn = std::sqrt(ground.normal.x * ground.normal.x + ground.normal.y * ground.normal.y +
-                              ground.normal.z * ground.normal.z);
-  if (std::fabs(nn - 1.0) > 1e-9) throw ConfigError("ground.normal", "must be unit length");
-  if (ground.friction < 0) throw ConfigError("ground.friction", "must be >= 0");
-  if (!programs.empty() && programs.size() != bodies.size())
-    throw ConfigError("programs", "must be parallel to bodies");
-}
-
-Solver::Solver(const Scene& scene, const SolverConfig& cfg, int device) {
+Solver::Solver(const Scene& scene, const SolverConfig& cfg, int device) : dt_(cfg.dt()) {
   scene.validate();
   cfg.validate();
   Flat f;
@@ -292,25 +187,49 @@ Solver::~Solver() { pbdr_gpu_destroy(h_); }
 void Solver::step(long substeps) { check(pbdr_gpu_step(h_, substeps)); }
 void Solver::step_frames(long frames) { check(pbdr_gpu_step_frames(h_, frames)); }
 
-void Solver::download(Scene& scene) const {
-  const size_t n = scene.particles.size();
-  std::vector<double> p(3 * n), v(3 * n);
-  check(pbdr_gpu_read_particles(h_, p.data(), v.data()));
-  for (size_t i = 0; i < n; ++i) {
-    scene.particles[i].position = {p[3 * i], p[3 * i + 1], p[3 * i + 2]};
-    scene.particles[i].velocity = {v[3 * i], v[3 * i + 1], v[3 * i + 2]};
-  }
-}
+namespace {
 
-void Solver::upload(const Scene& scene) {
+void pack_state(const Scene& scene, std::vector<double>& p, std::vector<double>& v) {
   const size_t n = scene.particles.size();
-  std::vector<double> p(3 * n), v(3 * n);
+  p.resize(3 * n);
+  v.resize(3 * n);
   for (size_t i = 0; i < n; ++i) {
     const Particle& q = scene.particles[i];
     p[3 * i] = q.position.x; p[3 * i + 1] = q.position.y; p[3 * i + 2] = q.position.z;
     v[3 * i] = q.velocity.x; v[3 * i + 1] = q.velocity.y; v[3 * i + 2] = q.velocity.z;
   }
+}
+
+void unpack_state(Scene& scene, const std::vector<double>& p, const std::vector<double>& v) {
+  for (size_t i = 0; i < scene.particles.size(); ++i) {
+    scene.particles[i].position = {p[3 * i], p[3 * i + 1], p[3 * i + 2]};
+    scene.particles[i].velocity = {v[3 * i], v[3 * i + 1], v[3 * i + 2]};
+  }
+}
+
+}  // namespace
+
+void Solver::download(Scene& scene) const {
+  std::vector<double> p(3 * scene.particles.size()), v(p.size());
+  check(pbdr_gpu_read_particles(h_, p.data(), v.data()));
+  unpack_state(scene, p, v);
+}
+
+void Solver::upload(const Scene& scene) {
+  std::vector<double> p, v;
+  pack_state(scene, p, v);
   check(pbdr_gpu_write_particles(h_, p.data(), v.data()));
+}
+
+void Solver::set_time(double t) {
+  if (!(t >= 0)) throw ConfigError("time", "must be >= 0");
+  check(pbdr_gpu_set_time(h_, static_cast<int64_t>(std::llround(t / dt_))));
+}
+
+double Solver::time() const {
+  int64_t k = 0;
+  check(pbdr_gpu_get_time(h_, &k));
+  return static_cast<double>(k) * dt_;
 }
 
 std::vector<pbdr_body_stats> Solver::body_stats() const {
@@ -327,10 +246,103 @@ pbdr_info Solver::info() const {
   return in;
 }
 
-void step(Scene& scene, const SolverConfig& cfg) {
-  Solver s(scene, cfg, 0);
-  s.step(1);
-  s.download(scene);
+namespace {
+
+// FNV-1a over raw bytes: fingerprints of the scene's static part (bodies,
+// masses, radii, programs, planes, config) and of the state step() wrote back.
+struct Fnv {
+  uint64_t h = 1469598103934665603ull;
+  void add(const void* data, size_t bytes) {
+    const unsigned char* b = static_cast<const unsigned char*>(data);
+    for (size_t i = 0; i < bytes; ++i) h = (h ^ b[i]) * 1099511628211ull;
+  }
+  template <typename T>
+  void pod(const T& x) { add(&x, sizeof x); }
+};
+
+uint64_t static_fingerprint(const Scene& s, const SolverConfig& c) {
+  Fnv f;
+  const pbdr_solver_cfg cc = to_c(c);
+  f.pod(cc);
+  const uint64_t n = s.particles.size(), nb = s.bodies.size();
+  f.pod(n);
+  f.pod(nb);
+  for (const Particle& p : s.particles) {
+    f.pod(p.inv_mass);
+    f.pod(p.radius);
+    f.pod(p.body_id);
+  }
+  for (const Body& b : s.bodies) {
+    f.add(b.particle_indices.data(), sizeof(int) * b.particle_indices.size());
+    f.add(b.rest_offsets.data(), sizeof(Vec3) * b.rest_offsets.size());
+    f.pod(b.total_mass);
+    f.pod(b.rest_com);
+  }
+  for (const ForceProgram& p : s.programs) {
+    f.pod(p.force);
+    f.pod(p.torque);
+    f.pod(p.t_start);
+    f.pod(p.t_stop);
+    f.pod(p.gravity_exempt);
+  }
+  const pbdr_plane g = to_c(s.ground);
+  f.pod(g);
+  f.pod(s.has_ground);
+  f.pod(s.contact_relaxation);
+  for (const Plane& w : s.walls) {
+    const pbdr_plane pw = to_c(w);
+    f.pod(pw);
+  }
+  f.add(s.body_scene.data(), sizeof(int) * s.body_scene.size());
+  return f.h;
+}
+
+uint64_t state_fingerprint(const std::vector<double>& p, const std::vector<double>& v) {
+  Fnv f;
+  f.add(p.data(), sizeof(double) * p.size());
+  f.add(v.data(), sizeof(double) * v.size());
+  return f.h;
+}
+
+// One cached device handle per thread for the stateless step().
+struct StepCache {
+  const Scene* scene = nullptr;
+  uint64_t statics = 0;
+  uint64_t written = 0;  // fingerprint of the state the last call wrote back
+  std::unique_ptr<Solver> solver;
+};
+thread_local StepCache g_step;
+
+}  // namespace
+
+void step(Scene& scene, const SolverConfig& cfg, double t) {
+  StepCache& c = g_step;
+  const uint64_t statics = static_fingerprint(scene, cfg);
+  std::vector<double> p, v;
+  pack_state(scene, p, v);
+  const bool same_scene = c.solver && c.scene == &scene && c.statics == statics;
+  if (!same_scene) {
+    c.solver.reset();  // free the previous scene's device memory first
+    c.solver = std::make_unique<Solver>(scene, cfg, 0);
+    c.scene = &scene;
+    c.statics = statics;
+    if (t > 0) c.solver->set_time(t);
+  } else if (t >= 0 || state_fingerprint(p, v) != c.written) {
+    // A new state (or an explicit clock): the step of a fresh handle on it.
+    c.solver->upload(scene);
+    c.solver->set_time(t >= 0 ? t : 0.0);
+  }  // else: continue from the device state and clock this call left
+  c.written = 0;
+  try {
+    c.solver->step(1);
+  } catch (...) {
+    c.solver.reset();  // a failed step leaves the device error record set
+    c.scene = nullptr;
+    throw;
+  }
+  c.solver->download(scene);
+  pack_state(scene, p, v);
+  c.written = state_fingerprint(p, v);
 }
 
 }  // namespace pbdr

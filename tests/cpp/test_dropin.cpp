@@ -5,9 +5,15 @@
 #include <cmath>
 #include <algorithm>
 #include <cstdio>
+#include <string>
 #include <vector>
 
-#include "pbdr/pbdr_b200.hpp"
+// The reference's own include paths (proj/include/pbdr/...), unchanged.
+#include "pbdr/body.hpp"
+#include "pbdr/errors.hpp"
+#include "pbdr/math.hpp"
+#include "pbdr/scene.hpp"
+#include "pbdr/solver.hpp"
 
 namespace {
 
@@ -110,6 +116,97 @@ void config_errors() {
   EXPECT(threw, "kDouble must raise ConfigError('precision')");
 }
 
+// step(scene, cfg) -> scene at t + dt. Stateless calls carry the
+// clock: a force window [10 dt, 11 dt) opens on the 11th consecutive call,
+// exactly as in a resident Solver; an explicit t starts the clock there.
+void stateless_step_carries_time() {
+  pbdr::SolverConfig cfg;
+  cfg.gravity = 0.0;
+  const double dt = cfg.dt();
+  auto make = [&]() {
+    pbdr::Scene s;
+    s.has_ground = false;
+    pbdr::add_packed_body(s, lattice(3, 0.05), 0.05, 1.0, pbdr::Rotation(), {0, 0, 1}, 0.0, 0);
+    s.programs.resize(1);
+    s.programs[0].force = {2.0, 0, 0};
+    s.programs[0].t_start = 10 * dt;
+    s.programs[0].t_stop = 11 * dt;
+    return s;
+  };
+  pbdr::Scene a = make();
+  for (int k = 0; k < 12; ++k) pbdr::step(a, cfg);
+  const pbdr::MomentumState ma = pbdr::compute_momentum(a.bodies[0], a.particles);
+  EXPECT(std::fabs(ma.linear.x - 2.0 * dt) < 1e-6, "window applied once: P_x = %.9g", ma.linear.x);
+  pbdr::Scene b = make();
+  pbdr::Solver solver(b, cfg);
+  solver.step(12);
+  solver.download(b);
+  double worst = 0;
+  for (size_t i = 0; i < a.particles.size(); ++i)
+    worst = std::max(worst, pbdr::norm(a.particles[i].position - b.particles[i].position));
+  EXPECT(worst == 0.0, "12 stateless steps == Solver::step(12) bit for bit (max |dx| %.3g)", worst);
+  EXPECT(std::fabs(solver.time() - 12 * dt) < 1e-12, "Solver::time %.9g", solver.time());
+  pbdr::Scene c = make();
+  pbdr::step(c, cfg, 10 * dt);  // explicit clock: the window is open for this step
+  const pbdr::MomentumState mc = pbdr::compute_momentum(c.bodies[0], c.particles);
+  EXPECT(std::fabs(mc.linear.x - 2.0 * dt) < 1e-6, "explicit t: P_x = %.9g", mc.linear.x);
+}
+
+// errors.hpp:32-44 message formats through the C-ABI.
+void error_formats() {
+  pbdr::Scene s;
+  s.has_ground = false;
+  pbdr::add_packed_body(s, lattice(2, 0.05), 0.05, 1.0, pbdr::Rotation(), {0, 0, 1}, 0.0, 0);
+  pbdr::SolverConfig cfg;
+  cfg.precision = pbdr::Precision::kDouble;
+  try {
+    pbdr::Solver solver(s, cfg);
+    EXPECT(false, "expected ConfigError");
+  } catch (const pbdr::ConfigError& e) {
+    const std::string w = e.what();
+    EXPECT(w.rfind("config key 'precision': ", 0) == 0 && w.find("config key", 5) == std::string::npos,
+           "ConfigError what() = %s", e.what());
+  }
+  // A NaN velocity: SimulationError "... (frame 0)" exactly once.
+  pbdr::Scene n;
+  n.has_ground = false;
+  pbdr::add_packed_body(n, lattice(3, 0.05), 0.05, 1.0, pbdr::Rotation(), {0, 0, 1}, 0.0, 0);
+  n.particles[3].velocity.x = std::nan("");
+  try {
+    pbdr::step(n, pbdr::SolverConfig{});
+    EXPECT(false, "expected SimulationError");
+  } catch (const pbdr::SimulationError& e) {
+    const std::string w = e.what();
+    EXPECT(e.frame_index == 0 && w.size() > 10 && w.compare(w.size() - 10, 10, " (frame 0)") == 0 &&
+               w.find("(frame", 0) == w.rfind("(frame"),
+           "SimulationError what() = %s", e.what());
+  }
+}
+
+// body.hpp helpers on a host scene (pinned against the reference's compiled
+// code in tests/test_dropin_headers.py): a cube rotated by R reports R.
+void host_helpers() {
+  pbdr::Scene s;
+  pbdr::add_packed_body(s, lattice(4, 0.025), 0.025, 4.0, pbdr::Rotation(), {0, 0, 1}, 0.0, 0);
+  const pbdr::Rotation R = pbdr::Rotation::axis_angle({1, 2, 3}, 0.7);
+  std::vector<pbdr::Particle> moved = s.particles;
+  for (auto& p : moved) p.position = R.rotate(p.position - pbdr::Vec3{0, 0, 1}) + pbdr::Vec3{1, 2, 3};
+  const pbdr::Pose pose = pbdr::extract_pose(s.bodies[0], moved);
+  EXPECT(pbdr::geodesic_angle_deg(pose.orientation, R) < 1e-6, "pose angle");
+  EXPECT(pbdr::norm(pose.com - pbdr::Vec3{1, 2, 3}) < 1e-12, "pose com");
+  const pbdr::Mat3 I = pbdr::compute_inertia(s.bodies[0], s.particles);
+  EXPECT(std::fabs(I(0, 0) - 0.025) < 1e-12, "I_xx = %.12g (SPEC.md: 0.025)", I(0, 0));
+  const auto f = pbdr::distribute_wrench(s.bodies[0], s.particles, {1, 0, 0}, {0, 0, 0.5});
+  pbdr::Vec3 F{0, 0, 0}, T{0, 0, 0};
+  const pbdr::Vec3 c = pbdr::compute_com(s.bodies[0], s.particles);
+  for (size_t k = 0; k < f.size(); ++k) {
+    F += f[k];
+    T += pbdr::cross(s.particles[k].position - c, f[k]);
+  }
+  EXPECT(pbdr::norm(F - pbdr::Vec3{1, 0, 0}) < 1e-12 && pbdr::norm(T - pbdr::Vec3{0, 0, 0.5}) < 1e-12,
+         "wrench sums");
+}
+
 }  // namespace
 
 int main() {
@@ -118,6 +215,9 @@ int main() {
     zero_delta_velocity();
     resting_box();
     config_errors();
+    stateless_step_carries_time();
+    error_formats();
+    host_helpers();
   } catch (const pbdr::Error& e) {
     std::printf("FAIL: uncaught pbdr::Error: %s\n", e.what());
     return 2;
