@@ -77,6 +77,16 @@ def olib():
         L.oracle_kat_body_iteration.restype = C.c_uint
         L.oracle_kat_momentum.argtypes = [C.c_int, vp, vp, vp, vp, vp, C.c_float, C.c_int, C.c_int, vp, vp, vp]
         L.oracle_kat_momentum.restype = C.c_uint
+        L.o64_create.argtypes = [vp, vp, C.c_int, C.POINTER(vp)]
+        L.o64_destroy.argtypes = [vp]
+        L.o64_destroy.restype = None
+        L.o64_step.argtypes = [vp, C.c_int64]
+        for name in ("o64_read", "o64_write"):
+            getattr(L, name).argtypes = [vp, vp, vp]
+            getattr(L, name).restype = None
+        L.o64_body_stats.argtypes = [vp, vp]
+        L.o64_body_stats.restype = None
+        L.o64_error.argtypes = [vp, vp, vp, vp]
         _olib = L
     return _olib
 
@@ -256,6 +266,62 @@ class Oracle:
     @property
     def cell_size(self):
         return olib().oracle_cell_size(self._h)
+
+
+class Oracle64:
+    """The independent fp64 restatement (oracle/pbdr_oracle64.cpp): plain
+    fp64 body sums, the reference's cold scaled-Newton polar and SPD
+    pseudo-inverse, caller particle order. Compared with the GPU at the
+    north_star tolerances, never bit for bit."""
+
+    def __init__(self, desc, cfg, threads: int = 0):
+        L = olib()
+        if threads <= 0:
+            threads = os.cpu_count() or 1
+        h = C.c_void_p()
+        st = L.o64_create(C.addressof(desc), C.addressof(cfg), threads, C.byref(h))
+        if st != 0:
+            raise RuntimeError(f"o64_create failed with status {st}")
+        self._h = h
+        self.n = desc.num_particles
+        self.nb = desc.num_bodies
+
+    def close(self):
+        if getattr(self, "_h", None):
+            olib().o64_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def step(self, substeps=1) -> int:
+        return olib().o64_step(self._h, substeps)
+
+    def read_particles(self):
+        p = np.empty((self.n, 3))
+        v = np.empty((self.n, 3))
+        olib().o64_read(self._h, _p(p), _p(v))
+        return p, v
+
+    def write_particles(self, pos=None, vel=None):
+        pos = None if pos is None else np.ascontiguousarray(pos, np.float64)
+        vel = None if vel is None else np.ascontiguousarray(vel, np.float64)
+        olib().o64_write(self._h, _p(pos), _p(vel))
+
+    def body_stats(self):
+        out = np.zeros((self.nb, 13))
+        olib().o64_body_stats(self._h, _p(out))
+        return out
+
+    def error(self):
+        bits = C.c_uint32()
+        body = C.c_int32()
+        axis = np.zeros(3)
+        olib().o64_error(self._h, C.byref(bits), C.byref(body), _p(axis))
+        return bits.value, body.value, axis
 
 
 def polar(a):

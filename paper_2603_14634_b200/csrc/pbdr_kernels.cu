@@ -180,6 +180,16 @@ __device__ __forceinline__ void bulk_g2s_stream(void* dst, const void* src, uint
 #endif
 }
 
+// Bulk prefetch of a byte range into L2 (no shared memory, no registers): the
+// next tile's staging ranges are pulled in while the current tile computes, so
+// its bulk copies hit L2. Address rounded down / size up to 16 B.
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  const uintptr_t a0 = a & ~uintptr_t(15);
+  const uint32_t sz = static_cast<uint32_t>((a - a0 + bytes + 15) & ~uintptr_t(15));
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"(sz) : "memory");
+}
+
 // Asynchronous global -> shared copies (no register staging) for the next
 // tile's body table.
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
@@ -895,6 +905,16 @@ __global__ void __launch_bounds__(128) k_neighbours(NeighbourArgs A) {
 // tiles, one-wave cooperative grids, or one cluster per batched scene), and
 // -- FUSE -- the substep's last iteration followed by the next integrate.
 // ---------------------------------------------------------------------------
+// PBDR_CAND_ROLLED: keep the candidate loop rolled (code size; the compiler
+// otherwise unrolls it 4x for each of the KP particles of a lane).
+#ifndef PBDR_CAND_ROLLED
+#define PBDR_CAND_ROLLED 0
+#endif
+// PBDR_PREFETCH_NEXT: after phase A, one lane pulls the next tile's staging
+// ranges (pos, vel, rest) and its candidate counts into L2.
+#ifndef PBDR_PREFETCH_NEXT
+#define PBDR_PREFETCH_NEXT 0
+#endif
 // Pinned fused multiply-adds (P8): only these explicit fmaf() are
 // contracted (the library builds with --fmad=false); the oracle uses std::fmaf
 // at the same places, and IEEE fma is correctly rounded on both sides.
@@ -991,6 +1011,9 @@ __device__ __forceinline__ void phase_a_particle(const IterArgs& A, int it, int6
     }
   }
   float dPP[3] = {0.0f, 0.0f, 0.0f};
+#if PBDR_CAND_ROLLED
+#pragma unroll 1
+#endif
   for (int c = 0; c < nc; ++c) {
     const int j = A.cand_j[static_cast<int64_t>(c) * A.n + p];
     const float rr = A.cand_rr[static_cast<int64_t>(c) * A.n + p];
@@ -1423,6 +1446,15 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
     if ((lane & 1) == 0) s_part[warp][lane >> 1] = t16;
     if ((lane & 3) == 0 && (lane >> 2) < 5) s_part[warp][16 + (lane >> 2)] = t5;
   }
+#if PBDR_PREFETCH_NEXT
+  if (it == 0 && warp == kWarps - 1 && lane == 0 && tile_next < ntiles) {
+    const uint32_t bytes = static_cast<uint32_t>(cd_n.y) * 16u;
+    bulk_prefetch_l2(A.pos_in + cd_n.x, bytes);
+    bulk_prefetch_l2(A.vel + cd_n.x, bytes);
+    bulk_prefetch_l2(A.rest + cd_n.x, bytes);
+    bulk_prefetch_l2(A.ncand + cd_n.x, static_cast<uint32_t>(cd_n.y) * 4u);
+  }
+#endif
   __syncthreads();
   if (tm && threadIdx.x == 0) tm[2] = clock64();
 

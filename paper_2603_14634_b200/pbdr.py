@@ -20,7 +20,7 @@ LIB_PATH = os.environ.get("PBDR_LIB_PATH") or os.path.join(_HERE, "lib", "libpbd
 # Host-only half of the ABI (scene generation, RNG, pack_box, last-error
 # state): no CUDA. libpbdr_gpu.so links against it, so both handles see one
 # error state; the CPU reference arm loads only this one.
-HOST_LIB_PATH = os.path.join(os.path.dirname(LIB_PATH), "libpbdr_host.so")
+HOST_LIB_PATH = os.environ.get("PBDR_HOST_LIB_PATH") or os.path.join(_HERE, "lib", "libpbdr_host.so")
 
 NBR_CAP = 32
 KCLASS_NAMES = ("integrate_key", "sort_histogram", "sort_onesweep", "cell_ranges",
