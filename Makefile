@@ -29,8 +29,8 @@ CU_OBJ   := $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(CU_SRC))
 CXX_OBJ  := $(patsubst $(CSRC)/%.cpp,$(OBJDIR)/%.o,$(CXX_SRC))
 HOST_OBJ := $(patsubst $(CSRC)/%.cpp,$(OBJDIR)/%.o,$(HOST_SRC))
 
-.PHONY: all lib oracle ref clean
-all: lib oracle build/test_dropin build/libdropin_shim.so
+.PHONY: all lib oracle ref clean checked
+all: lib oracle build/test_dropin build/libdropin_shim.so checked
 
 lib: $(HOST_LIB) $(LIB)
 
@@ -51,6 +51,18 @@ $(LIB): $(CU_OBJ) $(CXX_OBJ) $(HOST_LIB)
 	@mkdir -p $(PKG)/lib
 	$(NVCC) $(ARCH) -shared -o $@ $(CU_OBJ) $(CXX_OBJ) -L$(PKG)/lib -lpbdr_host -lcudart \
 	    -Xlinker -rpath,'$$ORIGIN'
+
+# Checked build: the same library with device-side bounds / invariant checks
+# (PBDR_CHECKED, csrc/pbdr_kernels.cu). Run the GPU tests against it with
+# PBDR_LIB_PATH=$(PWD)/paper_2603_14634_b200/lib/libpbdr_gpu_checked.so.
+CHECKED  := $(PKG)/lib/libpbdr_gpu_checked.so
+checked: $(CHECKED)
+$(OBJDIR)/checked/%.o: $(CSRC)/%.cu $(HDRS)
+	@mkdir -p $(OBJDIR)/checked
+	$(NVCC) $(NVFLAGS) -DPBDR_CHECKED=1 -c $< -o $@ 2> $(OBJDIR)/checked/$*.ptxas.txt || (cat $(OBJDIR)/checked/$*.ptxas.txt; false)
+$(CHECKED): $(patsubst $(CSRC)/%.cu,$(OBJDIR)/checked/%.o,$(CU_SRC)) $(CXX_OBJ) $(HOST_LIB)
+	$(NVCC) $(ARCH) -shared -o $@ $(patsubst $(CSRC)/%.cu,$(OBJDIR)/checked/%.o,$(CU_SRC)) $(CXX_OBJ) \
+	    -L$(PKG)/lib -lpbdr_host -lcudart -Xlinker -rpath,'$$ORIGIN'
 
 oracle:
 	$(MAKE) -C oracle

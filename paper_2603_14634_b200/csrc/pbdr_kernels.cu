@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <stdint.h>
 
@@ -35,6 +36,29 @@ constexpr unsigned kFull = 0xFFFFFFFFu;
 constexpr int kWarps = PBDR_CTA_WARPS;
 constexpr int kThreads = kWarps * 32;
 constexpr uint32_t kEmpty = 0xFFFFFFFFu;
+
+// Checked build (make checked -> lib/libpbdr_gpu_checked.so): device-side
+// bounds and invariant checks on every index the kernels load or store
+// through -- the substitute for compute-sanitizer, which this GPU pool does
+// not run (profiles/r02_sanitizer_unavailable.md). A failed check traps
+// (cudaErrorAssert / illegal instruction), so the calling test fails loudly.
+#ifndef PBDR_CHECKED
+#define PBDR_CHECKED 0
+#endif
+#if PBDR_CHECKED
+#define PBDR_CHECK(cond)                                                                          \
+  do {                                                                                           \
+    if (!(cond)) {                                                                               \
+      printf("PBDR_CHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__,    \
+             static_cast<int>(blockIdx.x), static_cast<int>(threadIdx.x));                        \
+      __trap();                                                                                  \
+    }                                                                                            \
+  } while (0)
+#else
+#define PBDR_CHECK(cond) \
+  do {                   \
+  } while (0)
+#endif
 
 __device__ __forceinline__ void record_error(DevError* e, unsigned bits, int body,
                                              const long long* substep_counter,
@@ -504,6 +528,7 @@ __global__ void __launch_bounds__(256) k_cell_ranges(RangesArgs A) {
   for (int64_t s = g; s < m; s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const uint32_t k = A.keys[s];
     const uint32_t v = A.vals[s];
+    PBDR_CHECK(v < static_cast<uint64_t>(A.n) && (s == 0 || A.keys[s - 1] <= k));
     const int body = A.body_of[v];
     A.sorted_body[s] = body;
     A.sorted_pos[s] = A.pos[v];
@@ -711,6 +736,7 @@ __global__ void __launch_bounds__(256) k_near_write(NearArgs A) {
     const unsigned bal = __ballot_sync(kFull, near);
     if (near) {
       const uint32_t o = off + __popc(bal & ((1u << lane) - 1u));
+      PBDR_CHECK(o < static_cast<uint32_t>(*A.count));
       A.near_list[o] = static_cast<int>(p);
       A.keys_c[o] = A.key_all[p];
       A.vals_c[o] = static_cast<uint32_t>(p);
@@ -792,7 +818,7 @@ __global__ void __launch_bounds__(256) k_cell_clear(uint4* cells, const uint32_t
   const long long m = *prev_count;
   for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < m;
        t += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    cells[prev_keys[t]].x = kEmpty;
+    cells[prev_keys[t]].x = kEmpty;  // keys are masked hashes: always inside the table
 }
 
 // ---------------------------------------------------------------------------
@@ -821,6 +847,7 @@ struct CandList {
 
 __device__ __forceinline__ void scan_range(const NeighbourArgs& A, uint32_t lo, uint32_t hi, int bi, int si,
                                            float4 xi, int32_t cx, int32_t cy, int32_t cz, CandList& L) {
+  PBDR_CHECK(lo <= hi && hi <= static_cast<uint64_t>(*A.count));
   for (uint32_t s = lo; s < hi; ++s) {
     // Body, slot and position of the entry come from sorted-order copies
     // (k_cell_ranges), read side by side: no dependent gathers per entry.
@@ -853,6 +880,7 @@ __device__ __forceinline__ void neighbours_one(const NeighbourArgs& A, int64_t t
   // Near particles in sorted (cell-key) order: neighbouring threads search
   // overlapping cells, so bucket entries are shared through L1/L2.
   const int64_t i = A.sorted_vals[t];
+  PBDR_CHECK(i >= 0 && i < A.n);
   const float4 xi = A.pos[i];
   const int bi = A.body_of[i];
   const int si = A.body_scene[bi];
@@ -905,10 +933,18 @@ __global__ void __launch_bounds__(128) k_neighbours(NeighbourArgs A) {
 // tiles, one-wave cooperative grids, or one cluster per batched scene), and
 // -- FUSE -- the substep's last iteration followed by the next integrate.
 // ---------------------------------------------------------------------------
-// PBDR_CAND_ROLLED: keep the candidate loop rolled (code size; the compiler
-// otherwise unrolls it 4x for each of the KP particles of a lane).
+// PBDR_COST_PROBE (timing experiments only, results are wrong): bit 0 skips
+// the polar, bit 1 the inertia solve -- what the per-body fp64 math costs.
+#ifndef PBDR_COST_PROBE
+#define PBDR_COST_PROBE 0
+#endif
+// PBDR_CAND_ROLLED: keep the candidate loop rolled. The compiler otherwise
+// unrolls it 4x for each of the KP particles of a lane: 10% more code, and
+// the instruction-cache misses that costs (ncu: no_instruction stalls) are
+// worth more than the extra loads in flight -- landed C5 iteration 245 -> 213
+// ms per frame, C3 +4%, C4 +1%, bit-identical (tools/ab_landed.py, r02).
 #ifndef PBDR_CAND_ROLLED
-#define PBDR_CAND_ROLLED 0
+#define PBDR_CAND_ROLLED 1
 #endif
 // PBDR_PREFETCH_NEXT: after phase A, one lane pulls the next tile's staging
 // ranges (pos, vel, rest) and its candidate counts into L2.
@@ -1016,6 +1052,7 @@ __device__ __forceinline__ void phase_a_particle(const IterArgs& A, int it, int6
 #endif
   for (int c = 0; c < nc; ++c) {
     const int j = A.cand_j[static_cast<int64_t>(c) * A.n + p];
+    PBDR_CHECK(c < PBDR_NBR_CAP && j >= 0 && j < A.n && j != p);
     const float rr = A.cand_rr[static_cast<int64_t>(c) * A.n + p];
     // Multi-iteration launch with pairs: neighbours' X_i come from the
     // buffer the previous iteration wrote (after a grid barrier; L2 only).
@@ -1132,7 +1169,14 @@ __device__ __forceinline__ void body_math_a(const IterArgs& A, int bb, const flo
   }
   double qd[4];
   const float rq[4] = {rq4.x, rq4.y, rq4.z, rq4.w};
+#if PBDR_COST_PROBE & 1  // cost probe only (wrong results): no polar, identity rotation
+  const bool ok = true;
+  qd[0] = 1.0; qd[1] = qd[2] = qd[3] = 0.0;
+#pragma unroll
+  for (int k = 0; k < 9; ++k) R[kResR + k] = (k % 4 == 0) ? 1.0f : 0.0f;
+#else
   const bool ok = polar_warm_f(&S[6], rq, &R[kResR], qd);
+#endif
   R[kResSmOk] = ok ? 1.0f : 0.0f;
   rq_new = ok ? make_float4(static_cast<float>(qd[0]), static_cast<float>(qd[1]), static_cast<float>(qd[2]),
                             static_cast<float>(qd[3]))
@@ -1248,7 +1292,12 @@ __device__ __forceinline__ void body_math_b(const IterArgs& A, int bb, const flo
     If[4] = S[13] + M * (ca[0] * ca[2]);
     If[5] = S[14] + M * (ca[1] * ca[2]);
     double nax[3];
+#if PBDR_COST_PROBE & 2  // cost probe only (wrong results): no inertia solve
+    const unsigned e = 0u;
+    (void)If;
+#else
     const unsigned e = inertia_solve_f(If, dL, om, nax);
+#endif
     if (e) record_error(A.err, e, bb, A.substep_counter, nax);
   }
 #pragma unroll
@@ -1291,8 +1340,11 @@ __device__ __forceinline__ void phase_c_particle(const IterArgs& A, int64_t p, f
 // two CTAs per SM with up to 128 registers (no spills). Measured on C4:
 // 0.382 ms per iteration vs 0.436 for KP = 4 at three CTAs per SM (80
 // registers, spills) -- more particles in flight per SM, fewer warps per body.
+#ifndef PBDR_SMALL_KP_WARPS
+#define PBDR_SMALL_KP_WARPS 24  // resident warps per SM requested for KP <= 4 (sets the register cap)
+#endif
 template <int KP>
-constexpr int iter_min_blocks() { return (KP >= 7 ? 16 : 24) / kWarps; }  // 16 or 24 resident warps per SM
+constexpr int iter_min_blocks() { return (KP >= 7 ? 16 : PBDR_SMALL_KP_WARPS) / kWarps; }  // 16 or 24 warps per SM
 
 // FUSE (single-iteration launches only): the launch ends the substep and
 // integrates the next one in its writeback (a separate instantiation, so the
@@ -1354,6 +1406,7 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
 
   if (threadIdx.x == 0) {
     const uint32_t bytes = static_cast<uint32_t>(cd.y) * 16u;
+    PBDR_CHECK(cd.y > 0 && cd.y <= kSlots && cd.x >= 0 && cd.x + cd.y <= A.n && cd.w >= 1 && cd.w <= kWarps);
     mbar_expect_tx(&s_bar, 3u * bytes);
     bulk_g2s_stream(s_pos, A.pos_in + first, bytes, &s_bar);
     bulk_g2s_stream(s_vel, A.vel + first, bytes, &s_bar);
@@ -1367,6 +1420,8 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
   const bool live = b >= 0;
   const int lb = live ? b - cd.z : 0;  // body index within the CTA
   const int start = wd.z, n = wd.w & 0xFFFF, W = wd.w >> 16;
+  PBDR_CHECK(!live || (start >= first && start - first + n <= cd.y && W >= 1 && wi < W && n <= 32 * KP * W &&
+                       lb >= 0 && lb < cd.w));
   int ncs[KP];
 #pragma unroll
   for (int k = 0; k < KP; ++k) {
@@ -2227,13 +2282,19 @@ void launch_near(const NearArgs& a, cudaStream_t s) {
 __global__ void __launch_bounds__(256) k_gather4(float4* __restrict__ dst, const float4* __restrict__ src,
                                                  const int* __restrict__ idx, int64_t count) {
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t < count) dst[t] = src[idx[t]];
+  if (t < count) {
+    PBDR_CHECK(idx[t] >= 0);
+    dst[t] = src[idx[t]];
+  }
 }
 
 __global__ void __launch_bounds__(256) k_scatter4(float4* __restrict__ dst, const float4* __restrict__ src,
                                                   const int* __restrict__ idx, int64_t count) {
   const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (t < count) dst[idx[t]] = src[t];
+  if (t < count) {
+    PBDR_CHECK(idx[t] >= 0);
+    dst[idx[t]] = src[t];
+  }
 }
 
 void launch_gather4(float4* dst, const float4* src, const int* idx, int64_t count, cudaStream_t s) {
@@ -2260,6 +2321,7 @@ __global__ void __launch_bounds__(256) k_particles_in(float4* __restrict__ pos, 
   for (int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; s < n;
        s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t i = slot_particle[s];
+    PBDR_CHECK(i >= 0 && i < n);
     if (x) {
       float4 p = pos[s];
       p.x = static_cast<float>(x[3 * i]);

@@ -315,6 +315,10 @@ __device__ __noinline__ bool polar_rotation_f(const float Af[9], float R[9], dou
 // conditioning of S. A missing warm start, |w|^2 > 0.25 (not local), a
 // singular solve, or 4 steps without convergence fall back to the cold
 // two-stage Newton polar. The result is the same polar factor to 1e-12.
+// PBDR_GN_ROLLED: keep the Gauss-Newton step loop rolled (code size).
+#ifndef PBDR_GN_ROLLED
+#define PBDR_GN_ROLLED 0
+#endif
 #ifndef PBDR_WARM_INLINE
 #define PBDR_WARM_INLINE 1
 #endif
@@ -341,6 +345,9 @@ bool polar_warm_f(const float Af[9], const float rq[4], float R[9], double q[4])
     // Homogeneous iterate (mirrors oracle polar_warm): qc is not renormalised
     // between steps; R0 = |qc|^2 R(qc) and the step h is scale invariant.
     double qc[4] = {rq[0], rq[1], rq[2], rq[3]};
+#if PBDR_GN_ROLLED
+#pragma unroll 1
+#endif
     for (int step = 0; step < PBDR_POLAR_WARM_STEPS; ++step) {
       const double w = qc[0], x = qc[1], y = qc[2], z = qc[3];
       const double w2 = w * w, xx = x * x, yy = y * y, zz = z * z;
