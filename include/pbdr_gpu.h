@@ -205,8 +205,10 @@ int pbdr_gpu_debug_read_sorted(pbdr_handle* h, uint32_t* keys, uint32_t* vals);
 int pbdr_gpu_debug_near_count(pbdr_handle* h, int64_t* count);
 int pbdr_gpu_debug_read_candidates(pbdr_handle* h, int32_t* counts, int32_t* lists /* n*CAP */);
 int pbdr_gpu_debug_read_init(pbdr_handle* h, float* init4);
-/* Runs one iteration launch with per-CTA clock64 stamps (8 per CTA: start,
- * staged, phase A, body math A, phase B, body math B, end, SM id). */
+/* Runs one iteration launch with per-CTA clock64 stamps (16 per CTA: start,
+ * staged, phase A, body math A, phase B, body math B, end, SM id; then for the
+ * CTA's first body: sums read A, body math A done, sums read B, body math B
+ * done, polar start, polar end, 2 spare). */
 int pbdr_gpu_debug_phase_timing(pbdr_handle* h, long long* out);
 /* Body anchors (fp32 xyz per body) used by the anchored body sums. */
 int pbdr_gpu_debug_read_anchor(pbdr_handle* h, float* anchor3);

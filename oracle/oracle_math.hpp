@@ -316,11 +316,88 @@ inline bool polar_rotation(const M3& A, M3& R, double q[4]) {
 // conditioning of S. A missing warm start, |w|^2 > 0.25 (not local), a
 // singular solve, or 4 steps without convergence fall back to the cold
 // two-stage Newton polar. The result is the same polar factor to 1e-12.
+// PBDR_POLAR_WARM_F32 (pbdr_pinned.h): the same iteration in fp32 on the
+// fp32 body sum A (exactly representable: A holds float values).
+inline bool polar_warm_f32(const M3& A, const float rq[4], M3& R, double q[4], bool bad) {
+  float Af[9];
+  for (int i = 0; i < 9; ++i) Af[i] = static_cast<float>(A.a[i / 3][i % 3]);
+  float qc[4] = {rq[0], rq[1], rq[2], rq[3]};
+  for (int step = 0; step < PBDR_POLAR_WARM_STEPS; ++step) {
+    const float w = qc[0], x = qc[1], y = qc[2], z = qc[3];
+    const float w2 = w * w, xx = x * x, yy = y * y, zz = z * z;
+    const float xy = x * y, xz = x * z, yz = y * z;
+    const float wx = w * x, wy = w * y, wz = w * z;
+    float R0[3][3];
+    R0[0][0] = (w2 + xx) - (yy + zz);
+    R0[0][1] = 2.0f * (xy - wz);
+    R0[0][2] = 2.0f * (xz + wy);
+    R0[1][0] = 2.0f * (xy + wz);
+    R0[1][1] = (w2 + yy) - (xx + zz);
+    R0[1][2] = 2.0f * (yz - wx);
+    R0[2][0] = 2.0f * (xz - wy);
+    R0[2][1] = 2.0f * (yz + wx);
+    R0[2][2] = (w2 + zz) - (xx + yy);
+    float B[3][3];
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) B[i][j] = (R0[0][i] * Af[j] + R0[1][i] * Af[3 + j]) + R0[2][i] * Af[6 + j];
+    const float sv[3] = {B[2][1] - B[1][2], B[0][2] - B[2][0], B[1][0] - B[0][1]};
+    float M[3][3];
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) M[i][j] = -(0.5f * (B[i][j] + B[j][i]));
+    const float tr = (-M[0][0] + -M[1][1]) + -M[2][2];
+    M[0][0] = tr + M[0][0];
+    M[1][1] = tr + M[1][1];
+    M[2][2] = tr + M[2][2];
+    const float dm = M[0][0] * (M[1][1] * M[2][2] - M[1][2] * M[2][1]) -
+                     M[0][1] * (M[1][0] * M[2][2] - M[1][2] * M[2][0]) +
+                     M[0][2] * (M[1][0] * M[2][1] - M[1][1] * M[2][0]);
+    if (!(dm > 0.0f) || !std::isfinite(dm)) break;
+    const float idm = 1.0f / dm;
+    const float c00 = (M[1][1] * M[2][2] - M[1][2] * M[2][1]) * idm;
+    const float c01 = (M[0][2] * M[2][1] - M[0][1] * M[2][2]) * idm;
+    const float c02 = (M[0][1] * M[1][2] - M[0][2] * M[1][1]) * idm;
+    const float c11 = (M[0][0] * M[2][2] - M[0][2] * M[2][0]) * idm;
+    const float c12 = (M[0][2] * M[1][0] - M[0][0] * M[1][2]) * idm;
+    const float c22 = (M[0][0] * M[1][1] - M[0][1] * M[1][0]) * idm;
+    const float h[3] = {0.5f * ((c00 * sv[0] + c01 * sv[1]) + c02 * sv[2]),
+                        0.5f * ((c01 * sv[0] + c11 * sv[1]) + c12 * sv[2]),
+                        0.5f * ((c02 * sv[0] + c12 * sv[1]) + c22 * sv[2])};
+    const float ww = 4.0f * ((h[0] * h[0] + h[1] * h[1]) + h[2] * h[2]);
+    if (!(ww <= static_cast<float>(PBDR_POLAR_WARM_MAX2))) break;
+    float qn[4];
+    qn[0] = qc[0] - ((qc[1] * h[0] + qc[2] * h[1]) + qc[3] * h[2]);
+    qn[1] = (qc[0] * h[0] + qc[1]) + (qc[2] * h[2] - qc[3] * h[1]);
+    qn[2] = (qc[0] * h[1] + qc[2]) + (qc[3] * h[0] - qc[1] * h[2]);
+    qn[3] = (qc[0] * h[2] + qc[3]) + (qc[1] * h[1] - qc[2] * h[0]);
+    if (ww <= static_cast<float>(PBDR_POLAR_WARM_TOLQ)) {
+      if (bad) return false;
+      const float n2 = ((qn[0] * qn[0] + qn[1] * qn[1]) + qn[2] * qn[2]) + qn[3] * qn[3];
+      const float r = 1.0f / n2;
+      const float s = 1.5f - 0.5f * n2;
+      const float a = qn[0], b = qn[1], c = qn[2], d = qn[3];
+      const float a2 = a * a, bb = b * b, cc = c * c, dd = d * d;
+      const float bc = b * c, bd = b * d, cd = c * d, ab = a * b, ac = a * c, ad = a * d;
+      const float Rf[9] = {((a2 + bb) - (cc + dd)) * r, (2.0f * (bc - ad)) * r, (2.0f * (bd + ac)) * r,
+                           (2.0f * (bc + ad)) * r, ((a2 + cc) - (bb + dd)) * r, (2.0f * (cd - ab)) * r,
+                           (2.0f * (bd - ac)) * r, (2.0f * (cd + ab)) * r, ((a2 + dd) - (bb + cc)) * r};
+      for (int i = 0; i < 9; ++i) R.a[i / 3][i % 3] = static_cast<double>(Rf[i]);
+      for (int k = 0; k < 4; ++k) q[k] = static_cast<double>(qn[k] * s);
+      return true;
+    }
+    for (int k = 0; k < 4; ++k) qc[k] = qn[k];
+  }
+  if (bad) return false;
+  return polar_rotation(A, R, q);
+}
+
 inline bool polar_warm(const M3& A, const float rq[4], M3& R, double q[4]) {
   const double d0 = det3(A);
   const double c3 = frob2(A) * PBDR_ONE_THIRD;
   const bool bad =
       !finite3(A) || !(d0 > 0.0) || d0 * d0 <= (PBDR_POLAR_REL_DET * PBDR_POLAR_REL_DET) * ((c3 * c3) * c3);
+#if PBDR_POLAR_WARM_F32
+  if (rq[0] != 0.0f || rq[1] != 0.0f || rq[2] != 0.0f || rq[3] != 0.0f) return polar_warm_f32(A, rq, R, q, bad);
+#endif
   if (rq[0] != 0.0f || rq[1] != 0.0f || rq[2] != 0.0f || rq[3] != 0.0f) {
     // Homogeneous iterate: qc is not renormalised between steps; R0 below is
     // |qc|^2 R(qc), and the step h is invariant under that uniform scale.

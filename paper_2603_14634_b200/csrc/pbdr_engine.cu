@@ -1411,15 +1411,15 @@ int pbdr_gpu_debug_phase_timing(pbdr_handle* h, long long* out) {
   PBDR_CUDA(cudaSetDevice(h->device));
   if (!h->timing_buf) {
     void* p = nullptr;
-    PBDR_CUDA(cudaMalloc(&p, sizeof(long long) * 8 * h->ctas));
+    PBDR_CUDA(cudaMalloc(&p, sizeof(long long) * 16 * h->ctas));
     h->allocations.push_back(p);
     h->timing_buf = static_cast<long long*>(p);
   }
-  PBDR_CUDA(cudaMemsetAsync(h->timing_buf, 0, sizeof(long long) * 8 * h->ctas, h->stream));
+  PBDR_CUDA(cudaMemsetAsync(h->timing_buf, 0, sizeof(long long) * 16 * h->ctas, h->stream));
   h->timing = h->timing_buf;  // only this launch is instrumented
   enqueue_iteration(h, 0, nullptr);
   h->timing = nullptr;
-  PBDR_CUDA(cudaMemcpyAsync(out, h->timing_buf, sizeof(long long) * 8 * h->ctas, cudaMemcpyDeviceToHost,
+  PBDR_CUDA(cudaMemcpyAsync(out, h->timing_buf, sizeof(long long) * 16 * h->ctas, cudaMemcpyDeviceToHost,
                             h->stream));
   PBDR_CUDA(cudaStreamSynchronize(h->stream));
   return check_errors(h);

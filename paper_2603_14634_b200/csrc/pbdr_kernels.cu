@@ -935,6 +935,9 @@ __global__ void __launch_bounds__(128) k_neighbours(NeighbourArgs A) {
 // ---------------------------------------------------------------------------
 // PBDR_COST_PROBE (timing experiments only, results are wrong): bit 0 skips
 // the polar, bit 1 the inertia solve -- what the per-body fp64 math costs.
+#ifndef PBDR_GN_PROBE
+#define PBDR_GN_PROBE 0
+#endif
 #ifndef PBDR_COST_PROBE
 #define PBDR_COST_PROBE 0
 #endif
@@ -943,6 +946,11 @@ __global__ void __launch_bounds__(128) k_neighbours(NeighbourArgs A) {
 // the instruction-cache misses that costs (ncu: no_instruction stalls) are
 // worth more than the extra loads in flight -- landed C5 iteration 245 -> 213
 // ms per frame, C3 +4%, C4 +1%, bit-identical (tools/ab_landed.py, r02).
+// PBDR_INTILE_SMEM: contact candidates inside the tile read X_j from the
+// staged shared-memory copy.
+#ifndef PBDR_INTILE_SMEM
+#define PBDR_INTILE_SMEM 0
+#endif
 #ifndef PBDR_CAND_ROLLED
 #define PBDR_CAND_ROLLED 1
 #endif
@@ -1004,7 +1012,8 @@ __device__ __forceinline__ void multi_barrier(const IterArgs& A) {
 template <bool MULTI>
 __device__ __forceinline__ void phase_a_particle(const IterArgs& A, int it, int64_t p, float4 x4, float4 v4,
                                                  float4 r4, int nc, const float a[3], float (&dXk)[3],
-                                                 float (&acc)[21]) {
+                                                 float (&acc)[21], const float4* s_tile, int tile_first,
+                                                 int tile_count) {
   const float x[3] = {x4.x, x4.y, x4.z};
   const float m = v4.w;
 
@@ -1056,7 +1065,17 @@ __device__ __forceinline__ void phase_a_particle(const IterArgs& A, int it, int6
     const float rr = A.cand_rr[static_cast<int64_t>(c) * A.n + p];
     // Multi-iteration launch with pairs: neighbours' X_i come from the
     // buffer the previous iteration wrote (after a grid barrier; L2 only).
+#if PBDR_INTILE_SMEM
+    // Candidates in this tile's own slot range are read from the staged X_i
+    // in shared memory (identical values: the same snapshot) instead of L2.
+    const uint32_t jt = static_cast<uint32_t>(j - tile_first);
+    const float4 xj = jt < static_cast<uint32_t>(tile_count)
+                          ? s_tile[jt]
+                          : ((MULTI && A.multi_pairs) ? __ldcg(&A.pos_b[it & 1][j]) : A.pos_in[j]);
+#else
+    (void)s_tile; (void)tile_first; (void)tile_count;
     const float4 xj = (MULTI && A.multi_pairs) ? __ldcg(&A.pos_b[it & 1][j]) : A.pos_in[j];
+#endif
     pp_contact(x, x4.w, p, xj, j, rr, A.relax, dPP);
   }
   const float v[3] = {v4.x, v4.y, v4.z};
@@ -1130,6 +1149,7 @@ __device__ __forceinline__ void warp_box_commit(const IterArgs& A, int b, const 
 }
 
 constexpr int kResF = 32;
+constexpr int kTimingSlots = 16;  // debug phase clocks per CTA (pbdr_gpu_debug_phase_timing)
 enum ResSlot {
   kResC = 0,      // c (3), anchor-relative com of X_i
   kResLb = 3,     // L_bsm (3)
@@ -1148,7 +1168,7 @@ enum ResSlot {
 template <bool kStore = true>  // false: the caller stores rquat / anchor (after a cluster barrier)
 __device__ __forceinline__ void body_math_a(const IterArgs& A, int bb, const float (&S)[21], float4 an,
                                             float invM, float4 rq4, float* R, float4& rq_new,
-                                            float4& an_new) {
+                                            float4& an_new, long long* stamp = nullptr) {
   bool finite = true;
 #pragma unroll
   for (int f = 0; f < 21; ++f) finite = finite && isfinite(S[f]);
@@ -1169,14 +1189,23 @@ __device__ __forceinline__ void body_math_a(const IterArgs& A, int bb, const flo
   }
   double qd[4];
   const float rq[4] = {rq4.x, rq4.y, rq4.z, rq4.w};
+  if (stamp) stamp[0] = clock64();  // debug phase clocks: polar start
 #if PBDR_COST_PROBE & 1  // cost probe only (wrong results): no polar, identity rotation
   const bool ok = true;
   qd[0] = 1.0; qd[1] = qd[2] = qd[3] = 0.0;
 #pragma unroll
   for (int k = 0; k < 9; ++k) R[kResR + k] = (k % 4 == 0) ? 1.0f : 0.0f;
 #else
+#if PBDR_GN_PROBE  // debug: Gauss-Newton steps of this body (15 = cold polar) into the phase stamps
+  int steps = 0;
+  const bool ok = polar_warm_f(&S[6], rq, &R[kResR], qd, &steps);
+  if (A.timing) atomicAdd(reinterpret_cast<unsigned long long*>(A.timing + kTimingSlots * static_cast<int64_t>(blockIdx.x) + 7),
+                          1ull << (16 + 4 * (steps <= 4 ? steps : 5)));
+#else
   const bool ok = polar_warm_f(&S[6], rq, &R[kResR], qd);
 #endif
+#endif
+  if (stamp) stamp[1] = clock64();  // polar end
   R[kResSmOk] = ok ? 1.0f : 0.0f;
   rq_new = ok ? make_float4(static_cast<float>(qd[0]), static_cast<float>(qd[1]), static_cast<float>(qd[2]),
                             static_cast<float>(qd[3]))
@@ -1340,6 +1369,13 @@ __device__ __forceinline__ void phase_c_particle(const IterArgs& A, int64_t p, f
 // two CTAs per SM with up to 128 registers (no spills). Measured on C4:
 // 0.382 ms per iteration vs 0.436 for KP = 4 at three CTAs per SM (80
 // registers, spills) -- more particles in flight per SM, fewer warps per body.
+// Rolled particle loops with the deltas in shared memory (KP <= 4 tiles only:
+// at KP >= 7 the extra 32 KB would cost a CTA per SM).
+#ifndef PBDR_ROLL_PARTICLES
+#define PBDR_ROLL_PARTICLES 1
+#endif
+template <int KP>
+constexpr bool iter_rolled() { return PBDR_ROLL_PARTICLES != 0 && KP <= 4; }
 #ifndef PBDR_SMALL_KP_WARPS
 #define PBDR_SMALL_KP_WARPS 24  // resident warps per SM requested for KP <= 4 (sets the register cap)
 #endif
@@ -1352,7 +1388,8 @@ constexpr int iter_min_blocks() { return (KP >= 7 ? 16 : PBDR_SMALL_KP_WARPS) / 
 template <int KP, bool MULTI, bool FUSE = false>
 __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(IterArgs A) {
   constexpr int kSlots = kThreads * KP;  // particle slots staged per CTA
-  extern __shared__ float4 s_stage[];  // pos | vel | rest, kSlots each
+  constexpr bool kRoll = PBDR_ROLL_PARTICLES != 0 && KP <= 4;  // iter_rolled<KP>()
+  extern __shared__ float4 s_stage[];  // pos | vel | rest [| dX], kSlots each
   __shared__ float s_part[kWarps][21];
   __shared__ float s_res[kWarps][kResF];
   __shared__ __align__(8) uint64_t s_bar;
@@ -1360,6 +1397,7 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
   float4* s_pos = s_stage;
   float4* s_vel = s_stage + kSlots;
   float4* s_rest = s_stage + 2 * kSlots;
+  float4* s_dx = s_stage + 3 * kSlots;  // kRoll only
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -1422,12 +1460,26 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
   const int start = wd.z, n = wd.w & 0xFFFF, W = wd.w >> 16;
   PBDR_CHECK(!live || (start >= first && start - first + n <= cd.y && W >= 1 && wi < W && n <= 32 * KP * W &&
                        lb >= 0 && lb < cd.w));
-  int ncs[KP];
+  // Candidate counts of the lane's particles (prefetched: off the phase-A
+  // chain); kRoll packs them 8 bits each (<= PBDR_NBR_CAP) so that the rolled
+  // particle loops index them without local memory.
+  int ncs_a[kRoll ? 1 : KP];
+  uint32_t ncs_pk = 0;
 #pragma unroll
   for (int k = 0; k < KP; ++k) {
     const int q = k * 32 * W + wi * 32 + lane;
-    ncs[k] = (live && q < n) ? A.ncand[start + q] : 0;  // prefetched: off the phase-A chain
+    const int c = (live && q < n) ? A.ncand[start + q] : 0;
+    if constexpr (kRoll)
+      ncs_pk |= static_cast<uint32_t>(c) << (8 * k);
+    else
+      ncs_a[k] = c;
   }
+  auto ncs = [&](int k) -> int {
+    if constexpr (kRoll)
+      return static_cast<int>((ncs_pk >> (8 * k)) & 0xFFu);
+    else
+      return ncs_a[k];
+  };
   // First candidate of each particle: its slot now, and its position and
   // contact radius pulled into L2, while the tile's staging copies are in
   // flight -- in contact-rich states phase A otherwise waits on two dependent
@@ -1435,7 +1487,7 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
   if (!MULTI || !A.multi_pairs) {
 #pragma unroll
     for (int k = 0; k < KP; ++k) {
-      if (ncs[k] > 0) {
+      if (ncs(k) > 0) {
         const int64_t p = start + k * 32 * W + wi * 32 + lane;
         const int j = __ldg(&A.cand_j[p]);
         prefetch_l2(&A.pos_in[j]);
@@ -1445,7 +1497,7 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
   }
   const int off = start - first;
 
-  long long* tm = A.timing ? A.timing + 8 * static_cast<int64_t>(tile) : nullptr;
+  long long* tm = A.timing ? A.timing + kTimingSlots * static_cast<int64_t>(tile) : nullptr;
   if (tm && threadIdx.x == 0) tm[0] = t_entry;  // CTA entry: stage = descriptors + table + bulk copies
   __syncthreads();  // barrier initialised, per-body table filled, next tile claimed
   const int tile_next = s_next;
@@ -1473,20 +1525,50 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
     a[0] = an.x; a[1] = an.y; a[2] = an.z;
   }
 
-  float dX[KP][3];
+  // Per-particle deltas dX: registers (unrolled particle loops), or -- kRoll
+  // -- shared memory next to the staged state, so the three particle loops
+  // stay rolled (a quarter of the code: the tile loop then fits the SM's
+  // instruction cache better) and no delta is live across the body math.
+  float dX[kRoll ? 1 : KP][3];
+  if constexpr (!kRoll) {
+#pragma unroll
+    for (int k = 0; k < KP; ++k) dX[k][0] = dX[k][1] = dX[k][2] = 0.0f;
+  }
+  auto dx_load = [&](int k, int q, float (&d)[3]) {
+    if constexpr (kRoll) {
+      const float4 t = s_dx[off + q];
+      d[0] = t.x; d[1] = t.y; d[2] = t.z;
+    } else {
+      d[0] = dX[k][0]; d[1] = dX[k][1]; d[2] = dX[k][2];
+    }
+  };
+  auto dx_store = [&](int k, int q, const float (&d)[3]) {
+    if constexpr (kRoll) {
+      s_dx[off + q] = make_float4(d[0], d[1], d[2], 0.0f);
+    } else {
+      dX[k][0] = d[0]; dX[k][1] = d[1]; dX[k][2] = d[2];
+    }
+  };
 
   // ---- Phase A: contacts, bsm sums -----------------------------------------
   float acc[21];
 #pragma unroll
   for (int f = 0; f < 21; ++f) acc[f] = 0.0f;
-#pragma unroll
-  for (int k = 0; k < KP; ++k) dX[k][0] = dX[k][1] = dX[k][2] = 0.0f;
-#pragma unroll
-  for (int k = 0; k < KP; ++k) {
+  auto phase_a_k = [&](int k) {
     const int q = k * 32 * W + wi * 32 + lane;
-    if (!(live && q < n)) continue;
+    if (!(live && q < n)) return;
     const int64_t p = start + q;
-    phase_a_particle<MULTI>(A, it, p, s_pos[off + q], s_vel[off + q], s_rest[off + q], ncs[k], a, dX[k], acc);
+    float d[3] = {0.0f, 0.0f, 0.0f};
+    phase_a_particle<MULTI>(A, it, p, s_pos[off + q], s_vel[off + q], s_rest[off + q], ncs(k), a, d, acc, s_pos,
+                            first, cd.y);
+    dx_store(k, q, d);
+  };
+  if constexpr (kRoll) {
+#pragma unroll 1
+    for (int k = 0; k < KP; ++k) phase_a_k(k);
+  } else {
+#pragma unroll
+    for (int k = 0; k < KP; ++k) phase_a_k(k);
   }
   if (live) {
     // 21 fields as 16 + 5 (each its own power-of-two reduce-scatter: fewer
@@ -1530,7 +1612,10 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
 #pragma unroll
       for (int f = 0; f < 21; ++f) S[f] = S[f] + s_part[fw + u][f];
     float4 rq_new, an_new;
-    body_math_a(A, bb, S, an, invM, s_trq[tb][lane], &s_res[lane][0], rq_new, an_new);
+    if (tm && lane == 0) tm[8] = clock64();  // body sums read
+    body_math_a(A, bb, S, an, invM, s_trq[tb][lane], &s_res[lane][0], rq_new, an_new,
+                (tm && lane == 0) ? tm + 12 : nullptr);
+    if (tm && lane == 0) tm[9] = clock64();
     s_trq[tb][lane] = rq_new;   // next iteration of a multi-iteration launch
     s_tanc[tb][lane] = an_new;
   }
@@ -1553,16 +1638,17 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
     for (int f = 0; f < 9; ++f) Rf[f] = res[kResR + f];
 #pragma unroll
     for (int k = 0; k < 3; ++k) c[k] = res[kResC + k];
-#pragma unroll
-    for (int k = 0; k < KP; ++k) {
+    auto phase_b_k = [&](int k) {
       const int q = k * 32 * W + wi * 32 + lane;
-      if (!(q < n)) continue;
+      if (!(q < n)) return;
       const float4 x4 = s_pos[off + q];
       const float4 v4 = s_vel[off + q];
-      float xa[3], va[3], pa[3];
-      phase_b_particle(A, start + q, x4, v4, s_rest[off + q], a, sm_ok, Rf, c, dX[k], xa, va, pa);
+      float xa[3], va[3], pa[3], d[3];
+      dx_load(k, q, d);
+      phase_b_particle(A, start + q, x4, v4, s_rest[off + q], a, sm_ok, Rf, c, d, xa, va, pa);
+      dx_store(k, q, d);
       if (fixes) {
-        accum_b(v4.w, dX[k], va, pa, accB);
+        accum_b(v4.w, d, va, pa, accB);
       } else {
         const int64_t p = start + q;
         if (MULTI) {
@@ -1570,12 +1656,19 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
           s_vel[off + q] = make_float4(va[0], va[1], va[2], v4.w);
           // Only particles with candidates are gathered by others (the
           // candidate relation is symmetric, P4), so only they are published.
-          if (A.multi_pairs && it + 1 < n_iters && ncs[k] > 0) __stcg(&A.pos_b[(it + 1) & 1][p], s_pos[off + q]);
+          if (A.multi_pairs && it + 1 < n_iters && ncs(k) > 0) __stcg(&A.pos_b[(it + 1) & 1][p], s_pos[off + q]);
         } else {
           store_final(A, p, b, make_float4(xa[0], xa[1], xa[2], x4.w), make_float4(va[0], va[1], va[2], v4.w),
                       fuse_out, flo, fhi);
         }
       }
+    };
+    if constexpr (kRoll) {
+#pragma unroll 1
+      for (int k = 0; k < KP; ++k) phase_b_k(k);
+    } else {
+#pragma unroll
+      for (int k = 0; k < KP; ++k) phase_b_k(k);
     }
     if (fuse_out && !fixes) warp_box_commit(A, b, flo, fhi, lane);
   }
@@ -1601,7 +1694,9 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
     for (int u = 1; u < bw.y; ++u)
 #pragma unroll
       for (int f = 0; f < 15; ++f) S[f] = S[f] + s_part[fw + u][f];
+    if (tm && lane == 0) tm[10] = clock64();
     body_math_b(A, bb, S, mass, &s_res[lane][0], iter_index, last_iter);
+    if (tm && lane == 0) tm[11] = clock64();
   }
   __syncthreads();
   if (tm && threadIdx.x == 0) tm[5] = clock64();
@@ -1615,23 +1710,30 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
     dv[k] = res[kResDv + k];
     om[k] = res[kResW + k];
   }
-#pragma unroll
-  for (int k = 0; k < KP; ++k) {
+  auto phase_c_k = [&](int k) {
     const int q = k * 32 * W + wi * 32 + lane;
-    if (!(q < n)) continue;
+    if (!(q < n)) return;
     const float4 x4 = s_pos[off + q];
     const float4 v4 = s_vel[off + q];
     const int64_t p = start + q;
-    float xo[3], vo[3];
-    phase_c_particle(A, p, x4, v4, a, dX[k], ca, dv, om, xo, vo);
+    float xo[3], vo[3], d[3];
+    dx_load(k, q, d);
+    phase_c_particle(A, p, x4, v4, a, d, ca, dv, om, xo, vo);
     if (MULTI) {
       s_pos[off + q] = make_float4(xo[0], xo[1], xo[2], x4.w);
       s_vel[off + q] = make_float4(vo[0], vo[1], vo[2], v4.w);
-      if (A.multi_pairs && it + 1 < n_iters && ncs[k] > 0) __stcg(&A.pos_b[(it + 1) & 1][p], s_pos[off + q]);
+      if (A.multi_pairs && it + 1 < n_iters && ncs(k) > 0) __stcg(&A.pos_b[(it + 1) & 1][p], s_pos[off + q]);
     } else {
       store_final(A, p, b, make_float4(xo[0], xo[1], xo[2], x4.w), make_float4(vo[0], vo[1], vo[2], v4.w),
                   fuse_out, flo, fhi);
     }
+  };
+  if constexpr (kRoll) {
+#pragma unroll 1
+    for (int k = 0; k < KP; ++k) phase_c_k(k);
+  } else {
+#pragma unroll
+    for (int k = 0; k < KP; ++k) phase_c_k(k);
   }
   if (fuse_out) warp_box_commit(A, b, flo, fhi, lane);
   }  // live
@@ -1695,7 +1797,11 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
     tm[6] = clock64();
     unsigned smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+#if PBDR_GN_PROBE
+    atomicAdd(reinterpret_cast<unsigned long long*>(&tm[7]), static_cast<unsigned long long>(smid));
+#else
     tm[7] = smid;
+#endif
   }
   if (tile_next < ntiles && warp == 0 && lane < cd_n.w) {
     const int bb = cd_n.z + lane;
@@ -1824,7 +1930,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_iteration_big(IterArgs A) {
       const int q = k * 32 * W + wi * 32 + lane;
       if (!(live && q < n)) continue;
       const int li = k * nt + threadIdx.x;
-      phase_a_particle<false>(A, it, start + q, s_pos[li], s_vel[li], s_rest[li], ncs[k], a, dX[k], acc);
+      phase_a_particle<false>(A, it, start + q, s_pos[li], s_vel[li], s_rest[li], ncs[k], a, dX[k], acc, nullptr, 0,
+                              0);
     }
     if (live) {
       float a16[16], a5[5];  // 16 + 5 fields, as in k_iteration
@@ -2231,7 +2338,9 @@ __global__ void __launch_bounds__(kThreads) k_body_wrench_big(WrenchArgs A) {
 
 }  // namespace
 
-size_t iteration_smem_bytes(int kp) { return sizeof(float4) * 3 * kThreads * kp; }
+size_t iteration_smem_bytes(int kp) {
+  return sizeof(float4) * ((PBDR_ROLL_PARTICLES != 0 && kp <= 4) ? 4 : 3) * kThreads * kp;
+}
 
 void launch_integrate(const IntegrateArgs& a, cudaStream_t s) {
   const unsigned blocks = static_cast<unsigned>((a.n - a.p0 + 255) / 256);

@@ -327,7 +327,7 @@ __device__ __forceinline__  // inlined: no call frame / spills around it (measur
 #else
 __device__ __noinline__
 #endif
-bool polar_warm_f(const float Af[9], const float rq[4], float R[9], double q[4]) {
+bool polar_warm_f(const float Af[9], const float rq[4], float R[9], double q[4], int* steps_used = nullptr) {
   D3 A;
   bool finite = true;
 #pragma unroll
@@ -341,6 +341,92 @@ bool polar_warm_f(const float Af[9], const float rq[4], float R[9], double q[4])
   const double c3 = d3_frob2(A) * PBDR_ONE_THIRD;
   const bool bad =
       !finite || !(d0 > 0.0) || d0 * d0 <= (PBDR_POLAR_REL_DET * PBDR_POLAR_REL_DET) * ((c3 * c3) * c3);
+#if PBDR_POLAR_WARM_F32
+  if (rq[0] != 0.0f || rq[1] != 0.0f || rq[2] != 0.0f || rq[3] != 0.0f) {
+    // The same homogeneous Gauss-Newton iteration in fp32 (mirrors oracle
+    // polar_warm_f32): A is the fp32 body sum itself.
+    float qc[4] = {rq[0], rq[1], rq[2], rq[3]};
+#if PBDR_GN_ROLLED
+#pragma unroll 1
+#endif
+    for (int step = 0; step < PBDR_POLAR_WARM_STEPS; ++step) {
+      const float w = qc[0], x = qc[1], y = qc[2], z = qc[3];
+      const float w2 = w * w, xx = x * x, yy = y * y, zz = z * z;
+      const float xy = x * y, xz = x * z, yz = y * z;
+      const float wx = w * x, wy = w * y, wz = w * z;
+      float R0[3][3];
+      R0[0][0] = (w2 + xx) - (yy + zz);
+      R0[0][1] = 2.0f * (xy - wz);
+      R0[0][2] = 2.0f * (xz + wy);
+      R0[1][0] = 2.0f * (xy + wz);
+      R0[1][1] = (w2 + yy) - (xx + zz);
+      R0[1][2] = 2.0f * (yz - wx);
+      R0[2][0] = 2.0f * (xz - wy);
+      R0[2][1] = 2.0f * (yz + wx);
+      R0[2][2] = (w2 + zz) - (xx + yy);
+      float B[3][3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) B[i][j] = (R0[0][i] * Af[j] + R0[1][i] * Af[3 + j]) + R0[2][i] * Af[6 + j];
+      const float sv[3] = {B[2][1] - B[1][2], B[0][2] - B[2][0], B[1][0] - B[0][1]};
+      float M[3][3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) M[i][j] = -(0.5f * (B[i][j] + B[j][i]));
+      const float tr = (-M[0][0] + -M[1][1]) + -M[2][2];
+      M[0][0] = tr + M[0][0];
+      M[1][1] = tr + M[1][1];
+      M[2][2] = tr + M[2][2];
+      const float dm = M[0][0] * (M[1][1] * M[2][2] - M[1][2] * M[2][1]) -
+                       M[0][1] * (M[1][0] * M[2][2] - M[1][2] * M[2][0]) +
+                       M[0][2] * (M[1][0] * M[2][1] - M[1][1] * M[2][0]);
+      if (!(dm > 0.0f) || !isfinite(dm)) break;
+      const float idm = 1.0f / dm;
+      const float c00 = (M[1][1] * M[2][2] - M[1][2] * M[2][1]) * idm;
+      const float c01 = (M[0][2] * M[2][1] - M[0][1] * M[2][2]) * idm;
+      const float c02 = (M[0][1] * M[1][2] - M[0][2] * M[1][1]) * idm;
+      const float c11 = (M[0][0] * M[2][2] - M[0][2] * M[2][0]) * idm;
+      const float c12 = (M[0][2] * M[1][0] - M[0][0] * M[1][2]) * idm;
+      const float c22 = (M[0][0] * M[1][1] - M[0][1] * M[1][0]) * idm;
+      const float h[3] = {0.5f * ((c00 * sv[0] + c01 * sv[1]) + c02 * sv[2]),
+                          0.5f * ((c01 * sv[0] + c11 * sv[1]) + c12 * sv[2]),
+                          0.5f * ((c02 * sv[0] + c12 * sv[1]) + c22 * sv[2])};
+      const float ww = 4.0f * ((h[0] * h[0] + h[1] * h[1]) + h[2] * h[2]);
+      if (!(ww <= static_cast<float>(PBDR_POLAR_WARM_MAX2))) break;
+      float qn[4];
+      qn[0] = qc[0] - ((qc[1] * h[0] + qc[2] * h[1]) + qc[3] * h[2]);
+      qn[1] = (qc[0] * h[0] + qc[1]) + (qc[2] * h[2] - qc[3] * h[1]);
+      qn[2] = (qc[0] * h[1] + qc[2]) + (qc[3] * h[0] - qc[1] * h[2]);
+      qn[3] = (qc[0] * h[2] + qc[3]) + (qc[1] * h[1] - qc[2] * h[0]);
+      if (ww <= static_cast<float>(PBDR_POLAR_WARM_TOLQ)) {
+        if (steps_used) *steps_used = step + 1;
+        if (bad) return false;
+        const float n2 = ((qn[0] * qn[0] + qn[1] * qn[1]) + qn[2] * qn[2]) + qn[3] * qn[3];
+        const float r = 1.0f / n2;
+        const float s = 1.5f - 0.5f * n2;
+        const float a = qn[0], b = qn[1], c = qn[2], d = qn[3];
+        const float a2 = a * a, bb = b * b, cc = c * c, dd = d * d;
+        const float bc = b * c, bd = b * d, cd = c * d, ab = a * b, ac = a * c, ad = a * d;
+        R[0] = ((a2 + bb) - (cc + dd)) * r;
+        R[1] = (2.0f * (bc - ad)) * r;
+        R[2] = (2.0f * (bd + ac)) * r;
+        R[3] = (2.0f * (bc + ad)) * r;
+        R[4] = ((a2 + cc) - (bb + dd)) * r;
+        R[5] = (2.0f * (cd - ab)) * r;
+        R[6] = (2.0f * (bd - ac)) * r;
+        R[7] = (2.0f * (cd + ab)) * r;
+        R[8] = ((a2 + dd) - (bb + cc)) * r;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) q[k] = static_cast<double>(qn[k] * s);
+        return true;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) qc[k] = qn[k];
+    }
+  }
+#else
   if (rq[0] != 0.0f || rq[1] != 0.0f || rq[2] != 0.0f || rq[3] != 0.0f) {
     // Homogeneous iterate (mirrors oracle polar_warm): qc is not renormalised
     // between steps; R0 = |qc|^2 R(qc) and the step h is scale invariant.
@@ -401,6 +487,7 @@ bool polar_warm_f(const float Af[9], const float rq[4], float R[9], double q[4])
       qn[2] = (qc[0] * h[1] + qc[2]) + (qc[3] * h[0] - qc[1] * h[2]);
       qn[3] = (qc[0] * h[2] + qc[3]) + (qc[1] * h[1] - qc[2] * h[0]);
       if (ww <= PBDR_POLAR_WARM_TOLQ) {
+        if (steps_used) *steps_used = step + 1;
         if (bad) return false;
         // R = |qn|^-2 (homogeneous rotation of qn); the stored quaternion gets
         // one Newton step of 1/sqrt from |qn|^2 ~ 1 (error O((|qn|^2 - 1)^2)).
@@ -416,8 +503,20 @@ bool polar_warm_f(const float Af[9], const float rq[4], float R[9], double q[4])
       for (int k = 0; k < 4; ++k) qc[k] = qn[k];
     }
   }
+#endif
+  if (steps_used) *steps_used = 15;  // cold fallback
   if (bad) return false;
-  return polar_rotation_f(Af, R, q);
+  // Cold path through copies: no array of the caller's hot path has its
+  // address taken (address-taken arrays live in local memory on every path,
+  // and in contact-rich states those local loads miss L1).
+  float Ac[9];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) Ac[i] = Af[i];
+  double qc[4];
+  const bool ok = polar_rotation_f(Ac, R, qc);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) q[k] = qc[k];
+  return ok;
 }
 
 __device__ void d3_sym_eigen(const D3& m, double ev[3], D3& V) {
@@ -500,7 +599,18 @@ __device__ __forceinline__ unsigned inertia_solve_f(const float If[6] /* xx yy z
       w[r] = static_cast<float>((inv.a[r][0] * dL[0] + inv.a[r][1] * dL[1]) + inv.a[r][2] * dL[2]);
     return 0u;
   }
-  return inertia_solve_slow(I, dL, w, null_axis);
+  // Through copies, as polar_warm_f's cold path (keeps the callers' arrays
+  // out of local memory).
+  D3 Ic = I;
+  double dLc[3] = {dL[0], dL[1], dL[2]}, nc[3] = {0.0, 0.0, 0.0};
+  float wc[3];
+  const unsigned e = inertia_solve_slow(Ic, dLc, wc, nc);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    w[k] = wc[k];
+    null_axis[k] = nc[k];
+  }
+  return e;
 }
 
 // Cyclic-Jacobi pseudo-inverse path (rank-deficient or ill-conditioned I).

@@ -145,6 +145,15 @@ PBDR_HD int32_t pbdr_cell_coord(float x, float inv_h) {
  * 1e-9 tolerance and three orders below fp32 particle resolution. Most
  * iterations after the first of a substep need one step. */
 #define PBDR_POLAR_WARM_TOLQ 1e-10
+/* Arithmetic of the warm Gauss-Newton steps: 1 = fp32 (the warm start is an
+ * fp32 quaternion and the returned rotation is rounded to fp32 anyway; the
+ * step's fp32 noise, ~1e-7 rad, sits far below the 1e-5 stop threshold),
+ * 0 = fp64. Both sides (pbdr_mat3.cuh, oracle_math.hpp) follow the switch, so
+ * parity stays bit-exact either way; the degeneracy test and the cold polar
+ * stay fp64. */
+#ifndef PBDR_POLAR_WARM_F32
+#define PBDR_POLAR_WARM_F32 0
+#endif
 /* fp32 warm-up stage of the polar (then fp64 polish to PBDR_POLAR_TOL). */
 #define PBDR_POLAR_F32_TOL2 1e-12f
 #define PBDR_POLAR_F32_TOLQ 1e-7f

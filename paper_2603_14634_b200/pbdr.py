@@ -590,7 +590,7 @@ class GpuSolver:
 
     def debug_phase_timing(self):
         """clock64 stamps per CTA of one iteration launch (see pbdr_gpu.h)."""
-        out = np.zeros((self.info.num_ctas, 8), np.int64)
+        out = np.zeros((self.info.num_ctas, 16), np.int64)
         raise_status(lib().pbdr_gpu_debug_phase_timing(self._h, _ptr(out)))
         return out
 

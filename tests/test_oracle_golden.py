@@ -156,7 +156,9 @@ def test_extract_pose_matches_reference(pbdr, pyoracle, golden):
 
 def test_warm_started_polar_matches_cold(pyoracle, golden):
     # The warm start (previous rotation, Gauss-Newton on the symmetry
-    # condition) converges to the same polar factor as the cold Newton path.
+    # condition) converges to the same polar factor as the cold Newton path --
+    # to fp32 resolution: the warm steps run in fp32 (PBDR_POLAR_WARM_F32,
+    # pbdr_pinned.h; their rotation is rounded to fp32 for the particles anyway).
     rs = np.random.default_rng(11)
     for case in golden["polar"]:
         if case["status"] != 0:
@@ -172,6 +174,7 @@ def test_warm_started_polar_matches_cold(pyoracle, golden):
             rq = np.concatenate([[w0 * w1 - v0 @ v1], w0 * v1 + w1 * v0 + np.cross(v0, v1)])
             okw, Rw, _ = pyoracle.polar_warm(A, rq)
             assert okw
-            np.testing.assert_allclose(Rw, Rc, atol=1e-10)
+            np.testing.assert_allclose(Rw, Rc, atol=1e-6)
+            np.testing.assert_allclose(Rw @ Rw.T, np.eye(3), atol=1e-6)
     ok, R, _ = pyoracle.polar_warm(np.eye(3), np.zeros(4))
     assert ok and np.allclose(R, np.eye(3))

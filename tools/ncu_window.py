@@ -39,6 +39,19 @@ if a.phase:
               f"p90 {np.percentile(d[:, i], 90):9.0f}")
     life = t[:, 6] - t[:, 0]
     print(f"  CTA lifetime mean {life.mean():.0f} cyc; kernel span {(t[:, 6].max() - t[:, 0].min()):.0f} cyc")
+    sub = t[:, 8:14]
+    ok = sub[:, 5] > 0
+    if ok.any():
+        sa = sub[ok]
+        print(f"  body math A: sums read {np.mean(sa[:, 0] - t[ok, 2]):.0f}, pre-polar {np.mean(sa[:, 4] - sa[:, 0]):.0f}, "
+              f"polar {np.mean(sa[:, 5] - sa[:, 4]):.0f}, post-polar {np.mean(sa[:, 1] - sa[:, 5]):.0f}, "
+              f"to barrier exit {np.mean(t[ok, 3] - sa[:, 1]):.0f} cyc")
+        print(f"  body math B: sums read {np.mean(sa[:, 2] - t[ok, 4]):.0f}, math {np.mean(sa[:, 3] - sa[:, 2]):.0f}, "
+              f"to barrier exit {np.mean(t[ok, 5] - sa[:, 3]):.0f} cyc")
+    hist = (t[:, 7].astype(np.int64) >> 16)
+    if hist.max() > 0:  # PBDR_GN_PROBE build: Gauss-Newton steps per body (5 = cold polar)
+        counts = [int(((hist >> (4 * k)) & 15).sum()) for k in range(6)]
+        print("  GN steps histogram (0..4, cold):", counts)
     sys.exit(0)
 rt = C.CDLL("libcudart.so.12")
 rt.cudaDeviceSynchronize()

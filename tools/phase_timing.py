@@ -19,6 +19,7 @@ s.step_frames(a.frames)
 s.debug_prologue()
 s.debug_iteration()
 t = s.debug_phase_timing().astype(np.float64)
+sub = t[:, 8:14]
 names = ["stage(TMA)", "phaseA", "bodymathA", "phaseB", "bodymathB", "phaseC"]
 d = np.diff(t[:, :7], axis=1)
 print(f"config {a.config}: {s.n} particles, {s.info.num_ctas} CTAs")
