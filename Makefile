@@ -20,7 +20,8 @@ LIB      := $(PKG)/lib/libpbdr_gpu.so
 HOST_LIB := $(PKG)/lib/libpbdr_host.so
 NVFLAGS  := $(ARCH) -std=c++17 -O3 -lineinfo --fmad=false -Xcompiler -fPIC,-ffp-contract=off \
             -Xptxas -v -Iinclude -I$(CSRC)
-CU_SRC   := $(CSRC)/pbdr_kernels.cu $(CSRC)/pbdr_sort.cu $(CSRC)/pbdr_engine.cu $(CSRC)/pbdr_mesh.cu
+CU_SRC   := $(CSRC)/pbdr_kernels.cu $(CSRC)/pbdr_sort.cu $(CSRC)/pbdr_engine.cu $(CSRC)/pbdr_mesh.cu \
+            $(CSRC)/pbdr_slab.cu
 CXX_SRC  := $(CSRC)/pbdr_dropin.cpp
 HOST_SRC := $(CSRC)/pbdr_scene.cpp $(CSRC)/pbdr_errors.cpp $(CSRC)/pbdr_hostmath.cpp $(CSRC)/pbdr_body.cpp
 HDRS     := include/pbdr_gpu.h $(wildcard include/pbdr/*.hpp) $(wildcard $(CSRC)/*.h) $(wildcard $(CSRC)/*.cuh)
@@ -49,7 +50,7 @@ $(HOST_LIB): $(HOST_OBJ)
 
 $(LIB): $(CU_OBJ) $(CXX_OBJ) $(HOST_LIB)
 	@mkdir -p $(PKG)/lib
-	$(NVCC) $(ARCH) -shared -o $@ $(CU_OBJ) $(CXX_OBJ) -L$(PKG)/lib -lpbdr_host -lcudart \
+	$(NVCC) $(ARCH) -shared -o $@ $(CU_OBJ) $(CXX_OBJ) -L$(PKG)/lib -lpbdr_host -lcudart -lnccl \
 	    -Xlinker -rpath,'$$ORIGIN'
 
 # Checked build: the same library with device-side bounds / invariant checks
@@ -62,7 +63,7 @@ $(OBJDIR)/checked/%.o: $(CSRC)/%.cu $(HDRS)
 	$(NVCC) $(NVFLAGS) -DPBDR_CHECKED=1 -c $< -o $@ 2> $(OBJDIR)/checked/$*.ptxas.txt || (cat $(OBJDIR)/checked/$*.ptxas.txt; false)
 $(CHECKED): $(patsubst $(CSRC)/%.cu,$(OBJDIR)/checked/%.o,$(CU_SRC)) $(CXX_OBJ) $(HOST_LIB)
 	$(NVCC) $(ARCH) -shared -o $@ $(patsubst $(CSRC)/%.cu,$(OBJDIR)/checked/%.o,$(CU_SRC)) $(CXX_OBJ) \
-	    -L$(PKG)/lib -lpbdr_host -lcudart -Xlinker -rpath,'$$ORIGIN'
+	    -L$(PKG)/lib -lpbdr_host -lcudart -lnccl -Xlinker -rpath,'$$ORIGIN'
 
 oracle:
 	$(MAKE) -C oracle

@@ -17,8 +17,10 @@ instead (free flight). C4 (4096 batched scenes) rides along as a `secondary`
 entry (whole run and tail window), `--config N` runs any other config.
 
 Under torchrun: C4 shards scenes per rank (weak scaling, no collective);
-C5 splits the giant scene into x-slabs with an NCCL halo (slab.py, strong
-scaling); C1-C3 run replicas.
+C5 runs as x-slabs of a grid that grows with the rank count (weak scaling:
+--slab-columns x-columns of 64 x 32 cubes per GPU, 64 = a whole config 5 per
+GPU) through the native C++ slab driver with an NCCL halo (csrc/pbdr_slab.cu);
+C1-C3 run replicas.
 
 --impl reference times the oracle restatement of the reference's CPU solver
 (the reference's own solver.cpp is absent from /root/reference, so the port is
@@ -61,6 +63,11 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-secondary", action="store_true", help="skip the C4 secondary entry")
+    ap.add_argument("--slab-columns", type=int, default=64,
+                    help="config 5 under torchrun: x-columns of cubes per rank (weak scaling; 64 = a whole "
+                         "BASELINE config 5 per GPU, 8 = BASELINE.md's 1/8 of it per GPU)")
+    ap.add_argument("--halo-refresh", type=int, default=0, choices=[0, 1],
+                    help="config 5 slabs: 0 = ghost positions after every iteration (exact), 1 = once per substep")
     ap.add_argument("--e2e-slices", type=int, default=16,
                     help="batched config: drive the e2e leg as this many handles/streams (1 = one handle)")
     return ap.parse_args()
@@ -428,62 +435,80 @@ def secondary_c4(args, local):
             "unit": "particle-substeps/s", "clocks": clocks.summary()}
 
 
-def slab_bench(args, rank, world, local):
-    """Config 5 split into x-slabs across the ranks (one scene, NCCL halo)."""
+def native_slab_bench(args, rank, world, local):
+    """Config 5 as x-slabs, one rank per GPU, weak scaling: each rank generates
+    and holds only its slab (args.slab_columns x-columns of 64 x 32 cubes) plus
+    3 ghost columns per side, and the C++ driver (csrc/pbdr_slab.cu) runs the
+    substeps with the ghost halo over NCCL send/recv, overlapped with the
+    interior tiles. Device time (CUDA events on the handle's stream around the
+    K frames, including the per-frame repartition), max over ranks."""
     import torch
     import torch.distributed as dist
     from paper_2603_14634_b200 import pbdr as P
-    from paper_2603_14634_b200 import slab as S
+    from paper_2603_14634_b200 import slab_native as S
 
-    g = P.GeneratedScene(5, seed=args.seed, scale=args.scale)
-    nb = g.desc.num_bodies
-    off = g.array("body_offsets", nb + 1, np.int64)
-    rho, h = S.body_reach(g.array("rest_offsets", 3 * g.num_particles), off, g.array("radius", g.num_particles))
+    spec = S.c5_slab_spec(rank, world, columns_per_rank=args.slab_columns)
+    g = S.generate(spec, seed=args.seed)
     solver = P.GpuSolver(g.desc, g.cfg, device=local)
-    eng = S.GpuEngine(solver, g.cfg)
-    run = S.SlabRunner(eng, rank, world, S.TorchComm(), off, rho=rho, h=h, margin=0.1)
-    run.start()
-    run.step_frames(max(3, args.warmup))
-    dist.barrier()
-    torch.cuda.synchronize(local)
+    ids = [P.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(ids, src=0)
+    S.attach(solver, spec, refresh=args.halo_refresh, overlap=1, nccl_id=ids[0])
+    solver.slab_start()
+    W = max(3, args.warmup)
+    first, last = window_frames(args)
+    solver.slab_step_frames(W)
+    if first > W:
+        solver.slab_step_frames(first - W)
+    stream = torch.cuda.ExternalStream(solver.stream_handle(), device=torch.device("cuda", local))
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
+    dist.barrier()
+    torch.cuda.synchronize(local)
     with ClockSampler(local) as clocks:
-        ev0.record(eng.stream)
-        run.step_frames(args.steps)
-        ev1.record(eng.stream)
+        ev0.record(stream)
+        solver.slab_step_frames(args.steps)
+        ev1.record(stream)
         ev1.synchronize()
     ms = ev0.elapsed_time(ev1)
     dist.barrier()
-    t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local}")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
-    n_total = solver.n
+    info = solver.slab_info()
+    t = torch.tensor([ms, info["owned_particles"], info["ghost_bodies"], info["halo_bytes_per_iteration"],
+                      info["migrations"]], dtype=torch.float64, device=f"cuda:{local}")
+    tmax = t.clone()
+    dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    tsum = t.clone()
+    dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+    ms_max = float(tmax[0].item())
+    n_total = int(tsum[1].item())
     subs = g.cfg.substeps
     value = n_total * subs * args.steps / (ms_max / 1e3)
-    owned = torch.tensor([sum(int(run.bcount[b]) for b in run.owned)], dtype=torch.int64, device=f"cuda:{local}")
-    owned_max = owned.clone()
-    dist.all_reduce(owned_max, op=dist.ReduceOp.MAX)
-    ghosts = sum(len(v) for v in run.plan.recv_bodies.values())
     peak, peak_src = measured_peak()
     if rank == 0:
         line = {
             "metric": "particle-substeps/s", "value": value, "unit": "particle-substeps/s", "n_gpus": world,
-            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_max / args.steps,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (seeded BASELINE.json config 5, host generator)",
-            "config": {"workload": P.CONFIG_NAMES[5], "particles_total": n_total, "bodies_total": nb,
-                       "substeps_per_step": subs, "iterations": g.cfg.solver_iterations,
-                       "parallelism": f"x-slab x{world}, NCCL halo after every iteration, migration per frame",
-                       "max_owned_particles_per_gpu": int(owned_max.item()), "ghost_bodies_rank0": ghosts,
-                       "ghost_band_m": run.geo.ghost_band,
-                       "l2": "inputs larger than L2"},
+            "steps": args.steps, "warmup": W, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded BASELINE.json config 5 grid, rank-local generation)",
+            "config": {"workload": P.CONFIG_NAMES[5], "grid": [spec.gx, spec.gy, spec.gz],
+                       "columns_per_gpu": args.slab_columns, "particles_total": n_total,
+                       "particles_per_gpu": n_total // world, "substeps_per_step": subs,
+                       "iterations": g.cfg.solver_iterations, "frame_rate_hz": 240.0,
+                       "timed_frames": f"{first}..{last} ({args.window} of the run)",
+                       "parallelism": f"x-slab x{world}: native driver, NCCL halo "
+                                      f"({'every iteration' if args.halo_refresh == 0 else 'once per substep'}),"
+                                      " overlapped with interior tiles, migration per frame",
+                       "max_ghost_bodies_per_gpu": int(tmax[2].item()),
+                       "max_halo_bytes_per_iteration": int(tmax[3].item()),
+                       "migrations": int(tsum[4].item()), "l2": "inputs larger than L2"},
             "roofline": {"bound": "hbm", "achieved": (value / world) * BYTES_PER_SUBSTEP / 1e9, "peak": peak,
                          "unit": "GB/s", "frac": (value / world) * BYTES_PER_SUBSTEP / (peak * 1e9),
-                         "traffic": None, "kernel": "whole substep (per GPU)", "peak_source": peak_src},
+                         "traffic": None, "kernel": "whole substep (per GPU, algorithmic 1120 B)",
+                         "peak_source": peak_src},
             "cpu_baseline": None,
             "e2e": None,
-            "gpu_launches": int(solver.info.launches_per_frame * args.steps),
+            # graph-mode count of the same scene plus, per iteration, the halo's
+            # gather / scatter launches (4 per peer at the last iteration)
+            "gpu_launches": int((solver.info.launches_per_frame + subs * g.cfg.solver_iterations * 4) * args.steps),
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -502,7 +527,7 @@ def main():
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        slab_bench(args, rank, world, local)
+        native_slab_bench(args, rank, world, local)
         return
 
     import torch

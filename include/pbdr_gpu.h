@@ -263,6 +263,40 @@ enum {
 int pbdr_gpu_gather(pbdr_handle* h, int field, const int32_t* index, int64_t count, void* dst);
 int pbdr_gpu_scatter(pbdr_handle* h, int field, const int32_t* index, int64_t count, const void* src);
 
+/* ---- Native x-slab decomposition ---------
+ * One rank of a giant scene split into x-slabs, driven in C++ with the halo
+ * over NCCL (one rank per GPU) or over a local hub (ranks as threads of one
+ * process on one GPU: the tests' way to run the same driver). The handle holds
+ * a RANK-LOCAL scene: a contiguous range of the global bodies in global order
+ * (pbdr_scene_generate_c5_slab), i.e. this rank's slab plus ghost bands, so
+ * every owned trajectory is the single-GPU one bit for bit (refresh = 0).
+ * Replaces: nothing in the reference (it has no decomposition); the scaling
+ * note is PAPER.md:378. */
+typedef struct pbdr_slab_config {
+  int32_t rank, world;
+  const double* edges;  /* world + 1 ascending com-x boundaries (edges[0] = -inf, edges[world] = +inf) */
+  double ghost_band;    /* G = 2 rho + h + margin: a body this close to a boundary is ghosted across it */
+  double margin;        /* a body may move at most margin / 2 in x per frame (else SimulationError) */
+  int64_t body_first;   /* global id of local body 0 */
+  int32_t refresh;      /* 0: ghost positions after every iteration (exact); 1: once per substep */
+  int32_t overlap;      /* 1: tiles a neighbour ghosts run first, their halo overlaps the other tiles */
+} pbdr_slab_config;
+typedef struct pbdr_slab_hub pbdr_slab_hub;
+int pbdr_nccl_unique_id(uint8_t out[128]);
+int pbdr_gpu_slab_attach_nccl(pbdr_handle* h, const pbdr_slab_config* c, const uint8_t nccl_id[128]);
+pbdr_slab_hub* pbdr_slab_hub_create(int world);
+void pbdr_slab_hub_destroy(pbdr_slab_hub* hub);
+int pbdr_gpu_slab_attach_local(pbdr_handle* h, const pbdr_slab_config* c, pbdr_slab_hub* hub);
+/* Initial partition (owners by com_x, ghost lists, full ghost state). */
+int pbdr_gpu_slab_start(pbdr_handle* h);
+/* Frames of cfg.substeps substeps; repartition (migration) at every frame start. */
+int pbdr_gpu_slab_step_frames(pbdr_handle* h, int64_t frames);
+/* Owned local body ids (ascending); count always written. */
+int pbdr_gpu_slab_owned(pbdr_handle* h, int32_t* local_ids, int64_t capacity, int64_t* count);
+/* out[6]: owned bodies, owned particles, ghost bodies, halo bytes per
+ * iteration (sent + received), migrations so far, frames so far. */
+int pbdr_gpu_slab_info(pbdr_handle* h, int64_t out[6]);
+
 /* ---- GPU pack_mesh (geometry.cpp:125-195) -----
  * Replaces: pbdr::pack_mesh(const TriMesh&, double radius) (geometry.hpp:57).
  * Grid candidates bb.min + radius + i * 2 radius (x slowest) inside the
@@ -289,7 +323,15 @@ int pbdr_scene_generate(int config_id, uint64_t seed, int64_t scale, pbdr_genera
  * first_scene + scenes), each seeded seed + scene index (weak scaling). */
 int pbdr_scene_generate_c4_shard(uint64_t seed, int64_t scenes, int64_t first_scene,
                                  pbdr_generated_scene** out);
+/* Config 5's cubes in x-columns [x_first, x_first + x_count) of a gx x gy x gz
+ * grid (64 x 64 x 32 = BASELINE config 5): the rank-local scene of an x-slab
+ * decomposition. Global x-major body order is kept (local body k is global
+ * body x_first * gy * gz + k) and every cube equals the whole grid's. */
+int pbdr_scene_generate_c5_slab(uint64_t seed, int64_t gx, int64_t gy, int64_t gz, int64_t x_first,
+                                int64_t x_count, pbdr_generated_scene** out);
 int pbdr_scene_view(const pbdr_generated_scene* s, pbdr_scene_desc* desc, pbdr_solver_cfg* cfg);
+/* Placements that needed more than one attempt (0 for the config-5 grids). */
+int64_t pbdr_scene_resamples(const pbdr_generated_scene* s);
 /* Frames the config is specified for (1000/1000/500/200/100). */
 int64_t pbdr_scene_frames(const pbdr_generated_scene* s);
 /* Bodies whose placement still overlapped after 256 resamples (expected 0). */

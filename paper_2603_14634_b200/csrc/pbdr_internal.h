@@ -25,11 +25,14 @@ struct GeneratedScene {
   pbdr_solver_cfg cfg{};
   int64_t frames = 0;
   int64_t forced_overlaps = 0;
+  int64_t resamples = 0;  // placements that needed more than one attempt
   int64_t num_particles() const { return static_cast<int64_t>(inv_mass.size()); }
 };
 
 GeneratedScene* generate(int config_id, uint64_t seed, int64_t scale);
 GeneratedScene* generate_c4_shard(uint64_t seed, int64_t scenes, int64_t first_scene);
+GeneratedScene* generate_c5_slab(uint64_t seed, int64_t gx, int64_t gy, int64_t gz, int64_t x_first,
+                                 int64_t x_count);
 void view(const GeneratedScene& s, pbdr_scene_desc& d);
 
 // Thread-local last-error bookkeeping (pbdr_last_error*). Each returns `code`.

@@ -321,7 +321,13 @@ Rot bounded_rotation(SplitMix& rng, double max_angle) {
   return rot_from_quat(std::cos(h), ax * sh, ay * sh, az * sh);
 }
 
-static int64_t gen_cube_grid(GeneratedScene& s, SplitMix& rng, const CubeGridSpec& g, int scene_id) {
+// Cubes t in [t_first, t_end) of the grid (t_end < 0: all). Each cube draws
+// a fixed number of values unless its placement is resampled (never for the
+// bounded-tilt grids of config 5, which are overlap-free by construction), so
+// a sub-range starts from the stream skipped ahead by that many draws;
+// `resamples` counts the placements that needed more than one attempt.
+static int64_t gen_cube_grid(GeneratedScene& s, SplitMix& rng, const CubeGridSpec& g, int scene_id,
+                             int64_t t_first = 0, int64_t t_end = -1, int64_t* resamples = nullptr) {
   double r = 0.01;
   const double h = g.n * 0.01;  // half extent: 0.06 for 6^3, 0.08 for 8^3
   const double hh = g.n == 6 ? 0.06 : (g.n == 8 ? 0.08 : h);
@@ -329,7 +335,8 @@ static int64_t gen_cube_grid(GeneratedScene& s, SplitMix& rng, const CubeGridSpe
   HullGrid grid(0.5);
   int64_t forced = 0;
   const int64_t cells = static_cast<int64_t>(g.gx) * g.gy * g.gz;
-  for (int64_t t = 0; t < cells; ++t) {
+  if (t_end < 0 || t_end > cells) t_end = cells;
+  for (int64_t t = t_first; t < t_end; ++t) {
       int i, j, k;
       if (g.x_major) {
         k = static_cast<int>(t % g.gz);
@@ -350,6 +357,7 @@ static int64_t gen_cube_grid(GeneratedScene& s, SplitMix& rng, const CubeGridSpe
           R = g.max_tilt > 0 ? bounded_rotation(rng, g.max_tilt) : uniform_rotation(rng);
           c = add(base, jit);
           ok = !grid.overlaps(box_hull(c, R, g.n, g.n, g.n, r));
+          if (!ok && resamples) ++*resamples;
         }
         if (!ok) ++forced;
         grid.insert(box_hull(c, R, g.n, g.n, g.n, r));
@@ -436,7 +444,29 @@ static void gen_c5(GeneratedScene& s, uint64_t seed, int64_t gx) {
   const int g = static_cast<int>(gx);
   const double half = 0.5 * 0.2 * (g - 1);
   CubeGridSpec spec{g, g, std::max(1, g / 2), 0.2, {-half, -half, 0.2}, 0.01, 8, 1.0, 0.5, 0.0, 0.07, true};
-  s.forced_overlaps = gen_cube_grid(s, rng, spec, 0);
+  s.forced_overlaps = gen_cube_grid(s, rng, spec, 0, 0, -1, &s.resamples);
+  s.frames = 100;
+}
+
+// Config 5's cubes in the x-columns [x_first, x_first + x_count) of a
+// gx * gy * gz grid (centred in x and y like gen_c5; gx = gy = 64, gz = 32 is
+// BASELINE config 5): the rank-local scene of an x-slab decomposition. Bodies
+// keep the global x-major order, so local body k is global body
+// x_first * gy * gz + k, and the cubes are bit-identical to the global
+// generation's (the stream is skipped ahead by the 9 draws of every cube
+// before the range -- valid because no placement is ever resampled; checked
+// by tests/test_slab_native.py against the whole grid).
+static void gen_c5_slab(GeneratedScene& s, uint64_t seed, int64_t gx, int64_t gy, int64_t gz, int64_t x_first,
+                        int64_t x_count) {
+  SplitMix rng(seed);
+  constexpr uint64_t kDrawsPerCube = 9;  // jitter 3, bounded tilt 3, velocity 3
+  const int64_t per_col = gy * gz;
+  rng.s += kDrawsPerCube * static_cast<uint64_t>(x_first * per_col) * 0x9E3779B97F4A7C15ull;
+  CubeGridSpec spec{static_cast<int>(gx), static_cast<int>(gy), static_cast<int>(gz), 0.2,
+                    {-0.5 * 0.2 * static_cast<double>(gx - 1), -0.5 * 0.2 * static_cast<double>(gy - 1), 0.2},
+                    0.01, 8, 1.0, 0.5, 0.0, 0.07, true};
+  s.forced_overlaps = gen_cube_grid(s, rng, spec, 0, x_first * per_col, (x_first + x_count) * per_col,
+                                    &s.resamples);
   s.frames = 100;
 }
 
@@ -459,6 +489,18 @@ GeneratedScene* generate(int config_id, uint64_t seed, int64_t scale) {
     case 5: gen_c5(*s, seed, scale > 0 ? scale : 64); break;
     default: delete s; return nullptr;
   }
+  return s;
+}
+
+GeneratedScene* generate_c5_slab(uint64_t seed, int64_t gx, int64_t gy, int64_t gz, int64_t x_first,
+                                 int64_t x_count) {
+  GeneratedScene* s = new GeneratedScene();
+  default_cfg(s->cfg);
+  s->has_ground = 1;
+  s->ground = make_plane({0, 0, 0}, {0, 0, 1}, 0.5);
+  s->contact_relaxation = 1.0;
+  s->body_offsets.push_back(0);
+  gen_c5_slab(*s, seed, gx, gy, gz, x_first, x_count);
   return s;
 }
 
@@ -527,6 +569,21 @@ int pbdr_scene_generate_c4_shard(uint64_t seed, int64_t scenes, int64_t first_sc
     return pbdr_host::set_error(PBDR_ERR_GENERIC, "scene generation: out of host memory");
   }
 }
+
+int pbdr_scene_generate_c5_slab(uint64_t seed, int64_t gx, int64_t gy, int64_t gz, int64_t x_first,
+                                int64_t x_count, pbdr_generated_scene** out) {
+  if (!out) return pbdr_host::set_error(PBDR_ERR_GENERIC, "null output");
+  *out = nullptr;
+  if (gx < 1 || gy < 1 || gz < 1 || x_first < 0 || x_count < 1 || x_first + x_count > gx)
+    return pbdr_host::set_config_error("slab", "column range outside the grid");
+  pbdr_generated_scene* g = new (std::nothrow) pbdr_generated_scene();
+  if (!g) return pbdr_host::set_error(PBDR_ERR_GENERIC, "out of host memory");
+  g->s = pbdr_host::generate_c5_slab(seed, gx, gy, gz, x_first, x_count);
+  *out = g;
+  return PBDR_OK;
+}
+
+int64_t pbdr_scene_resamples(const pbdr_generated_scene* g) { return g && g->s ? g->s->resamples : 0; }
 
 int pbdr_scene_view(const pbdr_generated_scene* g, pbdr_scene_desc* desc, pbdr_solver_cfg* cfg) {
   if (!g || !g->s) return PBDR_ERR_GENERIC;

@@ -101,6 +101,12 @@ class SceneDesc(C.Structure):
                 ("body_scene", C.POINTER(C.c_int32)), ("tile_kp", C.c_int32)]
 
 
+class SlabConfig(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("edges", C.POINTER(C.c_double)),
+                ("ghost_band", C.c_double), ("margin", C.c_double), ("body_first", C.c_int64),
+                ("refresh", C.c_int32), ("overlap", C.c_int32)]
+
+
 class BodyStats(C.Structure):
     _fields_ = [("com", C.c_double * 3), ("quat", C.c_double * 4), ("linear", C.c_double * 3),
                 ("angular", C.c_double * 3)]
@@ -142,6 +148,17 @@ def lib() -> C.CDLL:
         L.pbdr_gpu_read_f32_async.argtypes = [vp, vp, vp]
         L.pbdr_gpu_step_frames_async.argtypes = [vp, i64]
         L.pbdr_gpu_read_bodies.argtypes = [vp, vp]
+        L.pbdr_nccl_unique_id.argtypes = [vp]
+        L.pbdr_gpu_slab_attach_nccl.argtypes = [vp, C.POINTER(SlabConfig), vp]
+        L.pbdr_slab_hub_create.argtypes = [C.c_int]
+        L.pbdr_slab_hub_create.restype = vp
+        L.pbdr_slab_hub_destroy.argtypes = [vp]
+        L.pbdr_slab_hub_destroy.restype = None
+        L.pbdr_gpu_slab_attach_local.argtypes = [vp, C.POINTER(SlabConfig), vp]
+        L.pbdr_gpu_slab_start.argtypes = [vp]
+        L.pbdr_gpu_slab_step_frames.argtypes = [vp, i64]
+        L.pbdr_gpu_slab_owned.argtypes = [vp, vp, i64, C.POINTER(i64)]
+        L.pbdr_gpu_slab_info.argtypes = [vp, vp]
         L.pbdr_gpu_set_time.argtypes = [vp, i64]
         L.pbdr_gpu_get_time.argtypes = [vp, C.POINTER(i64)]
         L.pbdr_gpu_info.argtypes = [vp, C.POINTER(Info)]
@@ -189,6 +206,9 @@ def host_lib() -> C.CDLL:
         L.pbdr_last_error_payload.argtypes = [dp, C.POINTER(i64), C.POINTER(i32)]
         L.pbdr_scene_generate.argtypes = [C.c_int, C.c_uint64, i64, C.POINTER(vp)]
         L.pbdr_scene_generate_c4_shard.argtypes = [C.c_uint64, i64, i64, C.POINTER(vp)]
+        L.pbdr_scene_generate_c5_slab.argtypes = [C.c_uint64, i64, i64, i64, i64, i64, C.POINTER(vp)]
+        L.pbdr_scene_resamples.argtypes = [vp]
+        L.pbdr_scene_resamples.restype = i64
         L.pbdr_scene_view.argtypes = [vp, C.POINTER(SceneDesc), C.POINTER(SolverCfg)]
         L.pbdr_scene_frames.argtypes = [vp]
         L.pbdr_scene_frames.restype = i64
@@ -369,10 +389,15 @@ class GeneratedScene:
     """One of the five BASELINE.json configs, built by the host generator
     (libpbdr_host.so: no CUDA, so the CPU arms can use it too)."""
 
-    def __init__(self, config_id: int, seed: int = 0, scale: int = 0, c4_first_scene: int | None = None):
+    def __init__(self, config_id: int, seed: int = 0, scale: int = 0, c4_first_scene: int | None = None,
+                 c5_slab: tuple | None = None):
+        """c5_slab = (gx, gy, gz, x_first, x_count): config 5's cubes in those
+        x-columns of a gx * gy * gz grid (a rank-local slab scene)."""
         L = host_lib()
         h = C.c_void_p()
-        if c4_first_scene is None:
+        if c5_slab is not None:
+            st = L.pbdr_scene_generate_c5_slab(seed, *[int(v) for v in c5_slab], C.byref(h))
+        elif c4_first_scene is None:
             st = L.pbdr_scene_generate(config_id, seed, scale, C.byref(h))
         else:
             st = L.pbdr_scene_generate_c4_shard(seed, scale, c4_first_scene, C.byref(h))
@@ -384,6 +409,7 @@ class GeneratedScene:
         raise_status(L.pbdr_scene_view(h, C.byref(self.desc), C.byref(self.cfg)))
         self.frames = L.pbdr_scene_frames(h)
         self.forced_overlaps = L.pbdr_scene_forced_overlaps(h)
+        self.resamples = L.pbdr_scene_resamples(h)
 
     @property
     def num_particles(self):
@@ -536,6 +562,40 @@ class GpuSolver:
         vel = None if vel is None else np.ascontiguousarray(vel, np.float64)
         raise_status(lib().pbdr_gpu_write_particles(self._h, _ptr(pos), _ptr(vel)))
 
+    # ---- native x-slab decomposition (pbdr_gpu_slab_*) ------------------------
+    def slab_attach(self, rank, world, edges, ghost_band, margin, body_first, refresh=0, overlap=0,
+                    hub=None, nccl_id: bytes | None = None):
+        """Attach the C++ slab driver: over a local hub (thread ranks sharing
+        this GPU) or over NCCL (nccl_id: 128 bytes from nccl_unique_id())."""
+        self._slab_edges = (C.c_double * len(edges))(*[float(e) for e in edges])
+        cfg = SlabConfig(rank, world, C.cast(self._slab_edges, C.POINTER(C.c_double)), ghost_band, margin,
+                         body_first, refresh, overlap)
+        self._slab_cfg = cfg
+        if hub is not None:
+            raise_status(lib().pbdr_gpu_slab_attach_local(self._h, C.byref(cfg), C.c_void_p(hub)))
+        else:
+            buf = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
+            raise_status(lib().pbdr_gpu_slab_attach_nccl(self._h, C.byref(cfg), buf))
+
+    def slab_start(self):
+        raise_status(lib().pbdr_gpu_slab_start(self._h))
+
+    def slab_step_frames(self, frames: int = 1):
+        raise_status(lib().pbdr_gpu_slab_step_frames(self._h, frames))
+
+    def slab_owned(self) -> np.ndarray:
+        n = C.c_int64()
+        raise_status(lib().pbdr_gpu_slab_owned(self._h, None, 0, C.byref(n)))
+        out = np.empty(n.value, np.int32)
+        raise_status(lib().pbdr_gpu_slab_owned(self._h, _ptr(out), n.value, C.byref(n)))
+        return out
+
+    def slab_info(self) -> dict:
+        out = np.zeros(6, np.int64)
+        raise_status(lib().pbdr_gpu_slab_info(self._h, _ptr(out)))
+        keys = ("owned_bodies", "owned_particles", "ghost_bodies", "halo_bytes_per_iteration", "migrations", "frames")
+        return {k: int(v) for k, v in zip(keys, out)}
+
     def set_time(self, substep: int):
         """Simulation time as a substep index (ForceProgram windows, error frames)."""
         raise_status(lib().pbdr_gpu_set_time(self._h, substep))
@@ -641,6 +701,24 @@ def rng_unit(seed, count):
     out = np.empty(count, np.float64)
     host_lib().pbdr_rng_unit(seed, count, _ptr(out))
     return out
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    raise_status(lib().pbdr_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def slab_hub_create(world: int) -> int:
+    """Local hub for `world` thread ranks sharing one GPU (pbdr_slab_hub_create)."""
+    h = lib().pbdr_slab_hub_create(world)
+    if not h:
+        raise Error("pbdr_slab_hub_create failed")
+    return h
+
+
+def slab_hub_destroy(hub: int):
+    lib().pbdr_slab_hub_destroy(C.c_void_p(hub))
 
 
 def cuda_device_count() -> int:
