@@ -115,3 +115,21 @@ def test_native_slabs_substep_refresh_aggregates(pbdr):
     ke, ke_ref = (v[:, :3] ** 2).sum(), (v_ref[:, :3] ** 2).sum()
     assert np.abs(com - com_ref).max() <= 0.01 * np.abs(com_ref).max()
     assert abs(ke - ke_ref) <= 0.01 * ke_ref
+
+
+@pytest.mark.gpu
+def test_nccl_transport_single_rank(pbdr):
+    # The NCCL transport end to end on the one GPU this pool provides: a
+    # world-1 communicator (no peers, so no exchange), the driver's per-frame
+    # repartition and role set-up on the whole grid; equal to the plain handle.
+    frames = 5
+    p_ref, v_ref = _whole(16, frames)
+    spec = S.c5_slab_spec(0, 1, columns_per_rank=16, gy=16, gz=8)
+    g = S.generate(spec)
+    s = P.GpuSolver(g.desc, g.cfg)
+    S.attach(s, spec, overlap=1, nccl_id=P.nccl_unique_id())
+    s.slab_start()
+    s.slab_step_frames(frames)
+    ids, slots, p4, v4 = S.owned_state(s, g, spec)
+    assert len(ids) == g.num_bodies
+    assert np.array_equal(p4, p_ref[slots]) and np.array_equal(v4, v_ref[slots])
