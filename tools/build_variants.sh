@@ -13,6 +13,6 @@ while [ $# -ge 2 ]; do
     -c paper_2603_14634_b200/csrc/pbdr_kernels.cu -o build/variants/k_$name.o 2> build/variants/k_$name.ptxas.txt
   grep -A2 "k_iterationILi4ELb0ELb0" build/variants/k_$name.ptxas.txt | grep -E "Used|spill" | sed "s/^/$name: /" || true
   /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -o build/variants/lib_$name.so \
-    build/variants/k_$name.o build/obj/pbdr_sort.o build/obj/pbdr_engine.o build/obj/pbdr_mesh.o build/obj/pbdr_dropin.o \
-    -Lpaper_2603_14634_b200/lib -lpbdr_host -lcudart -Xlinker -rpath,'$ORIGIN/../../paper_2603_14634_b200/lib'
+    build/variants/k_$name.o build/obj/pbdr_sort.o build/obj/pbdr_engine.o build/obj/pbdr_mesh.o build/obj/pbdr_slab.o build/obj/pbdr_dropin.o \
+    -Lpaper_2603_14634_b200/lib -lpbdr_host -lcudart -lnccl -Xlinker -rpath,'$ORIGIN/../../paper_2603_14634_b200/lib'
 done
