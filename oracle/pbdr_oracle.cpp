@@ -47,6 +47,8 @@
 // has no reference implementation or trajectory fixture to pin against.
 // ============================================================================
 #include <algorithm>
+#include <climits>
+#include <cstdlib>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -93,6 +95,7 @@ struct State {
   bool incremental = true, linfix = true, angfix = true;
   int64_t substep_index = 0;
   uint32_t mask = 0;
+  pbdr_key_layout layout{};
   std::vector<int32_t> ncand, cand;
   std::vector<float> cand_rr;
   uint32_t err_bits = 0;
@@ -826,7 +829,22 @@ int oracle_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* cfg, int thre
   s->h = static_cast<float>(2.0 * rmax);
   s->inv_h = 1.0f / s->h;
   s->h2 = s->h * s->h;
-  s->mask = (1u << pbdr_hash_bits(n)) - 1u;
+  {
+    // Bucket key layout: the library's rule on the same fp32 positions.
+    bool single = true;
+    for (int32_t b = 0; b < s->nb && single; ++b) single = s->bscene[b] == 0;
+    int32_t cmin[3] = {INT32_MAX, INT32_MAX, INT32_MAX}, cmax[3] = {INT32_MIN, INT32_MIN, INT32_MIN};
+    for (int64_t p = 0; p < n; ++p)
+      for (int a = 0; a < 3; ++a) {
+        const int32_t c = pbdr_cell_coord(s->pos[4 * p + a], s->inv_h);
+        cmin[a] = std::min(cmin[a], c);
+        cmax[a] = std::max(cmax[a], c);
+      }
+    s->layout = pbdr_choose_key_layout(single ? 1 : 0, cmin, cmax, n);
+    if (const char* e = std::getenv("PBDR_LINEAR_KEYS"))
+      if (std::atoi(e) == 0) s->layout = pbdr_choose_key_layout(0, cmin, cmax, n);
+  }
+  s->mask = static_cast<uint32_t>((uint64_t(1) << s->layout.bits) - 1u);
   *out = s;
   return PBDR_OK;
 }
@@ -963,7 +981,7 @@ void oracle_read_keys(void* st, uint32_t* hash, int32_t* cell) {
     if (cell) {
       cell[3 * p] = cx; cell[3 * p + 1] = cy; cell[3 * p + 2] = cz;
     }
-    if (hash) hash[p] = pbdr_cell_hash(cx, cy, cz, static_cast<uint32_t>(s.bscene[s.body_of[p]]), s.mask);
+    if (hash) hash[p] = pbdr_cell_key(cx, cy, cz, static_cast<uint32_t>(s.bscene[s.body_of[p]]), s.mask, s.layout);
   }
 }
 

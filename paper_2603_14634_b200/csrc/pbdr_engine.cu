@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <cstdlib>
 #include <cmath>
 #include <cstdio>
@@ -123,6 +124,7 @@ pbdr_dev::IntegrateArgs integrate_args(const pbdr_handle* h) {
   ia.inv_h = h->inv_h;
   ia.dt_d = h->dt_d;
   ia.mask = h->mask;
+  ia.layout = h->key_layout;
   return ia;
 }
 
@@ -297,6 +299,7 @@ void enqueue_substep(pbdr_handle* h, pbdr_dev::LaunchHook* hook, bool integrated
   na.inv_h = h->inv_h;
   na.h2 = h->h2;
   na.mask = h->mask;
+  na.layout = h->key_layout;
   if (hook) hook->before(kHookNeighbours);
   launch_neighbours(na, h->stream);
   if (hook) hook->after(kHookNeighbours);
@@ -730,7 +733,25 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
     h->max_extent = 2.2f * qmax + 2.0f * h->h;
     h->inv_cell_b = 1.0f / (h->max_extent + 2.0f * h->h);
   }
-  h->hash_bits = pbdr_hash_bits(n);
+  {
+    // Bucket keys: spatially ordered for single scenes that fit (pinned
+    // pbdr_choose_key_layout, from the fp32 positions the oracle also starts from).
+    bool single = true;
+    for (int32_t b = 0; b < nb && single; ++b) single = scene[b] == 0;
+    int32_t cmin[3] = {INT32_MAX, INT32_MAX, INT32_MAX}, cmax[3] = {INT32_MIN, INT32_MIN, INT32_MIN};
+    for (int64_t k = 0; k < n; ++k) {
+      const int32_t c[3] = {pbdr_cell_coord(pos[k].x, h->inv_h), pbdr_cell_coord(pos[k].y, h->inv_h),
+                            pbdr_cell_coord(pos[k].z, h->inv_h)};
+      for (int a = 0; a < 3; ++a) {
+        cmin[a] = std::min(cmin[a], c[a]);
+        cmax[a] = std::max(cmax[a], c[a]);
+      }
+    }
+    h->key_layout = pbdr_choose_key_layout(single ? 1 : 0, cmin, cmax, n);
+    if (const char* e = std::getenv("PBDR_LINEAR_KEYS"))
+      if (std::atoi(e) == 0) h->key_layout = pbdr_choose_key_layout(0, cmin, cmax, n);
+  }
+  h->hash_bits = h->key_layout.bits;
   h->passes = (h->hash_bits + 7) / 8;
   h->mask = static_cast<uint32_t>((uint64_t(1) << h->hash_bits) - 1u);
   auto add_plane = [&](const pbdr_plane& p) {

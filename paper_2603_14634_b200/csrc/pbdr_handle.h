@@ -116,6 +116,7 @@ struct pbdr_handle {
   int sorted_buf = 0;  // keys/vals buffer holding the last sorted pairs
   int ctas = 0;
   int hash_bits = 10;
+  pbdr_key_layout key_layout{};  // bucket keys (pbdr_choose_key_layout)
   int passes = 2;
   uint32_t mask = 0;
   float dt = 0, inv_dt = 0, gravity = 0, relax = 1, h = 0, inv_h = 0, h2 = 0;

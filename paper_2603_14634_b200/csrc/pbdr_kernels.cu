@@ -294,7 +294,7 @@ __device__ __forceinline__ uint32_t integrate_key(const IntegrateArgs& A, int b,
   const int32_t cx = pbdr_cell_coord(xn.x, A.inv_h);
   const int32_t cy = pbdr_cell_coord(xn.y, A.inv_h);
   const int32_t cz = pbdr_cell_coord(xn.z, A.inv_h);
-  return pbdr_cell_hash(cx, cy, cz, static_cast<uint32_t>(A.body_scene[b]), A.mask);
+  return pbdr_cell_key(cx, cy, cz, static_cast<uint32_t>(A.body_scene[b]), A.mask, A.layout);
 }
 
 __global__ void __launch_bounds__(256) k_integrate_key(IntegrateArgs A) {
@@ -557,9 +557,18 @@ __global__ void __launch_bounds__(256) k_cell_ranges(RangesArgs A) {
 // ---------------------------------------------------------------------------
 constexpr int kScanTile = 4096;
 
+__device__ __forceinline__ void obb_axes(float4 q, float R[9]);
+
 struct NearBoxes {
   float lo[3], hi[3];  // lane k < np: partner k's box inflated by h (+ relative guard)
+  // PBDR_NEAR_FAST: partner k's oriented box, prepared once per body instead
+  // of once per (particle, partner): frame R, centre, bounds with in_obb's
+  // margins applied (the same float operations, so the same bits).
+  float R[9], c[3], olo[3], ohi[3];
 };
+#ifndef PBDR_NEAR_FAST
+#define PBDR_NEAR_FAST 1
+#endif
 
 __device__ __forceinline__ int near_body_setup(const NearArgs& A, int t, int lane, int& b, int& start, int& n,
                                                NearBoxes& bx) {
@@ -579,6 +588,20 @@ __device__ __forceinline__ int near_body_setup(const NearArgs& A, int t, int lan
       bx.lo[c] = lo[c] - m;
       bx.hi[c] = hi[c] + m;
     }
+#if PBDR_NEAR_FAST
+    if (A.obb_q) {
+      const float4 olo = A.obb_lo[o], ohi = A.obb_hi[o], oc = A.obb_c[o];
+      obb_axes(A.obb_q[o], bx.R);
+      bx.c[0] = oc.x; bx.c[1] = oc.y; bx.c[2] = oc.z;
+      const float lv[3] = {olo.x, olo.y, olo.z}, hv[3] = {ohi.x, ohi.y, ohi.z};
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const float m = A.inflate * 1.0001f + 1e-5f * (fabsf(lv[k]) + fabsf(hv[k])) + 1e-6f;
+        bx.olo[k] = lv[k] - m;
+        bx.ohi[k] = hv[k] + m;
+      }
+    }
+#endif
   }
   return np;
 }
@@ -691,8 +714,32 @@ __device__ __forceinline__ bool near_test(const NearArgs& A, bool valid, int64_t
       hi[c] = __shfl_sync(kFull, bx.hi[c], k);
     }
     bool in = xi.x >= lo[0] && xi.x <= hi[0] && xi.y >= lo[1] && xi.y <= hi[1] && xi.z >= lo[2] && xi.z <= hi[2];
+#if PBDR_NEAR_FAST
+    // Oriented test with the partner's prepared frame, only when some lane
+    // is inside the axis-aligned box; the warp stops once every lane is near.
+    if (A.obb_q && __any_sync(kFull, in)) {
+      float R[9], c[3], ol[3], oh[3];
+#pragma unroll
+      for (int e = 0; e < 9; ++e) R[e] = __shfl_sync(kFull, bx.R[e], k);
+#pragma unroll
+      for (int e = 0; e < 3; ++e) {
+        c[e] = __shfl_sync(kFull, bx.c[e], k);
+        ol[e] = __shfl_sync(kFull, bx.olo[e], k);
+        oh[e] = __shfl_sync(kFull, bx.ohi[e], k);
+      }
+      const float d[3] = {xi.x - c[0], xi.y - c[1], xi.z - c[2]};
+#pragma unroll
+      for (int e = 0; e < 3; ++e) {
+        const float r = (R[e] * d[0] + R[3 + e] * d[1]) + R[6 + e] * d[2];
+        in = in && r >= ol[e] && r <= oh[e];
+      }
+    }
+    in_any = in_any || in;
+    if (__all_sync(kFull, in_any || !valid)) break;
+#else
     if (in && A.obb_q) in = in_obb(A, partners[k], xi);
     in_any = in_any || in;
+#endif
   }
   return valid && in_any;
 }
@@ -888,7 +935,11 @@ __device__ __forceinline__ void neighbours_one(const NeighbourArgs& A, int64_t t
   const int32_t cy = pbdr_cell_coord(xi.y, A.inv_h);
   const int32_t cz = pbdr_cell_coord(xi.z, A.inv_h);
   const int xl = cx & ((1 << PBDR_XRUN_BITS) - 1);
-  const bool inner = xl != 0 && xl != (1 << PBDR_XRUN_BITS) - 1;
+  const bool linear = A.layout.linear != 0;
+  // Consecutive keys for the row's three cells: inside an x-run (hashed
+  // layout) or inside the box's x range (linear layout).
+  const bool inner = linear ? static_cast<uint32_t>(cx - 1 - A.layout.ox) + 2u < (1u << A.layout.bx)
+                            : (xl != 0 && xl != (1 << PBDR_XRUN_BITS) - 1);
 
   CandList L;
   L.count = 0;
@@ -896,9 +947,9 @@ __device__ __forceinline__ void neighbours_one(const NeighbourArgs& A, int64_t t
   for (int r = 0; r < 9; ++r) {
     const int32_t yy = cy + (r % 3) - 1, zz = cz + (r / 3) - 1;
     // Row cells cx-1, cx, cx+1: consecutive keys inside an x-run.
-    const uint32_t km = pbdr_cell_hash(cx - 1, yy, zz, static_cast<uint32_t>(si), A.mask);
-    const uint32_t k0 = inner ? km + 1 : pbdr_cell_hash(cx, yy, zz, static_cast<uint32_t>(si), A.mask);
-    const uint32_t kp = inner ? km + 2 : pbdr_cell_hash(cx + 1, yy, zz, static_cast<uint32_t>(si), A.mask);
+    const uint32_t km = pbdr_cell_key(cx - 1, yy, zz, static_cast<uint32_t>(si), A.mask, A.layout);
+    const uint32_t k0 = inner ? (km + 1) & A.mask : pbdr_cell_key(cx, yy, zz, static_cast<uint32_t>(si), A.mask, A.layout);
+    const uint32_t kp = inner ? (km + 2) & A.mask : pbdr_cell_key(cx + 1, yy, zz, static_cast<uint32_t>(si), A.mask, A.layout);
     scan_bucket(A, km, bi, si, xi, cx, cy, cz, L);
     scan_bucket(A, k0, bi, si, xi, cx, cy, cz, L);
     scan_bucket(A, kp, bi, si, xi, cx, cy, cz, L);

@@ -73,6 +73,7 @@ struct IntegrateArgs {
   float dt, gravity, inv_h;
   double dt_d;
   uint32_t mask;
+  pbdr_key_layout layout;  // bucket keys (pbdr_cell_key)
 };
 
 // Body broadphase (acceleration only; the candidate set is unchanged): a
@@ -171,6 +172,7 @@ struct NeighbourArgs {
   int64_t n;
   float inv_h, h2;
   uint32_t mask;
+  pbdr_key_layout layout;
 };
 
 struct IterArgs {

@@ -104,6 +104,63 @@ PBDR_HD int pbdr_hash_bits(int64_t n) {
   return b;
 }
 
+/* Spatially ordered bucket keys for single scenes. With hashed x-runs (above)
+ * the 9 stencil rows of a cell sit at random places of the sorted arrays, so
+ * the neighbour search streams them from DRAM once per row that reads them.
+ * A scene whose cells fit a 2^29-bucket box instead gets the LINEAR key
+ * ((cz - oz) << (bx + by)) + ((cy - oy) << bx) + (cx - ox) (mod the table): x-
+ * neighbours are consecutive keys, y- and z-neighbours a fixed stride away, so
+ * the sweep over sorted particles touches each row's entries while they are
+ * in L2. The box is the scene's cell range at creation, padded by an eighth
+ * of its extent + 32 cells per side in x and y and + 40 in z; cells that
+ * later leave it alias into other rows of the table -- bucket collisions, which
+ * the search already tolerates (it re-checks cell coordinates). The layout is
+ * chosen from the fp32 positions the device and the oracle both start from,
+ * and changes no candidate (P4: the set is geometric). */
+typedef struct pbdr_key_layout {
+  int32_t linear;      /* 0: hashed x-runs */
+  int32_t bits;        /* table bits */
+  int32_t bx, by;      /* bits of the x and y ranges (linear) */
+  int32_t ox, oy, oz;  /* cell origin of the box (linear) */
+} pbdr_key_layout;
+
+PBDR_HD int pbdr_ceil_log2(int64_t v) {
+  int b = 0;
+  while (((int64_t)1 << b) < v) ++b;
+  return b;
+}
+
+PBDR_HD pbdr_key_layout pbdr_choose_key_layout(int single_scene, const int32_t cmin[3], const int32_t cmax[3],
+                                               int64_t n_particles) {
+  pbdr_key_layout L;
+  L.linear = 0;
+  L.bits = pbdr_hash_bits(n_particles);
+  L.bx = L.by = 0;
+  L.ox = L.oy = L.oz = 0;
+  if (!single_scene) return L;
+  const int64_t ex = (int64_t)cmax[0] - cmin[0] + 1, ey = (int64_t)cmax[1] - cmin[1] + 1;
+  const int64_t ez = (int64_t)cmax[2] - cmin[2] + 1;
+  const int64_t px = ex / 8 + 32, py = ey / 8 + 32;
+  const int bx = pbdr_ceil_log2(ex + 2 * px), by = pbdr_ceil_log2(ey + 2 * py);
+  const int bz = pbdr_ceil_log2(ez + ez / 8 + 40 + 16);
+  if (bx + by > 24 || bx + by + bz > 29) return L;
+  L.linear = 1;
+  L.bx = bx;
+  L.by = by;
+  L.ox = (int32_t)(cmin[0] - px);
+  L.oy = (int32_t)(cmin[1] - py);
+  L.oz = cmin[2] - 16;
+  if (bx + by + bz > L.bits) L.bits = bx + by + bz;
+  return L;
+}
+
+PBDR_HD uint32_t pbdr_cell_key(int32_t cx, int32_t cy, int32_t cz, uint32_t scene, uint32_t mask,
+                               pbdr_key_layout L) {
+  if (!L.linear) return pbdr_cell_hash(cx, cy, cz, scene, mask);
+  return (((uint32_t)(cz - L.oz) << (L.bx + L.by)) + ((uint32_t)(cy - L.oy) << L.bx) + (uint32_t)(cx - L.ox)) &
+         mask;
+}
+
 PBDR_HD int32_t pbdr_cell_coord(float x, float inv_h) {
   float c = floorf(x * inv_h);
   c = fminf(fmaxf(c, -PBDR_CELL_CLAMP), PBDR_CELL_CLAMP);
