@@ -1064,7 +1064,7 @@ template <bool MULTI>
 __device__ __forceinline__ void phase_a_particle(const IterArgs& A, int it, int64_t p, float4 x4, float4 v4,
                                                  float4 r4, int nc, const float a[3], float (&dXk)[3],
                                                  float (&acc)[21], const float4* s_tile, int tile_first,
-                                                 int tile_count) {
+                                                 int tile_count, const float* dpp_pre = nullptr) {
   const float x[3] = {x4.x, x4.y, x4.z};
   const float m = v4.w;
 
@@ -1107,6 +1107,12 @@ __device__ __forceinline__ void phase_a_particle(const IterArgs& A, int it, int6
     }
   }
   float dPP[3] = {0.0f, 0.0f, 0.0f};
+  if (dpp_pre) {  // contacts already summed (PBDR_CAND_COLUMNS), same order
+    dPP[0] = dpp_pre[0];
+    dPP[1] = dpp_pre[1];
+    dPP[2] = dpp_pre[2];
+    nc = 0;
+  }
 #if PBDR_CAND_ROLLED
 #pragma unroll 1
 #endif
@@ -1420,6 +1426,11 @@ __device__ __forceinline__ void phase_c_particle(const IterArgs& A, int64_t p, f
 // two CTAs per SM with up to 128 registers (no spills). Measured on C4:
 // 0.382 ms per iteration vs 0.436 for KP = 4 at three CTAs per SM (80
 // registers, spills) -- more particles in flight per SM, fewer warps per body.
+// Contacts of a lane's particles processed side by side per candidate rank
+// (needs the rolled layout's s_dx).
+#ifndef PBDR_CAND_COLUMNS
+#define PBDR_CAND_COLUMNS 0
+#endif
 // Rolled particle loops with the deltas in shared memory (KP <= 4 tiles only:
 // at KP >= 7 the extra 32 KB would cost a CTA per SM).
 #ifndef PBDR_ROLL_PARTICLES
@@ -1440,6 +1451,7 @@ template <int KP, bool MULTI, bool FUSE = false>
 __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(IterArgs A) {
   constexpr int kSlots = kThreads * KP;  // particle slots staged per CTA
   constexpr bool kRoll = PBDR_ROLL_PARTICLES != 0 && KP <= 4;  // iter_rolled<KP>()
+  constexpr bool kColumns = kRoll && PBDR_CAND_COLUMNS != 0;
   extern __shared__ float4 s_stage[];  // pos | vel | rest [| dX], kSlots each
   __shared__ float s_part[kWarps][21];
   __shared__ float s_res[kWarps][kResF];
@@ -1605,13 +1617,54 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
   float acc[21];
 #pragma unroll
   for (int f = 0; f < 21; ++f) acc[f] = 0.0f;
+  if constexpr (kColumns) {
+    // Phase A1: the particle-particle contacts of the lane's KP particles side
+    // by side, candidate rank by rank -- up to KP independent gathers in flight
+    // where the per-particle loop has one -- summed per particle in ascending
+    // candidate order as before, and parked in s_dx for phase A2.
+    float dpp[KP][3];
+#pragma unroll
+    for (int k = 0; k < KP; ++k) dpp[k][0] = dpp[k][1] = dpp[k][2] = 0.0f;
+    int maxc = 0;
+#pragma unroll
+    for (int k = 0; k < KP; ++k) maxc = max(maxc, ncs(k));
+#pragma unroll 1
+    for (int c = 0; c < maxc; ++c) {
+#pragma unroll
+      for (int k = 0; k < KP; ++k) {
+        if (c < ncs(k)) {
+          const int q = k * 32 * W + wi * 32 + lane;
+          const int64_t p = start + q;
+          const int j = A.cand_j[static_cast<int64_t>(c) * A.n + p];
+          PBDR_CHECK(j >= 0 && j < A.n && j != p);
+          const float rr = A.cand_rr[static_cast<int64_t>(c) * A.n + p];
+          const float4 xj = (MULTI && A.multi_pairs) ? __ldcg(&A.pos_b[it & 1][j]) : A.pos_in[j];
+          const float4 x4 = s_pos[off + q];
+          const float x[3] = {x4.x, x4.y, x4.z};
+          pp_contact(x, x4.w, p, xj, j, rr, A.relax, dpp[k]);
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < KP; ++k) {
+      const int q = k * 32 * W + wi * 32 + lane;
+      if (live && q < n) s_dx[off + q] = make_float4(dpp[k][0], dpp[k][1], dpp[k][2], 0.0f);
+    }
+  }
   auto phase_a_k = [&](int k) {
     const int q = k * 32 * W + wi * 32 + lane;
     if (!(live && q < n)) return;
     const int64_t p = start + q;
     float d[3] = {0.0f, 0.0f, 0.0f};
-    phase_a_particle<MULTI>(A, it, p, s_pos[off + q], s_vel[off + q], s_rest[off + q], ncs(k), a, d, acc, s_pos,
-                            first, cd.y);
+    if constexpr (kColumns) {
+      const float4 t = s_dx[off + q];
+      const float pre[3] = {t.x, t.y, t.z};
+      phase_a_particle<MULTI>(A, it, p, s_pos[off + q], s_vel[off + q], s_rest[off + q], 0, a, d, acc, s_pos,
+                              first, cd.y, pre);
+    } else {
+      phase_a_particle<MULTI>(A, it, p, s_pos[off + q], s_vel[off + q], s_rest[off + q], ncs(k), a, d, acc,
+                              s_pos, first, cd.y);
+    }
     dx_store(k, q, d);
   };
   if constexpr (kRoll) {
