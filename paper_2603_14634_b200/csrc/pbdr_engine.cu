@@ -269,7 +269,6 @@ void enqueue_substep(pbdr_handle* h, pbdr_dev::LaunchHook* hook, bool integrated
   ra.prev_count = h->near_count + 1;
   ra.body_of = h->body_of;
   ra.cells = h->cells;
-  ra.sorted_body = h->sorted_body;
   ra.pos = h->pos[h->cur];
   ra.sorted_pos = h->sorted_pos;
   ra.substep_counter = h->counter;
@@ -286,7 +285,6 @@ void enqueue_substep(pbdr_handle* h, pbdr_dev::LaunchHook* hook, bool integrated
   na.body_of = h->body_of;
   na.body_scene = h->body_scene;
   na.cells = h->cells;
-  na.sorted_body = h->sorted_body;
   na.sorted_vals = h->vals[sb];
   na.sorted_pos = h->sorted_pos;
   na.single_scene = h->single_scene ? 1 : 0;
@@ -816,7 +814,6 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
   rc |= dalloc(h, &h->npartners, nb);
   rc |= dalloc(h, &h->partners, static_cast<size_t>(nb) * PBDR_PARTNER_CAP);
   rc |= dalloc(h, &h->oversize, 1);
-  rc |= dalloc(h, &h->sorted_body, n);
   rc |= dalloc(h, &h->sorted_pos, n);
   rc |= dalloc(h, &h->near_flag, n);
   {

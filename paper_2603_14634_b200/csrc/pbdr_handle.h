@@ -98,7 +98,6 @@ struct pbdr_handle {
   float inv_cell_b = 0, max_extent = 0, inflate = 0;
   long long* timing = nullptr;      // set only while an instrumented launch is enqueued
   long long* timing_buf = nullptr;  // per-CTA phase clocks (debug hook only)
-  int* sorted_body = nullptr;
   int* ncand = nullptr;
   int* cand_j = nullptr;
   float* cand_rr = nullptr;

@@ -242,6 +242,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+// PBDR_PREFETCH_L1: the iteration's staging-time prefetch of each particle's
+// first candidate goes to L1 instead of L2.
+#ifndef PBDR_PREFETCH_L1
+#define PBDR_PREFETCH_L1 0
+#endif
 
 // Order-preserving float <-> uint encoding for atomicMin/atomicMax boxes.
 __device__ __forceinline__ uint32_t f2ord(float f) {
@@ -530,8 +538,10 @@ __global__ void __launch_bounds__(256) k_cell_ranges(RangesArgs A) {
     const uint32_t v = A.vals[s];
     PBDR_CHECK(v < static_cast<uint64_t>(A.n) && (s == 0 || A.keys[s - 1] <= k));
     const int body = A.body_of[v];
-    A.sorted_body[s] = body;
-    A.sorted_pos[s] = A.pos[v];
+    // X~ of the entry with its body in .w: the search reads one float4 per
+    // entry (and a CTA stages runs of them, k_neighbours_staged).
+    const float4 x = A.pos[v];
+    A.sorted_pos[s] = make_float4(x.x, x.y, x.z, __int_as_float(body));
     // Entries of a bucket ascend by slot, hence by body: the first entry holds
     // the bucket's smallest body, the last its largest.
     if (s == 0 || A.keys[s - 1] != k) {
@@ -898,10 +908,10 @@ __device__ __forceinline__ void scan_range(const NeighbourArgs& A, uint32_t lo, 
   for (uint32_t s = lo; s < hi; ++s) {
     // Body, slot and position of the entry come from sorted-order copies
     // (k_cell_ranges), read side by side: no dependent gathers per entry.
-    const int bj = A.sorted_body[s];
+    const float4 xj = A.sorted_pos[s];
+    const int bj = __float_as_int(xj.w);
     if (bj == bi) continue;
     if (!A.single_scene && A.body_scene[bj] != si) continue;
-    const float4 xj = A.sorted_pos[s];
     const int j = static_cast<int>(A.sorted_vals[s]);
     const int32_t jx = pbdr_cell_coord(xj.x, A.inv_h);
     const int32_t jy = pbdr_cell_coord(xj.y, A.inv_h);
@@ -928,9 +938,9 @@ __device__ __forceinline__ void neighbours_one(const NeighbourArgs& A, int64_t t
   // overlapping cells, so bucket entries are shared through L1/L2.
   const int64_t i = A.sorted_vals[t];
   PBDR_CHECK(i >= 0 && i < A.n);
-  const float4 xi = A.pos[i];
-  const int bi = A.body_of[i];
-  const int si = A.body_scene[bi];
+  const float4 xi = A.sorted_pos[t];  // X~ of particle i, its body in .w
+  const int bi = __float_as_int(xi.w);
+  const int si = A.single_scene ? 0 : A.body_scene[bi];
   const int32_t cx = pbdr_cell_coord(xi.x, A.inv_h);
   const int32_t cy = pbdr_cell_coord(xi.y, A.inv_h);
   const int32_t cz = pbdr_cell_coord(xi.z, A.inv_h);
@@ -973,6 +983,173 @@ __global__ void __launch_bounds__(128) k_neighbours(NeighbourArgs A) {
     neighbours_one(A, t);
 }
 
+// Staged search (single scenes with the linear key layout, P4). With linear
+// keys a stencil row -- cells (cx-1..cx+1, y, z) -- is three consecutive keys,
+// so its bucket entries are one contiguous run of the sorted arrays; and a
+// CTA's chunk of kNbrChunk consecutive sorted near particles (one x-stretch of
+// a few cell rows) needs, for each of the 9 (dy, dz) row offsets, one run of
+// entries that is about as long as the chunk. The CTA reduces the 9 runs'
+// bounds over its threads, merges overlapping runs, and stages them into
+// shared memory with cp.async.bulk (one mbarrier); every thread then scans
+// its rows from shared memory. Rows that are not three consecutive keys (the
+// box's x edge, key wrap-around) or runs beyond the staging capacity are read
+// from global memory bucket by bucket as in k_neighbours. The scanned entries
+// are the same, and the candidate list keeps the CAP smallest distinct j
+// whatever the order, so the result is bit-identical to k_neighbours.
+#ifndef PBDR_NBR_STAGED
+#define PBDR_NBR_STAGED 0
+#endif
+constexpr int kNbrChunk = 128;
+constexpr int kNbrStage = 2048;  // staged entries per CTA (32 KB of float4)
+
+__global__ void __launch_bounds__(kNbrChunk) k_neighbours_staged(NeighbourArgs A) {
+  __shared__ __align__(16) float4 s_ent[kNbrStage];
+  __shared__ __align__(8) uint64_t s_bar;
+  __shared__ uint32_t s_lo[9], s_hi[9];
+  __shared__ int s_base[9];  // shared index of entry s_lo[r], or -1 (row read from global)
+  const long long m = *A.count;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) mbar_init(&s_bar, 1);
+  __syncthreads();
+  uint32_t parity = 0;
+  for (int64_t c0 = static_cast<int64_t>(blockIdx.x) * kNbrChunk; c0 < m;
+       c0 += static_cast<int64_t>(gridDim.x) * kNbrChunk, parity ^= 1u) {
+    if (threadIdx.x < 9) {
+      s_lo[threadIdx.x] = 0xFFFFFFFFu;
+      s_hi[threadIdx.x] = 0u;
+    }
+    const int64_t t = c0 + threadIdx.x;
+    const bool act = t < m;
+    int64_t i = 0;
+    float4 xi = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    int bi = -1;
+    int32_t cx = 0, cy = 0, cz = 0;
+    if (act) {
+      i = A.sorted_vals[t];
+      PBDR_CHECK(i >= 0 && i < A.n);
+      xi = A.sorted_pos[t];
+      bi = __float_as_int(xi.w);
+      cx = pbdr_cell_coord(xi.x, A.inv_h);
+      cy = pbdr_cell_coord(xi.y, A.inv_h);
+      cz = pbdr_cell_coord(xi.z, A.inv_h);
+    }
+    const bool xin = static_cast<uint32_t>(cx - 1 - A.layout.ox) + 2u < (1u << A.layout.bx);
+    // Per row: the contiguous run [lo, hi) of its three buckets (empty: lo =
+    // hi = 0; not contiguous: lo = ~0, read bucket by bucket from global).
+    uint32_t lo[9], hi[9];
+    __syncthreads();  // s_lo / s_hi reset before the reductions below
+#pragma unroll
+    for (int r = 0; r < 9; ++r) {
+      lo[r] = 0u;
+      hi[r] = 0u;
+      if (act) {
+        const int32_t yy = cy + (r % 3) - 1, zz = cz + (r / 3) - 1;
+        const uint32_t km = pbdr_cell_key(cx - 1, yy, zz, 0u, A.mask, A.layout);
+        if (xin && km + 2u <= A.mask) {
+          const uint4 e0 = A.cells[km], e1 = A.cells[km + 1], e2 = A.cells[km + 2];
+          const bool n0 = e0.x != kEmpty, n1 = e1.x != kEmpty, n2 = e2.x != kEmpty;
+          const uint32_t ub = static_cast<uint32_t>(bi);
+          const bool own = (!n0 || (e0.z == ub && e0.w == ub)) && (!n1 || (e1.z == ub && e1.w == ub)) &&
+                           (!n2 || (e2.z == ub && e2.w == ub));
+          if ((n0 || n1 || n2) && !own) {
+            lo[r] = n0 ? e0.x : (n1 ? e1.x : e2.x);
+            hi[r] = n2 ? e2.y : (n1 ? e1.y : e0.y);
+          }
+        } else {
+          lo[r] = 0xFFFFFFFFu;
+        }
+      }
+      const bool has = lo[r] < hi[r];
+      const uint32_t wl = __reduce_min_sync(kFull, has ? lo[r] : 0xFFFFFFFFu);
+      const uint32_t wh = __reduce_max_sync(kFull, has ? hi[r] : 0u);
+      if (lane == 0 && wl < wh) {
+        atomicMin(&s_lo[r], wl);
+        atomicMax(&s_hi[r], wh);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      // Merge the 9 runs (sorted by start) into disjoint segments, stage the
+      // segments that fit, in ascending order.
+      int ord[9], nr = 0;
+      for (int r = 0; r < 9; ++r) {
+        s_base[r] = -1;
+        if (s_lo[r] < s_hi[r]) {
+          int k = nr++;
+          while (k > 0 && s_lo[ord[k - 1]] > s_lo[r]) {
+            ord[k] = ord[k - 1];
+            --k;
+          }
+          ord[k] = r;
+        }
+      }
+      uint32_t bytes = 0;
+      int used = 0;
+      for (int a = 0; a < nr;) {
+        uint32_t seg_lo = s_lo[ord[a]], seg_hi = s_hi[ord[a]];
+        int b = a + 1;
+        while (b < nr && s_lo[ord[b]] <= seg_hi) {
+          seg_hi = max(seg_hi, s_hi[ord[b]]);
+          ++b;
+        }
+        const int len = static_cast<int>(seg_hi - seg_lo);
+        if (used + len <= kNbrStage) {
+          for (int k = a; k < b; ++k) s_base[ord[k]] = used + static_cast<int>(s_lo[ord[k]] - seg_lo);
+          bulk_g2s(&s_ent[used], A.sorted_pos + seg_lo, static_cast<uint32_t>(len) * 16u, &s_bar);
+          used += len;
+          bytes += static_cast<uint32_t>(len) * 16u;
+        }
+        a = b;
+      }
+      mbar_expect_tx(&s_bar, bytes);  // arrives once; the phase completes when the bytes have landed
+    }
+    __syncthreads();  // s_base published
+    mbar_wait(&s_bar, parity);
+    if (act) {
+      CandList L;
+      L.count = 0;
+      L.overflow = false;
+#pragma unroll 1
+      for (int r = 0; r < 9; ++r) {
+        if (lo[r] == 0xFFFFFFFFu) {  // row not contiguous: bucket by bucket from global
+          const int32_t yy = cy + (r % 3) - 1, zz = cz + (r / 3) - 1;
+          for (int dx = -1; dx <= 1; ++dx)
+            scan_bucket(A, pbdr_cell_key(cx + dx, yy, zz, 0u, A.mask, A.layout), bi, 0, xi, cx, cy, cz, L);
+          continue;
+        }
+        if (lo[r] >= hi[r]) continue;
+        const int base = s_base[r];
+        if (base < 0) {
+          scan_range(A, lo[r], hi[r], bi, 0, xi, cx, cy, cz, L);
+          continue;
+        }
+        const uint32_t r0 = s_lo[r];
+        for (uint32_t s = lo[r]; s < hi[r]; ++s) {
+          const float4 xj = s_ent[base + static_cast<int>(s - r0)];
+          if (__float_as_int(xj.w) == bi) continue;
+          const int32_t jx = pbdr_cell_coord(xj.x, A.inv_h);
+          const int32_t jy = pbdr_cell_coord(xj.y, A.inv_h);
+          const int32_t jz = pbdr_cell_coord(xj.z, A.inv_h);
+          if (jx < cx - 1 || jx > cx + 1 || jy < cy - 1 || jy > cy + 1 || jz < cz - 1 || jz > cz + 1) continue;
+          const float ex = xi.x - xj.x, ey = xi.y - xj.y, ez = xi.z - xj.z;
+          const float d2 = (ex * ex + ey * ey) + ez * ez;
+          if (!(d2 < A.h2)) continue;
+          L.insert(static_cast<int>(A.sorted_vals[s]));
+        }
+      }
+      if (L.overflow) record_error(A.err, PBDR_DEVERR_NBR_OVERFLOW, bi, A.substep_counter);
+      A.ncand[i] = L.count;
+      const float ri = A.rest[i].w;
+      for (int k = 0; k < L.count; ++k) {
+        const int j = L.j[k];
+        A.cand_j[static_cast<int64_t>(k) * A.n + i] = j;
+        A.cand_rr[static_cast<int64_t>(k) * A.n + i] = ri + A.rest[j].w;
+      }
+    }
+    __syncthreads();  // staged entries read before the next chunk's copies overwrite them
+  }
+}
+
 // ---------------------------------------------------------------------------
 // One solver iteration, fused (pinned P1-P8). A CTA (8 warps) holds whole,
 // consecutive bodies; its contiguous slot range of pos/vel/rest is staged in
@@ -1009,6 +1186,11 @@ __global__ void __launch_bounds__(128) k_neighbours(NeighbourArgs A) {
 // ranges (pos, vel, rest) and its candidate counts into L2.
 #ifndef PBDR_PREFETCH_NEXT
 #define PBDR_PREFETCH_NEXT 0
+#endif
+// PBDR_PREFETCH_ALL_CANDS: the staging-time prefetch covers every candidate
+// of a particle, not only the first.
+#ifndef PBDR_PREFETCH_ALL_CANDS
+#define PBDR_PREFETCH_ALL_CANDS 0
 #endif
 // Pinned fused multiply-adds (P8): only these explicit fmaf() are
 // contracted (the library builds with --fmad=false); the oracle uses std::fmaf
@@ -1203,6 +1385,55 @@ __device__ __forceinline__ void warp_box_commit(const IterArgs& A, int b, const 
       atomicMin(&A.ia.box_min[3 * b + c], l[c]);
       atomicMax(&A.ia.box_max[3 * b + c], h[c]);
     }
+}
+
+// Cross-warp body sums (stage 3 of the P7 tree): S[f] = ((w0 + w1) + w2) ...
+// over the body's warps nw, in warp order. PBDR_PART_VEC reads each warp's
+// partials as float4 (rows padded to 24 floats): 6 shared loads instead of
+// 21 -- warp 0 runs this while the other CTAs of the SM keep the L1/shared
+// pipeline busy with contact gathers, where every load instruction queues.
+#ifndef PBDR_PART_VEC
+#define PBDR_PART_VEC 1
+#endif
+#ifndef PBDR_PART_UNROLL
+#define PBDR_PART_UNROLL 1
+#endif
+constexpr int kPartStride = PBDR_PART_VEC ? 24 : 21;
+constexpr int kPartUnroll = PBDR_PART_UNROLL;
+template <int F>
+__device__ __forceinline__ void part_sum(const float* part, int fw, int nw, float (&S)[F]) {
+#if PBDR_PART_VEC
+  constexpr int V = (F + 3) / 4;
+  const float4* r = reinterpret_cast<const float4*>(part + fw * kPartStride);
+#pragma unroll
+  for (int v = 0; v < V; ++v) {
+    const float4 t = r[v];
+    const float tv[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if (4 * v + e < F) S[4 * v + e] = tv[e];
+  }
+  // Kept rolled (with the plane loop: smaller code, C3 +5%, C5 +3%).
+#pragma unroll kPartUnroll
+  for (int u = 1; u < nw; ++u) {
+    r = reinterpret_cast<const float4*>(part + (fw + u) * kPartStride);
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const float4 t = r[v];
+      const float tv[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        if (4 * v + e < F) S[4 * v + e] = S[4 * v + e] + tv[e];
+    }
+  }
+#else
+#pragma unroll
+  for (int f = 0; f < F; ++f) S[f] = part[fw * kPartStride + f];
+#pragma unroll 1
+  for (int u = 1; u < nw; ++u)
+#pragma unroll
+    for (int f = 0; f < F; ++f) S[f] = S[f] + part[(fw + u) * kPartStride + f];
+#endif
 }
 
 constexpr int kResF = 32;
@@ -1453,7 +1684,7 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
   constexpr bool kRoll = PBDR_ROLL_PARTICLES != 0 && KP <= 4;  // iter_rolled<KP>()
   constexpr bool kColumns = kRoll && PBDR_CAND_COLUMNS != 0;
   extern __shared__ float4 s_stage[];  // pos | vel | rest [| dX], kSlots each
-  __shared__ float s_part[kWarps][21];
+  __shared__ __align__(16) float s_part[kWarps][kPartStride];
   __shared__ float s_res[kWarps][kResF];
   __shared__ __align__(8) uint64_t s_bar;
 
@@ -1553,8 +1784,23 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
       if (ncs(k) > 0) {
         const int64_t p = start + k * 32 * W + wi * 32 + lane;
         const int j = __ldg(&A.cand_j[p]);
+#if PBDR_PREFETCH_L1
+        prefetch_l1(&A.pos_in[j]);
+        prefetch_l1(&A.cand_rr[p]);
+#else
         prefetch_l2(&A.pos_in[j]);
         prefetch_l2(&A.cand_rr[p]);
+#endif
+#if PBDR_PREFETCH_ALL_CANDS
+        // ... and every further candidate (settled piles: p90 phase A was
+        // one dependent L2/HBM round trip per candidate, in series).
+#pragma unroll 1
+        for (int c = 1; c < ncs(k); ++c) {
+          const int jc = __ldg(&A.cand_j[static_cast<int64_t>(c) * A.n + p]);
+          prefetch_l2(&A.pos_in[jc]);
+          prefetch_l2(&A.cand_rr[static_cast<int64_t>(c) * A.n + p]);
+        }
+#endif
       }
     }
   }
@@ -1708,13 +1954,7 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
     const int2 bw = make_int2(s_tdesc[tb][lane].w, s_tdesc[tb][lane].z);
     const int fw = bw.x;
     float S[21];
-#pragma unroll
-    for (int f = 0; f < 21; ++f) S[f] = s_part[fw][f];
-    // Kept rolled (with the plane loop: smaller code, C3 +5%, C5 +3%).
-#pragma unroll 1
-    for (int u = 1; u < bw.y; ++u)
-#pragma unroll
-      for (int f = 0; f < 21; ++f) S[f] = S[f] + s_part[fw + u][f];
+    part_sum(&s_part[0][0], fw, bw.y, S);
     float4 rq_new, an_new;
     if (tm && lane == 0) tm[8] = clock64();  // body sums read
     body_math_a(A, bb, S, an, invM, s_trq[tb][lane], &s_res[lane][0], rq_new, an_new,
@@ -1792,12 +2032,7 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
     const int2 bw = make_int2(s_tdesc[tb][lane].w, s_tdesc[tb][lane].z);
     const int fw = bw.x;
     float S[15];
-#pragma unroll
-    for (int f = 0; f < 15; ++f) S[f] = s_part[fw][f];
-#pragma unroll 1
-    for (int u = 1; u < bw.y; ++u)
-#pragma unroll
-      for (int f = 0; f < 15; ++f) S[f] = S[f] + s_part[fw + u][f];
+    part_sum(&s_part[0][0], fw, bw.y, S);
     if (tm && lane == 0) tm[10] = clock64();
     body_math_b(A, bb, S, mass, &s_res[lane][0], iter_index, last_iter);
     if (tm && lane == 0) tm[11] = clock64();
@@ -2620,6 +2855,17 @@ void launch_ranges(const RangesArgs& a, cudaStream_t s) {
 }
 
 void launch_neighbours(const NeighbourArgs& a, cudaStream_t s) {
+  static const bool staged = [] {
+    const char* e = std::getenv("PBDR_NBR_STAGED");
+    return PBDR_NBR_STAGED != 0 && !(e && e[0] == '0');
+  }();
+  if (staged && a.layout.linear && a.single_scene) {
+    // Persistent: 6 CTAs of 128 threads (33 KB shared) per SM.
+    const unsigned blocks = static_cast<unsigned>(
+        std::max<int64_t>(1, std::min<int64_t>((a.n + kNbrChunk - 1) / kNbrChunk, 148 * 6)));
+    k_neighbours_staged<<<blocks, kNbrChunk, 0, s>>>(a);
+    return;
+  }
   const unsigned blocks = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((a.n + 127) / 128, 148 * 64)));
   k_neighbours<<<blocks, 128, 0, s>>>(a);
 }

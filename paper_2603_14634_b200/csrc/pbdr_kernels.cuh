@@ -145,9 +145,8 @@ struct RangesArgs {
   long long* prev_count;     // saved for the next substep's table clear
   const int* body_of;
   uint4* cells;  // per bucket (start, end, first body, last body); start = ~0 when empty
-  int* sorted_body;
   const float4* pos;     // X~
-  float4* sorted_pos;    // X~ of every sorted entry
+  float4* sorted_pos;    // X~ of every sorted entry, its body's index in .w (int bits)
   long long* substep_counter;
   int64_t n;
 };
@@ -160,9 +159,8 @@ struct NeighbourArgs {
   const int* body_of;
   const int* body_scene;
   const uint4* cells;
-  const int* sorted_body;
   const uint32_t* sorted_vals;
-  const float4* sorted_pos;  // X~ of the sorted entries (k_cell_ranges)
+  const float4* sorted_pos;  // X~ of the sorted entries, body in .w (k_cell_ranges)
   int single_scene;          // every body in scene 0: no scene test per entry
   int* ncand;
   int* cand_j;     // slot-major: [k * n + i]

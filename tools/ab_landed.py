@@ -31,7 +31,10 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--prep", action="store_true")
 ap.add_argument("--frames", type=int, default=5)
 ap.add_argument("--only", type=int, default=0)
+ap.add_argument("--states", default="", help="config:frame list, e.g. 5:80,3:480 (default: the three above)")
 a = ap.parse_args()
+if a.states:
+    STATES = [tuple(int(x) for x in t.split(":")) for t in a.states.split(",")]
 
 for cid, f in STATES:
     if a.only and cid != a.only:
