@@ -1791,7 +1791,7 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
         prefetch_l2(&A.pos_in[j]);
         prefetch_l2(&A.cand_rr[p]);
 #endif
-#if PBDR_PREFETCH_ALL_CANDS
+#if PBDR_PREFETCH_ALL_CANDS == 1
         // ... and every further candidate (settled piles: p90 phase A was
         // one dependent L2/HBM round trip per candidate, in series).
 #pragma unroll 1
@@ -1803,6 +1803,31 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
 #endif
       }
     }
+#if PBDR_PREFETCH_ALL_CANDS >= 2
+    // Candidates 1 .. kPfDepth of every particle of the lane: all their slot
+    // loads issued back to back (independent, up to KP * kPfDepth in flight),
+    // then all the position prefetches -- the per-candidate chain
+    // (slot load -> position gather) of phase A then finds both in L1 / L2.
+    constexpr int kPfDepth = PBDR_PREFETCH_ALL_CANDS;
+    int jc[KP][kPfDepth];
+#pragma unroll
+    for (int k = 0; k < KP; ++k) {
+      const int64_t p = start + k * 32 * W + wi * 32 + lane;
+#pragma unroll
+      for (int c = 1; c <= kPfDepth; ++c)
+        jc[k][c - 1] = c < ncs(k) ? __ldg(&A.cand_j[static_cast<int64_t>(c) * A.n + p]) : -1;
+    }
+#pragma unroll
+    for (int k = 0; k < KP; ++k) {
+      const int64_t p = start + k * 32 * W + wi * 32 + lane;
+#pragma unroll
+      for (int c = 1; c <= kPfDepth; ++c)
+        if (jc[k][c - 1] >= 0) {
+          prefetch_l2(&A.pos_in[jc[k][c - 1]]);
+          prefetch_l2(&A.cand_rr[static_cast<int64_t>(c) * A.n + p]);
+        }
+    }
+#endif
   }
   const int off = start - first;
 

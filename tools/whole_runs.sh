@@ -1,10 +1,16 @@
 #!/bin/bash
-# Whole runs of the pile configs: frames 4 to the config's own step count
-# (BASELINE.json: C3 500 steps, C4 200, C5 100), after 3 warm-up frames.
-for spec in "3 497" "4 197" "5 97"; do set -- $spec
-  timeout 1500 python bench.py --config $1 --steps $2 --warmup 3 --no-cpu-baseline --no-e2e | python -c "
+# The pile configs over their own step counts (BASELINE.json: C3 500 frames,
+# C4 200, C5 100): every frame after 3 warm-up frames is timed on the device;
+# `tail` is the last 20 frames (contact-rich), `whole` frames 3..end, `head`
+# the frames before the tail window. Clocks are sampled over the tail window.
+for c in ${@:-3 4 5}; do
+  timeout 1500 python bench.py --config $c --steps 20 --warmup 3 --no-cpu-baseline --no-e2e --no-secondary | python -c "
 import json,sys
 d=json.loads(sys.stdin.readline())
-print('C$1 whole run frames', d['config']['timed_frames'], 'value=%.3e' % d['value'], 'ms/frame=%.2f' % d['ms_per_step'],
-      'substep_frac=%.3f' % d['roofline']['whole_substep_frac'])"
+r=d['roofline']
+print('C$c', 'N=%d' % d['config']['particles_per_gpu'], 'tail', d['config']['timed_frames'].split(' ')[0], 'value=%.3e' % d['value'],
+      'ms/frame=%.2f' % d['ms_per_step'], 'substep_frac=%.3f' % r['whole_substep_frac'],
+      'whole %s value=%.3e' % (d['runs']['whole_run']['frames'], d['runs']['whole_run']['value']),
+      'head %s value=%.3e' % (d['runs']['before_window']['frames'], d['runs']['before_window']['value']),
+      'iter_frac=%.3f' % r['frac'], {k: round(v, 2) for k, v in r['per_kernel_ms_per_frame'].items()}, 'clocks', d['clocks'])"
 done
