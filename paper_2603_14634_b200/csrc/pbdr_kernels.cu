@@ -1301,7 +1301,11 @@ __device__ __forceinline__ void phase_a_particle(const IterArgs& A, int it, int6
   for (int c = 0; c < nc; ++c) {
     const int j = A.cand_j[static_cast<int64_t>(c) * A.n + p];
     PBDR_CHECK(c < PBDR_NBR_CAP && j >= 0 && j < A.n && j != p);
+#ifdef PBDR_RR_UNIFORM  // A/B probe only: every contact radius sum is this constant
+    const float rr = PBDR_RR_UNIFORM;
+#else
     const float rr = A.cand_rr[static_cast<int64_t>(c) * A.n + p];
+#endif
     // Multi-iteration launch with pairs: neighbours' X_i come from the
     // buffer the previous iteration wrote (after a grid barrier; L2 only).
 #if PBDR_INTILE_SMEM
@@ -1840,6 +1844,17 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
     cd_n = ld_keep_nc(&A.cta_desc[t1]);
     wd_n = ld_keep_nc(&A.warp_desc[t1 * kWarps + warp]);
   }
+#if PBDR_PREFETCH_NEXT == 2
+  // Next tile's staging ranges pulled into L2 as soon as its descriptor is
+  // known: two tiles' worth of HBM reads in flight per CTA.
+  if (warp == kWarps - 1 && lane == 0 && tile_next < ntiles) {
+    const uint32_t bytes = static_cast<uint32_t>(cd_n.y) * 16u;
+    bulk_prefetch_l2(A.pos_in + cd_n.x, bytes);
+    bulk_prefetch_l2(A.vel + cd_n.x, bytes);
+    bulk_prefetch_l2(A.rest + cd_n.x, bytes);
+    bulk_prefetch_l2(A.ncand + cd_n.x, static_cast<uint32_t>(cd_n.y) * 4u);
+  }
+#endif
   mbar_wait(&s_bar, it_parity);
   if (tm && threadIdx.x == 0) tm[1] = clock64();
 
@@ -1958,7 +1973,7 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
     if ((lane & 1) == 0) s_part[warp][lane >> 1] = t16;
     if ((lane & 3) == 0 && (lane >> 2) < 5) s_part[warp][16 + (lane >> 2)] = t5;
   }
-#if PBDR_PREFETCH_NEXT
+#if PBDR_PREFETCH_NEXT == 1
   if (it == 0 && warp == kWarps - 1 && lane == 0 && tile_next < ntiles) {
     const uint32_t bytes = static_cast<uint32_t>(cd_n.y) * 16u;
     bulk_prefetch_l2(A.pos_in + cd_n.x, bytes);
