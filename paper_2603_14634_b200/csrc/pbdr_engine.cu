@@ -30,7 +30,7 @@ using pbdr_host::set_config_error;
 using pbdr_host::set_error;
 
 int cuda_fail(cudaError_t e, const char* what) {
-  return set_error(PBDR_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return set_error(PBDR_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e) + pbdr_dev::checked_failure());
 }
 
 #define PBDR_CUDA(call)                                   \
@@ -341,6 +341,15 @@ void enqueue_iteration(pbdr_handle* h, int iter_index, pbdr_dev::LaunchHook* hoo
   it.mom_acc = h->mom_acc;
   it.cta_desc = h->pk_iter.cta;
   it.warp_desc = h->pk_iter.warp;
+  // The isolated / contact lists of this substep come with their descriptors
+  // copied in list order: claim c reads entry c directly.
+  for (int l = 0; l < 2; ++l)
+    if (list != nullptr && list == (l == 0 ? h->iso_list : h->contact_list) && h->list_cd[l] != nullptr &&
+        !h->timing) {
+      it.cta_desc = h->list_cd[l];
+      it.warp_desc = h->list_wd[l];
+      it.tile_list = nullptr;
+    }
   it.body_desc = h->pk_iter.body;
   it.body_mass = h->body_mass;
   it.err = h->err;
@@ -384,6 +393,11 @@ void enqueue_isolated(pbdr_handle* h, pbdr_dev::LaunchHook* hook, bool fuse_inte
   ca.contact_list = h->contact_list;
   ca.counts = h->tile_counts;
   ca.ntiles = h->pk_iter.ctas;
+  ca.warp_desc = h->pk_iter.warp;
+  ca.iso_cd = h->list_cd[0];
+  ca.iso_wd = h->list_wd[0];
+  ca.contact_cd = h->list_cd[1];
+  ca.contact_wd = h->list_wd[1];
   if (hook) hook->before(kHookBroadphase);
   launch_classify_tiles(ca, h->stream);
   if (hook) hook->after(kHookBroadphase);
@@ -913,6 +927,12 @@ int pbdr_gpu_create(const pbdr_scene_desc* d, const pbdr_solver_cfg* c, int devi
     int rc2 = dalloc(h, &h->iso_list, static_cast<size_t>(h->ctas));
     rc2 |= dalloc(h, &h->contact_list, static_cast<size_t>(h->ctas));
     rc2 |= dalloc(h, &h->tile_counts, 2);
+    bool compact = true;
+    if (const char* e = std::getenv("PBDR_COMPACT_DESC")) compact = std::atoi(e) != 0;
+    for (int l = 0; l < 2 && compact; ++l) {
+      rc2 |= dalloc(h, &h->list_cd[l], static_cast<size_t>(h->ctas));
+      rc2 |= dalloc(h, &h->list_wd[l], static_cast<size_t>(h->ctas) * PBDR_CTA_WARPS);
+    }
     if (rc2 != PBDR_OK) {
       const int code = pbdr_last_error_payload(nullptr, nullptr, nullptr);
       release(h);

@@ -65,6 +65,8 @@ struct pbdr_handle {
   int* iso_list = nullptr;    // [ctas] isolated tiles of the current substep
   int* contact_list = nullptr;  // [ctas] the other tiles
   int* tile_counts = nullptr;   // [2] sizes of the two lists (device)
+  int4* list_cd[2] = {nullptr, nullptr};  // tile / warp descriptors copied in list order (isolated,
+  int4* list_wd[2] = {nullptr, nullptr};  // contact) by k_classify_tiles; PBDR_COMPACT_DESC=0 disables
   bool broadphase = true;     // body-box filter before the hash grid (PBDR_BROADPHASE=0 disables)
   int kp = 4;                 // tile shape: particles per lane (pbdr_choose_kp)
   int launch_kp = 4;          // instantiation the tiles run on (kp, or 7 for one-warp bodies at kp 8)

@@ -46,13 +46,28 @@ constexpr uint32_t kEmpty = 0xFFFFFFFFu;
 #define PBDR_CHECKED 0
 #endif
 #if PBDR_CHECKED
-#define PBDR_CHECK(cond)                                                                          \
-  do {                                                                                           \
-    if (!(cond)) {                                                                               \
-      printf("PBDR_CHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__,    \
-             static_cast<int>(blockIdx.x), static_cast<int>(threadIdx.x));                        \
-      __trap();                                                                                  \
-    }                                                                                            \
+// Checked build: a failed check writes (line, block, thread) into a record in
+// mapped host memory -- readable after the context is gone -- and traps; the
+// host appends the record to the CUDA error message (checked_failure()).
+// No printf: its call frames would change the very code under test.
+struct CheckRecord {
+  int hit, line, block, thread;
+};
+__device__ CheckRecord* g_check_record = nullptr;
+__device__ __noinline__ void check_fail(int line) {
+  CheckRecord* r = g_check_record;
+  if (r) {
+    r->line = line;
+    r->block = static_cast<int>(blockIdx.x);
+    r->thread = static_cast<int>(threadIdx.x);
+    r->hit = 1;
+    __threadfence_system();
+  }
+  __trap();
+}
+#define PBDR_CHECK(cond)                 \
+  do {                                   \
+    if (!(cond)) check_fail(__LINE__);   \
   } while (0)
 #else
 #define PBDR_CHECK(cond) \
@@ -516,10 +531,15 @@ __global__ void __launch_bounds__(256) k_classify_tiles(ClassifyArgs A) {
   const int4 cd = A.cta_desc[t];
   bool iso = true;
   for (int i = 0; i < cd.w && iso; ++i) iso = A.npartners[cd.z + i] == 0;
-  if (iso)
-    A.iso_list[atomicAdd(&A.counts[0], 1)] = t;
-  else
-    A.contact_list[atomicAdd(&A.counts[1], 1)] = t;
+  const int c = atomicAdd(&A.counts[iso ? 0 : 1], 1);
+  (iso ? A.iso_list : A.contact_list)[c] = t;
+  if (A.iso_cd) {
+    int4* cdo = iso ? A.iso_cd : A.contact_cd;
+    int4* wdo = iso ? A.iso_wd : A.contact_wd;
+    cdo[c] = cd;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) wdo[c * kWarps + w] = A.warp_desc[t * kWarps + w];
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1187,6 +1207,21 @@ __global__ void __launch_bounds__(kNbrChunk) k_neighbours_staged(NeighbourArgs A
 #ifndef PBDR_PREFETCH_NEXT
 #define PBDR_PREFETCH_NEXT 0
 #endif
+// PBDR_DESC_SMEM: the next tile's descriptors are copied into shared memory
+// by cp.async instead of being loaded into registers one tile ahead (ncu: 6%
+// of the landed-C5 stall samples sat on those loads' first uses).
+#ifndef PBDR_DESC_SMEM
+#define PBDR_DESC_SMEM 1
+#endif
+// PBDR_ANCHOR_EARLY: body math A publishes the new anchor before the polar.
+// PBDR_CLAIM_AHEAD = w: launches of at least w waves of tiles claim two tiles
+// ahead (0 = off).
+#ifndef PBDR_CLAIM_AHEAD
+#define PBDR_CLAIM_AHEAD 0
+#endif
+#ifndef PBDR_ANCHOR_EARLY
+#define PBDR_ANCHOR_EARLY 1
+#endif
 // PBDR_PREFETCH_ALL_CANDS: the staging-time prefetch covers every candidate
 // of a particle, not only the first.
 #ifndef PBDR_PREFETCH_ALL_CANDS
@@ -1460,7 +1495,8 @@ enum ResSlot {
 template <bool kStore = true>  // false: the caller stores rquat / anchor (after a cluster barrier)
 __device__ __forceinline__ void body_math_a(const IterArgs& A, int bb, const float (&S)[21], float4 an,
                                             float invM, float4 rq4, float* R, float4& rq_new,
-                                            float4& an_new, long long* stamp = nullptr) {
+                                            float4& an_new, long long* stamp = nullptr,
+                                            float4* an_slot = nullptr) {
   bool finite = true;
 #pragma unroll
   for (int f = 0; f < 21; ++f) finite = finite && isfinite(S[f]);
@@ -1478,6 +1514,14 @@ __device__ __forceinline__ void body_math_a(const IterArgs& A, int bb, const flo
     R[kResC + k] = c[k];
     R[kResPb + k] = Pb[k];
     R[kResLb + k] = S[18 + k] - tmp[k];
+  }
+  // The new anchor does not depend on the polar: with an_slot (the tile's
+  // table entry) it is published now, so that neither it nor an / c stays
+  // live (spilled: ncu showed their reloads missing the small L1) across it.
+  an_new = make_float4(an.x + c[0], an.y + c[1], an.z + c[2], 0.0f);
+  if (kStore && an_slot) {
+    A.anchor[bb] = an_new;
+    *an_slot = an_new;
   }
   double qd[4];
   const float rq[4] = {rq4.x, rq4.y, rq4.z, rq4.w};
@@ -1502,10 +1546,9 @@ __device__ __forceinline__ void body_math_a(const IterArgs& A, int bb, const flo
   rq_new = ok ? make_float4(static_cast<float>(qd[0]), static_cast<float>(qd[1]), static_cast<float>(qd[2]),
                             static_cast<float>(qd[3]))
               : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-  an_new = make_float4(an.x + c[0], an.y + c[1], an.z + c[2], 0.0f);
   if (kStore) A.rquat[bb] = rq_new;
   if (!ok) record_error(A.err, PBDR_DEVERR_DEGENERATE, bb, A.substep_counter);
-  if (kStore) A.anchor[bb] = an_new;
+  if (kStore && !an_slot) A.anchor[bb] = an_new;
 }
 
 // Phase B of one particle: shape-matching delta (R q0 + c - p, when the polar
@@ -1661,10 +1704,18 @@ __device__ __forceinline__ void phase_c_particle(const IterArgs& A, int64_t p, f
 // two CTAs per SM with up to 128 registers (no spills). Measured on C4:
 // 0.382 ms per iteration vs 0.436 for KP = 4 at three CTAs per SM (80
 // registers, spills) -- more particles in flight per SM, fewer warps per body.
-// Contacts of a lane's particles processed side by side per candidate rank
-// (needs the rolled layout's s_dx).
+// PBDR_CAND_COLUMNS (KP <= 4 tiles; needs the rolled layout's s_dx): the
+// particle-particle contacts of a lane's KP particles run side by side,
+// candidate rank by rank, in a pass of their own before phase A, with all of
+// a rank's loads issued before any arithmetic (2; 3 also overlaps the next
+// rank's slot loads) -- KP gather chains in flight per lane instead of one,
+// only in the warps that have a candidate at all. Per particle the deltas are
+// still summed in ascending candidate order, so results are bit-identical.
+// Landed C5 iteration -8.7%, C3 -2.5% together with PBDR_DESC_SMEM and
+// PBDR_ANCHOR_EARLY (tools/ab_landed.py, round 2). 1 = the first version
+// (loads inside per-particle branches: no overlap, slower than off).
 #ifndef PBDR_CAND_COLUMNS
-#define PBDR_CAND_COLUMNS 0
+#define PBDR_CAND_COLUMNS 2
 #endif
 // Rolled particle loops with the deltas in shared memory (KP <= 4 tiles only:
 // at KP >= 7 the extra 32 KB would cost a CTA per SM).
@@ -1707,6 +1758,14 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
   __shared__ int4 s_tdesc[2][kWarps];
   __shared__ float4 s_trq[2][kWarps];
   __shared__ int s_next;
+  // Tile and warp descriptors of the current / next tile, double-buffered like
+  // the body table and filled by cp.async: no register waits on them
+  // (kDescSmem: the single-iteration launches, whose persistent CTAs walk
+  // many tiles; the multi-iteration launches keep them in registers).
+  constexpr bool kDescSmem = PBDR_DESC_SMEM != 0 && !MULTI;
+  static_assert(!(PBDR_DESC_SMEM != 0 && PBDR_PREFETCH_NEXT != 0), "the next-tile prefetch reads cd_n from registers");
+  __shared__ int4 s_cd[2];
+  __shared__ int4 s_wd[2][kWarps];
   const bool fixes = A.linfix || A.angfix;
   const long long t_entry = A.timing ? clock64() : 0;  // phase clocks (debug launches only)
   // One CTA per tile (grid == ntiles): static; otherwise tiles are claimed
@@ -1715,9 +1774,21 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
   const int ntiles = A.tile_count ? *A.tile_count : A.ntiles;
   const bool dynamic = A.tile_count != nullptr || static_cast<int>(gridDim.x) < ntiles;
   auto tid = [&](int c) { return A.tile_list ? A.tile_list[c] : c; };
+#if PBDR_CLAIM_AHEAD
+  // Launches of many waves claim two tiles ahead: the claim written at a
+  // tile's start was issued a whole tile earlier, so nobody waits on the
+  // atomic's round trip at the first barrier (ncu: 5% of the stall samples).
+  // Short launches keep the one-ahead claim (a CTA must not sit on a tile
+  // while others run dry).
+  const bool claim_ahead = dynamic && ntiles >= PBDR_CLAIM_AHEAD * static_cast<int>(gridDim.x);
+  int pending = ntiles;
+#endif
   if (threadIdx.x == 0) {
     mbar_init(&s_bar, 1);
     s_next = dynamic ? atomicAdd(A.tile_ctr, 1) : static_cast<int>(blockIdx.x);
+#if PBDR_CLAIM_AHEAD
+    if (claim_ahead) pending = atomicAdd(A.tile_ctr, 1);
+#endif
   }
   __syncthreads();
   int tile = s_next;
@@ -1734,10 +1805,15 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
       s_tmass[0][lane] = ld_keep_nc(&A.body_mass[bb]);
       s_trq[0][lane] = ld_keep(&A.rquat[bb]);
     }
+    if constexpr (kDescSmem) {
+      if (lane == 0) s_wd[0][warp] = wd_n;
+      if (threadIdx.x == 0) s_cd[0] = cd_n;
+    }
   }
+  if constexpr (kDescSmem) __syncthreads();
   for (uint32_t it_parity = 0; tile < ntiles; it_parity ^= 1u) {
-  const int4 cd = cd_n;  // first slot, slot count, first body, bodies
-  const int4 wd = wd_n;
+  const int4 cd = kDescSmem ? s_cd[tb] : cd_n;  // first slot, slot count, first body, bodies
+  const int4 wd = kDescSmem ? s_wd[tb][warp] : wd_n;
   const int first = cd.x;
 
   if (threadIdx.x == 0) {
@@ -1747,6 +1823,12 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
     bulk_g2s_stream(s_pos, A.pos_in + first, bytes, &s_bar);
     bulk_g2s_stream(s_vel, A.vel + first, bytes, &s_bar);
     bulk_g2s_stream(s_rest, A.rest + first, bytes, &s_bar);
+#if PBDR_CLAIM_AHEAD
+    if (claim_ahead) {
+      s_next = pending;
+      pending = atomicAdd(A.tile_ctr, 1);
+    } else
+#endif
     s_next = dynamic ? atomicAdd(A.tile_ctr, 1) : ntiles;  // the tile after this one
   }
   cp_async_wait_all();  // this tile's table (prefetched during the previous tile)
@@ -1788,6 +1870,7 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
       if (ncs(k) > 0) {
         const int64_t p = start + k * 32 * W + wi * 32 + lane;
         const int j = __ldg(&A.cand_j[p]);
+        PBDR_CHECK(j >= 0 && j < A.n);
 #if PBDR_PREFETCH_L1
         prefetch_l1(&A.pos_in[j]);
         prefetch_l1(&A.cand_rr[p]);
@@ -1839,7 +1922,18 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
   if (tm && threadIdx.x == 0) tm[0] = t_entry;  // CTA entry: stage = descriptors + table + bulk copies
   __syncthreads();  // barrier initialised, per-body table filled, next tile claimed
   const int tile_next = s_next;
-  if (tile_next < ntiles) {  // next tile's descriptors, consumed at its start
+  if constexpr (kDescSmem) {
+    if (tile_next < ntiles && warp == kWarps - 1 && lane <= kWarps) {
+      // Next tile's descriptors into the other buffer (asynchronous; complete
+      // before the tile-end barrier through cp.async.wait_all there).
+      const int t1 = tid(tile_next);
+      if (lane < kWarps)
+        cp_async16(&s_wd[tb ^ 1][lane], &A.warp_desc[t1 * kWarps + lane]);
+      else
+        cp_async16(&s_cd[tb ^ 1], &A.cta_desc[t1]);
+      cp_async_commit();
+    }
+  } else if (tile_next < ntiles) {  // next tile's descriptors, consumed at its start
     const int t1 = tid(tile_next);
     cd_n = ld_keep_nc(&A.cta_desc[t1]);
     wd_n = ld_keep_nc(&A.warp_desc[t1 * kWarps + warp]);
@@ -1903,17 +1997,76 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
   float acc[21];
 #pragma unroll
   for (int f = 0; f < 21; ++f) acc[f] = 0.0f;
+  bool warp_has_cands = false;  // kColumns
   if constexpr (kColumns) {
     // Phase A1: the particle-particle contacts of the lane's KP particles side
     // by side, candidate rank by rank -- up to KP independent gathers in flight
     // where the per-particle loop has one -- summed per particle in ascending
     // candidate order as before, and parked in s_dx for phase A2.
+    // ncs_pk != 0 <=> some particle of the lane has a candidate. Warps without
+    // any (most warps: contacts sit on a few faces) skip the pass and its
+    // round trip through s_dx.
+    warp_has_cands = __any_sync(kFull, ncs_pk != 0u);
+    if (warp_has_cands) {
     float dpp[KP][3];
 #pragma unroll
     for (int k = 0; k < KP; ++k) dpp[k][0] = dpp[k][1] = dpp[k][2] = 0.0f;
     int maxc = 0;
 #pragma unroll
     for (int k = 0; k < KP; ++k) maxc = max(maxc, ncs(k));
+#if PBDR_CAND_COLUMNS >= 2
+    // All of a rank's loads first (slots and radii, then the positions they
+    // point at: KP independent chains in flight), arithmetic afterwards.
+    // With PBDR_CAND_COLUMNS == 3 the next rank's slots and radii are loaded
+    // while this rank's positions are in flight (one dependent round trip
+    // per rank instead of two).
+    int jj[KP];
+    float rrk[KP];
+    auto load_rank = [&](int c, int (&jo)[KP], float (&ro)[KP]) {
+#pragma unroll
+      for (int k = 0; k < KP; ++k) {
+        jo[k] = -1;
+        ro[k] = 0.0f;
+        if (c < ncs(k)) {  // predicated loads, no branch
+          const int64_t at = static_cast<int64_t>(c) * A.n + (start + k * 32 * W + wi * 32 + lane);
+          jo[k] = __ldg(&A.cand_j[at]);
+          ro[k] = __ldg(&A.cand_rr[at]);
+        }
+      }
+    };
+    if (PBDR_CAND_COLUMNS == 3) load_rank(0, jj, rrk);
+#pragma unroll 1
+    for (int c = 0; c < maxc; ++c) {
+      float4 xjk[KP];
+      if (PBDR_CAND_COLUMNS == 2) load_rank(c, jj, rrk);
+#pragma unroll
+      for (int k = 0; k < KP; ++k) {
+        xjk[k] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        if (jj[k] >= 0) xjk[k] = (MULTI && A.multi_pairs) ? __ldcg(&A.pos_b[it & 1][jj[k]]) : A.pos_in[jj[k]];
+      }
+      int jn[KP];
+      float rn[KP];
+      if (PBDR_CAND_COLUMNS == 3) load_rank(c + 1, jn, rn);
+#pragma unroll
+      for (int k = 0; k < KP; ++k) {
+        if (jj[k] >= 0) {
+          const int q = k * 32 * W + wi * 32 + lane;
+          const int64_t p = start + q;
+          PBDR_CHECK(jj[k] < A.n && jj[k] != p);
+          const float4 x4 = s_pos[off + q];
+          const float x[3] = {x4.x, x4.y, x4.z};
+          pp_contact(x, x4.w, p, xjk[k], jj[k], rrk[k], A.relax, dpp[k]);
+        }
+      }
+      if (PBDR_CAND_COLUMNS == 3) {
+#pragma unroll
+        for (int k = 0; k < KP; ++k) {
+          jj[k] = jn[k];
+          rrk[k] = rn[k];
+        }
+      }
+    }
+#else
 #pragma unroll 1
     for (int c = 0; c < maxc; ++c) {
 #pragma unroll
@@ -1931,11 +2084,13 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
         }
       }
     }
+#endif
 #pragma unroll
     for (int k = 0; k < KP; ++k) {
       const int q = k * 32 * W + wi * 32 + lane;
       if (live && q < n) s_dx[off + q] = make_float4(dpp[k][0], dpp[k][1], dpp[k][2], 0.0f);
     }
+    }  // warp_has_cands
   }
   auto phase_a_k = [&](int k) {
     const int q = k * 32 * W + wi * 32 + lane;
@@ -1943,8 +2098,11 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
     const int64_t p = start + q;
     float d[3] = {0.0f, 0.0f, 0.0f};
     if constexpr (kColumns) {
-      const float4 t = s_dx[off + q];
-      const float pre[3] = {t.x, t.y, t.z};
+      float pre[3] = {0.0f, 0.0f, 0.0f};
+      if (warp_has_cands) {
+        const float4 t = s_dx[off + q];
+        pre[0] = t.x; pre[1] = t.y; pre[2] = t.z;
+      }
       phase_a_particle<MULTI>(A, it, p, s_pos[off + q], s_vel[off + q], s_rest[off + q], 0, a, d, acc, s_pos,
                               first, cd.y, pre);
     } else {
@@ -1986,7 +2144,10 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
   if (tm && threadIdx.x == 0) tm[2] = clock64();
 
   // ---- per-body math A (warp 0, lane = body of the CTA) ---------------------
-  if ((warp == 0 && lane < cd.w)) {
+  // kDescSmem: the body count is re-read from shared memory, so the predicate
+  // is rebuilt after the barrier instead of being kept (spilled) across the
+  // particle phase.
+  if ((warp == 0 && lane < (kDescSmem ? s_cd[tb].w : cd.w))) {
     const int bb = cd.z + lane;
     const float4 an = make_float4(s_tanc[tb][lane].x, s_tanc[tb][lane].y,
                                   s_tanc[tb][lane].z, s_tmass[tb][lane].x);
@@ -1997,11 +2158,18 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
     part_sum(&s_part[0][0], fw, bw.y, S);
     float4 rq_new, an_new;
     if (tm && lane == 0) tm[8] = clock64();  // body sums read
+#if PBDR_ANCHOR_EARLY
+    body_math_a(A, bb, S, an, invM, s_trq[tb][lane], &s_res[lane][0], rq_new, an_new,
+                (tm && lane == 0) ? tm + 12 : nullptr, &s_tanc[tb][lane]);
+    if (tm && lane == 0) tm[9] = clock64();
+    s_trq[tb][lane] = rq_new;   // next iteration of a multi-iteration launch
+#else
     body_math_a(A, bb, S, an, invM, s_trq[tb][lane], &s_res[lane][0], rq_new, an_new,
                 (tm && lane == 0) ? tm + 12 : nullptr);
     if (tm && lane == 0) tm[9] = clock64();
     s_trq[tb][lane] = rq_new;   // next iteration of a multi-iteration launch
     s_tanc[tb][lane] = an_new;
+#endif
   }
   __syncthreads();
   if (tm && threadIdx.x == 0) tm[3] = clock64();
@@ -2066,7 +2234,10 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
   if (tm && threadIdx.x == 0) tm[4] = clock64();
 
   // ---- per-body math B: momentum corrections -------------------------------
-  if ((warp == 0 && lane < cd.w)) {
+  // kDescSmem: the body count is re-read from shared memory, so the predicate
+  // is rebuilt after the barrier instead of being kept (spilled) across the
+  // particle phase.
+  if ((warp == 0 && lane < (kDescSmem ? s_cd[tb].w : cd.w))) {
     const int bb = cd.z + lane;
     const float2 mass = s_tmass[tb][lane];
     const int2 bw = make_int2(s_tdesc[tb][lane].w, s_tdesc[tb][lane].z);
@@ -2182,7 +2353,15 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
     tm[7] = smid;
 #endif
   }
-  if (tile_next < ntiles && warp == 0 && lane < cd_n.w) {
+  constexpr int kTableWarp = kDescSmem ? kWarps - 1 : 0;  // the warp that copied the descriptors also copies the table
+  if constexpr (kDescSmem) {
+    if (tile_next < ntiles && warp == kTableWarp) {
+      cp_async_wait_all();  // its own descriptor copies, issued at this tile's start
+      __syncwarp();
+      cd_n = s_cd[tb ^ 1];
+    }
+  }
+  if (tile_next < ntiles && warp == kTableWarp && lane < cd_n.w) {
     const int bb = cd_n.z + lane;
     cp_async16(&s_tdesc[tb ^ 1][lane], &A.body_desc[bb]);
     cp_async16(&s_tanc[tb ^ 1][lane], &A.anchor[bb]);
@@ -2946,7 +3125,35 @@ static cudaError_t prepare_one() {
 #endif
 }
 
+#if PBDR_CHECKED
+static CheckRecord* g_check_host = nullptr;
+#endif
+// Checked build: the failed device check behind a CUDA error, if any
+// ("pbdr_kernels.cu:LINE block B thread T"); empty otherwise.
+std::string checked_failure() {
+#if PBDR_CHECKED
+  if (g_check_host && g_check_host->hit) {
+    char buf[160];
+    std::snprintf(buf, sizeof(buf), " [PBDR_CHECK failed at pbdr_kernels.cu:%d block %d thread %d]",
+                  g_check_host->line, g_check_host->block, g_check_host->thread);
+    return buf;
+  }
+#endif
+  return std::string();
+}
+
 cudaError_t prepare_iteration_kernel() {
+#if PBDR_CHECKED
+  if (!g_check_host) {
+    cudaError_t ce = cudaHostAlloc(reinterpret_cast<void**>(&g_check_host), sizeof(CheckRecord), cudaHostAllocMapped);
+    if (ce != cudaSuccess) return ce;
+    *g_check_host = CheckRecord{0, 0, 0, 0};
+    CheckRecord* dev = nullptr;
+    ce = cudaHostGetDevicePointer(reinterpret_cast<void**>(&dev), g_check_host, 0);
+    if (ce == cudaSuccess) ce = cudaMemcpyToSymbol(g_check_record, &dev, sizeof(dev));
+    if (ce != cudaSuccess) return ce;
+  }
+#endif
   cudaError_t e = prepare_one<2>();
   if (e == cudaSuccess) e = prepare_one<4>();
   if (e == cudaSuccess) e = prepare_one<7>();

@@ -1,5 +1,6 @@
 // Device kernels of the PBD-R substep loop (sm_100a). See pbdr_kernels.cu.
 #pragma once
+#include <string>
 
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -219,6 +220,11 @@ struct ClassifyArgs {
   const int* npartners;   // per body (-1: overflow, searched in full)
   int* iso_list;          // tiles whose bodies all have no partner
   int* contact_list;      // the other tiles
+  const int4* warp_desc;  // descriptors of the packing, copied in list order:
+  int4* iso_cd;           // iso_cd[c] = cta_desc[iso_list[c]], iso_wd[8 c + w] likewise, so the
+  int4* iso_wd;           // iteration kernel reads a claim's descriptors without the list
+  int4* contact_cd;       // indirection (one dependent load less at every tile start)
+  int4* contact_wd;
   int* counts;            // [2] sizes of the two lists (zeroed before the launch)
   int ntiles;
 };
@@ -259,6 +265,7 @@ void launch_ranges(const RangesArgs& a, cudaStream_t s);
 void launch_neighbours(const NeighbourArgs& a, cudaStream_t s);
 size_t iteration_smem_bytes(int kp);
 cudaError_t prepare_iteration_kernel();
+std::string checked_failure();  // checked build: the device check that failed, else empty
 void launch_iteration(const IterArgs& a, int ctas, int kp, cudaStream_t s);
 int iteration_coop_capacity(int kp);  // CTAs a cooperative multi-iteration launch may use
 int iteration_scene_clusters(int kp, int cluster);  // resident scene clusters of `cluster` CTAs (0: none)
