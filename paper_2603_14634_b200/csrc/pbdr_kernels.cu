@@ -1214,10 +1214,10 @@ __global__ void __launch_bounds__(kNbrChunk) k_neighbours_staged(NeighbourArgs A
 #define PBDR_DESC_SMEM 1
 #endif
 // PBDR_ANCHOR_EARLY: body math A publishes the new anchor before the polar.
-// PBDR_CLAIM_AHEAD = w: launches of at least w waves of tiles claim two tiles
-// ahead (0 = off).
-#ifndef PBDR_CLAIM_AHEAD
-#define PBDR_CLAIM_AHEAD 0
+// PBDR_PREFETCH_COUNTS: after phase A the next tile's candidate counts and
+// first-candidate rows are prefetched into L2.
+#ifndef PBDR_PREFETCH_COUNTS
+#define PBDR_PREFETCH_COUNTS 1
 #endif
 #ifndef PBDR_ANCHOR_EARLY
 #define PBDR_ANCHOR_EARLY 1
@@ -1774,21 +1774,9 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
   const int ntiles = A.tile_count ? *A.tile_count : A.ntiles;
   const bool dynamic = A.tile_count != nullptr || static_cast<int>(gridDim.x) < ntiles;
   auto tid = [&](int c) { return A.tile_list ? A.tile_list[c] : c; };
-#if PBDR_CLAIM_AHEAD
-  // Launches of many waves claim two tiles ahead: the claim written at a
-  // tile's start was issued a whole tile earlier, so nobody waits on the
-  // atomic's round trip at the first barrier (ncu: 5% of the stall samples).
-  // Short launches keep the one-ahead claim (a CTA must not sit on a tile
-  // while others run dry).
-  const bool claim_ahead = dynamic && ntiles >= PBDR_CLAIM_AHEAD * static_cast<int>(gridDim.x);
-  int pending = ntiles;
-#endif
   if (threadIdx.x == 0) {
     mbar_init(&s_bar, 1);
     s_next = dynamic ? atomicAdd(A.tile_ctr, 1) : static_cast<int>(blockIdx.x);
-#if PBDR_CLAIM_AHEAD
-    if (claim_ahead) pending = atomicAdd(A.tile_ctr, 1);
-#endif
   }
   __syncthreads();
   int tile = s_next;
@@ -1823,12 +1811,6 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
     bulk_g2s_stream(s_pos, A.pos_in + first, bytes, &s_bar);
     bulk_g2s_stream(s_vel, A.vel + first, bytes, &s_bar);
     bulk_g2s_stream(s_rest, A.rest + first, bytes, &s_bar);
-#if PBDR_CLAIM_AHEAD
-    if (claim_ahead) {
-      s_next = pending;
-      pending = atomicAdd(A.tile_ctr, 1);
-    } else
-#endif
     s_next = dynamic ? atomicAdd(A.tile_ctr, 1) : ntiles;  // the tile after this one
   }
   cp_async_wait_all();  // this tile's table (prefetched during the previous tile)
@@ -2140,6 +2122,35 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
     bulk_prefetch_l2(A.ncand + cd_n.x, static_cast<uint32_t>(cd_n.y) * 4u);
   }
 #endif
+#if PBDR_PREFETCH_COUNTS
+  if constexpr (kDescSmem) {
+    // The next tile's candidate counts and first-candidate slots and radii
+    // (contiguous ranges: row 0 of the candidate arrays) pulled into L2 now,
+    // a phase and the body math ahead of their use at its start -- the two
+    // dependent loads there were 9% of the landed-C5 stall samples. The
+    // descriptor copies issued at this tile's start have long landed.
+    if (warp == kWarps - 1 && tile_next < ntiles) {
+      cp_async_wait_all();
+      __syncwarp();
+      if (lane == 0) {
+        const int4 cdx = s_cd[tb ^ 1];
+        const uint32_t bytes = static_cast<uint32_t>(cdx.y) * 4u;
+        bulk_prefetch_l2(A.ncand + cdx.x, bytes);
+        bulk_prefetch_l2(A.cand_j + cdx.x, bytes);
+        bulk_prefetch_l2(A.cand_rr + cdx.x, bytes);
+        if (PBDR_PREFETCH_COUNTS & 2) {  // second candidate row
+          bulk_prefetch_l2(A.cand_j + A.n + cdx.x, bytes);
+          bulk_prefetch_l2(A.cand_rr + A.n + cdx.x, bytes);
+        }
+        if (PBDR_PREFETCH_COUNTS & 4) {  // the staging ranges themselves
+          bulk_prefetch_l2(A.pos_in + cdx.x, 4u * bytes);
+          bulk_prefetch_l2(A.vel + cdx.x, 4u * bytes);
+          bulk_prefetch_l2(A.rest + cdx.x, 4u * bytes);
+        }
+      }
+    }
+  }
+#endif
   __syncthreads();
   if (tm && threadIdx.x == 0) tm[2] = clock64();
 
@@ -2175,7 +2186,12 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
   if (tm && threadIdx.x == 0) tm[3] = clock64();
 
   // ---- Phase B: shape matching, position + velocity update ----------------
-  const float* res = &s_res[live ? lb : 0][0];
+  // kDescSmem: the body's index in the tile is rebuilt from the shared
+  // descriptors (two LDS) rather than reloaded from a spill slot after the
+  // barrier (ncu: an LDL that misses the small L1).
+  int lb_b = live ? lb : 0;
+  if constexpr (kDescSmem) lb_b = live ? s_wd[tb][warp].x - s_cd[tb].z : 0;
+  const float* res = &s_res[lb_b][0];
   float accB[15];
 #pragma unroll
   for (int f = 0; f < 15; ++f) accB[f] = 0.0f;
