@@ -256,7 +256,7 @@ void enqueue_substep(pbdr_handle* h, pbdr_dev::LaunchHook* hook, bool integrated
   }
   if (hook) hook->before(kHookBroadphase);
   launch_near(nr, h->stream);
-  if (hook) hook->after(kHookBroadphase, (obb && h->broadphase) ? 5 : 4);
+  if (hook) hook->after(kHookBroadphase, ((obb && h->broadphase) ? 5 : 4) + ((nr.nbl > 0 && nr.nbl < (1 << 16)) ? 1 : 0));
 
   const int sb = sort_pairs(h->keys, h->vals, h->n, h->hash_bits, h->sort_temp, h->sm_count,
                             h->stream, hook, h->near_count);

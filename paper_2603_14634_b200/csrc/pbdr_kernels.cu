@@ -774,8 +774,15 @@ __device__ __forceinline__ bool near_test(const NearArgs& A, bool valid, int64_t
   return valid && in_any;
 }
 
+// SPLIT warps per body (scenes of few bodies: config 3's 8192 bodies are
+// 0.9 waves of warps at one warp per body, and a 1000-particle body with 15
+// partners is a 19K-instruction serial loop): warp `sub` of a body takes
+// every SPLIT-th chunk of 32 particles and adds its count to the body's
+// (integer atomics on a zeroed array: the total does not depend on order).
+template <int SPLIT>
 __global__ void __launch_bounds__(256) k_near_count(NearArgs A) {
-  const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int t = wg / SPLIT, sub = wg % SPLIT;
   const int lane = threadIdx.x & 31;
   if (t >= A.nbl) return;  // warp-uniform
   int b, start, n;
@@ -783,9 +790,9 @@ __global__ void __launch_bounds__(256) k_near_count(NearArgs A) {
   const int np = near_body_setup(A, t, lane, b, start, n, bx);
   uint32_t cnt = 0;
   if (np < 0) {
-    cnt = static_cast<uint32_t>(n);
+    cnt = sub == 0 ? static_cast<uint32_t>(n) : 0u;
   } else if (np > 0) {
-    for (int base = 0; base < n; base += 32) {
+    for (int base = 32 * sub; base < n; base += 32 * SPLIT) {
       const int q = base + lane;
       const int64_t p = start + static_cast<int64_t>(q);
       const bool near = near_test(A, q < n, p, np, bx, A.partners + static_cast<int64_t>(b) * PBDR_PARTNER_CAP);
@@ -793,7 +800,12 @@ __global__ void __launch_bounds__(256) k_near_count(NearArgs A) {
       cnt += __popc(__ballot_sync(kFull, near));
     }
   }
-  if (lane == 0) A.body_near[t] = cnt;
+  if (lane == 0) {
+    if (SPLIT == 1)
+      A.body_near[t] = cnt;
+    else if (cnt != 0u)
+      atomicAdd(&A.body_near[t], cnt);
+  }
 }
 
 __global__ void __launch_bounds__(256) k_near_write(NearArgs A) {
@@ -1737,7 +1749,10 @@ template <int KP, bool MULTI, bool FUSE = false>
 __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(IterArgs A) {
   constexpr int kSlots = kThreads * KP;  // particle slots staged per CTA
   constexpr bool kRoll = PBDR_ROLL_PARTICLES != 0 && KP <= 4;  // iter_rolled<KP>()
-  constexpr bool kColumns = kRoll && PBDR_CAND_COLUMNS != 0;
+  // Single-iteration launches only: the multi-iteration launches are the
+  // isolated tiles (no candidates at all) and small latency-bound scenes, and
+  // the extra pass cost their instantiation spills (C3 / C5 free flight -6%).
+  constexpr bool kColumns = kRoll && PBDR_CAND_COLUMNS != 0 && !MULTI;
   extern __shared__ float4 s_stage[];  // pos | vel | rest [| dX], kSlots each
   __shared__ __align__(16) float s_part[kWarps][kPartStride];
   __shared__ float s_res[kWarps][kResF];
@@ -2952,7 +2967,14 @@ void launch_near(const NearArgs& a, cudaStream_t s) {
     const unsigned wblocks = static_cast<unsigned>((static_cast<int64_t>(a.nbl) * 32 + 255) / 256);
     if (a.obb_q && !a.all_near)
       k_body_obb<<<std::min<unsigned>(wblocks, 148u * 16u), 256, 0, s>>>(a);
-    k_near_count<<<wblocks, 256, 0, s>>>(a);
+    // One warp per body fills the GPU from ~64K bodies on; below that, eight.
+    if (a.nbl >= (1 << 16)) {
+      k_near_count<1><<<wblocks, 256, 0, s>>>(a);
+    } else {
+      constexpr int kSplit = 8;
+      cudaMemsetAsync(a.body_near, 0, sizeof(uint32_t) * static_cast<size_t>(a.nbl), s);
+      k_near_count<kSplit><<<static_cast<unsigned>((static_cast<int64_t>(a.nbl) * kSplit * 32 + 255) / 256), 256, 0, s>>>(a);
+    }
     k_near_scan_tiles<<<(a.nbl + kScanTile - 1) / kScanTile, 1024, 0, s>>>(a);
     k_near_scan_top<<<1, 1024, 0, s>>>(a);
     k_near_write<<<wblocks, 256, 0, s>>>(a);
