@@ -127,3 +127,22 @@ def test_persistent_grid_path(pbdr, pyoracle, monkeypatch, cid, scale, frames):
     monkeypatch.delenv("PBDR_ITER_GRID_CAP")
     g1 = P.GeneratedScene(1)
     P.GpuSolver(g1.desc, g1.cfg).close()  # restores the uncapped grid for later handles
+
+
+def test_list_ordered_descriptors_off(pbdr, pyoracle, monkeypatch):
+    # The isolated / contact tile lists come with their descriptors copied in
+    # list order (k_classify_tiles); PBDR_COMPACT_DESC=0 makes the iteration
+    # kernel go through the list indirection instead. Same results, here on the
+    # capped (multi-tile, dynamically claimed) grid through landing and contact.
+    monkeypatch.setenv("PBDR_ITER_GRID_CAP", "4")
+    monkeypatch.setenv("PBDR_COOP_ITERS", "0")
+    monkeypatch.setenv("PBDR_COMPACT_DESC", "0")
+    g = P.GeneratedScene(2)
+    gpu = P.GpuSolver(g.desc, g.cfg)
+    orc = pyoracle.Oracle(g.desc, g.cfg)
+    gpu.step_frames(60)
+    assert orc.step(60 * g.cfg.substeps) == 0
+    compare_state(gpu, orc, "C2 capped grid, list indirection, 60 frames")
+    monkeypatch.delenv("PBDR_ITER_GRID_CAP")
+    g1 = P.GeneratedScene(1)
+    P.GpuSolver(g1.desc, g1.cfg).close()  # restores the uncapped grid for later handles
