@@ -1754,8 +1754,13 @@ __device__ __forceinline__ void phase_c_particle(const IterArgs& A, int64_t p, f
 // Landed C5 iteration -8.7%, C3 -2.5% together with PBDR_DESC_SMEM and
 // PBDR_ANCHOR_EARLY (tools/ab_landed.py, round 2). 1 = the first version
 // (loads inside per-particle branches: no overlap, slower than off).
+// 4 = the same pass worked off by the whole CTA from a shared list of the
+// tile's particles that have candidates (kCoop in k_iteration), one particle
+// per thread with up to four ranks' loads in flight: the contact work no
+// longer sits on the few warps that own those particles while the others
+// wait at the barrier -- landed C3 iteration -7.4%, C5 -0.9%.
 #ifndef PBDR_CAND_COLUMNS
-#define PBDR_CAND_COLUMNS 2
+#define PBDR_CAND_COLUMNS 4
 #endif
 // Rolled particle loops with the deltas in shared memory (KP <= 4 tiles only:
 // at KP >= 7 the extra 32 KB would cost a CTA per SM).
@@ -1781,6 +1786,14 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
   // isolated tiles (no candidates at all) and small latency-bound scenes, and
   // the extra pass cost their instantiation spills (C3 / C5 free flight -6%).
   constexpr bool kColumns = kRoll && PBDR_CAND_COLUMNS != 0 && !MULTI;
+  // kCoop (PBDR_CAND_COLUMNS == 4): the tile's particles that have candidates
+  // are listed in shared memory during the prelude and the whole CTA works the
+  // list off, one particle per thread, spread over the warps -- instead of the
+  // few warps that own those particles doing it while the others wait at the
+  // next barrier. Each particle's candidates are still summed in rank order.
+  constexpr bool kCoop = kColumns && PBDR_CAND_COLUMNS == 4;
+  __shared__ unsigned short s_clist[kCoop ? kThreads * KP : 1];
+  __shared__ int s_ccount;
   extern __shared__ float4 s_stage[];  // pos | vel | rest [| dX], kSlots each
   __shared__ __align__(16) float s_part[kWarps][kPartStride];
   __shared__ float s_res[kWarps][kResF];
@@ -1820,6 +1833,7 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
   if (threadIdx.x == 0) {
     mbar_init(&s_bar, 1);
     s_next = dynamic ? atomicAdd(A.tile_ctr, 1) : static_cast<int>(blockIdx.x);
+    s_ccount = 0;
   }
   __syncthreads();
   int tile = s_next;
@@ -1885,6 +1899,16 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
     else
       return ncs_a[k];
   };
+  if constexpr (kCoop) {
+#pragma unroll
+    for (int k = 0; k < KP; ++k) {
+      if (ncs(k) > 0) {
+        const int idx = (start - first) + k * 32 * W + wi * 32 + lane;
+        PBDR_CHECK(idx >= 0 && idx < kSlots && ncs(k) <= 32);
+        s_clist[atomicAdd(&s_ccount, 1)] = static_cast<unsigned short>(((ncs(k) - 1) << 10) | idx);
+      }
+    }
+  }
   // First candidate of each particle: its slot now, and its position and
   // contact radius pulled into L2, while the tile's staging copies are in
   // flight -- in contact-rich states phase A otherwise waits on two dependent
@@ -2032,7 +2056,49 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
     // any (most warps: contacts sit on a few faces) skip the pass and its
     // round trip through s_dx.
     warp_has_cands = __any_sync(kFull, ncs_pk != 0u);
-    if (warp_has_cands) {
+    if constexpr (kCoop) {
+      const int count = s_ccount;  // complete since the first barrier of the tile
+      // Entry e goes to warp e % 8, lane e / 8: the list spreads over the warps.
+      for (int e = lane * kWarps + warp; e < count; e += kThreads) {
+        const int ent = s_clist[e];
+        const int idx = ent & 1023, nc = (ent >> 10) + 1;
+        const int64_t p = first + idx;
+        const float4 x4 = s_pos[idx];
+        const float x[3] = {x4.x, x4.y, x4.z};
+        float d[3] = {0.0f, 0.0f, 0.0f};
+#pragma unroll 1
+        for (int c0 = 0; c0 < nc; c0 += 4) {
+          int jq[4];
+          float rq[4];
+          float4 xq[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            jq[u] = -1;
+            rq[u] = 0.0f;
+            if (c0 + u < nc) {  // predicated loads, no branch
+              const int64_t at = static_cast<int64_t>(c0 + u) * A.n + p;
+              jq[u] = __ldg(&A.cand_j[at]);
+              rq[u] = __ldg(&A.cand_rr[at]);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            xq[u] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+            if (jq[u] >= 0) xq[u] = A.pos_in[jq[u]];
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (jq[u] >= 0) {
+              PBDR_CHECK(jq[u] < A.n && jq[u] != p);
+              pp_contact(x, x4.w, p, xq[u], jq[u], rq[u], A.relax, d);
+            }
+          }
+        }
+        s_dx[idx] = make_float4(d[0], d[1], d[2], 0.0f);
+      }
+      __syncthreads();  // every listed particle's contact delta is in s_dx
+    }
+    if (!kCoop && warp_has_cands) {
     float dpp[KP][3];
 #pragma unroll
     for (int k = 0; k < KP; ++k) dpp[k][0] = dpp[k][1] = dpp[k][2] = 0.0f;
@@ -2124,7 +2190,7 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
     float d[3] = {0.0f, 0.0f, 0.0f};
     if constexpr (kColumns) {
       float pre[3] = {0.0f, 0.0f, 0.0f};
-      if (warp_has_cands) {
+      if (kCoop ? ncs(k) > 0 : warp_has_cands) {
         const float4 t = s_dx[off + q];
         pre[0] = t.x; pre[1] = t.y; pre[2] = t.z;
       }
@@ -2428,6 +2494,7 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
     cp_async16(&s_trq[tb ^ 1][lane], &A.rquat[bb]);
   }
   cp_async_commit();
+  if (kCoop && threadIdx.x == 0) s_ccount = 0;  // every thread read it long ago (phase A)
   __syncthreads();  // the next tile's bulk copies overwrite the staging buffers
   tile = tile_next;
   tb ^= 1;
