@@ -1756,11 +1756,18 @@ __device__ __forceinline__ void phase_c_particle(const IterArgs& A, int64_t p, f
 // (loads inside per-particle branches: no overlap, slower than off).
 // 4 = the same pass worked off by the whole CTA from a shared list of the
 // tile's particles that have candidates (kCoop in k_iteration), one particle
-// per thread with up to four ranks' loads in flight: the contact work no
+// per thread with two ranks' loads in flight: the contact work no
 // longer sits on the few warps that own those particles while the others
 // wait at the barrier -- landed C3 iteration -7.4%, C5 -0.9%.
 #ifndef PBDR_CAND_COLUMNS
 #define PBDR_CAND_COLUMNS 4
+#endif
+// Ranks in flight per listed particle in the CTA-wide pass. Two, not four:
+// the four-rank version's extra registers came out of the kernel's 80 as
+// spills (local loads x4), which cost the landing frames of C5 4% and its
+// landed frames everything the pass had gained (tools/scratch A/B, r02).
+#ifndef PBDR_COOP_BATCH
+#define PBDR_COOP_BATCH 2
 #endif
 // Rolled particle loops with the deltas in shared memory (KP <= 4 tiles only:
 // at KP >= 7 the extra 32 KB would cost a CTA per SM).
@@ -1792,6 +1799,7 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
   // few warps that own those particles doing it while the others wait at the
   // next barrier. Each particle's candidates are still summed in rank order.
   constexpr bool kCoop = kColumns && PBDR_CAND_COLUMNS == 4;
+  constexpr int kCoopBatch = PBDR_COOP_BATCH;  // candidate ranks in flight per listed particle
   __shared__ unsigned short s_clist[kCoop ? kThreads * KP : 1];
   __shared__ int s_ccount;
   extern __shared__ float4 s_stage[];  // pos | vel | rest [| dX], kSlots each
@@ -2067,12 +2075,12 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
         const float x[3] = {x4.x, x4.y, x4.z};
         float d[3] = {0.0f, 0.0f, 0.0f};
 #pragma unroll 1
-        for (int c0 = 0; c0 < nc; c0 += 4) {
-          int jq[4];
-          float rq[4];
-          float4 xq[4];
+        for (int c0 = 0; c0 < nc; c0 += kCoopBatch) {
+          int jq[kCoopBatch];
+          float rq[kCoopBatch];
+          float4 xq[kCoopBatch];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
+          for (int u = 0; u < kCoopBatch; ++u) {
             jq[u] = -1;
             rq[u] = 0.0f;
             if (c0 + u < nc) {  // predicated loads, no branch
@@ -2082,12 +2090,12 @@ __global__ void __launch_bounds__(kThreads, iter_min_blocks<KP>()) k_iteration(I
             }
           }
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
+          for (int u = 0; u < kCoopBatch; ++u) {
             xq[u] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
             if (jq[u] >= 0) xq[u] = A.pos_in[jq[u]];
           }
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
+          for (int u = 0; u < kCoopBatch; ++u) {
             if (jq[u] >= 0) {
               PBDR_CHECK(jq[u] < A.n && jq[u] != p);
               pp_contact(x, x4.w, p, xq[u], jq[u], rq[u], A.relax, d);
